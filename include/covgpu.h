@@ -1,0 +1,119 @@
+/*
+ * covgpu — B200-native windowed covariance estimation (arXiv 1303.2285).
+ *
+ * C ABI of libcovgpu.so.  No torch or CUDA types appear in the signatures:
+ * device pointers are plain `void*`, the CUDA stream is passed as `void*`
+ * (a cudaStream_t, NULL = the legacy default stream).
+ *
+ * Every entry point returns 0 on success and a negative COVGPU_E* code on
+ * failure; nothing throws across the ABI.  covgpu_last_error() returns the
+ * calling thread's last error text.  Calls are thread-safe per (device,
+ * stream).  Like the reference, kernels never validate numeric content; all
+ * argument checks happen here, before any launch.
+ *
+ * Replaces (the drop-in seam):
+ *   - engine._load_kernels / engine._run_class
+ *       /root/reference/pkg/src/covcomb/engine.py:78-83, :95-101
+ *     and the per-class kernels they dispatch to
+ *       _numba_kernels.combination_scratch  _numba_kernels.py:62-107
+ *       _numba_kernels.combination_direct   _numba_kernels.py:35-59
+ *       _numpy_kernels.apply_combination    _numpy_kernels.py:67-68
+ *     with ONE call per estimate (covgpu_estimate / covgpu_plan_execute);
+ *   - the per-class call shape itself is kept as covgpu_combination
+ *     (same arguments as combination_scratch(a, dr, dc, p, q, out, ...));
+ *   - _numba_kernels.warmup (_numba_kernels.py:110-119) -> covgpu_init.
+ */
+#ifndef COVGPU_H
+#define COVGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes */
+#define COVGPU_OK 0
+#define COVGPU_EINVAL -1   /* bad argument (reference: ValueError)          */
+#define COVGPU_ECUDA -2    /* CUDA runtime failure (reference: RuntimeError) */
+#define COVGPU_ENOMEM -3   /* device allocation failed                      */
+#define COVGPU_ECAPACITY -4 /* packed triangle beyond 2^31-1 (core.py:147-151) */
+
+/* element types of A and R */
+#define COVGPU_C128 0 /* complex double, interleaved re/im (numpy complex128) */
+#define COVGPU_C64 1  /* complex float  (numpy complex64)                     */
+
+/* output layouts */
+#define COVGPU_DENSE 0   /* (batch, PQ, PQ) row-major, exactly Hermitian       */
+#define COVGPU_PACKED 1  /* (batch, PQ(PQ+1)/2) upper triangle, row-major    */
+                         /* = reference CovarianceMatrix.packed (core.py:140-162) */
+#define COVGPU_COMPACT 2 /* (batch, sum_c eta_c) class-major slot order:      */
+                         /* class c in UC order, then u-major, then v         */
+
+typedef struct covgpu_plan* covgpu_plan_t;
+
+/* Context creation + one warm launch on `device` (replaces numba warmup). */
+int covgpu_init(int device);
+
+/* Text of the calling thread's last error ("" if none). */
+const char* covgpu_last_error(void);
+
+/* Library version string. */
+const char* covgpu_version(void);
+
+/* Number of offset classes |UC| = PQ + (P-1)(Q-1) (combinations.py:53-62). */
+int64_t covgpu_num_classes(int32_t p, int32_t q);
+
+/* Elements of R for a layout (batch included).  For COVGPU_COMPACT with a
+ * class subset, only the selected classes' slots are counted. */
+int64_t covgpu_output_elems(int64_t batch, int64_t n, int64_t m, int32_t p, int32_t q,
+                            int32_t layout, const int32_t* class_ids, int32_t n_classes);
+
+/* Build an execution plan: class table, bulk work groups, device workspace.
+ * class_ids (UC indices, NULL = all classes) selects a shard of the classes.
+ * Validation mirrors the reference: n,m >= 1; 1 <= p <= n; 1 <= q <= m
+ * (core.py:82-93, :101-106); packed size <= 2^31-1 (core.py:147-151). */
+int covgpu_plan_create(covgpu_plan_t* plan, int device, int64_t batch, int64_t n, int64_t m,
+                       int32_t p, int32_t q, int32_t dtype, const int32_t* class_ids,
+                       int32_t n_classes);
+
+/* R = scale * sum_windows x x^H for every selected class, written in `layout`.
+ * A_dev: (batch, n, m) device array of `dtype`; R_dev: covgpu_output_elems
+ * elements of `dtype`.  With every class selected every element of R is
+ * written exactly once (single writer, no atomics); with a subset the other
+ * elements are left untouched.  Asynchronous on `stream`. */
+int covgpu_plan_execute(covgpu_plan_t plan, const void* A_dev, void* R_dev, int32_t layout,
+                        double scale, void* stream);
+
+/* Bytes of device workspace the plan holds. */
+int64_t covgpu_plan_workspace_bytes(covgpu_plan_t plan);
+
+/* Number of bulk work groups and kernel launches one execute issues. */
+int32_t covgpu_plan_num_groups(covgpu_plan_t plan);
+int32_t covgpu_plan_launches(covgpu_plan_t plan);
+
+int covgpu_plan_destroy(covgpu_plan_t plan);
+
+/* One-shot estimate on device buffers (plan cached per shape internally). */
+int covgpu_estimate(const void* A_dev, int64_t batch, int64_t n, int64_t m, int32_t p,
+                    int32_t q, int32_t dtype, int32_t layout, const int32_t* class_ids,
+                    int32_t n_classes, double scale, void* R_dev, void* stream);
+
+/* End-to-end estimate on HOST buffers: H2D of A, compute, D2H of R, all on
+ * `stream`; returns after the result is in R_host. */
+int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m, int32_t p,
+                         int32_t q, int32_t dtype, int32_t layout, double scale, void* R_host,
+                         int device);
+
+/* Per-class call with the reference kernel's argument shape
+ * (combination_scratch(a, dr, dc, p, q, out, ...), _numba_kernels.py:62-107):
+ * writes ONLY class (dr, dc)'s slots of the packed upper triangle `out_dev`
+ * (unnormalised, as the reference does).  A_dev is (n, m) complex128. */
+int covgpu_combination(const void* A_dev, int64_t n, int64_t m, int32_t dr, int32_t dc,
+                       int32_t p, int32_t q, void* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COVGPU_H */

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the pinned oracle and
+the reference's golden vectors.  Tolerances are those of BASELINE.json's
+north_star: relative Frobenius <= 1e-12 (complex128), <= 1e-5 (complex64),
+and the dense result exactly Hermitian with an exactly real diagonal."""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import c4_instances, checksum, checksum_close, ref_random
+from oracle import covoracle as co
+from paper_1303_2285_b200 import (
+    WindowSpec,
+    estimate_batch,
+    estimate_batch_tensor,
+    estimate_combinations,
+    estimate_parallel,
+    estimate_tensor,
+    unique_combinations,
+)
+from paper_1303_2285_b200.workloads import make_input, workload
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+def packed_of(dense: np.ndarray) -> np.ndarray:
+    r, c = np.triu_indices(dense.shape[0])
+    return dense[r, c]
+
+
+def assert_hermitian(dense: np.ndarray) -> None:
+    assert np.array_equal(dense, dense.conj().T)
+    assert np.all(dense.diagonal().imag == 0)
+
+
+def test_known_answers(cuda):
+    cov, counters = estimate_combinations([[2 + 1j]], WindowSpec(1, 1))
+    assert cov.numpy().tolist() == [[5 + 0j]]
+    assert counters.multiplications == 1
+    cov, _ = estimate_combinations(np.ones((2, 2)), WindowSpec(1, 1))
+    assert cov.numpy().tolist() == [[1 + 0j]]  # 4 placements / K=4
+    cov, counters = estimate_combinations(np.zeros((6, 6)), WindowSpec(2, 2))
+    assert not cov.numpy().any()
+    assert counters.multiplications == co.um_count(6, 6, 2, 2)
+
+
+def test_cfg1(cuda, golden):
+    a = make_input("cfg1")
+    cov, _ = estimate_combinations(a, WindowSpec(4, 4))
+    got = cov.numpy()
+    assert_hermitian(got)
+    assert co.rel_frobenius(packed_of(got) * 841, golden["cfg1_packed"]) <= TOL64
+    assert co.rel_frobenius(got, co.covariance(a, 4, 4)) <= TOL64
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1, 1), (5, 1, 2, 1), (1, 6, 1, 3), (4, 4, 4, 4), (7, 5, 1, 1),
+                                   (3, 2, 3, 2), (20, 20, 8, 8), (12, 11, 4, 3), (10, 9, 3, 3)])
+def test_shapes(cuda, golden, shape):
+    n, m, p, q = shape
+    key = f"shape_{n}_{m}_{p}_{q}"
+    k = (n - p + 1) * (m - q + 1)
+    for mode in ("seq", "seq-opt", "par"):
+        cov, _ = estimate_combinations(golden[key + "_a"], WindowSpec(p, q), mode, threads=2)
+        got = cov.numpy()
+        assert_hermitian(got)
+        assert co.rel_frobenius(packed_of(got) * k, golden[key + "_naive"]) <= TOL64
+
+
+def test_single_window_is_outer_product(cuda):
+    a = ref_random(3, 2, 5)
+    cov, _ = estimate_combinations(a, WindowSpec(3, 2))
+    v = a.ravel(order="F")
+    np.testing.assert_allclose(cov.numpy(), np.outer(v, v.conj()), rtol=1e-12, atol=1e-12)
+
+
+def test_c4_sweep(cuda, golden):
+    """All 200 seeded instances of the reference's criterion 4 (N, M <= 24)."""
+    worst = 0.0
+    for i, (n, m, p, q, seed) in enumerate(c4_instances()):
+        a = ref_random(n, m, seed)
+        k = (n - p + 1) * (m - q + 1)
+        got = estimate_tensor(a, WindowSpec(p, q)).cpu().numpy()
+        assert_hermitian(got)
+        packed = packed_of(got) * k
+        assert checksum_close(checksum(packed), golden["c4_checksums"][i], 1e-11), (i, n, m, p, q)
+        err = co.rel_frobenius(packed, co.estimate_packed(a, p, q))
+        worst = max(worst, err)
+        assert err <= TOL64, (i, n, m, p, q, err)
+    print(f"C4 worst relF {worst:.3e}")
+
+
+@pytest.mark.parametrize("n,m,p,q", [(32, 32, 13, 13), (64, 64, 16, 16), (40, 70, 7, 19), (70, 40, 19, 7),
+                                     (33, 65, 1, 9), (65, 33, 9, 1), (100, 37, 17, 18), (18, 18, 10, 10),
+                                     (34, 34, 18, 18), (31, 97, 16, 3)])
+def test_medium_shapes_vs_oracle(cuda, n, m, p, q):
+    a = ref_random(n, m, n * 1000 + m * 10 + p + q)
+    got = estimate_tensor(a, WindowSpec(p, q)).cpu().numpy()
+    assert_hermitian(got)
+    assert co.rel_frobenius(got, co.covariance(a, p, q)) <= TOL64
+
+
+def test_cfg2_c128(cuda, golden):
+    w = workload("cfg2")
+    a = make_input(w)
+    got = estimate_tensor(a, WindowSpec(w.p, w.q)).cpu().numpy()
+    assert_hermitian(got)
+    packed = packed_of(got) * w.k
+    assert co.rel_frobenius(packed[golden["cfg2_idx"]], golden["cfg2_vals"]) <= TOL64
+    assert checksum_close(checksum(packed), golden["cfg2_checksum"], 1e-11)
+    assert co.rel_frobenius(got, co.covariance(a, w.p, w.q)) <= TOL64
+
+
+def test_cfg2_c64(cuda, golden):
+    w = workload("cfg2-c64")
+    a = make_input(w)
+    assert a.dtype == np.complex64
+    got_t = estimate_tensor(a, WindowSpec(w.p, w.q))
+    assert got_t.dtype == torch.complex64
+    got = got_t.cpu().numpy()
+    assert_hermitian(got)
+    ref = co.covariance(a.astype(np.complex128), w.p, w.q)
+    err = co.rel_frobenius(got.astype(np.complex128), ref)
+    print(f"cfg2-c64 relF {err:.3e}")
+    assert err <= TOL32
+    packed = packed_of(got.astype(np.complex128)) * w.k
+    assert co.rel_frobenius(packed[golden["cfg2_c64_idx"]], golden["cfg2_c64_vals"]) <= TOL32
+
+
+def test_cfg3(cuda, golden):
+    w = workload("cfg3")
+    a = make_input(w)
+    got = estimate_tensor(a, WindowSpec(w.p, w.q)).cpu().numpy()
+    assert_hermitian(got)
+    packed = packed_of(got) * w.k
+    assert co.rel_frobenius(packed[golden["cfg3_idx"]], golden["cfg3_vals"]) <= TOL64
+    assert checksum_close(checksum(packed), golden["cfg3_checksum"], 1e-11)
+
+
+def test_cfg4_batch(cuda, golden):
+    w = workload("cfg4")
+    stack = make_input(w)
+    got = estimate_batch_tensor(stack, WindowSpec(w.p, w.q))
+    assert got.shape == (w.batch, w.pq, w.pq) and got.dtype == torch.complex64
+    host = got.cpu().numpy()
+    for i in range(16):
+        assert_hermitian(host[i])
+        packed = packed_of(host[i].astype(np.complex128)) * w.k
+        assert checksum_close(checksum(packed), golden["cfg4_checksums"][i], 1e-5), i
+    for i in (0, 7, 511, 1023):
+        ref = co.covariance(stack[i].astype(np.complex128), w.p, w.q)
+        assert co.rel_frobenius(host[i].astype(np.complex128), ref) <= TOL32
+    # batch equals individual runs, bitwise (test_engine.py:150-158)
+    single = estimate_tensor(stack[511], WindowSpec(w.p, w.q)).cpu().numpy()
+    assert np.array_equal(single, host[511])
+
+
+def test_cfg5_sampled_classes(cuda, golden_cfg5):
+    """Full-size cfg5: every slot of 24 stratified classes against the
+    reference's own class kernel output, plus exact Hermitian structure."""
+    w = workload("cfg5")
+    a = make_input(w)
+    got = estimate_tensor(a, WindowSpec(w.p, w.q))
+    assert torch.equal(got, got.conj().T)
+    assert bool((got.diagonal().imag == 0).all())
+    for ci in golden_cfg5["picked"]:
+        dr, dc = (int(x) for x in golden_cfg5[f"cls_{ci}"])
+        s1 = max(-dr, 0)
+        pv, qu = w.p - abs(dr), w.q - dc
+        u = np.arange(qu)[:, None]
+        v = np.arange(pv)[None, :]
+        k1 = torch.as_tensor((w.p * u + s1 + v).reshape(-1), device=got.device)
+        vals = got[k1, k1 + dc * w.p + dr].cpu().numpy() * w.k
+        assert co.rel_frobenius(vals, golden_cfg5[f"sums_{ci}"]) <= TOL64, (ci, dr, dc)
+
+
+def test_batch_list_api_bitwise(cuda):
+    mats = [ref_random(10, 10, s) for s in (1, 2, 3)]
+    covs = estimate_batch(mats, WindowSpec(4, 4), threads=3)
+    assert len(covs) == 3
+    for mat, cov in zip(mats, covs):
+        single, _ = estimate_parallel(mat, WindowSpec(4, 4), threads=1)
+        assert torch.equal(cov.dense(), single.dense())
+    with pytest.raises(ValueError):
+        estimate_batch([ref_random(8, 8, 1), ref_random(8, 7, 1)], WindowSpec(2, 2))
+    with pytest.raises(ValueError):
+        estimate_batch([], WindowSpec(2, 2))
+
+
+def test_modes_bitwise_identical(cuda):
+    a = ref_random(14, 13, 3)
+    w = WindowSpec(5, 4)
+    base = estimate_combinations(a, w, "seq")[0].dense()
+    for mode in ("seq-opt", "par"):
+        for threads in (1, 2, 7):
+            assert torch.equal(estimate_combinations(a, w, mode, threads=threads)[0].dense(), base)
+
+
+def test_shards_union_bitwise(cuda):
+    """Class shards computed separately reassemble the full result bit for bit
+    (the multi-GPU contract)."""
+    from paper_1303_2285_b200.partition import partition_classes
+
+    w = workload("cfg2")
+    a = torch.as_tensor(make_input(w), device=cuda)
+    win = WindowSpec(w.p, w.q)
+    full = estimate_tensor(a, win)
+    for g in (2, 3, 8):
+        acc = torch.zeros_like(full)
+        for shard in partition_classes(w.n, w.m, win, g):
+            acc += estimate_tensor(a, win, class_ids=shard)
+        assert torch.equal(acc, full), g
+
+
+def test_validation_errors(cuda):
+    with pytest.raises(ValueError):
+        estimate_combinations(np.ones((3, 3)), WindowSpec(2, 2), mode="fast")
+    with pytest.raises(ValueError):
+        estimate_combinations(np.ones((3, 3)), WindowSpec(4, 1))
+    with pytest.raises(ValueError):
+        estimate_parallel(np.ones((3, 3)), WindowSpec(2, 2), threads=0)
+    with pytest.raises(ValueError):
+        estimate_combinations(np.ones((2, 2, 2)), WindowSpec(1, 1))
+    with pytest.raises(ValueError):
+        estimate_combinations(np.ones((0, 3)), WindowSpec(1, 1))
+    with pytest.raises(RuntimeError):
+        estimate_combinations(np.ones((3, 3)), WindowSpec(1, 1), backend="numba")
+
+
+def test_counters(cuda):
+    _, counters = estimate_combinations(ref_random(32, 32, 1), WindowSpec(13, 13))
+    assert counters.multiplications == 207880  # test_engine.py:112-115
+    assert [r[0] for r in counters.per_combination] == unique_combinations(WindowSpec(13, 13))
