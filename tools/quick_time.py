@@ -6,14 +6,18 @@ import torch
 from paper_1303_2285_b200 import WindowSpec, estimate_tensor, estimate_batch_tensor, um_count
 from paper_1303_2285_b200.workloads import make_input, workload
 
-for name in sys.argv[1:] or ["cfg1", "cfg2", "cfg2-c64", "cfg3", "cfg4", "cfg5"]:
+REPS = 5
+args = [x for x in sys.argv[1:] if not x.startswith("--reps=")]
+for x in sys.argv[1:]:
+    if x.startswith("--reps="): REPS = int(x[7:])
+for name in args or ["cfg1", "cfg2", "cfg2-c64", "cfg3", "cfg4", "cfg5"]:
     w = workload(name)
     a = torch.as_tensor(make_input(w), device="cuda")
     win = WindowSpec(w.p, w.q)
     f = (lambda: estimate_batch_tensor(a, win)) if w.batch > 1 else (lambda: estimate_tensor(a, win))
     out = f(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    reps = 5
+    reps = REPS
     e0.record()
     for _ in range(reps):
         out = f()
