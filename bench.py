@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the covgpu hot path (contract: ONE JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
+    python bench.py --impl reference ...          # CPU reference arm
+
+A step = one full estimate of R for the configured workload (default cfg5:
+2048x2048 complex128, P=Q=64 — BASELINE.json's largest config, which fits one
+GPU).  `value` is dense R entries per second with A resident in HBM; every
+step is bracketed by a barrier and device syncs, timed with CUDA events on the
+launch stream, and L2 is flushed (256 MiB write) between steps.  Under
+torchrun the offset classes are sharded across ranks (strong scaling: total
+work fixed), A is broadcast from rank 0 inside the timed region over NCCL,
+and the time is the max over ranks.
+
+Extra keys: `roofline` (bulk kernel = the dominant one: algorithmic FP64/FP32
+flops per launch / its CUDA-event duration, against the FMA peak measured on
+this GPU right before the run), `cpu_baseline` (the oracle's multithreaded
+C port of the reference's class kernel on this host's cores, bounded sample,
+extrapolated by product count), `e2e` (same metric through the C ABI with
+pinned HOST buffers: H2D of A + compute + D2H of the packed triangle, wall
+clock), `clocks` (nvidia-smi sampled during the timed region).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "R entries/s and effective GFLOP/s vs FP64/FP32 roofline at 1/2/4/8 B200"
+UNIT = "R entries/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def products(w):
+    """(UM, bulk-kernel products, edge-row products, corner products) per snapshot."""
+    from paper_1303_2285_b200.combinations import um_count, unique_combinations
+    from paper_1303_2285_b200.core import WindowSpec
+
+    n, m, p, q = w.n, w.m, w.p, w.q
+    bulk = edge = corner = 0
+    for c in unique_combinations(WindowSpec(p, q)):
+        ar, ac = p - abs(c.dr) - 1, q - c.dc - 1
+        bulk += (n - 2 * p + 2 + abs(c.dr)) * (m - c.dc)
+        edge += 2 * ar * (m - 2 * q + 2 + c.dc)
+        corner += 4 * ar * ac
+    return um_count(n, m, p, q), bulk, edge, corner
+
+
+def cpu_reference(w, budget_s: float, seed: int = 0):
+    """Time the oracle's C port of the reference's class kernel (SAT per
+    class, thread pool over classes) on a stratified class sample; return
+    (entries/s extrapolated by product count, sample description, threads)."""
+    from oracle import covoracle_c
+    from paper_1303_2285_b200.combinations import pair_count, unique_combinations
+    from paper_1303_2285_b200.core import WindowSpec
+    from paper_1303_2285_b200.workloads import make_input
+
+    a = make_input(w)
+    a0 = (a if w.batch == 1 else a[0]).astype(np.complex128)
+    combos = unique_combinations(WindowSpec(w.p, w.q))
+    mu = np.array([pair_count(c, w.n, w.m) for c in combos], dtype=np.float64)
+    threads = covoracle_c.max_threads()
+    # calibrate on a small stratified sample, then size the timed sample
+    ncls = len(combos)
+    probe = np.linspace(0, ncls - 1, min(ncls, max(threads, 16))).round().astype(np.int32)
+    t0 = time.perf_counter()
+    covoracle_c.estimate_packed(a0, w.p, w.q, probe, threads)
+    t_probe = max(time.perf_counter() - t0, 1e-6)
+    per_prod = t_probe / mu[probe].sum()
+    want = int(ncls * min(1.0, budget_s / max(per_prod * mu.sum(), 1e-9)))
+    want = max(min(ncls, want), min(ncls, threads))
+    ids = np.unique(np.linspace(0, ncls - 1, want).round().astype(np.int32))
+    t0 = time.perf_counter()
+    covoracle_c.estimate_packed(a0, w.p, w.q, ids, threads)
+    t = time.perf_counter() - t0
+    t_full = t * mu.sum() / mu[ids].sum() * w.batch
+    entries = float(w.pq) ** 2 * w.batch
+    frac = mu[ids].sum() / mu.sum()
+    sample = (f"{len(ids)} of {ncls} offset classes (stratified, {frac:.1%} of the products) of "
+              f"{'1 snapshot of ' if w.batch > 1 else ''}{w.name} in {t:.2f} s on {threads} threads, "
+              f"extrapolated by product count to the full workload ({t_full:.1f} s)")
+    return entries / t_full, sample, threads, t_full
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path("/tmp") / f"covgpu_clocks_{os.getpid()}_{index}.csv"
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        load = [s for s in sm if s > 500] or sm
+        return {
+            "sm_mhz": statistics.median(load) if load else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "power_w_max": max(power) if power else None,
+            "samples": len(sm),
+            "reasons": sorted(reasons),
+        }
+
+
+def run_reference(args, rank: int) -> None:
+    from paper_1303_2285_b200.workloads import workload
+
+    if rank != 0:
+        return
+    w = workload(args.config)
+    for _ in range(args.warmup):
+        cpu_reference(w, args.ref_budget)
+    vals, samples, threads = [], None, 1
+    for _ in range(args.steps):
+        v, samples, threads, _t = cpu_reference(w, args.ref_budget)
+        vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(w.pq) ** 2 * w.batch / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic ({w.name}: seeded, BASELINE.json config)",
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
+                   "input": w.dtype, "path": "oracle C port of the reference class kernel"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": samples},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--impl", default="covgpu", choices=["covgpu", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of CPU-baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=4.0, help="seconds per reference-arm step")
+    ap.add_argument("--layout", default="dense", choices=["dense", "packed", "compact"])
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1303_2285_b200.core import WindowSpec
+    from paper_1303_2285_b200.partition import partition_classes, shard_cost
+    from paper_1303_2285_b200.plan import Plan, probe_fma_peak
+    from paper_1303_2285_b200.workloads import make_input, workload
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    w = workload(args.config)
+    win = WindowSpec(w.p, w.q)
+    tdt = torch.complex128 if w.dtype == "c128" else torch.complex64
+    ids = None
+    if world > 1:
+        ids = partition_classes(w.n, w.m, win, world)[rank]
+    plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, class_ids=ids, device=dev)
+    layout = args.layout if world == 1 else "compact"
+    host_a = make_input(w) if rank == 0 else None
+    a = torch.empty((w.batch, w.n, w.m), dtype=tdt, device=dev)
+    if rank == 0:
+        a.copy_(torch.from_numpy(host_a).reshape(a.shape))
+    out = plan.alloc_output(layout)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    # roofline denominator: FMA pipe measured on this GPU (not in MEASURED_PEAKS.json)
+    peak = probe_fma_peak(local, fp64=(w.dtype == "c128"), seconds=1.5)
+
+    def step():
+        if world > 1:
+            dist.broadcast(a, src=0)
+        plan.execute(a, out, layout)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    plan.set_timing(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    total_ms = 0.0
+    kern = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)  # evict A/R from L2 between steps (untimed)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            total_ms += e0.elapsed_time(e1)
+            kern.append(plan.kernel_times())
+    plan.set_timing(False)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+
+    um, bulk_p, edge_p, corner_p = products(w)
+    entries = float(w.pq) ** 2 * w.batch
+    value = entries / (ms * 1e-3)
+    flops = 8.0 * um * w.batch
+    kt = np.array(kern) if kern and all(len(k) == len(kern[0]) for k in kern) else None
+    kernel_ms = {}
+    if kt is not None and kt.size:
+        for name, col in zip(["bulk", "edge_rows", "finalize"], kt.mean(axis=0)):
+            kernel_ms[name] = float(col)
+    shard_frac = 1.0 if ids is None else shard_cost(w.n, w.m, win, ids) / um
+    roof = None
+    if "bulk" in kernel_ms and kernel_ms["bulk"] > 0:
+        achieved = 8.0 * bulk_p * w.batch * shard_frac / (kernel_ms["bulk"] * 1e-3) / 1e12
+        traffic = None
+        prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
+        if prof.exists():
+            try:
+                traffic = json.loads(prof.read_text()).get("bulk_dram_bytes_per_launch")
+            except (ValueError, OSError):
+                traffic = None
+        roof = {"bound": "fp64" if w.dtype == "c128" else "fp32", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_bulk", "peak_source": "FMA-loop probe measured on this GPU in this run "
+                "(MEASURED_PEAKS.json has no FP64/FP32 figure)",
+                "algorithmic_flops_per_launch": 8.0 * bulk_p * w.batch * shard_frac,
+                "nominal_peak": 148 * (64 if w.dtype == "c128" else 128) * 2 * 1.965e9 / 1e12}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if w.dtype == "c128" else "f32",
+        "data": f"synthetic ({w.name}: seeded CN(0,1)/sinusoid inputs of BASELINE.json)",
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
+                   "input": w.dtype, "output": layout, "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"class-shard x{world}" if world > 1 else "single GPU"},
+        "effective_gflops": flops / (ms * 1e-3) / 1e9,
+        "kernel_ms": kernel_ms,
+        "gpu_launches": plan.launches * args.steps,
+        "roofline": roof,
+        "clocks": clocks.summary(),
+    }
+
+    # end to end through the C ABI with pinned host buffers
+    if not args.no_e2e:
+        e2e_layout = "packed" if world == 1 else "compact"
+        a_host = torch.from_numpy(host_a if rank == 0 else make_input(w)).reshape(
+            w.batch, w.n, w.m).pin_memory()
+        r_host = torch.empty(plan.output_elems(e2e_layout), dtype=tdt).pin_memory()
+        plan.execute_host(a_host, r_host, e2e_layout)  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.execute_host(a_host, r_host, e2e_layout)
+        te = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        esz = r_host.element_size()
+        line["e2e"] = {"value": entries / float(te.item()), "unit": UNIT,
+                       "h2d_bytes_per_step": a_host.numel() * esz,
+                       "d2h_bytes_per_step": r_host.numel() * esz,
+                       "ms_per_step": float(te.item()) * 1e3,
+                       "path": f"covgpu_plan_execute_host, pinned host buffers, {e2e_layout} R, wall clock"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, sample, threads, t_full = cpu_reference(w, args.cpu_budget)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

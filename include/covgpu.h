@@ -92,6 +92,14 @@ int64_t covgpu_plan_workspace_bytes(covgpu_plan_t plan);
 int32_t covgpu_plan_num_groups(covgpu_plan_t plan);
 int32_t covgpu_plan_launches(covgpu_plan_t plan);
 
+/* Record CUDA events around every kernel of subsequent executes (on the
+ * execute's stream) so covgpu_plan_kernel_times can report per-kernel times. */
+int covgpu_plan_set_timing(covgpu_plan_t plan, int32_t enable);
+
+/* Per-kernel durations (ms) of the last timed execute, in launch order
+ * (bulk, edge rows, finalize); waits for it.  Returns the count written. */
+int32_t covgpu_plan_kernel_times(covgpu_plan_t plan, float* ms, int32_t max_n);
+
 int covgpu_plan_destroy(covgpu_plan_t plan);
 
 /* One-shot estimate on device buffers (plan cached per shape internally). */
@@ -99,11 +107,22 @@ int covgpu_estimate(const void* A_dev, int64_t batch, int64_t n, int64_t m, int3
                     int32_t q, int32_t dtype, int32_t layout, const int32_t* class_ids,
                     int32_t n_classes, double scale, void* R_dev, void* stream);
 
-/* End-to-end estimate on HOST buffers: H2D of A, compute, D2H of R, all on
- * `stream`; returns after the result is in R_host. */
+/* End-to-end estimate on HOST buffers: H2D of A, compute, D2H of R on a
+ * library-owned stream (device buffers cached with the plan); returns after
+ * the result is in R_host.  Pinned host buffers give full PCIe bandwidth. */
 int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m, int32_t p,
                          int32_t q, int32_t dtype, int32_t layout, double scale, void* R_host,
                          int device);
+
+/* End-to-end execute of a plan on HOST buffers (its class shard only; for a
+ * shard use COVGPU_COMPACT to receive just the shard's slots). */
+int covgpu_plan_execute_host(covgpu_plan_t plan, const void* A_host, void* R_host, int32_t layout,
+                             double scale);
+
+/* Bench utility: FP64 (dtype COVGPU_C128) or FP32 (COVGPU_C64) FMA-pipe
+ * throughput in TFLOP/s, measured for about `seconds` on `device` — the
+ * roofline denominator of the covariance kernels. */
+int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tflops);
 
 /* Per-class call with the reference kernel's argument shape
  * (combination_scratch(a, dr, dc, p, q, out, ...), _numba_kernels.py:62-107):

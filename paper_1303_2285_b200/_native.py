@@ -48,6 +48,8 @@ _SIGS = {
     "covgpu_plan_workspace_bytes": (_i64, [_vp]),
     "covgpu_plan_num_groups": (_i32, [_vp]),
     "covgpu_plan_launches": (_i32, [_vp]),
+    "covgpu_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
+    "covgpu_plan_kernel_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), _i32]),
     "covgpu_plan_destroy": (ctypes.c_int, [_vp]),
     "covgpu_estimate": (
         ctypes.c_int,
@@ -57,6 +59,8 @@ _SIGS = {
         ctypes.c_int,
         [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _dbl, _vp, ctypes.c_int],
     ),
+    "covgpu_plan_execute_host": (ctypes.c_int, [_vp, _vp, _vp, _i32, _dbl]),
+    "covgpu_probe_fma_peak": (ctypes.c_int, [ctypes.c_int, _i32, _dbl, ctypes.POINTER(_dbl)]),
     "covgpu_combination": (ctypes.c_int, [_vp, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)

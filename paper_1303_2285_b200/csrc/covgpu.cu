@@ -42,6 +42,7 @@
 #include "edge.cuh"
 #include "finalize.cuh"
 #include "general.cuh"
+#include "probe.cuh"
 
 using namespace covgpu;
 
@@ -100,6 +101,16 @@ struct covgpu_plan {
   long long ws_bytes = 0;
   size_t fin_smem = 0;
   int launches = 0;
+  // optional per-kernel timing of the last execute (events on its stream)
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  int nev = 0;
+  // end-to-end host path: cached stream and device buffers
+  cudaStream_t host_stream = nullptr;
+  void* hA = nullptr;
+  void* hR = nullptr;
+  size_t hA_bytes = 0, hR_bytes = 0;
+  std::mutex host_mu;
 };
 
 namespace {
@@ -137,6 +148,11 @@ int dalloc(X** p, size_t count, long long* acc) {
 }
 
 void plan_free(covgpu_plan* pl) {
+  for (auto& e : pl->ev)
+    if (e) cudaEventDestroy(e);
+  if (pl->host_stream) cudaStreamDestroy(pl->host_stream);
+  cudaFree(pl->hA);
+  cudaFree(pl->hR);
   cudaFree(pl->d_cls);
   cudaFree(pl->d_cls_slot);
   cudaFree(pl->d_ccpart);
@@ -237,12 +253,18 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   }
 
   CUDA_TRY(set_attrs());
+  pl->nev = 0;
+  auto mark = [&]() {
+    if (pl->timing && pl->nev < 8) cudaEventRecord(pl->ev[pl->nev++], st);
+  };
+  mark();
   switch (pl->E) {
     case 4: launch_bulk<T, 4>(pl, A, st); break;
     case 8: launch_bulk<T, 8>(pl, A, st); break;
     default: launch_bulk<T, 16>(pl, A, st);
   }
   ++launches;
+  mark();
   if (pl->S > 0) {
     switch (pl->D) {
       case 4: launch_edge<T, 4>(pl, A, st); break;
@@ -250,12 +272,14 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       default: launch_edge<T, 16>(pl, A, st);
     }
     ++launches;
+    mark();
   }
   const long long ntasks = (long long)B * pl->nclasses;
   k_finalize<T><<<(unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS), FIN_WARPS * 32, pl->fin_smem, st>>>(
       A, pr, pl->d_cls, pl->nclasses, pl->ncb, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc,
       pl->tot_rc, pl->nseg, pl->d_slots, pl->tot_slots, R, layout, r_bstride, scale, ntasks, pr.Q);
   ++launches;
+  mark();
   CUDA_TRY(cudaGetLastError());
   pl->launches = launches;
   return COVGPU_OK;
@@ -278,6 +302,9 @@ std::map<PlanKey, covgpu_plan*> g_cache;
 }  // namespace
 
 extern "C" {
+
+int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
+                             double scale);
 
 const char* covgpu_last_error(void) { return g_last_error.c_str(); }
 
@@ -471,6 +498,25 @@ int32_t covgpu_plan_num_groups(covgpu_plan_t pl) {
 }
 int32_t covgpu_plan_launches(covgpu_plan_t pl) { return pl ? pl->launches : -1; }
 
+int covgpu_plan_set_timing(covgpu_plan_t pl, int32_t enable) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  if (enable)
+    for (auto& e : pl->ev)
+      if (!e) CUDA_TRY(cudaEventCreate(&e));
+  pl->timing = enable != 0;
+  return COVGPU_OK;
+}
+
+int32_t covgpu_plan_kernel_times(covgpu_plan_t pl, float* ms, int32_t max_n) {
+  if (!pl || !pl->timing || pl->nev < 2) return 0;
+  if (cudaEventSynchronize(pl->ev[pl->nev - 1]) != cudaSuccess) return fail(COVGPU_ECUDA, "event sync");
+  int n = 0;
+  for (int i = 0; i + 1 < pl->nev && n < max_n; ++i, ++n)
+    if (cudaEventElapsedTime(&ms[n], pl->ev[i], pl->ev[i + 1]) != cudaSuccess) ms[n] = -1.0f;
+  return n;
+}
+
 int covgpu_plan_destroy(covgpu_plan_t pl) {
   if (!pl) return COVGPU_OK;
   cudaSetDevice(pl->device);
@@ -515,37 +561,96 @@ int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m
                          int device) {
   int rc = validate(batch, n, m, p, q, dtype);
   if (rc) return rc;
-  if (!A_host || !R_host) return fail(COVGPU_EINVAL, "host buffers must be non-NULL");
   CUDA_TRY(cudaSetDevice(device));
   covgpu_plan_t pl = nullptr;
   rc = cached_plan(&pl, device, batch, n, m, p, q, dtype, nullptr, 0);
   if (rc) return rc;
-  const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
-  const size_t a_bytes = (size_t)batch * n * m * esz;
-  const int64_t r_elems = covgpu_output_elems(batch, n, m, p, q, layout, nullptr, 0);
-  if (r_elems < 0) return fail(COVGPU_EINVAL, "unknown layout");
+  return covgpu_plan_execute_host(pl, A_host, R_host, layout, scale);
+}
+
+int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tflops) {
+  if (!tflops) return fail(COVGPU_EINVAL, "tflops is NULL");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  const int blocks = prop.multiProcessorCount * 8, threads = 256;
+  void* out = nullptr;
+  CUDA_TRY(cudaMalloc(&out, 16));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto run = [&](int iters) -> float {
+    cudaEventRecord(e0);
+    if (dtype == COVGPU_C128)
+      k_fma_probe<double><<<blocks, threads>>>((double*)out, iters, 0.999999);
+    else
+      k_fma_probe<float><<<blocks, threads>>>((float*)out, iters, 0.999999f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms;
+  };
+  int iters = 1024;
+  float ms = run(iters);
+  while (ms < 20.f && iters < (1 << 26)) {
+    iters *= 2;
+    ms = run(iters);
+  }
+  // repeat for ~`seconds`, keep the best (sustained clocks, not a cold burst)
+  const int reps = std::max(3, (int)(seconds * 1000.0 / std::max(ms, 1.f)));
+  float best = ms;
+  for (int r = 0; r < reps; ++r) best = std::min(best, run(iters));
+  cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (e != cudaSuccess) return fail(COVGPU_ECUDA, cudaGetErrorString(e));
+  const double flops = 2.0 * 16.0 * (double)iters * blocks * threads;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return COVGPU_OK;
+}
+
+int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
+                             double scale) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  if (!A_host || !R_host) return fail(COVGPU_EINVAL, "host buffers must be non-NULL");
+  if (layout < COVGPU_DENSE || layout > COVGPU_COMPACT) return fail(COVGPU_EINVAL, "unknown layout");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  const Problem& pr = pl->pr;
+  const size_t esz = pl->dtype == COVGPU_C128 ? 16 : 8;
+  const size_t a_bytes = (size_t)pl->batch * pr.N * pr.M * esz;
+  long long r_elems;
+  if (layout == COVGPU_DENSE)
+    r_elems = pl->batch * (long long)pr.PQ * pr.PQ;
+  else if (layout == COVGPU_PACKED)
+    r_elems = pl->batch * ((long long)pr.PQ * (pr.PQ + 1) / 2);
+  else
+    r_elems = pl->batch * pl->compact_elems;
   const size_t r_bytes = (size_t)r_elems * esz;
-  void *dA = nullptr, *dR = nullptr;
-  cudaStream_t st;
-  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  cudaError_t e = cudaMallocAsync(&dA, a_bytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dR, r_bytes, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A_host, a_bytes, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) {
-    cudaStreamDestroy(st);
-    return fail(COVGPU_ECUDA, std::string("estimate_host: ") + cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(pl->host_mu);
+  if (!pl->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->host_stream, cudaStreamNonBlocking));
+  if (pl->hA_bytes < a_bytes) {
+    cudaFree(pl->hA);
+    pl->hA = nullptr;
+    pl->hA_bytes = 0;
+    CUDA_TRY(cudaMalloc(&pl->hA, a_bytes));
+    pl->hA_bytes = a_bytes;
   }
-  rc = covgpu_plan_execute(pl, dA, dR, layout, scale, st);
-  if (rc == COVGPU_OK) {
-    e = cudaMemcpyAsync(R_host, dR, r_bytes, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) rc = fail(COVGPU_ECUDA, std::string("estimate_host: ") + cudaGetErrorString(e));
+  if (pl->hR_bytes < r_bytes) {
+    cudaFree(pl->hR);
+    pl->hR = nullptr;
+    pl->hR_bytes = 0;
+    CUDA_TRY(cudaMalloc(&pl->hR, r_bytes));
+    pl->hR_bytes = r_bytes;
   }
-  cudaFreeAsync(dA, st);
-  cudaFreeAsync(dR, st);
-  cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
-  return rc;
+  cudaStream_t st = pl->host_stream;
+  CUDA_TRY(cudaMemcpyAsync(pl->hA, A_host, a_bytes, cudaMemcpyHostToDevice, st));
+  int rc = covgpu_plan_execute(pl, pl->hA, pl->hR, layout, scale, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(R_host, pl->hR, r_bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return COVGPU_OK;
 }
 
 int covgpu_combination(const void* A_dev, int64_t n, int64_t m, int32_t dr, int32_t dc, int32_t p,

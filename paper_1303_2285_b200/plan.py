@@ -1,0 +1,106 @@
+"""Execution plans: the reusable form of one estimate (``covgpu_plan_*`` in
+include/covgpu.h).  A plan fixes the shape, dtype and class shard, owns the
+device workspace, and can be executed repeatedly on device or host buffers —
+what the benchmark, the multi-GPU driver and long-running callers use."""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+from .core import WindowSpec
+
+__all__ = ["Plan", "probe_fma_peak", "LAYOUTS"]
+
+LAYOUTS = {"dense": _native.DENSE, "packed": _native.PACKED, "compact": _native.COMPACT}
+_DT = {torch.complex128: _native.C128, torch.complex64: _native.C64}
+
+
+class Plan:
+    def __init__(self, n: int, m: int, window: WindowSpec, batch: int = 1,
+                 dtype: torch.dtype = torch.complex128, class_ids=None, device=None) -> None:
+        self.lib = _native.lib()
+        self.n, self.m, self.window, self.batch, self.dtype = n, m, window, batch, dtype
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.class_ids = None if class_ids is None else [int(x) for x in class_ids]
+        self._ids, self._nids = _native.id_array(self.class_ids)
+        handle = ctypes.c_void_p()
+        rc = self.lib.covgpu_plan_create(ctypes.byref(handle), self.device.index, batch, n, m,
+                                         window.p, window.q, _DT[dtype], self._ids, self._nids)
+        _native.check(rc, "covgpu_plan_create")
+        self.handle = handle
+
+    @property
+    def k(self) -> int:
+        return (self.n - self.window.p + 1) * (self.m - self.window.q + 1)
+
+    def output_elems(self, layout: str = "dense") -> int:
+        return int(self.lib.covgpu_output_elems(self.batch, self.n, self.m, self.window.p,
+                                                self.window.q, LAYOUTS[layout], self._ids, self._nids))
+
+    def alloc_output(self, layout: str = "dense", zero: bool = False) -> torch.Tensor:
+        fn = torch.zeros if zero else torch.empty
+        return fn(self.output_elems(layout), dtype=self.dtype, device=self.device)
+
+    def execute(self, a: torch.Tensor, out: torch.Tensor, layout: str = "dense",
+                scale: float | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        if a.dtype != self.dtype or not a.is_contiguous() or a.numel() != self.batch * self.n * self.m:
+            raise ValueError("input does not match the plan (shape, dtype, contiguity)")
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.covgpu_plan_execute(self.handle, ctypes.c_void_p(a.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), LAYOUTS[layout],
+                                          1.0 / self.k if scale is None else scale,
+                                          ctypes.c_void_p(st.cuda_stream))
+        _native.check(rc, "covgpu_plan_execute")
+        return out
+
+    def execute_host(self, a_host: torch.Tensor, out_host: torch.Tensor, layout: str = "packed",
+                     scale: float | None = None) -> torch.Tensor:
+        """End to end on host buffers (pin them for full PCIe bandwidth)."""
+        rc = self.lib.covgpu_plan_execute_host(self.handle, ctypes.c_void_p(a_host.data_ptr()),
+                                               ctypes.c_void_p(out_host.data_ptr()), LAYOUTS[layout],
+                                               1.0 / self.k if scale is None else scale)
+        _native.check(rc, "covgpu_plan_execute_host")
+        return out_host
+
+    def set_timing(self, enable: bool = True) -> None:
+        _native.check(self.lib.covgpu_plan_set_timing(self.handle, int(enable)), "set_timing")
+
+    def kernel_times(self) -> list[float]:
+        buf = (ctypes.c_float * 8)()
+        n = self.lib.covgpu_plan_kernel_times(self.handle, buf, 8)
+        if n < 0:
+            _native.check(n, "kernel_times")
+        return [float(buf[i]) for i in range(n)]
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.covgpu_plan_launches(self.handle))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self.lib.covgpu_plan_workspace_bytes(self.handle))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.covgpu_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def probe_fma_peak(device: int = 0, fp64: bool = True, seconds: float = 1.0) -> float:
+    """Measured FMA-pipe peak (TFLOP/s) — the roofline denominator."""
+    lib = _native.lib()
+    out = ctypes.c_double()
+    rc = lib.covgpu_probe_fma_peak(device, _native.C128 if fp64 else _native.C64, seconds,
+                                   ctypes.byref(out))
+    _native.check(rc, "covgpu_probe_fma_peak")
+    return float(out.value)
