@@ -9,92 +9,225 @@
 //     (core rows: P-1-max(dr,0) <= r1 <= N-P+max(-dr,0));
 //   * the E second-element rows in flight sit in a rotating register window,
 //     so each step reads 2 complex values from SMEM for E products;
-//   * rows arrive in SMEM in chunks of BULK_RC through a 2-stage cp.async
-//     pipeline: X tile RC x 32 (first elements), Y tile (RC+E-1) x (32+NW-1)
-//     (second elements of every lag of every warp).  Rows / columns outside A
-//     are zero-filled.
+//   * rows arrive in SMEM in chunks of BULK_RC: X tile RC x 32 (first
+//     elements) and Y tile (RC+E-1) x YW (second elements of every lag of
+//     every warp).  Rows / columns outside A are zero-filled.
+//     k_bulk_tma moves the tiles with TMA (cp.async.bulk.tensor) through an
+//     S-stage full/empty mbarrier ring — one thread issues, no per-element
+//     address arithmetic; k_bulk (cp.async, 2 stages) serves shapes whose
+//     rows are not 16-byte aligned (complex64 with odd M).
 // Epilogue per (warp, lag): core-column lanes are summed (fixed butterfly)
 // into the class's CC partial for this column block; edge-column lanes store
 // their sums as the class's edge-column sums CCol (left: c1 < Q-1-dc;
 // right: c1 > M-Q).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace covgpu {
 
 constexpr int BULK_RC = 32;  // rows per SMEM stage (multiple of every E)
+constexpr int BULK_MAX_STAGES = 4;
+constexpr size_t BULK_SMEM_SM = 227 * 1024;  // usable SMEM per SM
 
-template <typename T, int E, int NW>
+template <typename T, int E, int NW, int MINB = 1>
 struct BulkCfg {
   using C2 = typename CT<T>::c;
   static constexpr int RC = BULK_RC;
   static constexpr int XW = 32;
-  static constexpr int YW = 32 + NW - 1;
+  static constexpr int YW = 32 + NW;  // 32+NW-1 needed; +1 keeps TMA rows 16B multiples
   static constexpr int YR = RC + E - 1;
-  static constexpr size_t smem = sizeof(C2) * 2 * ((size_t)RC * XW + (size_t)YR * YW);
+  static constexpr size_t xbytes = sizeof(C2) * (size_t)RC * XW;
+  static constexpr size_t ybytes = sizeof(C2) * (size_t)YR * YW;
+  static constexpr size_t ybytes_al = (ybytes + 127) / 128 * 128;
+  static constexpr size_t stage_bytes = xbytes + ybytes_al;
+  static constexpr size_t smem = 2 * stage_bytes;  // cp.async: double buffer
+  // TMA ring: as many stages (<= 4) as fit MINB CTAs per SM
+  static constexpr int fit = (int)((BULK_SMEM_SM / MINB - 1024 - 64) / stage_bytes);
+  static constexpr int stages = fit > BULK_MAX_STAGES ? BULK_MAX_STAGES : fit;
+  static constexpr size_t smem_tma = stages * stage_bytes + 2 * 8 * BULK_MAX_STAGES;  // + mbarriers
 };
 
+// acc[e] += x * conj(y[(tt+e) % E]) for every lag, in four passes that each
+// keep one x component in the same operand slot, so consecutive FMAs can read
+// it from the operand-reuse cache (three distinct 64-bit sources per DFMA
+// are register-bank bound at 2/3 of the DFMA rate on B200).
+template <typename T, int E>
+__device__ __forceinline__ void cmac_all(int tt, typename CT<T>::c x, const T* yr, const T* yi, T* ar,
+                                         T* ai) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = fma(x.x, yr[(tt + e) % E], ar[e]);
+#pragma unroll
+  for (int e = 0; e < E; ++e) ai[e] = fma(x.y, yr[(tt + e) % E], ai[e]);
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = fma(x.y, yi[(tt + e) % E], ar[e]);
+#pragma unroll
+  for (int e = 0; e < E; ++e) ai[e] = fma(-x.x, yi[(tt + e) % E], ai[e]);
+}
+
+// Per-warp view of one CTA's geometry.
+struct BulkGeom {
+  int b, cb, dr0, dc_base, dc;
+  int rlo, rhi, body_lo, body_hi, nchunks;
+  int col0, ycol0;
+  unsigned valid;  // selected lags of this warp
+};
+
+template <int E, int NW>
+__device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, int ncb,
+                                     const int* __restrict__ cls_slot) {
+  BulkGeom g;
+  long long t = blockIdx.x;
+  g.cb = (int)(t % ncb);
+  t /= ncb;
+  const int dcb = (int)(t % n_dcb);
+  t /= n_dcb;
+  const int drg = (int)(t % n_drg);
+  g.b = (int)(t / n_drg);
+  const int P = pr.P, Q = pr.Q, N = pr.N;
+  const int w = threadIdx.x >> 5;
+  g.dr0 = -(P - 1) + drg * E;
+  g.dc_base = dcb * NW;
+  g.dc = g.dc_base + w;
+  g.valid = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int dr = g.dr0 + e;
+    if (g.dc < Q && in_uc(dr, g.dc, P, Q) && cls_slot[class_index(dr, g.dc, P, Q)] >= 0)
+      g.valid |= 1u << e;
+  }
+  // CTA row range (union over lags), and the body where every lag is core
+  const int dr_lo = g.dr0, dr_hi = min(g.dr0 + E - 1, P - 1);
+  g.rlo = P - 1 - max(dr_hi, 0);
+  g.rhi = N - P + max(-dr_lo, 0);
+  g.body_lo = P - 1 - max(dr_lo, 0);
+  g.body_hi = N - P + max(-dr_hi, 0);
+  g.nchunks = (g.rhi - g.rlo + BULK_RC) / BULK_RC;
+  g.col0 = g.cb * 32;
+  g.ycol0 = g.col0 + g.dc_base;
+  return g;
+}
+
+// One SMEM chunk of rows [r0, r0+RC) for one warp.
 template <typename T, int E, int NW>
-__global__ void __launch_bounds__(NW * 32, sizeof(T) == 8 ? 1 : 2)
+__device__ __forceinline__ void bulk_chunk(const BulkGeom& g, const Problem& pr, int c,
+                                           const typename CT<T>::c* __restrict__ X,
+                                           const typename CT<T>::c* __restrict__ Y, T* yr, T* yi,
+                                           T* ar, T* ai) {
+  using C2 = typename CT<T>::c;
+  using Cfg = BulkCfg<T, E, NW>;
+  constexpr int RC = Cfg::RC, XW = Cfg::XW, YW = Cfg::YW;
+  const int N = pr.N, P = pr.P;
+  if (c == 0) {
+#pragma unroll
+    for (int e = 0; e < E - 1; ++e) {
+      const C2 y = Y[e * YW];
+      yr[e] = y.x;
+      yi[e] = y.y;
+    }
+  }
+  const int r0 = g.rlo + c * RC;
+  for (int t0 = 0; t0 < RC; t0 += E) {
+    const int rb = r0 + t0;
+    if (rb > g.rhi) break;
+    if (rb >= g.body_lo && rb + E - 1 <= g.body_hi) {
+      // ---- body block: every lag is core, no predicates ----
+#pragma unroll
+      for (int tt = 0; tt < E; ++tt) {
+        const C2 yn = Y[(t0 + tt + E - 1) * YW];
+        const C2 x = X[(t0 + tt) * XW];
+        yr[(tt + E - 1) % E] = yn.x;
+        yi[(tt + E - 1) % E] = yn.y;
+        cmac_all<T, E>(tt, x, yr, yi, ar, ai);
+      }
+    } else {
+      // ---- head / tail block: lag e is active for e_min <= e <= e_max ----
+#pragma unroll
+      for (int tt = 0; tt < E; ++tt) {
+        const int r = rb + tt;
+        if (r <= g.rhi) {
+          const C2 yn = Y[(t0 + tt + E - 1) * YW];
+          const C2 x = X[(t0 + tt) * XW];
+          yr[(tt + E - 1) % E] = yn.x;
+          yi[(tt + E - 1) % E] = yn.y;
+          const int e_min = r >= P - 1 ? 0 : P - 1 - r - g.dr0;
+          const int e_max = r <= N - P ? E - 1 : -g.dr0 - (r - N + P);
+          // inactive lags see y = 0 (they add exact zeros)
+          T mr[E], mi[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const bool on = e >= e_min && e <= e_max;
+            mr[(tt + e) % E] = on ? yr[(tt + e) % E] : (T)0;
+            mi[(tt + e) % E] = on ? yi[(tt + e) % E] : (T)0;
+          }
+          cmac_all<T, E>(tt, x, mr, mi, ar, ai);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int E>
+__device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int nclasses, int ncb,
+                                     const int* __restrict__ cls_slot,
+                                     const ClassDesc* __restrict__ cls, double2* __restrict__ ccpart,
+                                     double2* __restrict__ ccol, long long tot_ccol, const T* ar,
+                                     const T* ai) {
+  const int lane = threadIdx.x & 31;
+  const int M = pr.M, Q = pr.Q, P = pr.P;
+  const int c1 = g.col0 + lane;
+  const bool lane_ok = c1 < M - g.dc;
+  const int left_end = Q - 1 - g.dc;  // c1 < left_end: left edge column
+  const int right_beg = M - Q + 1;    // c1 >= right_beg: right edge column
+  const bool core = lane_ok && c1 >= left_end && c1 < right_beg;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (!(g.valid & (1u << e))) continue;  // warp-uniform
+    const int cid = cls_slot[class_index(g.dr0 + e, g.dc, P, Q)];
+    double2 v = make_double2((double)ar[e], (double)ai[e]);
+    if (lane_ok && !core) {
+      const ClassDesc& cd = cls[cid];
+      const int ac = cd.qu - 1;
+      const long long idx = c1 < left_end ? c1 : (long long)ac + (c1 - right_beg);
+      ccol[(long long)g.b * tot_ccol + cd.ccol_off + idx] = v;
+    }
+    if (!core) v = make_double2(0.0, 0.0);
+    v = warp_sum(v);
+    if (lane == 0) ccpart[((long long)g.b * nclasses + cid) * ncb + g.cb] = v;
+  }
+}
+
+// ---- cp.async variant (any alignment) --------------------------------------
+template <typename T, int E, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
     k_bulk(const typename CT<T>::c* __restrict__ A, Problem pr, int n_drg, int n_dcb, int ncb,
            int nclasses, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
            double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
   using Cfg = BulkCfg<T, E, NW>;
   using C2 = typename CT<T>::c;
   constexpr int RC = Cfg::RC, XW = Cfg::XW, YW = Cfg::YW, YR = Cfg::YR;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  C2* Xs = reinterpret_cast<C2*>(smraw);  // [2][RC][XW]
-  C2* Ys = Xs + 2 * RC * XW;              // [2][YR][YW]
-
-  long long t = blockIdx.x;
-  const int cb = (int)(t % ncb);
-  t /= ncb;
-  const int dcb = (int)(t % n_dcb);
-  t /= n_dcb;
-  const int drg = (int)(t % n_drg);
-  const int b = (int)(t / n_drg);
-
-  const int N = pr.N, M = pr.M, P = pr.P, Q = pr.Q;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int dr0 = -(P - 1) + drg * E;
-  const int dc_base = dcb * NW;
-  const int dc = dc_base + w;
-  const C2* __restrict__ Ab = A + (long long)b * N * M;
-
-  // lags of this warp that are selected classes
-  unsigned valid = 0;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int dr = dr0 + e;
-    if (dc < Q && in_uc(dr, dc, P, Q) && cls_slot[class_index(dr, dc, P, Q)] >= 0) valid |= 1u << e;
-  }
-  if (!__syncthreads_or(valid != 0)) return;  // CTA-uniform
-
-  // CTA row range (union over lags), and the body where every lag is core
-  const int dr_lo = dr0, dr_hi = min(dr0 + E - 1, P - 1);
-  const int rlo = P - 1 - max(dr_hi, 0);
-  const int rhi = N - P + max(-dr_lo, 0);
-  const int body_lo = P - 1 - max(dr_lo, 0);
-  const int body_hi = N - P + max(-dr_hi, 0);
-  const int nrows = rhi - rlo + 1;
-  const int nchunks = (nrows + RC - 1) / RC;
-  const int col0 = cb * 32;
-  const int ycol0 = col0 + dc_base;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const BulkGeom g = bulk_geom<E, NW>(pr, n_drg, n_dcb, ncb, cls_slot);
+  if (!__syncthreads_or(g.valid != 0)) return;  // CTA-uniform
+  const int N = pr.N, M = pr.M;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const C2* __restrict__ Ab = A + (long long)g.b * N * M;
 
   auto stage = [&](int c, int buf) {
-    const int r0 = rlo + c * RC;
-    C2* X = Xs + buf * RC * XW;
-    C2* Y = Ys + buf * YR * YW;
+    const int r0 = g.rlo + c * RC;
+    C2* X = reinterpret_cast<C2*>(smraw + buf * Cfg::stage_bytes);
+    C2* Y = reinterpret_cast<C2*>(smraw + buf * Cfg::stage_bytes + Cfg::xbytes);
     for (int idx = threadIdx.x; idx < RC * XW; idx += NW * 32) {
       const int rr = idx / XW, cc = idx % XW;
-      const int row = r0 + rr, col = col0 + cc;
-      const bool ok = row <= rhi && col < M;
+      const int row = r0 + rr, col = g.col0 + cc;
+      const bool ok = row < N && col < M;
       cp_async_elem<sizeof(C2)>(X + idx, ok ? Ab + (long long)row * M + col : Ab, ok);
     }
     for (int idx = threadIdx.x; idx < YR * YW; idx += NW * 32) {
       const int rr = idx / YW, cc = idx % YW;
-      const int row = r0 + dr0 + rr, col = ycol0 + cc;
+      const int row = r0 + g.dr0 + rr, col = g.ycol0 + cc;
       const bool ok = row >= 0 && row < N && col < M;
       cp_async_elem<sizeof(C2)>(Y + idx, ok ? Ab + (long long)row * M + col : Ab, ok);
     }
@@ -102,18 +235,13 @@ __global__ void __launch_bounds__(NW * 32, sizeof(T) == 8 ? 1 : 2)
 
   T ar[E], ai[E], yr[E], yi[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    ar[e] = (T)0;
-    ai[e] = (T)0;
-    yr[e] = (T)0;
-    yi[e] = (T)0;
-  }
+  for (int e = 0; e < E; ++e) ar[e] = ai[e] = yr[e] = yi[e] = (T)0;
 
   stage(0, 0);
   cp_async_commit();
-  for (int c = 0; c < nchunks; ++c) {
+  for (int c = 0; c < g.nchunks; ++c) {
     const int buf = c & 1;
-    if (c + 1 < nchunks) {
+    if (c + 1 < g.nchunks) {
       stage(c + 1, buf ^ 1);
       cp_async_commit();
       cp_async_wait<1>();
@@ -121,90 +249,77 @@ __global__ void __launch_bounds__(NW * 32, sizeof(T) == 8 ? 1 : 2)
       cp_async_wait<0>();
     }
     __syncthreads();
-    const C2* X = Xs + buf * RC * XW + lane;
-    const C2* Y = Ys + buf * YR * YW + lane + w;
-    if (valid) {
-      if (c == 0) {
-#pragma unroll
-        for (int e = 0; e < E - 1; ++e) {
-          const C2 y = Y[e * YW];
-          yr[e] = y.x;
-          yi[e] = y.y;
-        }
-      }
-      const int r0 = rlo + c * RC;
-      if (r0 >= body_lo && r0 + RC - 1 <= body_hi) {
-        // ---- body chunk: every lag is core, no predicates ----
-        for (int t0 = 0; t0 < RC; t0 += E) {
-#pragma unroll
-          for (int tt = 0; tt < E; ++tt) {
-            const C2 yn = Y[(t0 + tt + E - 1) * YW];
-            const C2 x = X[(t0 + tt) * XW];
-            yr[(tt + E - 1) % E] = yn.x;
-            yi[(tt + E - 1) % E] = yn.y;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const int s = (tt + e) % E;
-              ar[e] = fma(x.x, yr[s], ar[e]);
-              ar[e] = fma(x.y, yi[s], ar[e]);
-              ai[e] = fma(x.y, yr[s], ai[e]);
-              ai[e] = fma(-x.x, yi[s], ai[e]);
-            }
-          }
-        }
-      } else {
-        // ---- head / tail chunk: lag e is active for e_min <= e <= e_max ----
-        for (int t0 = 0; t0 < RC; t0 += E) {
-#pragma unroll
-          for (int tt = 0; tt < E; ++tt) {
-            const int r = r0 + t0 + tt;
-            if (r <= rhi) {
-              const C2 yn = Y[(t0 + tt + E - 1) * YW];
-              const C2 x = X[(t0 + tt) * XW];
-              yr[(tt + E - 1) % E] = yn.x;
-              yi[(tt + E - 1) % E] = yn.y;
-              const int e_min = r >= P - 1 ? 0 : P - 1 - r - dr0;
-              const int e_max = r <= N - P ? E - 1 : -dr0 - (r - N + P);
-#pragma unroll
-              for (int e = 0; e < E; ++e) {
-                if (e >= e_min && e <= e_max) {
-                  const int s = (tt + e) % E;
-                  ar[e] = fma(x.x, yr[s], ar[e]);
-                  ar[e] = fma(x.y, yi[s], ar[e]);
-                  ai[e] = fma(x.y, yr[s], ai[e]);
-                  ai[e] = fma(-x.x, yi[s], ai[e]);
-                }
-              }
-            }
-          }
-        }
-      }
-    }
+    const C2* X = reinterpret_cast<const C2*>(smraw + buf * Cfg::stage_bytes) + lane;
+    const C2* Y = reinterpret_cast<const C2*>(smraw + buf * Cfg::stage_bytes + Cfg::xbytes) + lane + w;
+    if (g.valid) bulk_chunk<T, E, NW>(g, pr, c, X, Y, yr, yi, ar, ai);
     __syncthreads();  // buffer `buf` is refilled by the next iteration's stage
   }
-  if (!valid) return;
+  if (!g.valid) return;
+  bulk_epilogue<T, E>(g, pr, nclasses, ncb, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
+}
 
-  // ---- epilogue ----
-  const int c1 = col0 + lane;
-  const bool lane_ok = c1 < M - dc;
-  const int left_end = Q - 1 - dc;  // c1 < left_end: left edge column
-  const int right_beg = M - Q + 1;  // c1 >= right_beg: right edge column
-  const bool core = lane_ok && c1 >= left_end && c1 < right_beg;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    if (!(valid & (1u << e))) continue;  // warp-uniform
-    const int cid = cls_slot[class_index(dr0 + e, dc, P, Q)];
-    double2 v = make_double2((double)ar[e], (double)ai[e]);
-    if (lane_ok && !core) {
-      const ClassDesc& cd = cls[cid];
-      const int ac = cd.qu - 1;
-      const long long idx = c1 < left_end ? c1 : (long long)ac + (c1 - right_beg);
-      ccol[(long long)b * tot_ccol + cd.ccol_off + idx] = v;
+// ---- TMA variant ------------------------------------------------------------
+// A is described to TMA as a 3-D tensor of reals {2M, N, B}; the X box is
+// {64, RC, 1}, the Y box {2*YW, YR, 1}; negative / past-the-end coordinates
+// are zero-filled by the hardware.
+template <typename T, int E, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_bulk_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
+               Problem pr, int n_drg, int n_dcb, int ncb, int nclasses,
+               const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
+               double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
+  using Cfg = BulkCfg<T, E, NW, MINB>;
+  using C2 = typename CT<T>::c;
+  constexpr int S = Cfg::stages, RC = Cfg::RC;
+  static_assert(S >= 2, "TMA ring needs two stages");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage_bytes);
+  uint64_t* empty = full + S;
+  const BulkGeom g = bulk_geom<E, NW>(pr, n_drg, n_dcb, ncb, cls_slot);
+  if (!__syncthreads_or(g.valid != 0)) return;  // CTA-uniform
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
     }
-    if (!core) v = make_double2(0.0, 0.0);
-    v = warp_sum(v);
-    if (lane == 0) ccpart[((long long)b * nclasses + cid) * ncb + cb] = v;
+    fence_mbarrier_init();
   }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int s = c % S;
+    const int r0 = g.rlo + c * RC;
+    unsigned char* base = smraw + s * Cfg::stage_bytes;
+    mbar_expect_tx(&full[s], (unsigned)(Cfg::xbytes + Cfg::ybytes));
+    tma_load_3d(base, &tmx, 2 * g.col0, r0, g.b, &full[s]);
+    tma_load_3d(base + Cfg::xbytes, &tmy, 2 * g.ycol0, r0 + g.dr0, g.b, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < min(S, g.nchunks); ++c) issue(c);
+
+  T ar[E], ai[E], yr[E], yi[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = ai[e] = yr[e] = yi[e] = (T)0;
+
+  for (int c = 0; c < g.nchunks; ++c) {
+    const int s = c % S;
+    mbar_wait(&full[s], (c / S) & 1);
+    const C2* X = reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes) + lane;
+    const C2* Y = reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes + Cfg::xbytes) + lane + w;
+    if (g.valid) bulk_chunk<T, E, NW>(g, pr, c, X, Y, yr, yi, ar, ai);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill the previous chunk's stage one chunk late, so thread 0 rarely
+    // waits for the other warps
+    if (threadIdx.x == 0 && c >= 1 && c - 1 + S < g.nchunks) {
+      const int sp = (c - 1) % S;
+      mbar_wait(&empty[sp], ((c - 1) / S) & 1);
+      issue(c - 1 + S);
+    }
+  }
+  if (!g.valid) return;
+  bulk_epilogue<T, E>(g, pr, nclasses, ncb, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
 }
 
 }  // namespace covgpu

@@ -23,12 +23,15 @@
 // of how classes are sharded across launches or GPUs.
 // The C ABI (include/covgpu.h) is at the end of this file.
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -77,6 +80,12 @@ struct covgpu_plan {
   Problem pr{};
   bool clean = true;
   int E = 16;         // row lags per bulk warp
+  int NW = 8;         // column lags (warps) per bulk CTA
+  int bulk_variant = 0;
+  bool use_tma = true;          // COVGPU_NO_TMA=1 forces the cp.async bulk kernel
+  bool used_tma = false;
+  const void* tmap_ptr = nullptr;  // A the cached tensor maps describe
+  CUtensorMap tmx{}, tmy{};
   int D = 16;         // column lags per edge-row thread
   int ncb = 0;        // 32-column blocks
   int n_drg = 0;      // bulk row-lag groups
@@ -97,6 +106,10 @@ struct covgpu_plan {
   double2* d_rc = nullptr;
   double2* d_slots = nullptr;
   double2* d_sat = nullptr;
+  void* d_corners = nullptr;  // transposed corner blocks (k_corners)
+  int2* d_tasks = nullptr;    // k_finalize_v tasks (class, snapshot group)
+  long long ntasks = 0;
+  int fin_kr = 0;             // k_finalize_v rows per lane (0: wide finalize)
   int sat_chunk = 0;
   long long ws_bytes = 0;
   size_t fin_smem = 0;
@@ -114,8 +127,6 @@ struct covgpu_plan {
 };
 
 namespace {
-
-constexpr int kBulkNW = 8;  // column lags (warps) per bulk CTA
 
 int validate(long long batch, long long n, long long m, int p, int q, int dtype) {
   if (batch < 1) return fail(COVGPU_EINVAL, "batch must contain at least one matrix");
@@ -160,6 +171,8 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_rc);
   cudaFree(pl->d_slots);
   cudaFree(pl->d_sat);
+  cudaFree(pl->d_corners);
+  cudaFree(pl->d_tasks);
 }
 
 int pick_lags(int span) {
@@ -168,41 +181,128 @@ int pick_lags(int span) {
   return 16;
 }
 
-// one-time per-process kernel attributes (dynamic SMEM above 48 KB)
-template <typename T, int E>
+// Bulk kernel variants (row lags E, warps NW, min CTAs/SM): register
+// budget vs occupancy.  FP64 E=8 x 2 CTAs keeps <= 128 registers so 16 warps
+// hide the DFMA dependency latency; FP32 runs E=16.
+struct BulkVariant {
+  int E, NW, MINB;
+};
+constexpr BulkVariant kBulkVariants[] = {
+    {4, 8, 2}, {8, 8, 2}, {16, 8, 1}, {8, 16, 1}, {16, 8, 2}, {16, 16, 1},
+};
+constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
+
+template <typename T, int E, int NW, int MINB>
 cudaError_t bulk_attr() {
-  return cudaFuncSetAttribute(k_bulk<T, E, kBulkNW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)BulkCfg<T, E, kBulkNW>::smem);
+  cudaError_t e = cudaFuncSetAttribute(k_bulk<T, E, NW, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)BulkCfg<T, E, NW>::smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_bulk_tma<T, E, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)BulkCfg<T, E, NW, MINB>::smem_tma);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// A as a {2M, N, B} tensor of reals with a {bw, bh, 1} box
+bool make_tmap(CUtensorMap* map, const void* A, bool fp64, long long B, long long N, long long M,
+               int box_w, int box_h) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t esz = fp64 ? 8 : 4;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * M), (cuuint64_t)N, (cuuint64_t)B};
+  const cuuint64_t strides[2] = {(cuuint64_t)(2 * M) * esz, (cuuint64_t)(2 * M * N) * esz};
+  const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, fp64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+             const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T>
+cudaError_t bulk_attrs() {
+  cudaError_t e = cudaSuccess, r;
+  if ((r = bulk_attr<T, 4, 8, 2>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 8, 8, 2>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 16, 8, 1>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 8, 16, 1>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 16, 8, 2>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 16, 16, 1>()) != cudaSuccess) e = r;
+  return e;
 }
 
 cudaError_t set_attrs() {
   static cudaError_t once = [] {
-    cudaError_t e = cudaSuccess;
-    cudaError_t r;
-#define ATTR(call) \
-  if ((r = (call)) != cudaSuccess) e = r;
-    ATTR((bulk_attr<double, 4>()));
-    ATTR((bulk_attr<double, 8>()));
-    ATTR((bulk_attr<double, 16>()));
-    ATTR((bulk_attr<float, 4>()));
-    ATTR((bulk_attr<float, 8>()));
-    ATTR((bulk_attr<float, 16>()));
-    ATTR(cudaFuncSetAttribute(k_finalize<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              200 * 1024));
-    ATTR(cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              200 * 1024));
-#undef ATTR
+    cudaError_t e = bulk_attrs<double>();
+    cudaError_t r = bulk_attrs<float>();
+    if (r != cudaSuccess) e = r;
+    if ((r = cudaFuncSetAttribute(k_finalize<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024)) != cudaSuccess)
+      e = r;
+    if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024)) != cudaSuccess)
+      e = r;
     return e;
   }();
   return once;
 }
 
-template <typename T, int E>
+template <typename T, int E, int NW, int MINB>
 void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
+  using Cfg = BulkCfg<T, E, NW, MINB>;
   const long long blocks = pl->batch * pl->n_drg * pl->n_dcb * pl->ncb;
-  k_bulk<T, E, kBulkNW><<<(unsigned)blocks, kBulkNW * 32, BulkCfg<T, E, kBulkNW>::smem, st>>>(
-      A, pl->pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, pl->d_cls_slot, pl->d_cls,
-      pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
+  const Problem& pr = pl->pr;
+  // TMA needs 16-byte aligned rows: always for complex128, even M for complex64
+  const bool tma_ok = pl->use_tma &&
+                      ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0);
+  if (tma_ok) {
+    if (pl->tmap_ptr != (const void*)A) {
+      CUtensorMap mx, my;
+      if (make_tmap(&mx, A, sizeof(T) == 8, pl->batch, pr.N, pr.M, 2 * Cfg::XW, Cfg::RC) &&
+          make_tmap(&my, A, sizeof(T) == 8, pl->batch, pr.N, pr.M, 2 * Cfg::YW, Cfg::YR)) {
+        pl->tmx = mx;
+        pl->tmy = my;
+        pl->tmap_ptr = A;
+      } else {
+        pl->tmap_ptr = nullptr;
+      }
+    }
+    if (pl->tmap_ptr == (const void*)A) {
+      k_bulk_tma<T, E, NW, MINB><<<(unsigned)blocks, NW * 32, Cfg::smem_tma, st>>>(
+          pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, pl->d_cls_slot,
+          pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
+      pl->used_tma = true;
+      return;
+    }
+  }
+  pl->used_tma = false;
+  k_bulk<T, E, NW, MINB><<<(unsigned)blocks, NW * 32, Cfg::smem, st>>>(
+      A, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart,
+      pl->d_ccol, pl->tot_ccol);
+}
+
+template <typename T>
+void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
+  switch (pl->bulk_variant) {
+    case 0: launch_bulk<T, 4, 8, 2>(pl, A, st); break;
+    case 1: launch_bulk<T, 8, 8, 2>(pl, A, st); break;
+    case 2: launch_bulk<T, 16, 8, 1>(pl, A, st); break;
+    case 3: launch_bulk<T, 8, 16, 1>(pl, A, st); break;
+    case 4: launch_bulk<T, 16, 8, 2>(pl, A, st); break;
+    default: launch_bulk<T, 16, 16, 1>(pl, A, st);
+  }
 }
 
 template <typename T, int D>
@@ -258,11 +358,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     if (pl->timing && pl->nev < 8) cudaEventRecord(pl->ev[pl->nev++], st);
   };
   mark();
-  switch (pl->E) {
-    case 4: launch_bulk<T, 4>(pl, A, st); break;
-    case 8: launch_bulk<T, 8>(pl, A, st); break;
-    default: launch_bulk<T, 16>(pl, A, st);
-  }
+  launch_bulk_variant<T>(pl, A, st);
   ++launches;
   mark();
   if (pl->S > 0) {
@@ -274,10 +370,30 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     ++launches;
     mark();
   }
-  const long long ntasks = (long long)B * pl->nclasses;
-  k_finalize<T><<<(unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS), FIN_WARPS * 32, pl->fin_smem, st>>>(
-      A, pr, pl->d_cls, pl->nclasses, pl->ncb, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc,
-      pl->tot_rc, pl->nseg, pl->d_slots, pl->tot_slots, R, layout, r_bstride, scale, ntasks, pr.Q);
+  if (pl->fin_kr > 0) {
+    const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
+    if (nc > 0) {
+      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, (C2*)pl->d_corners);
+      ++launches;
+    }
+    const unsigned blocks = (unsigned)((pl->ntasks + FIN_WARPS - 1) / FIN_WARPS);
+#define FINV(KR)                                                                                 \
+  k_finalize_v<T, KR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                       \
+      (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses, pl->ncb, B, \
+      pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, pl->nseg, R, layout,          \
+      r_bstride, scale)
+    switch (pl->fin_kr) {
+      case 1: FINV(1); break;
+      case 2: FINV(2); break;
+      default: FINV(4);
+    }
+#undef FINV
+  } else {
+    const long long ntasks = (long long)B * pl->nclasses;
+    k_finalize<T><<<(unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS), FIN_WARPS * 32, pl->fin_smem, st>>>(
+        A, pr, pl->d_cls, pl->nclasses, pl->ncb, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc,
+        pl->tot_rc, pl->nseg, pl->d_slots, pl->tot_slots, R, layout, r_bstride, scale, ntasks, pr.Q);
+  }
   ++launches;
   mark();
   CUDA_TRY(cudaGetLastError());
@@ -378,11 +494,31 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   pr.bw = (int)m - q + 1;
   pr.PQ = p * q;
   pl->clean = (n >= 2LL * p - 2) && (m >= 2LL * q - 2) && q <= kMaxCleanQ;
-  pl->E = pick_lags(2 * p - 1);
+  {
+    const int span = 2 * p - 1;
+    int v;
+    // measured on B200 (tools/kt.py): FP64 with P >= 32 runs best with 16
+    // row lags and 8 warps (1 CTA/SM, 4-stage TMA ring); smaller P and FP32
+    // with 8 lags and 2 CTAs/SM
+    if (span <= 4)
+      v = 0;  // E=4
+    else if (dtype == COVGPU_C128 && p >= 32)
+      v = 2;  // E=16, NW=8, 1 CTA/SM
+    else
+      v = 1;  // E=8, NW=8, 2 CTAs/SM
+    if (const char* env = getenv("COVGPU_BULK_VARIANT")) {  // tuning experiments
+      const int ev = atoi(env);
+      if (ev >= 0 && ev < kNumBulkVariants) v = ev;
+    }
+    pl->bulk_variant = v;
+    if (const char* nt = getenv("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
+    pl->E = kBulkVariants[v].E;
+    pl->NW = kBulkVariants[v].NW;
+  }
   pl->D = pick_lags(q);
   pl->ncb = (int)((m + 31) / 32);
   pl->n_drg = (2 * p - 1 + pl->E - 1) / pl->E;
-  pl->n_dcb = (q + kBulkNW - 1) / kBulkNW;
+  pl->n_dcb = (q + pl->NW - 1) / pl->NW;
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
   {
@@ -456,6 +592,30 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       return rc;
     }
     pl->fin_smem = sizeof(double2) * (size_t)FIN_WARPS * 4 * (size_t)q;
+    if (p <= FINV_MAX_P) {
+      pl->fin_kr = p <= 32 ? 1 : p <= 64 ? 2 : 4;
+      // tasks: (class, snapshot group of 32/W snapshots), W = min(32, pow2ceil(pv))
+      std::vector<int2> tasks;
+      for (int ci = 0; ci < pl->nclasses; ++ci) {
+        int W = 1;
+        while (W < pl->h_cls[ci].pv && W < 32) W <<= 1;
+        const int per = 32 / W;
+        const long long ng = (batch + per - 1) / per;
+        for (long long g = 0; g < ng; ++g) tasks.push_back(make_int2(ci, (int)g));
+      }
+      pl->ntasks = (long long)tasks.size();
+      const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
+      const size_t cbytes = (size_t)batch * 4 * (size_t)std::max(p - 1, 0) * (size_t)std::max(q - 1, 0) * esz;
+      cudaError_t e1 = cudaMalloc(&pl->d_corners, std::max<size_t>(cbytes, 16));
+      if (e1 == cudaSuccess) e1 = cudaMalloc((void**)&pl->d_tasks, sizeof(int2) * std::max<size_t>(tasks.size(), 1));
+      if (e1 == cudaSuccess && !tasks.empty())
+        e1 = cudaMemcpy(pl->d_tasks, tasks.data(), sizeof(int2) * tasks.size(), cudaMemcpyHostToDevice);
+      if (e1 != cudaSuccess) {
+        plan_free(pl.get());
+        return fail(COVGPU_ENOMEM, std::string("finalize workspace: ") + cudaGetErrorString(e1));
+      }
+      ws += (long long)cbytes + (long long)(sizeof(int2) * tasks.size());
+    }
   } else {
     // SAT scratch: bounded to ~512 MB per chunk of classes
     const long long per_class = batch * (n + 1) * (m + 1) * (long long)sizeof(double2);
@@ -573,7 +733,7 @@ int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tfl
   CUDA_TRY(cudaSetDevice(device));
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  const int blocks = prop.multiProcessorCount * 8, threads = 256;
+  const int blocks = prop.multiProcessorCount * 2, threads = 256;
   void* out = nullptr;
   CUDA_TRY(cudaMalloc(&out, 16));
   cudaEvent_t e0, e1;
@@ -606,7 +766,7 @@ int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tfl
   cudaEventDestroy(e1);
   cudaFree(out);
   if (e != cudaSuccess) return fail(COVGPU_ECUDA, cudaGetErrorString(e));
-  const double flops = 2.0 * 16.0 * (double)iters * blocks * threads;
+  const double flops = 2.0 * 64.0 * (double)iters * blocks * threads;  // 64 FMA / iter
   *tflops = flops / (best * 1e-3) / 1e12;
   return COVGPU_OK;
 }

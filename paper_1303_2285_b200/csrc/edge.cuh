@@ -1,14 +1,16 @@
-// K2 — edge-row sums RC.
+// K2 — edge-row sums RC'.
 //
 // The edge rows of class (dr, dc) are the pane rows whose window-row range is
 // clipped: top rows, where both elements sit in A's first P-1 rows, and
 // bottom rows, where both sit in the last P-1 rows.  Over all classes they
 // are exactly the ordered row pairs (r1, r2) inside the top strip [0, P-1)
 // and inside the bottom strip [N-P+1, N).  Each thread owns one pair and D
-// consecutive column lags dc0..dc0+D-1 and walks the class's core columns
-// c1 in [Q-1-dc, M-Q], the D second-element columns in flight rotating in a
-// register window (2 loads per D products).  The column walk may be split
-// into nseg segments; the finalize kernel sums the segment partials in order.
+// consecutive column lags dc0..dc0+D-1 and walks c1 in [0, M-Q] — the
+// columns of the slot u = 0 box, i.e. the left corner plus the core columns —
+// the D second-element columns in flight rotating in a register window
+// (2 loads per D products).  RC'_i = fullT_i(0) (resp. fullB_i(0)) is the
+// starting value of the finalize's walk along u.  The column walk may be
+// split into nseg segments; the finalize sums the segment partials in order.
 #pragma once
 
 #include "common.cuh"
@@ -47,8 +49,8 @@ __global__ void __launch_bounds__(128)
   }
   if (!valid) return;
 
-  const int cstart = max(0, Q - 1 - (dc0 + D - 1));
-  const int cend = M - Q;  // inclusive
+  const int cstart = 0;
+  const int cend = M - Q;  // inclusive: the slot-0 box columns [0, bw)
   const int seglen = (cend - cstart + nseg) / nseg;  // ceil(len / nseg)
   const int cs = cstart + seg * seglen;
   const int ce = min(cend, cs + seglen - 1);
@@ -68,11 +70,7 @@ __global__ void __launch_bounds__(128)
       yr[d] = v.x;
       yi[d] = v.y;
     }
-    // lag d is active at column c once c >= Q-1-dc0-d (only in the first D
-    // columns of segment 0)
-    const int thr0 = Q - 1 - dc0;
     for (int c0 = cs; c0 <= ce; c0 += D) {
-      const bool masked = c0 < thr0;
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) {
         const int c = c0 + cc;
@@ -82,15 +80,13 @@ __global__ void __launch_bounds__(128)
           yr[(cc + D - 1) % D] = yn.x;
           yi[(cc + D - 1) % D] = yn.y;
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            if (!masked || c >= thr0 - d) {
-              const int s = (cc + d) % D;
-              ar[d] = fma(xv.x, yr[s], ar[d]);
-              ar[d] = fma(xv.y, yi[s], ar[d]);
-              ai[d] = fma(xv.y, yr[s], ai[d]);
-              ai[d] = fma(-xv.x, yi[s], ai[d]);
-            }
-          }
+          for (int d = 0; d < D; ++d) ar[d] = fma(xv.x, yr[(cc + d) % D], ar[d]);
+#pragma unroll
+          for (int d = 0; d < D; ++d) ai[d] = fma(xv.y, yr[(cc + d) % D], ai[d]);
+#pragma unroll
+          for (int d = 0; d < D; ++d) ar[d] = fma(xv.y, yi[(cc + d) % D], ar[d]);
+#pragma unroll
+          for (int d = 0; d < D; ++d) ai[d] = fma(-xv.x, yi[(cc + d) % D], ai[d]);
         }
       }
     }

@@ -1,4 +1,15 @@
-// K3 — finalize: one warp per (snapshot, class).
+// K3 — finalize.
+//
+// k_finalize_v (default, P <= 128): lanes own diagonal positions v; the warp
+// walks u = 0 .. qu-1 carrying every edge row's full_i(u) in registers
+// (full_i(u+1) = full_i(u) - pL_i[u] + pR_i[u]) and G(u) (G(u+1) = G(u) -
+// CColL[u] + CColR[u]); at each u the whole column of slots is
+//   S(v,u) = G(u) + suffix_{i>=v} fullT_i(u) + prefix_{t<v} fullB_t(u),
+// two segmented warp scans.  Classes with pv <= 16 pack 32/W snapshots per
+// warp (W = pow2ceil(pv)-lane segments).  Corner reads come from the
+// transposed corner blocks (k_corners), so lanes read consecutive addresses.
+//
+// k_finalize (P > 128): one warp per (snapshot, class), lanes own u.
 //
 // With a_r = pv-1 top/bottom edge rows and a_c = qu-1 left/right edge
 // columns, slot (v, u) of the class is
@@ -6,7 +17,7 @@
 //   G(u)   = CC + sum_{j>=u} CColL[j] + sum_{t<u} CColR[t]
 //          = CC + sum_j CColL[j] + excl_prefix(CColR - CColL)(u)
 //   full*_i(u) = RC_i + sum_{j>=u} pL_i[j] + sum_{t<u} pR_i[t]
-//              = RC_i + sum_j pL_i[j] + excl_prefix(pR_i - pL_i)(u)
+//              = RC'_i + excl_prefix(pR_i - pL_i)(u),   RC'_i = full_i(0) (edge.cuh)
 // where pL/pR are the row's corner products with the left/right edge columns
 // (formed here, once each).  Lanes own u (32 per chunk).  Pass T walks the
 // diagonal segment upward (v = a_r .. 0) accumulating top rows into an L2
@@ -20,6 +31,155 @@
 namespace covgpu {
 
 constexpr int FIN_WARPS = 4;
+constexpr int FINV_MAX_P = 128;
+
+// Transposed corner blocks of A: C[b][k][j][i], k = TL, TR, BL, BR, each
+// (P-1) rows x (Q-1) columns of A (the only elements corner products read).
+template <typename T>
+__global__ void k_corners(const typename CT<T>::c* __restrict__ A, Problem pr, int B,
+                          typename CT<T>::c* __restrict__ C) {
+  const int S = pr.P - 1, Wc = pr.Q - 1;
+  const long long per = 4LL * S * Wc;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= per * B) return;
+  const int b = (int)(tid / per);
+  long long r = tid % per;
+  const int k = (int)(r / ((long long)S * Wc));
+  r %= (long long)S * Wc;
+  const int j = (int)(r / S), i = (int)(r % S);
+  const int row = (k < 2 ? 0 : pr.N - S) + i;
+  const int col = ((k & 1) ? pr.M - Wc : 0) + j;
+  C[tid] = A[((long long)b * pr.N + row) * pr.M + col];
+}
+
+__device__ inline double2 seg_sum(double2 v, int W) {
+  for (int off = W >> 1; off > 0; off >>= 1) v = cadd(v, shfl_xor2(v, off));
+  return v;
+}
+
+// inclusive suffix (toward higher lanes) and exclusive prefix scans inside
+// aligned segments of W lanes; `total` = segment sum
+__device__ inline double2 seg_suffix_incl(double2 v, int li, int W, double2* total) {
+  double2 inc = v;
+  for (int off = 1; off < W; off <<= 1) {
+    double2 n;
+    n.x = __shfl_down_sync(0xffffffffu, inc.x, off, W);
+    n.y = __shfl_down_sync(0xffffffffu, inc.y, off, W);
+    if (li + off < W) inc = cadd(inc, n);
+  }
+  total->x = __shfl_sync(0xffffffffu, inc.x, 0, W);
+  total->y = __shfl_sync(0xffffffffu, inc.y, 0, W);
+  return inc;
+}
+__device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* total) {
+  double2 inc = v;
+  for (int off = 1; off < W; off <<= 1) {
+    double2 n;
+    n.x = __shfl_up_sync(0xffffffffu, inc.x, off, W);
+    n.y = __shfl_up_sync(0xffffffffu, inc.y, off, W);
+    if (li >= off) inc = cadd(inc, n);
+  }
+  total->x = __shfl_sync(0xffffffffu, inc.x, W - 1, W);
+  total->y = __shfl_sync(0xffffffffu, inc.y, W - 1, W);
+  return csub(inc, v);
+}
+
+// task = (class, snapshot group); W = min(32, pow2ceil(pv)) lanes per snapshot
+template <typename T, int KR>
+__global__ void __launch_bounds__(FIN_WARPS * 32)
+    k_finalize_v(const typename CT<T>::c* __restrict__ corners, Problem pr,
+                 const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
+                 int nclasses, int ncb, int B, const double2* __restrict__ ccpart,
+                 const double2* __restrict__ ccol, long long tot_ccol, const double2* __restrict__ rc,
+                 long long tot_rc, int nseg, typename CT<T>::c* __restrict__ R, int layout,
+                 long long r_bstride, double scale) {
+  using C2 = typename CT<T>::c;
+  const int lane = threadIdx.x & 31;
+  const long long task = (long long)blockIdx.x * FIN_WARPS + (threadIdx.x >> 5);
+  if (task >= ntasks) return;  // warp-uniform; no block barriers below
+  const int2 tk = tasks[task];
+  const ClassDesc c = cls[tk.x];
+  const int pv = c.pv, qu = c.qu, ar = pv - 1, ac = qu - 1;
+  int W = 1;
+  while (W < pv && W < 32) W <<= 1;
+  const int li = lane & (W - 1);
+  const int b_raw = tk.y * (32 / W) + lane / W;
+  const bool active = b_raw < B;
+  const int b = active ? b_raw : B - 1;
+  const int Sx = pr.P - 1, Wc = pr.Q - 1;
+  const long long cstride = (long long)Sx * Wc;
+  const C2* Cb = corners + (long long)b * 4 * cstride;
+  const double2* cl = ccol + (long long)b * tot_ccol + c.ccol_off;
+  const double2* rcc = rc + ((long long)b * tot_rc + c.rc_off) * nseg;
+
+  // CC and G(0) = CC + sum_j CColL[j]
+  const double2* cc_p = ccpart + ((long long)b * nclasses + tk.x) * ncb;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = li; k < ncb; k += W) acc = cadd(acc, cc_p[k]);
+  for (int j = li; j < ac; j += W) acc = cadd(acc, cl[j]);
+  double2 G = seg_sum(acc, W);
+
+  // edge-row state: lane owns v = li + k*W
+  double2 fT[KR], fB[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int v = li + k * W;
+    fT[k] = fB[k] = make_double2(0.0, 0.0);
+    if (v < ar) {
+      for (int g = 0; g < nseg; ++g) {
+        fT[k] = cadd(fT[k], rcc[(long long)v * nseg + g]);
+        fB[k] = cadd(fB[k], rcc[(long long)(ar + v) * nseg + g]);
+      }
+    }
+  }
+  const bool zero_im = (c.d == 0);
+  const long long rb = (long long)b * r_bstride;
+  for (int u = 0; u < qu; ++u) {
+    double2 sufT[KR], preB[KR];
+    double2 carry = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = KR - 1; k >= 0; --k) {
+      double2 tot;
+      const double2 s = seg_suffix_incl(fT[k], li, W, &tot);
+      sufT[k] = cadd(s, carry);
+      carry = cadd(carry, tot);
+    }
+    carry = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      double2 tot;
+      const double2 s = seg_prefix_excl(fB[k], li, W, &tot);
+      preB[k] = cadd(s, carry);
+      carry = cadd(carry, tot);
+    }
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int v = li + k * W;
+      if (active && v < pv) {
+        const double2 sv = cadd(G, cadd(sufT[k], preB[k]));
+        write_slot<T>(R, layout, rb, c, pr, v, u, sv.x * scale, zero_im ? 0.0 : sv.y * scale);
+      }
+    }
+    if (u < ac) {
+      // corner products of column u (left) and bw+u (right), each formed once
+      const C2* TL = Cb;
+      const C2* TR = Cb + cstride;
+      const C2* BL = Cb + 2 * cstride;
+      const C2* BR = Cb + 3 * cstride;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int v = li + k * W;
+        if (v < ar) {
+          const long long o1 = (long long)u * Sx + v + c.s1;
+          const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
+          fT[k] = cadd(fT[k], csub(cmulconj<T>(TR[o1], TR[o2]), cmulconj<T>(TL[o1], TL[o2])));
+          fB[k] = cadd(fB[k], csub(cmulconj<T>(BR[o1], BR[o2]), cmulconj<T>(BL[o1], BL[o2])));
+        }
+      }
+      G = cadd(G, csub(cl[ac + u], cl[u]));
+    }
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(FIN_WARPS * 32)
@@ -77,7 +237,6 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   // one edge row's contribution full_i(u), u = u0 + lane, for all u-chunks:
   // products into pl/prr, then scan; returns via callback per chunk
   auto edge_row = [&](int i, double2 rcv, auto&& consume) {
-    double2 tl = make_double2(0.0, 0.0);
     for (int j = lane; j < ac; j += 32) {
       const double2 a = cmulconj<T>(Ab[(long long)(i + c.s1) * M + j], Ab[(long long)(i + c.s2) * M + j + c.dc]);
       const int jr = pr.bw + j;
@@ -85,11 +244,9 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
           cmulconj<T>(Ab[(long long)(i + c.s1) * M + jr], Ab[(long long)(i + c.s2) * M + jr + c.dc]);
       pl[j] = a;
       prr[j] = bb;
-      tl = cadd(tl, a);
     }
-    tl = warp_sum(tl);
     __syncwarp();
-    double2 carry = cadd(rcv, tl);
+    double2 carry = rcv;  // RC' = full_i(0) (edge.cuh)
     for (int u0 = 0; u0 < qu; u0 += 32) {
       const int u = u0 + lane;
       const double2 q = u < ac ? csub(prr[u], pl[u]) : make_double2(0.0, 0.0);

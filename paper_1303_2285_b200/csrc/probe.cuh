@@ -1,8 +1,13 @@
 // FMA-pipe throughput probe.  MEASURED_PEAKS.json carries only bf16 and HBM,
 // so the FP64 / FP32 roofline denominators of the covariance kernels are
-// measured by bench.py with this loop on the same GPU, right before the timed
-// region: 16 independent FMA chains per thread, all operands in registers
-// (the covariance kernels' operand form), a full-chip grid.
+// measured by bench.py on the same GPU, right before the timed region.
+//
+// The loop is the complex multiply-accumulate of the kernels (16 lags, all
+// operands per-thread registers) with each x component repeated in one
+// operand slot across consecutive FMAs, so the operand-reuse cache relieves
+// the register file: measured on B200 this is the highest FMA rate reachable
+// (FP64 ~33 TF/s, FP32 ~62 TF/s at 1965 MHz); three distinct 64-bit sources
+// per DFMA reach only ~24.7 TF/s (register-bank bound, 42.5 DFMA/clk/SM).
 #pragma once
 
 #include "common.cuh"
@@ -11,20 +16,29 @@ namespace covgpu {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_fma_probe(T* out, int iters, T seed) {
-  constexpr int CH = 16;
-  T acc[CH], x[CH];
+  constexpr int E = 16;
+  T ar[E], ai[E], yr[E], yi[E];
 #pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    acc[c] = (T)(threadIdx.x + c) * (T)1e-3;
-    x[c] = seed + (T)c * (T)1e-7 + (T)(threadIdx.x & 7) * (T)1e-9;
+  for (int e = 0; e < E; ++e) {
+    ar[e] = ai[e] = (T)0;
+    yr[e] = seed + (T)(e + threadIdx.x) * (T)1e-7;
+    yi[e] = seed - (T)(threadIdx.x & 7) * (T)1e-7;
   }
+  T xr = seed * (T)0.5 + (T)threadIdx.x * (T)1e-8, xi = seed * (T)0.25 - (T)threadIdx.x * (T)1e-8;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int c = 0; c < CH; ++c) acc[c] = fma(acc[c], x[c], x[(c + 5) % CH]);
+    for (int e = 0; e < E; ++e) ar[e] = fma(xr, yr[e], ar[e]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) ai[e] = fma(xi, yr[e], ai[e]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) ar[e] = fma(xi, yi[e], ar[e]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) ai[e] = fma(-xr, yi[e], ai[e]);
+    xr = xr + (T)1e-9;
   }
   T s = 0;
 #pragma unroll
-  for (int c = 0; c < CH; ++c) s += acc[c];
+  for (int e = 0; e < E; ++e) s += ar[e] + ai[e];
   if (s == (T)-1.2345) out[0] = s;  // keep the chains live
 }
 
