@@ -124,6 +124,17 @@ int covgpu_plan_execute_host(covgpu_plan_t plan, const void* A_host, void* R_hos
  * roofline denominator of the covariance kernels. */
 int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tflops);
 
+/* Bulk-kernel work unit of a shape: `lags` row lags x `warps` column lags
+ * per CTA.  The partitioner shards classes in whole units. */
+int covgpu_bulk_geometry(int32_t p, int32_t q, int32_t dtype, int32_t* lags, int32_t* warps);
+
+/* Scatter a COVGPU_COMPACT shard (the slots of `class_ids`, class-major) into
+ * a dense Hermitian R_dev (both triangles) — the root's half of the multi-GPU
+ * gather (reference CovarianceMatrix.dense(), core.py:170-176). */
+int covgpu_scatter_compact(const void* compact_dev, int64_t batch, int64_t n, int64_t m, int32_t p,
+                           int32_t q, int32_t dtype, const int32_t* class_ids, int32_t n_classes,
+                           void* R_dev, void* stream);
+
 /* Per-class call with the reference kernel's argument shape
  * (combination_scratch(a, dr, dc, p, q, out, ...), _numba_kernels.py:62-107):
  * writes ONLY class (dr, dc)'s slots of the packed upper triangle `out_dev`

@@ -192,6 +192,25 @@ constexpr BulkVariant kBulkVariants[] = {
 };
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
+// measured on B200 (tools/kt.py): FP64 with P >= 32 runs best with 16 row
+// lags and 8 warps (1 CTA/SM, 4-stage TMA ring); smaller P and FP32 with 8
+// lags and 2 CTAs/SM.  COVGPU_BULK_VARIANT overrides (tuning experiments).
+int pick_bulk_variant(int p, int dtype) {
+  const int span = 2 * p - 1;
+  int v;
+  if (span <= 4)
+    v = 0;  // E=4
+  else if (dtype == COVGPU_C128 && p >= 32)
+    v = 2;  // E=16, NW=8, 1 CTA/SM
+  else
+    v = 1;  // E=8, NW=8, 2 CTAs/SM
+  if (const char* env = getenv("COVGPU_BULK_VARIANT")) {
+    const int ev = atoi(env);
+    if (ev >= 0 && ev < kNumBulkVariants) v = ev;
+  }
+  return v;
+}
+
 template <typename T, int E, int NW, int MINB>
 cudaError_t bulk_attr() {
   cudaError_t e = cudaFuncSetAttribute(k_bulk<T, E, NW, MINB>,
@@ -495,21 +514,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   pr.PQ = p * q;
   pl->clean = (n >= 2LL * p - 2) && (m >= 2LL * q - 2) && q <= kMaxCleanQ;
   {
-    const int span = 2 * p - 1;
-    int v;
-    // measured on B200 (tools/kt.py): FP64 with P >= 32 runs best with 16
-    // row lags and 8 warps (1 CTA/SM, 4-stage TMA ring); smaller P and FP32
-    // with 8 lags and 2 CTAs/SM
-    if (span <= 4)
-      v = 0;  // E=4
-    else if (dtype == COVGPU_C128 && p >= 32)
-      v = 2;  // E=16, NW=8, 1 CTA/SM
-    else
-      v = 1;  // E=8, NW=8, 2 CTAs/SM
-    if (const char* env = getenv("COVGPU_BULK_VARIANT")) {  // tuning experiments
-      const int ev = atoi(env);
-      if (ev >= 0 && ev < kNumBulkVariants) v = ev;
-    }
+    const int v = pick_bulk_variant(p, dtype);
     pl->bulk_variant = v;
     if (const char* nt = getenv("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
     pl->E = kBulkVariants[v].E;
@@ -810,6 +815,40 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(R_host, pl->hR, r_bytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return COVGPU_OK;
+}
+
+int covgpu_bulk_geometry(int32_t p, int32_t q, int32_t dtype, int32_t* lags, int32_t* warps) {
+  (void)q;
+  if (p < 1 || !lags || !warps) return fail(COVGPU_EINVAL, "bad arguments");
+  const int v = pick_bulk_variant(p, dtype);
+  *lags = kBulkVariants[v].E;
+  *warps = kBulkVariants[v].NW;
+  return COVGPU_OK;
+}
+
+int covgpu_scatter_compact(const void* compact_dev, int64_t batch, int64_t n, int64_t m, int32_t p,
+                           int32_t q, int32_t dtype, const int32_t* class_ids, int32_t n_classes,
+                           void* R_dev, void* stream) {
+  int rc = validate(batch, n, m, p, q, dtype);
+  if (rc) return rc;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  covgpu_plan_t pl = nullptr;
+  rc = cached_plan(&pl, dev, batch, n, m, p, q, dtype, class_ids, n_classes);
+  if (rc) return rc;
+  if (pl->nclasses == 0 || pl->compact_elems == 0) return COVGPU_OK;
+  const long long total = pl->compact_elems * batch;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == COVGPU_C128)
+    k_scatter_compact<double><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        (const double2*)compact_dev, pl->pr, pl->d_cls, pl->nclasses, pl->compact_elems, (int)batch,
+        (double2*)R_dev);
+  else
+    k_scatter_compact<float><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        (const float2*)compact_dev, pl->pr, pl->d_cls, pl->nclasses, pl->compact_elems, (int)batch,
+        (float2*)R_dev);
+  CUDA_TRY(cudaGetLastError());
   return COVGPU_OK;
 }
 

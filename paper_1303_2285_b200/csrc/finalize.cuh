@@ -289,4 +289,28 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   }
 }
 
+// K4 — scatter a class-major compact shard into the dense Hermitian R
+// (the root's side of the multi-GPU gather; CovarianceMatrix.dense(),
+// core.py:170-176, for a shard).  Thread per compact slot.
+template <typename T>
+__global__ void k_scatter_compact(const typename CT<T>::c* __restrict__ compact, Problem pr,
+                                  const ClassDesc* __restrict__ cls, int nclasses, long long per_b,
+                                  int B, typename CT<T>::c* __restrict__ R) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= per_b * B) return;
+  const int b = (int)(tid / per_b);
+  const long long s = tid % per_b;
+  int lo = 0, hi = nclasses - 1;  // class whose slot range holds s
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cls[mid].slot_off <= s) lo = mid; else hi = mid - 1;
+  }
+  const ClassDesc c = cls[lo];
+  const long long r = s - c.slot_off;
+  const int u = (int)(r / c.pv), v = (int)(r % c.pv);
+  const auto val = compact[tid];
+  write_slot<T>(R, COVGPU_DENSE, (long long)b * pr.PQ * pr.PQ, c, pr, v, u, (double)val.x,
+                (double)val.y);
+}
+
 }  // namespace covgpu

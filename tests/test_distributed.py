@@ -1,0 +1,109 @@
+"""Multi-process (gloo, world size 2) tests of the multi-GPU driver's
+orchestration: broadcast of A, class / snapshot sharding, gather, root-side
+scatter.  The per-shard compute is the CPU oracle here (test
+infrastructure); on GPUs the same driver runs the CUDA library."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import covoracle as co
+from paper_1303_2285_b200 import WindowSpec
+from paper_1303_2285_b200.distributed import ShardOps, estimate_batch_sharded, estimate_sharded, shard_bounds
+from paper_1303_2285_b200.partition import partition_classes
+
+
+def oracle_ops() -> ShardOps:
+    def compute_compact(a, window, ids):
+        arr = a.numpy()
+        n, m = arr.shape
+        k = (n - window.p + 1) * (m - window.q + 1)
+        combos = co.unique_combinations(window.p, window.q)
+        parts = [co.class_slot_sums(arr, *combos[i], window.p, window.q) for i in sorted(set(ids))]
+        return torch.from_numpy(np.concatenate(parts) / k)
+
+    def scatter_dense(compacts, id_lists, window, n, m, dtype, device):
+        dim = window.stack_size
+        packed = np.zeros(dim * (dim + 1) // 2, dtype=np.complex128)
+        combos = co.unique_combinations(window.p, window.q)
+        for comp, ids in zip(compacts, id_lists):
+            pos = 0
+            vals = comp.numpy()
+            for i in sorted(set(ids)):
+                dr, dc = combos[i]
+                off = co.class_packed_offsets(dr, dc, window.p, window.q)
+                packed[off] = vals[pos:pos + off.size]
+                pos += off.size
+        return torch.from_numpy(co.dense_from_packed(packed, dim))
+
+    def compute_batch(a, window):
+        return torch.stack([torch.from_numpy(co.covariance(x.numpy(), window.p, window.q)) for x in a])
+
+    return ShardOps(compute_compact, scatter_dense, compute_batch)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(7)
+        n, m, p, q = 20, 18, 5, 4
+        a = torch.from_numpy(rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)))
+        dense, comp, ids = estimate_sharded(a if rank == 0 else None, (n, m), WindowSpec(p, q),
+                                            gather=True, ops=oracle_ops(), device=torch.device("cpu"))
+        out = {"ids": ids, "n_comp": int(comp.numel())}
+        if rank == 0:
+            ref = co.covariance(a.numpy(), p, q)
+            out["err"] = co.rel_frobenius(dense.numpy(), ref)
+            out["herm"] = bool(np.array_equal(dense.numpy(), dense.numpy().conj().T))
+        b, n2, m2 = 5, 12, 11
+        stack = torch.from_numpy(rng.standard_normal((b, n2, m2)) + 1j * rng.standard_normal((b, n2, m2)))
+        full, local, (lo, hi) = estimate_batch_sharded(stack if rank == 0 else None, (b, n2, m2),
+                                                       WindowSpec(3, 4), dtype=torch.complex128,
+                                                       gather=True, ops=oracle_ops(),
+                                                       device=torch.device("cpu"))
+        out["bounds"] = (lo, hi)
+        if rank == 0:
+            ref = np.stack([co.covariance(x, 3, 4) for x in stack.numpy()])
+            out["batch_err"] = co.rel_frobenius(full.numpy(), ref)
+        results[rank] = out
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_estimate():
+    world = 2
+    manager = mp.Manager()
+    results = manager.dict()
+    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    r0, r1 = results[0], results[1]
+    assert r0["err"] <= 1e-13 and r0["herm"]
+    assert r0["batch_err"] <= 1e-13
+    shards = partition_classes(20, 18, WindowSpec(5, 4), 2)
+    assert r0["ids"] == shards[0] and r1["ids"] == shards[1]
+    assert set(r0["ids"]).isdisjoint(r1["ids"])
+    assert r0["bounds"] == (0, 3) and r1["bounds"] == (3, 5)
+
+
+def test_shard_bounds_cover_batch():
+    for batch in (1, 7, 1024):
+        for world in (1, 2, 3, 8):
+            spans = [shard_bounds(batch, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == batch
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1

@@ -233,3 +233,91 @@ def test_counters(cuda):
     _, counters = estimate_combinations(ref_random(32, 32, 1), WindowSpec(13, 13))
     assert counters.multiplications == 207880  # test_engine.py:112-115
     assert [r[0] for r in counters.per_combination] == unique_combinations(WindowSpec(13, 13))
+
+
+def test_layouts_and_compact_scatter(cuda):
+    """packed / compact outputs agree bit for bit with the dense result, and
+    compact shards scattered on the root rebuild it (the multi-GPU gather)."""
+    from paper_1303_2285_b200 import _native
+    from paper_1303_2285_b200.distributed import cuda_ops, estimate_sharded
+    from paper_1303_2285_b200.engine import _run
+    from paper_1303_2285_b200.partition import partition_classes
+
+    w = workload("cfg2")
+    a = torch.as_tensor(make_input(w), device=cuda)
+    win = WindowSpec(w.p, w.q)
+    dense = _run(a.unsqueeze(0), win)[0]
+    packed = _run(a.unsqueeze(0), win, layout=_native.PACKED)[0]
+    r, c = torch.triu_indices(w.pq, w.pq, device=cuda)
+    assert torch.equal(packed, dense[r, c])
+    ops = cuda_ops()
+    shards = partition_classes(w.n, w.m, win, 4)
+    comps = [ops.compute_compact(a, win, ids) for ids in shards]
+    rebuilt = ops.scatter_dense(comps, shards, win, w.n, w.m, torch.complex128, cuda)
+    assert torch.equal(rebuilt, dense)
+    full, comp, ids = estimate_sharded(a, (w.n, w.m), win, gather=True)
+    assert torch.equal(full, dense)
+
+
+def test_batch_sharded_single_process(cuda):
+    from paper_1303_2285_b200.distributed import estimate_batch_sharded
+
+    stack = torch.as_tensor(make_input("cfg4")[:64], device=cuda)
+    win = WindowSpec(8, 16)
+    full, local, (lo, hi) = estimate_batch_sharded(stack, tuple(stack.shape), win, gather=True)
+    assert (lo, hi) == (0, 64)
+    assert torch.equal(full, estimate_batch_tensor(stack, win))
+
+
+def test_per_class_abi_call(cuda):
+    """covgpu_combination keeps the reference kernel's per-class call shape
+    (combination_scratch(a, dr, dc, p, q, out), _numba_kernels.py:62-107):
+    unnormalised, only that class's packed slots written."""
+    import ctypes
+
+    from paper_1303_2285_b200 import _native
+
+    a = ref_random(20, 18, 3)
+    p, q = 5, 4
+    at = torch.as_tensor(a, device=cuda)
+    ref = co.estimate_packed(a, p, q)
+    lib = _native.lib()
+    for dr, dc in [(0, 0), (2, 1), (-3, 2), (4, 3)]:
+        out = torch.zeros(p * q * (p * q + 1) // 2, dtype=torch.complex128, device=cuda)
+        rc = lib.covgpu_combination(ctypes.c_void_p(at.data_ptr()), 20, 18, dr, dc, p, q,
+                                    ctypes.c_void_p(out.data_ptr()),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        _native.check(rc)
+        off = co.class_packed_offsets(dr, dc, p, q)
+        got = out.cpu().numpy()
+        assert co.rel_frobenius(got[off], ref[off]) <= 1e-13
+        mask = np.ones(got.size, bool)
+        mask[off] = False
+        assert not got[mask].any()
+    with pytest.raises(ValueError):
+        _native.check(lib.covgpu_combination(ctypes.c_void_p(at.data_ptr()), 20, 18, -1, 0, p, q,
+                                             ctypes.c_void_p(out.data_ptr()), None))
+
+
+def test_host_buffer_path(cuda):
+    """covgpu_estimate_host / Plan.execute_host: host in, host out."""
+    from paper_1303_2285_b200.plan import Plan
+
+    w = workload("cfg2-c64")
+    a = torch.from_numpy(make_input(w)).reshape(1, w.n, w.m).pin_memory()
+    plan = Plan(w.n, w.m, WindowSpec(w.p, w.q), dtype=torch.complex64, device=cuda)
+    out = torch.empty(plan.output_elems("packed"), dtype=torch.complex64).pin_memory()
+    plan.execute_host(a, out, "packed")
+    dev = estimate_tensor(a[0], WindowSpec(w.p, w.q)).cpu()
+    r, c = torch.triu_indices(w.pq, w.pq)
+    assert torch.equal(out, dev[r, c])
+    plan.close()
+
+
+def test_odd_width_c64_uses_cp_async_path(cuda):
+    """complex64 rows that are not 16-byte multiples fall back to the cp.async
+    bulk kernel (TMA needs aligned rows); results must still match."""
+    a = (ref_random(67, 45, 11)).astype(np.complex64)
+    got = estimate_tensor(a, WindowSpec(9, 7)).cpu().numpy().astype(np.complex128)
+    ref = co.covariance(a.astype(np.complex128), 9, 7)
+    assert co.rel_frobenius(got, ref) <= TOL32
