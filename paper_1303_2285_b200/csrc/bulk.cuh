@@ -265,9 +265,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 template <typename T, int E, int NW, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_bulk_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
-               Problem pr, int n_drg, int n_dcb, int ncb, int nclasses,
+               Problem pr, int n_drg, int n_dcb, int ncb, int nclasses, int B, int nsnap,
                const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
                double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
+  // one CTA walks `nsnap` consecutive snapshots back to back: the TMA ring
+  // keeps streaming across snapshot boundaries, accumulators and the lag
+  // window restart, and the epilogue of one snapshot overlaps the next
+  // snapshot's loads
   using Cfg = BulkCfg<T, E, NW, MINB>;
   using C2 = typename CT<T>::c;
   constexpr int S = Cfg::stages, RC = Cfg::RC;
@@ -275,9 +279,12 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage_bytes);
   uint64_t* empty = full + S;
-  const BulkGeom g = bulk_geom<E, NW>(pr, n_drg, n_dcb, ncb, cls_slot);
-  if (!__syncthreads_or(g.valid != 0)) return;  // CTA-uniform
+  BulkGeom g = bulk_geom<E, NW>(pr, n_drg, n_dcb, ncb, cls_slot);  // g.b = snapshot group
+  const int b0 = g.b * nsnap;
+  const int nb = min(nsnap, B - b0);
+  if (!__syncthreads_or(g.valid != 0) || nb <= 0) return;  // CTA-uniform
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int total = nb * g.nchunks;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -287,39 +294,48 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     fence_mbarrier_init();
   }
   __syncthreads();
-  auto issue = [&](int c) {
-    const int s = c % S;
-    const int r0 = g.rlo + c * RC;
+  auto issue = [&](int k) {  // k = global chunk index over (snapshot, chunk)
+    const int s = k % S;
+    const int b = b0 + k / g.nchunks;
+    const int r0 = g.rlo + (k % g.nchunks) * RC;
     unsigned char* base = smraw + s * Cfg::stage_bytes;
     mbar_expect_tx(&full[s], (unsigned)(Cfg::xbytes + Cfg::ybytes));
-    tma_load_3d(base, &tmx, 2 * g.col0, r0, g.b, &full[s]);
-    tma_load_3d(base + Cfg::xbytes, &tmy, 2 * g.ycol0, r0 + g.dr0, g.b, &full[s]);
+    tma_load_3d(base, &tmx, 2 * g.col0, r0, b, &full[s]);
+    tma_load_3d(base + Cfg::xbytes, &tmy, 2 * g.ycol0, r0 + g.dr0, b, &full[s]);
   };
   if (threadIdx.x == 0)
-    for (int c = 0; c < min(S, g.nchunks); ++c) issue(c);
+    for (int k = 0; k < min(S, total); ++k) issue(k);
 
   T ar[E], ai[E], yr[E], yi[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) ar[e] = ai[e] = yr[e] = yi[e] = (T)0;
 
-  for (int c = 0; c < g.nchunks; ++c) {
-    const int s = c % S;
-    mbar_wait(&full[s], (c / S) & 1);
-    const C2* X = reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes) + lane;
-    const C2* Y = reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes + Cfg::xbytes) + lane + w;
-    if (g.valid) bulk_chunk<T, E, NW>(g, pr, c, X, Y, yr, yi, ar, ai);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    // refill the previous chunk's stage one chunk late, so thread 0 rarely
-    // waits for the other warps
-    if (threadIdx.x == 0 && c >= 1 && c - 1 + S < g.nchunks) {
-      const int sp = (c - 1) % S;
-      mbar_wait(&empty[sp], ((c - 1) / S) & 1);
-      issue(c - 1 + S);
+  int k = 0;  // global chunk index (ring stage and phase)
+  for (int bi = 0; bi < nb; ++bi) {
+    for (int c = 0; c < g.nchunks; ++c, ++k) {
+      const int s = k % S;
+      mbar_wait(&full[s], (k / S) & 1);
+      const C2* X = reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes) + lane;
+      const C2* Y =
+          reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes + Cfg::xbytes) + lane + w;
+      if (g.valid) bulk_chunk<T, E, NW>(g, pr, c, X, Y, yr, yi, ar, ai);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // refill the previous chunk's stage one chunk late, so thread 0 rarely
+      // waits for the other warps
+      if (threadIdx.x == 0 && k >= 1 && k - 1 + S < total) {
+        const int sp = (k - 1) % S;
+        mbar_wait(&empty[sp], ((k - 1) / S) & 1);
+        issue(k - 1 + S);
+      }
     }
+    if (g.valid) {  // snapshot done
+      g.b = b0 + bi;
+      bulk_epilogue<T, E>(g, pr, nclasses, ncb, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) ar[e] = ai[e] = (T)0;
   }
-  if (!g.valid) return;
-  bulk_epilogue<T, E>(g, pr, nclasses, ncb, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
 }
 
 }  // namespace covgpu

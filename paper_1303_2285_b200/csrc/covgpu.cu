@@ -281,7 +281,8 @@ cudaError_t set_attrs() {
 template <typename T, int E, int NW, int MINB>
 void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   using Cfg = BulkCfg<T, E, NW, MINB>;
-  const long long blocks = pl->batch * pl->n_drg * pl->n_dcb * pl->ncb;
+  const long long units = (long long)pl->n_drg * pl->n_dcb * pl->ncb;  // CTAs per snapshot
+  const long long blocks = pl->batch * units;
   const Problem& pr = pl->pr;
   // TMA needs 16-byte aligned rows: always for complex128, even M for complex64
   const bool tma_ok = pl->use_tma &&
@@ -299,9 +300,14 @@ void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
       }
     }
     if (pl->tmap_ptr == (const void*)A) {
-      k_bulk_tma<T, E, NW, MINB><<<(unsigned)blocks, NW * 32, Cfg::smem_tma, st>>>(
-          pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, pl->d_cls_slot,
-          pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
+      // snapshots per CTA: keep ~2 waves of CTAs, stream the rest through the ring
+      const long long slots = 148LL * MINB * 2;
+      long long nsnap = std::max(1LL, (blocks + slots - 1) / slots);
+      nsnap = std::min<long long>(nsnap, pl->batch);
+      const long long groups = (pl->batch + nsnap - 1) / nsnap;
+      k_bulk_tma<T, E, NW, MINB><<<(unsigned)(groups * units), NW * 32, Cfg::smem_tma, st>>>(
+          pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, (int)pl->batch,
+          (int)nsnap, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
       pl->used_tma = true;
       return;
     }

@@ -321,3 +321,52 @@ def test_odd_width_c64_uses_cp_async_path(cuda):
     got = estimate_tensor(a, WindowSpec(9, 7)).cpu().numpy().astype(np.complex128)
     ref = co.covariance(a.astype(np.complex128), 9, 7)
     assert co.rel_frobenius(got, ref) <= TOL32
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg3"])
+def test_full_size_against_gpu_gram(cuda, name):
+    """Every entry of R at full BASELINE size against the independent naive
+    Gram cross-check (X X^H over all K placements, cuBLAS; oracle/gpu_naive.py)."""
+    from oracle.gpu_naive import covariance_gram
+
+    w = workload(name)
+    a = torch.as_tensor(make_input(w), device=cuda)
+    got = estimate_tensor(a, WindowSpec(w.p, w.q))
+    ref = covariance_gram(a, w.p, w.q)
+    err = (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item()
+    print(f"{name} vs Gram relF {err:.3e}")
+    assert err <= TOL64
+
+
+def test_cfg4_all_snapshots_against_gpu_gram(cuda):
+    from oracle.gpu_naive import covariance_gram
+
+    w = workload("cfg4")
+    stack = torch.as_tensor(make_input(w), device=cuda)
+    got = estimate_batch_tensor(stack, WindowSpec(w.p, w.q))
+    worst = 0.0
+    for b in range(0, w.batch, 8):
+        ref = covariance_gram(stack[b], w.p, w.q)  # up-cast to complex128
+        err = (torch.linalg.norm(got[b].to(torch.complex128) - ref) / torch.linalg.norm(ref)).item()
+        worst = max(worst, err)
+    print(f"cfg4 worst relF vs Gram (every 8th snapshot) {worst:.3e}")
+    assert worst <= TOL32
+
+
+def test_exact_algebraic_properties(cuda):
+    """Size-independent identities at cfg5 size: R(2A) = 4 R(A) and
+    R(conj A) = conj R(A), both bit for bit; trace = weighted |A|^2 sum."""
+    w = workload("cfg5")
+    a = torch.as_tensor(make_input(w), device=cuda)
+    win = WindowSpec(w.p, w.q)
+    r = estimate_tensor(a, win)
+    assert torch.equal(estimate_tensor(2 * a, win), 4 * r)
+    assert torch.equal(estimate_tensor(a.conj().resolve_conj(), win), r.conj())
+    # trace: element (i, j) lies in cnt_r(i) * cnt_c(j) windows
+    n, m, p, q = w.n, w.m, w.p, w.q
+    ri = torch.arange(n, device=cuda)
+    cj = torch.arange(m, device=cuda)
+    cnt_r = (torch.minimum(ri, torch.tensor(n - p, device=cuda)) - torch.clamp(ri - p + 1, min=0) + 1)
+    cnt_c = (torch.minimum(cj, torch.tensor(m - q, device=cuda)) - torch.clamp(cj - q + 1, min=0) + 1)
+    tr = ((a.abs() ** 2) * cnt_r[:, None] * cnt_c[None, :]).sum() / w.k
+    assert abs(r.diagonal().real.sum().item() - tr.item()) <= 1e-12 * tr.item()

@@ -74,3 +74,16 @@ def test_dense_is_hermitian_and_normalised():
     assert np.array_equal(r, r.conj().T)
     assert np.all(r.diagonal().imag == 0)
     assert np.linalg.eigvalsh(r).min() >= -1e-12 * np.trace(r).real
+
+
+def test_gpu_naive_gram_definition_on_cpu():
+    """The Gram cross-check (oracle/gpu_naive.py) is the Eq. 2.2 definition:
+    pin it to the class-decomposition oracle on CPU tensors."""
+    import torch
+
+    from oracle.gpu_naive import covariance_gram
+
+    for n, m, p, q, seed in c4_instances()[:40] + [(40, 33, 7, 5, 3), (20, 20, 8, 8, 81)]:
+        a = ref_random(n, m, seed)
+        got = covariance_gram(torch.from_numpy(a), p, q, rows_per_chunk=3).numpy()
+        assert co.rel_frobenius(got, co.covariance(a, p, q)) <= 1e-13
