@@ -270,7 +270,7 @@ def main() -> None:
     kt = np.array(kern) if kern and all(len(k) == len(kern[0]) for k in kern) else None
     kernel_ms = {}
     if kt is not None and kt.size:
-        for name, col in zip(["bulk", "edge_rows", "finalize"], kt.mean(axis=0)):
+        for name, col in zip(["bulk", "edge_rows", "finalize", "expand"], kt.mean(axis=0)):
             kernel_ms[name] = float(col)
     shard_frac = 1.0 if ids is None else shard_cost(w.n, w.m, win, ids) / um
     roof = None

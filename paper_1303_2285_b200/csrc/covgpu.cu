@@ -108,6 +108,7 @@ struct covgpu_plan {
   double2* d_sat = nullptr;
   void* d_corners = nullptr;  // transposed corner blocks (k_corners)
   int2* d_tasks = nullptr;    // k_finalize_v tasks (class, snapshot group)
+  long long* d_uc_off = nullptr;  // compact offset per UC index (-1: not in shard)
   long long ntasks = 0;
   int fin_kr = 0;             // k_finalize_v rows per lane (0: wide finalize)
   int sat_chunk = 0;
@@ -173,6 +174,7 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_sat);
   cudaFree(pl->d_corners);
   cudaFree(pl->d_tasks);
+  cudaFree(pl->d_uc_off);
 }
 
 int pick_lags(int span) {
@@ -402,17 +404,29 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       ++launches;
     }
     const unsigned blocks = (unsigned)((pl->ntasks + FIN_WARPS - 1) / FIN_WARPS);
+    // finalize into the compact layout (R itself, or the plan's scratch),
+    // then expand to dense / packed with coalesced stores
+    C2* cdst = layout == COVGPU_COMPACT ? R : (C2*)pl->d_slots;
 #define FINV(KR)                                                                                 \
   k_finalize_v<T, KR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                       \
       (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses, pl->ncb, B, \
-      pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, pl->nseg, R, layout,          \
-      r_bstride, scale)
+      pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, pl->nseg, cdst,             \
+      pl->compact_elems, scale)
     switch (pl->fin_kr) {
       case 1: FINV(1); break;
       case 2: FINV(2); break;
       default: FINV(4);
     }
 #undef FINV
+    if (layout != COVGPU_COMPACT) {
+      ++launches;
+      mark();
+      const long long per = layout == COVGPU_DENSE ? (long long)pr.PQ * pr.PQ
+                                                   : (long long)pr.PQ * (pr.PQ + 1) / 2;
+      const long long tot = per * B;
+      k_expand<T><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          cdst, pl->compact_elems, pl->d_uc_off, pr, B, layout, R);
+    }
   } else {
     const long long ntasks = (long long)B * pl->nclasses;
     k_finalize<T><<<(unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS), FIN_WARPS * 32, pl->fin_smem, st>>>(
@@ -617,7 +631,12 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->ntasks = (long long)tasks.size();
       const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
       const size_t cbytes = (size_t)batch * 4 * (size_t)std::max(p - 1, 0) * (size_t)std::max(q - 1, 0) * esz;
+      std::vector<long long> uc_off(nuc, -1);
+      for (const auto& cd : pl->h_cls) uc_off[cd.uc] = cd.slot_off;
       cudaError_t e1 = cudaMalloc(&pl->d_corners, std::max<size_t>(cbytes, 16));
+      if (e1 == cudaSuccess) e1 = cudaMalloc((void**)&pl->d_uc_off, sizeof(long long) * nuc);
+      if (e1 == cudaSuccess)
+        e1 = cudaMemcpy(pl->d_uc_off, uc_off.data(), sizeof(long long) * nuc, cudaMemcpyHostToDevice);
       if (e1 == cudaSuccess) e1 = cudaMalloc((void**)&pl->d_tasks, sizeof(int2) * std::max<size_t>(tasks.size(), 1));
       if (e1 == cudaSuccess && !tasks.empty())
         e1 = cudaMemcpy(pl->d_tasks, tasks.data(), sizeof(int2) * tasks.size(), cudaMemcpyHostToDevice);

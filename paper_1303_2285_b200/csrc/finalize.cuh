@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
                  const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
                  int nclasses, int ncb, int B, const double2* __restrict__ ccpart,
                  const double2* __restrict__ ccol, long long tot_ccol, const double2* __restrict__ rc,
-                 long long tot_rc, int nseg, typename CT<T>::c* __restrict__ R, int layout,
+                 long long tot_rc, int nseg, typename CT<T>::c* __restrict__ R,
                  long long r_bstride, double scale) {
+  // R: compact (class-major) output, r_bstride elements per snapshot
   using C2 = typename CT<T>::c;
   const int lane = threadIdx.x & 31;
   const long long task = (long long)blockIdx.x * FIN_WARPS + (threadIdx.x >> 5);
@@ -157,7 +158,12 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
       const int v = li + k * W;
       if (active && v < pv) {
         const double2 sv = cadd(G, cadd(sufT[k], preB[k]));
-        write_slot<T>(R, layout, rb, c, pr, v, u, sv.x * scale, zero_im ? 0.0 : sv.y * scale);
+        // compact slot (u-major, then v): lanes write consecutive addresses;
+        // k_expand turns it into the dense / packed layout with coalesced stores
+        C2 val;
+        val.x = (T)(sv.x * scale);
+        val.y = (T)(zero_im ? 0.0 : sv.y * scale);
+        R[rb + c.slot_off + (long long)u * pv + v] = val;
       }
     }
     if (u < ac) {
@@ -311,6 +317,51 @@ __global__ void k_scatter_compact(const typename CT<T>::c* __restrict__ compact,
   const auto val = compact[tid];
   write_slot<T>(R, COVGPU_DENSE, (long long)b * pr.PQ * pr.PQ, c, pr, v, u, (double)val.x,
                 (double)val.y);
+}
+
+// K5 — expand the compact (class-major) result into the dense Hermitian R or
+// the packed upper triangle with coalesced stores: thread per output element
+// (k1, k2) reads its slot — class (dr, dc) = (k2%P - k1%P, k2/P - k1/P),
+// u = k1/P, v = k1%P - s1 — from the L2-resident compact buffer.
+// uc_off[uc] is the class's compact offset (-1: class not in this plan's
+// shard -> element untouched).  (A P x P-block SMEM-transpose variant was
+// measured no faster on B200: cfg5 0.155 vs 0.146 ms, cfg4 0.29 vs 0.12 ms.)
+template <typename T>
+__global__ void k_expand(const typename CT<T>::c* __restrict__ compact, long long cstride,
+                         const long long* __restrict__ uc_off, Problem pr, int B, int layout,
+                         typename CT<T>::c* __restrict__ R) {
+  using C2 = typename CT<T>::c;
+  const long long D = pr.PQ;
+  const long long per = layout == COVGPU_DENSE ? D * D : D * (D + 1) / 2;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= per * B) return;
+  const int b = (int)(tid / per);
+  const long long e = tid % per;
+  long long k1, k2;
+  if (layout == COVGPU_DENSE) {
+    k1 = e / D;
+    k2 = e % D;
+  } else {
+    // packed row k1 starts at k1*D - k1(k1-1)/2: invert with a float guess + fix-up
+    const double disc = (2.0 * D + 1.0) * (2.0 * D + 1.0) - 8.0 * (double)e;
+    long long r = (long long)(((2.0 * D + 1.0) - sqrt(disc)) / 2.0);
+    if (r < 0) r = 0;
+    while (r > 0 && r * D - (r * (r - 1)) / 2 > e) --r;
+    while ((r + 1) * D - ((r + 1) * r) / 2 <= e) ++r;
+    k1 = r;
+    k2 = k1 + (e - (k1 * D - (k1 * (k1 - 1)) / 2));
+  }
+  const bool lower = k2 < k1;
+  const long long a = lower ? k2 : k1, c2 = lower ? k1 : k2;  // a <= c2
+  const int P = pr.P, Q = pr.Q;
+  const int ra = (int)(a % P), ca = (int)(a / P), rc = (int)(c2 % P), cc = (int)(c2 / P);
+  const int dr = rc - ra, dc = cc - ca;
+  const long long off = uc_off[class_index(dr, dc, P, Q)];
+  if (off < 0) return;
+  const int pv = P - abs(dr), s1 = dr < 0 ? -dr : 0;
+  C2 val = compact[(long long)b * cstride + off + (long long)ca * pv + (ra - s1)];
+  if (lower) val.y = -val.y;
+  R[tid] = val;
 }
 
 }  // namespace covgpu
