@@ -240,11 +240,9 @@ def main() -> None:
         step()
     torch.cuda.synchronize(dev)
 
-    plan.set_timing(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     total_ms = 0.0
-    kern = []
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.fill_(1)  # evict A/R from L2 between steps (untimed)
@@ -256,7 +254,15 @@ def main() -> None:
             e1.record()
             torch.cuda.synchronize(dev)
             total_ms += e0.elapsed_time(e1)
-            kern.append(plan.kernel_times())
+    # per-kernel breakdown: separate steps with events between the launches
+    # (kernels serialised on one stream for this, so intervals are per kernel)
+    plan.set_timing(True)
+    kern = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(1)
+        torch.cuda.synchronize(dev)
+        plan.execute(a, out, layout)
+        kern.append(plan.kernel_times())
     plan.set_timing(False)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:

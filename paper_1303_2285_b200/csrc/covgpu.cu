@@ -119,6 +119,9 @@ struct covgpu_plan {
   bool timing = false;
   cudaEvent_t ev[8] = {};
   int nev = 0;
+  // side stream for the edge-row / corner kernels (overlap with the bulk)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // end-to-end host path: cached stream and device buffers
   cudaStream_t host_stream = nullptr;
   void* hA = nullptr;
@@ -163,6 +166,9 @@ void plan_free(covgpu_plan* pl) {
   for (auto& e : pl->ev)
     if (e) cudaEventDestroy(e);
   if (pl->host_stream) cudaStreamDestroy(pl->host_stream);
+  if (pl->side_stream) cudaStreamDestroy(pl->side_stream);
+  if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
+  if (pl->ev_join) cudaEventDestroy(pl->ev_join);
   cudaFree(pl->hA);
   cudaFree(pl->hR);
   cudaFree(pl->d_cls);
@@ -384,15 +390,25 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   auto mark = [&]() {
     if (pl->timing && pl->nev < 8) cudaEventRecord(pl->ev[pl->nev++], st);
   };
+  // The edge-row and corner kernels do not depend on the bulk kernel: run
+  // them on a side stream so they fill the SMs the bulk kernel's last wave
+  // leaves idle (fork/join with events).  With per-kernel timing enabled
+  // everything stays on `st` so the event intervals are per kernel.
+  const bool fork = !pl->timing && pl->side_stream != nullptr;
+  cudaStream_t es = fork ? pl->side_stream : st;
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(es, pl->ev_fork, 0));
+  }
   mark();
   launch_bulk_variant<T>(pl, A, st);
   ++launches;
   mark();
   if (pl->S > 0) {
     switch (pl->D) {
-      case 4: launch_edge<T, 4>(pl, A, st); break;
-      case 8: launch_edge<T, 8>(pl, A, st); break;
-      default: launch_edge<T, 16>(pl, A, st);
+      case 4: launch_edge<T, 4>(pl, A, es); break;
+      case 8: launch_edge<T, 8>(pl, A, es); break;
+      default: launch_edge<T, 16>(pl, A, es);
     }
     ++launches;
     mark();
@@ -400,9 +416,15 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->fin_kr > 0) {
     const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
     if (nc > 0) {
-      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, (C2*)pl->d_corners);
+      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, (C2*)pl->d_corners);
       ++launches;
     }
+  }
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(pl->ev_join, es));
+    CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
+  }
+  if (pl->fin_kr > 0) {
     const unsigned blocks = (unsigned)((pl->ntasks + FIN_WARPS - 1) / FIN_WARPS);
     // finalize into the compact layout (R itself, or the plan's scratch),
     // then expand to dense / packed with coalesced stores
@@ -658,6 +680,16 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     }
   }
   pl->ws_bytes = ws;
+  if (pl->clean) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&pl->side_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      plan_free(pl.get());
+      return fail(COVGPU_ECUDA, "side stream");
+    }
+  }
   cudaError_t e = cudaMemcpy(pl->d_cls, pl->h_cls.data(), sizeof(ClassDesc) * pl->h_cls.size(),
                              cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
