@@ -28,14 +28,15 @@
 
 namespace covgpu {
 
-constexpr int BULK_RC = 32;  // rows per SMEM stage (multiple of every E)
+constexpr int BULK_RC = 32;      // rows per SMEM stage (multiple of every E)
+constexpr int BULK_RC_BIG = 32;  // rows per stage for 1-CTA/SM variants
 constexpr int BULK_MAX_STAGES = 4;
 constexpr size_t BULK_SMEM_SM = 227 * 1024;  // usable SMEM per SM
 
 template <typename T, int E, int NW, int MINB = 1>
 struct BulkCfg {
   using C2 = typename CT<T>::c;
-  static constexpr int RC = BULK_RC;
+  static constexpr int RC = MINB == 1 ? BULK_RC_BIG : BULK_RC;
   static constexpr int XW = 32;
   static constexpr int YW = 32 + NW;  // 32+NW-1 needed; +1 keeps TMA rows 16B multiples
   static constexpr int YR = RC + E - 1;
@@ -75,7 +76,7 @@ struct BulkGeom {
   unsigned valid;  // selected lags of this warp
 };
 
-template <int E, int NW>
+template <int E, int NW, int RC>
 __device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, int ncb,
                                      const int* __restrict__ cls_slot) {
   BulkGeom g;
@@ -104,20 +105,20 @@ __device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, in
   g.rhi = N - P + max(-dr_lo, 0);
   g.body_lo = P - 1 - max(dr_lo, 0);
   g.body_hi = N - P + max(-dr_hi, 0);
-  g.nchunks = (g.rhi - g.rlo + BULK_RC) / BULK_RC;
+  g.nchunks = (g.rhi - g.rlo + RC) / RC;
   g.col0 = g.cb * 32;
   g.ycol0 = g.col0 + g.dc_base;
   return g;
 }
 
 // One SMEM chunk of rows [r0, r0+RC) for one warp.
-template <typename T, int E, int NW>
+template <typename T, int E, int NW, int MINB>
 __device__ __forceinline__ void bulk_chunk(const BulkGeom& g, const Problem& pr, int c,
                                            const typename CT<T>::c* __restrict__ X,
                                            const typename CT<T>::c* __restrict__ Y, T* yr, T* yi,
                                            T* ar, T* ai) {
   using C2 = typename CT<T>::c;
-  using Cfg = BulkCfg<T, E, NW>;
+  using Cfg = BulkCfg<T, E, NW, MINB>;
   constexpr int RC = Cfg::RC, XW = Cfg::XW, YW = Cfg::YW;
   const int N = pr.N, P = pr.P;
   if (c == 0) {
@@ -129,6 +130,21 @@ __device__ __forceinline__ void bulk_chunk(const BulkGeom& g, const Problem& pr,
     }
   }
   const int r0 = g.rlo + c * RC;
+  if (r0 >= g.body_lo && r0 + RC - 1 <= g.body_hi) {
+    // ---- whole chunk in the body: every lag is core, no predicates ----
+#pragma unroll 1
+    for (int t0 = 0; t0 < RC; t0 += E) {
+#pragma unroll
+      for (int tt = 0; tt < E; ++tt) {
+        const C2 yn = Y[(t0 + tt + E - 1) * YW];
+        const C2 x = X[(t0 + tt) * XW];
+        yr[(tt + E - 1) % E] = yn.x;
+        yi[(tt + E - 1) % E] = yn.y;
+        cmac_all<T, E>(tt, x, yr, yi, ar, ai);
+      }
+    }
+    return;
+  }
   for (int t0 = 0; t0 < RC; t0 += E) {
     const int rb = r0 + t0;
     if (rb > g.rhi) break;
@@ -205,11 +221,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     k_bulk(const typename CT<T>::c* __restrict__ A, Problem pr, int n_drg, int n_dcb, int ncb,
            int nclasses, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
            double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
-  using Cfg = BulkCfg<T, E, NW>;
+  using Cfg = BulkCfg<T, E, NW, MINB>;
   using C2 = typename CT<T>::c;
   constexpr int RC = Cfg::RC, XW = Cfg::XW, YW = Cfg::YW, YR = Cfg::YR;
   extern __shared__ __align__(128) unsigned char smraw[];
-  const BulkGeom g = bulk_geom<E, NW>(pr, n_drg, n_dcb, ncb, cls_slot);
+  const BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, cls_slot);
   if (!__syncthreads_or(g.valid != 0)) return;  // CTA-uniform
   const int N = pr.N, M = pr.M;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -251,7 +267,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     __syncthreads();
     const C2* X = reinterpret_cast<const C2*>(smraw + buf * Cfg::stage_bytes) + lane;
     const C2* Y = reinterpret_cast<const C2*>(smraw + buf * Cfg::stage_bytes + Cfg::xbytes) + lane + w;
-    if (g.valid) bulk_chunk<T, E, NW>(g, pr, c, X, Y, yr, yi, ar, ai);
+    if (g.valid) bulk_chunk<T, E, NW, MINB>(g, pr, c, X, Y, yr, yi, ar, ai);
     __syncthreads();  // buffer `buf` is refilled by the next iteration's stage
   }
   if (!g.valid) return;
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage_bytes);
   uint64_t* empty = full + S;
-  BulkGeom g = bulk_geom<E, NW>(pr, n_drg, n_dcb, ncb, cls_slot);  // g.b = snapshot group
+  BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, cls_slot);  // g.b = snapshot group
   const int b0 = g.b * nsnap;
   const int nb = min(nsnap, B - b0);
   if (!__syncthreads_or(g.valid != 0) || nb <= 0) return;  // CTA-uniform
@@ -318,7 +334,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const C2* X = reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes) + lane;
       const C2* Y =
           reinterpret_cast<const C2*>(smraw + s * Cfg::stage_bytes + Cfg::xbytes) + lane + w;
-      if (g.valid) bulk_chunk<T, E, NW>(g, pr, c, X, Y, yr, yi, ar, ai);
+      if (g.valid) bulk_chunk<T, E, NW, MINB>(g, pr, c, X, Y, yr, yi, ar, ai);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       // refill the previous chunk's stage one chunk late, so thread 0 rarely

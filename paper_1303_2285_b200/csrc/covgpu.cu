@@ -223,7 +223,7 @@ template <typename T, int E, int NW, int MINB>
 cudaError_t bulk_attr() {
   cudaError_t e = cudaFuncSetAttribute(k_bulk<T, E, NW, MINB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)BulkCfg<T, E, NW>::smem);
+                                       (int)BulkCfg<T, E, NW, MINB>::smem);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_bulk_tma<T, E, NW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)BulkCfg<T, E, NW, MINB>::smem_tma);
