@@ -93,11 +93,13 @@ __device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, in
   g.dc_base = dcb * NW;
   g.dc = g.dc_base + w;
   g.valid = 0;
+  if (w < NW) {  // (warp NW of the TMA variant is the producer)
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int dr = g.dr0 + e;
-    if (g.dc < Q && in_uc(dr, g.dc, P, Q) && cls_slot[class_index(dr, g.dc, P, Q)] >= 0)
-      g.valid |= 1u << e;
+    for (int e = 0; e < E; ++e) {
+      const int dr = g.dr0 + e;
+      if (g.dc < Q && in_uc(dr, g.dc, P, Q) && cls_slot[class_index(dr, g.dc, P, Q)] >= 0)
+        g.valid |= 1u << e;
+    }
   }
   // CTA row range (union over lags), and the body where every lag is core
   const int dr_lo = g.dr0, dr_hi = min(g.dr0 + E - 1, P - 1);
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 // {64, RC, 1}, the Y box {2*YW, YR, 1}; negative / past-the-end coordinates
 // are zero-filled by the hardware.
 template <typename T, int E, int NW, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB)
+__global__ void __launch_bounds__((NW + 1) * 32, MINB)
     k_bulk_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                Problem pr, int n_drg, int n_dcb, int ncb, int nclasses, int B, int nsnap,
                const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
@@ -319,8 +321,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     tma_load_3d(base, &tmx, 2 * g.col0, r0, b, &full[s]);
     tma_load_3d(base + Cfg::xbytes, &tmy, 2 * g.ycol0, r0 + g.dr0, b, &full[s]);
   };
-  if (threadIdx.x == 0)
-    for (int k = 0; k < min(S, total); ++k) issue(k);
+  if (w == NW) {  // producer warp: keep the ring full
+    if (lane == 0) {
+      for (int k = 0; k < total; ++k) {
+        if (k >= S) mbar_wait(&empty[k % S], ((k - S) / S) & 1);
+        issue(k);
+      }
+    }
+    return;
+  }
 
   T ar[E], ai[E], yr[E], yi[E];
 #pragma unroll
@@ -337,13 +346,6 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (g.valid) bulk_chunk<T, E, NW, MINB>(g, pr, c, X, Y, yr, yi, ar, ai);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      // refill the previous chunk's stage one chunk late, so thread 0 rarely
-      // waits for the other warps
-      if (threadIdx.x == 0 && k >= 1 && k - 1 + S < total) {
-        const int sp = (k - 1) % S;
-        mbar_wait(&empty[sp], ((k - 1) / S) & 1);
-        issue(k - 1 + S);
-      }
     }
     if (g.valid) {  // snapshot done
       g.b = b0 + bi;

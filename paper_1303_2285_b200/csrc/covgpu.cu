@@ -313,7 +313,7 @@ void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
       long long nsnap = std::max(1LL, (blocks + slots - 1) / slots);
       nsnap = std::min<long long>(nsnap, pl->batch);
       const long long groups = (pl->batch + nsnap - 1) / nsnap;
-      k_bulk_tma<T, E, NW, MINB><<<(unsigned)(groups * units), NW * 32, Cfg::smem_tma, st>>>(
+      k_bulk_tma<T, E, NW, MINB><<<(unsigned)(groups * units), (NW + 1) * 32, Cfg::smem_tma, st>>>(
           pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, (int)pl->batch,
           (int)nsnap, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
       pl->used_tma = true;
