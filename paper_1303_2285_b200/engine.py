@@ -221,3 +221,69 @@ def estimate_batch(
     dense = _run(stack, window)
     k = (n - window.p + 1) * (m - window.q + 1)
     return [CovarianceMatrix(dense[i], k) for i in range(b)]
+
+
+def measure_unit_times(a, window: WindowSpec, repeats: int = 3, device=None):
+    """Best-of-repeats GPU time of every bulk work unit (the partitioner's
+    unit: one walk over A's rows for `lags` x `warps` classes), each run as a
+    class-subset plan (edge rows and finalize of those classes included).
+    Returns [(class ids, seconds)] in unit order."""
+    from .partition import work_units
+    from .plan import Plan
+
+    if repeats < 1:
+        raise ValueError(f"repeats must be >= 1, got {repeats}")
+    t = _to_device_matrix(a, device, None, ndim=2)
+    n, m = t.shape
+    window.validate_for(n, m)
+    units = work_units(n, m, window, fp64=t.dtype == torch.complex128)
+    out = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a3 = t.unsqueeze(0)
+    for ids, _cost in units:
+        plan = Plan(n, m, window, dtype=t.dtype, class_ids=ids, device=t.device)
+        dst = plan.alloc_output("compact")
+        plan.execute(a3, dst, "compact")  # warm
+        best = float("inf")
+        for _ in range(repeats):
+            e0.record()
+            plan.execute(a3, dst, "compact")
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        plan.close()
+        out.append((ids, best))
+    return out
+
+
+def measure_combination_times(a, window: WindowSpec, backend: str | None = None, repeats: int = 3):
+    """Per-class GPU cost in UC order, the reference's trace contract
+    (``engine.py:258-288``): each bulk unit's measured time is apportioned to
+    its classes by product count mu.  Feeds ``write_cost_trace`` and the
+    reference's scheduling simulator (``schedsim.ingest_measured_costs``)."""
+    resolve_backend(backend)
+    t = _to_device_matrix(a, None, None, ndim=2)
+    n, m = t.shape
+    combos = _comb.unique_combinations(window)
+    cost = [0.0] * len(combos)
+    for ids, secs in measure_unit_times(t, window, repeats):
+        mus = [_comb.pair_count(combos[i], n, m) for i in ids]
+        tot = sum(mus)
+        for i, mu in zip(ids, mus):
+            cost[i] = secs * mu / tot
+    return [(combos[i], cost[i]) for i in range(len(combos))]
+
+
+TRACE_HEADER = ["task_id", "dr", "dc", "cost"]
+
+
+def write_cost_trace(path, entries) -> None:
+    """(Combination, cost) pairs as the reference's trace CSV
+    (``schedsim.py:164-171``, header task_id,dr,dc,cost)."""
+    import csv
+
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh)
+        w.writerow(TRACE_HEADER)
+        for task_id, (comb, c) in enumerate(entries):
+            w.writerow([task_id, comb.dr, comb.dc, repr(float(c))])
