@@ -86,6 +86,11 @@ struct covgpu_plan {
   bool used_tma = false;
   const void* tmap_ptr = nullptr;  // A the cached tensor maps describe
   CUtensorMap tmx{}, tmy{};
+  // edge-row kernel TMA variant (strips of >= 16 rows)
+  bool edge_tma = false;
+  int r2g = 1, n_r2g = 1;
+  const void* etmap_ptr = nullptr;
+  CUtensorMap etmx{}, etmy{};
   int D = 16;         // column lags per edge-row thread
   int ncb = 0;        // 32-column blocks
   int n_drg = 0;      // bulk row-lag groups
@@ -340,6 +345,35 @@ void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream
 
 template <typename T, int D>
 void launch_edge(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
+  const Problem& pr = pl->pr;
+  if (pl->edge_tma && ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0)) {
+    using Cfg = EdgeCfg<T, D>;
+    if (pl->etmap_ptr != (const void*)A) {
+      CUtensorMap mx, my;
+      if (make_tmap(&mx, A, sizeof(T) == 8, pl->batch, pr.N, pr.M, 2 * Cfg::XW, pl->S) &&
+          make_tmap(&my, A, sizeof(T) == 8, pl->batch, pr.N, pr.M, 2 * Cfg::YW, pl->r2g)) {
+        pl->etmx = mx;
+        pl->etmy = my;
+        pl->etmap_ptr = A;
+      } else {
+        pl->etmap_ptr = nullptr;
+      }
+    }
+    if (pl->etmap_ptr == (const void*)A) {
+      const size_t smem = Cfg::smem(pl->S, pl->r2g);
+      static bool attr_done[2] = {false, false};  // per dtype, set once per process
+      if (!attr_done[sizeof(T) == 8]) {
+        cudaFuncSetAttribute(k_edge_tma<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr_done[sizeof(T) == 8] = true;
+      }
+      const long long blocks = pl->batch * 2LL * pl->ndg * pl->n_r2g * pl->nseg;
+      k_edge_tma<T, D><<<(unsigned)blocks, (EDGE_WARPS + 1) * 32, smem, st>>>(
+          pl->etmx, pl->etmy, pr, pl->S, pl->r2g, pl->n_r2g, pl->ndg, pl->nseg, pl->d_cls_slot,
+          pl->d_cls, pl->d_rc, pl->tot_rc);
+      return;
+    }
+  }
   const long long total = pl->batch * 2LL * pl->ndg * pl->nseg * (long long)pl->S * pl->S;
   if (total == 0) return;
   k_edge_rows<T, D><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
@@ -568,7 +602,18 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   pl->n_dcb = (q + pl->NW - 1) / pl->NW;
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
-  {
+  pl->edge_tma = pl->S >= 16 && pl->use_tma;
+  if (pl->edge_tma) {
+    // TMA edge kernel: CTA = (strip, lag group, r2 group, column segment);
+    // aim for ~4 waves of 1-CTA/SM blocks
+    pl->r2g = std::max(1, std::min(pl->S, (EDGE_WARPS * 32) / pl->S));
+    pl->n_r2g = (pl->S + pl->r2g - 1) / pl->r2g;
+    const long long per = batch * 2LL * pl->ndg * pl->n_r2g;
+    const long long want = 148LL * 4;
+    const long long chunks = std::max(1LL, (long long)((m - q + 1 + EDGE_CW - 1) / EDGE_CW));
+    long long seg = std::max(1LL, (want + per - 1) / per);
+    pl->nseg = (int)std::max(1LL, std::min(seg, std::min(chunks, 16LL)));
+  } else {
     // split the edge-row column walk so the launch has >= ~4 waves of warps
     const long long threads = batch * 2LL * pl->ndg * (long long)pl->S * pl->S;
     const long long want = 148LL * 32 * 16 * 4;
