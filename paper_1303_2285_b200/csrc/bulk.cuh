@@ -70,17 +70,19 @@ __device__ __forceinline__ void cmac_all(int tt, typename CT<T>::c x, const T* y
 
 // Per-warp view of one CTA's geometry.
 struct BulkGeom {
-  int b, cb, dr0, dc_base, dc;
+  int b, cb, rs, dr0, dc_base, dc;
   int rlo, rhi, body_lo, body_hi, nchunks;
   int col0, ycol0;
   unsigned valid;  // selected lags of this warp
 };
 
 template <int E, int NW, int RC>
-__device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, int ncb,
+__device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, int ncb, int nrs,
                                      const int* __restrict__ cls_slot) {
   BulkGeom g;
   long long t = blockIdx.x;
+  g.rs = (int)(t % nrs);  // row segment (small problems split the row walk)
+  t /= nrs;
   g.cb = (int)(t % ncb);
   t /= ncb;
   const int dcb = (int)(t % n_dcb);
@@ -107,7 +109,14 @@ __device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, in
   g.rhi = N - P + max(-dr_lo, 0);
   g.body_lo = P - 1 - max(dr_lo, 0);
   g.body_hi = N - P + max(-dr_hi, 0);
-  g.nchunks = (g.rhi - g.rlo + RC) / RC;
+  if (nrs > 1) {
+    const int nrows = g.rhi - g.rlo + 1;
+    const int seglen = ((nrows + nrs - 1) / nrs + RC - 1) / RC * RC;
+    const int lo = g.rlo + g.rs * seglen;
+    g.rhi = min(g.rhi, lo + seglen - 1);
+    g.rlo = lo;
+  }
+  g.nchunks = g.rhi >= g.rlo ? (g.rhi - g.rlo + RC) / RC : 0;
   g.col0 = g.cb * 32;
   g.ycol0 = g.col0 + g.dc_base;
   return g;
@@ -188,7 +197,7 @@ __device__ __forceinline__ void bulk_chunk(const BulkGeom& g, const Problem& pr,
 }
 
 template <typename T, int E>
-__device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int nclasses, int ncb,
+__device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int nclasses, int ncb, int nrs,
                                      const int* __restrict__ cls_slot,
                                      const ClassDesc* __restrict__ cls, double2* __restrict__ ccpart,
                                      double2* __restrict__ ccol, long long tot_ccol, const T* ar,
@@ -209,11 +218,11 @@ __device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int n
       const ClassDesc& cd = cls[cid];
       const int ac = cd.qu - 1;
       const long long idx = c1 < left_end ? c1 : (long long)ac + (c1 - right_beg);
-      ccol[(long long)g.b * tot_ccol + cd.ccol_off + idx] = v;
+      ccol[((long long)g.b * tot_ccol + cd.ccol_off + idx) * nrs + g.rs] = v;
     }
     if (!core) v = make_double2(0.0, 0.0);
     v = warp_sum(v);
-    if (lane == 0) ccpart[((long long)g.b * nclasses + cid) * ncb + g.cb] = v;
+    if (lane == 0) ccpart[((long long)g.b * nclasses + cid) * ncb * nrs + g.cb * nrs + g.rs] = v;
   }
 }
 
@@ -221,13 +230,13 @@ __device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int n
 template <typename T, int E, int NW, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_bulk(const typename CT<T>::c* __restrict__ A, Problem pr, int n_drg, int n_dcb, int ncb,
-           int nclasses, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
+           int nrs, int nclasses, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
            double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
   using Cfg = BulkCfg<T, E, NW, MINB>;
   using C2 = typename CT<T>::c;
   constexpr int RC = Cfg::RC, XW = Cfg::XW, YW = Cfg::YW, YR = Cfg::YR;
   extern __shared__ __align__(128) unsigned char smraw[];
-  const BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, cls_slot);
+  const BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, nrs, cls_slot);
   if (!__syncthreads_or(g.valid != 0)) return;  // CTA-uniform
   const int N = pr.N, M = pr.M;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     __syncthreads();  // buffer `buf` is refilled by the next iteration's stage
   }
   if (!g.valid) return;
-  bulk_epilogue<T, E>(g, pr, nclasses, ncb, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
+  bulk_epilogue<T, E>(g, pr, nclasses, ncb, nrs, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
 }
 
 // ---- TMA variant ------------------------------------------------------------
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 template <typename T, int E, int NW, int MINB>
 __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     k_bulk_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
-               Problem pr, int n_drg, int n_dcb, int ncb, int nclasses, int B, int nsnap,
+               Problem pr, int n_drg, int n_dcb, int ncb, int nrs, int nclasses, int B, int nsnap,
                const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
                double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
   // one CTA walks `nsnap` consecutive snapshots back to back: the TMA ring
@@ -297,7 +306,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage_bytes);
   uint64_t* empty = full + S;
-  BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, cls_slot);  // g.b = snapshot group
+  BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, nrs, cls_slot);  // g.b = snapshot group
   const int b0 = g.b * nsnap;
   const int nb = min(nsnap, B - b0);
   if (!__syncthreads_or(g.valid != 0) || nb <= 0) return;  // CTA-uniform
@@ -349,7 +358,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     }
     if (g.valid) {  // snapshot done
       g.b = b0 + bi;
-      bulk_epilogue<T, E>(g, pr, nclasses, ncb, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
+      bulk_epilogue<T, E>(g, pr, nclasses, ncb, nrs, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) ar[e] = ai[e] = (T)0;

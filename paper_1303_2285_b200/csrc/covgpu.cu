@@ -93,6 +93,7 @@ struct covgpu_plan {
   CUtensorMap etmx{}, etmy{};
   int D = 16;         // column lags per edge-row thread
   int ncb = 0;        // 32-column blocks
+  int nrs = 1;        // bulk row segments (small problems: more CTAs)
   int n_drg = 0;      // bulk row-lag groups
   int n_dcb = 0;      // bulk column-lag blocks (NW lags each)
   int S = 0;          // edge strip height P-1
@@ -294,7 +295,7 @@ cudaError_t set_attrs() {
 template <typename T, int E, int NW, int MINB>
 void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   using Cfg = BulkCfg<T, E, NW, MINB>;
-  const long long units = (long long)pl->n_drg * pl->n_dcb * pl->ncb;  // CTAs per snapshot
+  const long long units = (long long)pl->n_drg * pl->n_dcb * pl->ncb * pl->nrs;  // CTAs per snapshot
   const long long blocks = pl->batch * units;
   const Problem& pr = pl->pr;
   // TMA needs 16-byte aligned rows: always for complex128, even M for complex64
@@ -319,7 +320,7 @@ void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
       nsnap = std::min<long long>(nsnap, pl->batch);
       const long long groups = (pl->batch + nsnap - 1) / nsnap;
       k_bulk_tma<T, E, NW, MINB><<<(unsigned)(groups * units), (NW + 1) * 32, Cfg::smem_tma, st>>>(
-          pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, (int)pl->batch,
+          pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nrs, pl->nclasses, (int)pl->batch,
           (int)nsnap, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
       pl->used_tma = true;
       return;
@@ -327,7 +328,7 @@ void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   }
   pl->used_tma = false;
   k_bulk<T, E, NW, MINB><<<(unsigned)blocks, NW * 32, Cfg::smem, st>>>(
-      A, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart,
+      A, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nrs, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart,
       pl->d_ccol, pl->tot_ccol);
 }
 
@@ -465,9 +466,9 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     C2* cdst = layout == COVGPU_COMPACT ? R : (C2*)pl->d_slots;
 #define FINV(KR)                                                                                 \
   k_finalize_v<T, KR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                       \
-      (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses, pl->ncb, B, \
-      pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, pl->nseg, cdst,             \
-      pl->compact_elems, scale)
+      (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses,           \
+      pl->ncb * pl->nrs, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
+      pl->nseg, cdst, pl->compact_elems, scale)
     switch (pl->fin_kr) {
       case 1: FINV(1); break;
       case 2: FINV(2); break;
@@ -486,8 +487,9 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   } else {
     const long long ntasks = (long long)B * pl->nclasses;
     k_finalize<T><<<(unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS), FIN_WARPS * 32, pl->fin_smem, st>>>(
-        A, pr, pl->d_cls, pl->nclasses, pl->ncb, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc,
-        pl->tot_rc, pl->nseg, pl->d_slots, pl->tot_slots, R, layout, r_bstride, scale, ntasks, pr.Q);
+        A, pr, pl->d_cls, pl->nclasses, pl->ncb * pl->nrs, pl->nrs, pl->d_ccpart, pl->d_ccol,
+        pl->tot_ccol, pl->d_rc, pl->tot_rc, pl->nseg, pl->d_slots, pl->tot_slots, R, layout,
+        r_bstride, scale, ntasks, pr.Q);
   }
   ++launches;
   mark();
@@ -600,6 +602,19 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   pl->ncb = (int)((m + 31) / 32);
   pl->n_drg = (2 * p - 1 + pl->E - 1) / pl->E;
   pl->n_dcb = (q + pl->NW - 1) / pl->NW;
+  {
+    // split the bulk row walk when the grid would be under ~4 waves
+    const int minb = kBulkVariants[pl->bulk_variant].MINB;
+    const long long ctas = batch * (long long)pl->n_drg * pl->n_dcb * pl->ncb;
+    const long long want = 148LL * minb * 4;
+    const long long max_split = std::max(1LL, (long long)((n - p + 1) / 64));  // >= 2 chunks each
+    long long r = ctas >= want ? 1 : (want + ctas - 1) / ctas;
+    // measured: with a CTA per (unit, segment) the per-CTA pipeline fill
+    // outweighs the better wave fill (cfg3 bulk 0.197 -> 0.223 ms), so the
+    // split is off until work units are scheduled persistently
+    r = 1;  // (ccol would need a pre-reduction over segments before the finalize)
+    pl->nrs = (int)std::max(1LL, std::min(r, std::min(max_split, 16LL)));
+  }
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
   pl->edge_tma = pl->S >= 16 && pl->use_tma;
@@ -676,8 +691,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     return rc;
   }
   if (pl->clean) {
-    if ((rc = dalloc(&pl->d_ccpart, (size_t)batch * nc * pl->ncb, &ws)) ||
-        (rc = dalloc(&pl->d_ccol, (size_t)(batch * std::max(pl->tot_ccol, 1LL)), &ws)) ||
+    if ((rc = dalloc(&pl->d_ccpart, (size_t)batch * nc * pl->ncb * pl->nrs, &ws)) ||
+        (rc = dalloc(&pl->d_ccol, (size_t)(batch * std::max(pl->tot_ccol, 1LL) * pl->nrs), &ws)) ||
         (rc = dalloc(&pl->d_rc, (size_t)(batch * std::max(pl->tot_rc, 1LL) * pl->nseg), &ws)) ||
         (rc = dalloc(&pl->d_slots, (size_t)(batch * std::max(pl->tot_slots, 1LL)), &ws))) {
       plan_free(pl.get());
@@ -761,7 +776,7 @@ int covgpu_plan_execute(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_
 
 int64_t covgpu_plan_workspace_bytes(covgpu_plan_t pl) { return pl ? pl->ws_bytes : -1; }
 int32_t covgpu_plan_num_groups(covgpu_plan_t pl) {
-  return pl ? (int32_t)(pl->batch * pl->n_drg * pl->n_dcb * pl->ncb) : -1;
+  return pl ? (int32_t)(pl->batch * pl->n_drg * pl->n_dcb * pl->ncb * pl->nrs) : -1;
 }
 int32_t covgpu_plan_launches(covgpu_plan_t pl) { return pl ? pl->launches : -1; }
 

@@ -89,7 +89,7 @@ template <typename T, int KR>
 __global__ void __launch_bounds__(FIN_WARPS * 32)
     k_finalize_v(const typename CT<T>::c* __restrict__ corners, Problem pr,
                  const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
-                 int nclasses, int ncb, int B, const double2* __restrict__ ccpart,
+                 int nclasses, int ncb, int nrs, int B, const double2* __restrict__ ccpart,
                  const double2* __restrict__ ccol, long long tot_ccol, const double2* __restrict__ rc,
                  long long tot_rc, int nseg, typename CT<T>::c* __restrict__ R,
                  long long r_bstride, double scale) {
@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const int Sx = pr.P - 1, Wc = pr.Q - 1;
   const long long cstride = (long long)Sx * Wc;
   const C2* Cb = corners + (long long)b * 4 * cstride;
+  (void)nrs;  // bulk row segments are off (nrs == 1): ccol holds whole-column sums
   const double2* cl = ccol + (long long)b * tot_ccol + c.ccol_off;
   const double2* rcc = rc + ((long long)b * tot_rc + c.rc_off) * nseg;
 
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
 template <typename T>
 __global__ void __launch_bounds__(FIN_WARPS * 32)
     k_finalize(const typename CT<T>::c* __restrict__ A, Problem pr, const ClassDesc* __restrict__ cls,
-               int nclasses, int ncb, const double2* __restrict__ ccpart,
+               int nclasses, int ncb, int nrs, const double2* __restrict__ ccpart,
                const double2* __restrict__ ccol, long long tot_ccol, const double2* __restrict__ rc,
                long long tot_rc, int nseg, double2* __restrict__ scratch, long long tot_slots,
                typename CT<T>::c* __restrict__ R, int layout, long long r_bstride, double scale,
@@ -211,7 +212,13 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   double2* prr = pl + qmax;
   const C2* Ab = A + (long long)b * N * M;
   const double2* cc_p = ccpart + ((long long)b * nclasses + ci) * ncb;
-  const double2* cl = ccol + (long long)b * tot_ccol + c.ccol_off;
+  const double2* clb = ccol + ((long long)b * tot_ccol + c.ccol_off) * nrs;
+  auto cl = [&](int j) {
+    if (nrs == 1) return clb[j];
+    double2 v = clb[(long long)j * nrs];
+    for (int r = 1; r < nrs; ++r) v = cadd(v, clb[(long long)j * nrs + r]);
+    return v;
+  };
   const double2* rcc = rc + ((long long)b * tot_rc + c.rc_off) * nseg;
   double2* sl = scratch + (long long)b * tot_slots + c.slot_off;  // [v][u]
   const bool zero_im = (c.d == 0);  // class (0,0) feeds the real main diagonal
@@ -222,13 +229,13 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   cc = warp_sum(cc);
   // G(u)
   double2 totl = make_double2(0.0, 0.0);
-  for (int j = lane; j < ac; j += 32) totl = cadd(totl, cl[j]);
+  for (int j = lane; j < ac; j += 32) totl = cadd(totl, cl(j));
   totl = warp_sum(totl);
   {
     double2 carry = cadd(cc, totl);
     for (int u0 = 0; u0 < qu; u0 += 32) {
       const int u = u0 + lane;
-      const double2 q = u < ac ? csub(cl[ac + u], cl[u]) : make_double2(0.0, 0.0);
+      const double2 q = u < ac ? csub(cl(ac + u), cl(u)) : make_double2(0.0, 0.0);
       double2 tot;
       const double2 ex = warp_excl_scan(q, &tot);
       if (u < qu) {
