@@ -126,7 +126,8 @@ int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tfl
 
 /* Bulk-kernel work unit of a shape: `lags` row lags x `warps` column lags
  * per CTA.  The partitioner shards classes in whole units. */
-int covgpu_bulk_geometry(int32_t p, int32_t q, int32_t dtype, int32_t* lags, int32_t* warps);
+int covgpu_bulk_geometry(int64_t batch, int64_t n, int64_t m, int32_t p, int32_t q, int32_t dtype,
+                         int32_t* lags, int32_t* warps);
 
 /* Scatter a COVGPU_COMPACT shard (the slots of `class_ids`, class-major) into
  * a dense Hermitian R_dev (both triangles) — the root's half of the multi-GPU

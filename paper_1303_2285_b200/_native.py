@@ -61,7 +61,7 @@ _SIGS = {
     ),
     "covgpu_plan_execute_host": (ctypes.c_int, [_vp, _vp, _vp, _i32, _dbl]),
     "covgpu_probe_fma_peak": (ctypes.c_int, [ctypes.c_int, _i32, _dbl, ctypes.POINTER(_dbl)]),
-    "covgpu_bulk_geometry": (ctypes.c_int, [_i32, _i32, _i32, _p32, _p32]),
+    "covgpu_bulk_geometry": (ctypes.c_int, [_i64, _i64, _i64, _i32, _i32, _i32, _p32, _p32]),
     "covgpu_scatter_compact": (
         ctypes.c_int, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _p32, _i32, _vp, _vp]),
     "covgpu_combination": (ctypes.c_int, [_vp, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),

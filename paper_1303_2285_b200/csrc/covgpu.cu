@@ -202,22 +202,30 @@ struct BulkVariant {
   int E, NW, MINB;
 };
 constexpr BulkVariant kBulkVariants[] = {
-    {4, 8, 2}, {8, 8, 2}, {16, 8, 1}, {8, 16, 1}, {16, 8, 2}, {16, 16, 1},
+    {4, 8, 2}, {8, 8, 2}, {16, 8, 1}, {8, 16, 1}, {16, 8, 2}, {16, 16, 1}, {16, 4, 2}, {8, 4, 2},
 };
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
-// measured on B200 (tools/kt.py): FP64 with P >= 32 runs best with 16 row
-// lags and 8 warps (1 CTA/SM, 4-stage TMA ring); smaller P and FP32 with 8
-// lags and 2 CTAs/SM.  COVGPU_BULK_VARIANT overrides (tuning experiments).
-int pick_bulk_variant(int p, int dtype) {
+// Bulk variant per shape, measured on B200 (tools/kt.py): 4 compute warps
+// (column lags) per CTA and 2 CTAs/SM beat 8-warp CTAs for FP64; 16 row lags
+// when the grid still has >= 6 waves (cfg5: bulk 9.09 -> 8.81 ms), else 8
+// lags for more CTAs (cfg3 0.196 -> 0.174 ms, cfg2 0.036 -> 0.027 ms).  FP32
+// keeps 8 warps x 8 lags on large grids (cfg4).  COVGPU_BULK_VARIANT
+// overrides (tuning experiments).
+int pick_bulk_variant(long long n, long long m, int p, int q, long long batch, int dtype) {
+  (void)n;
   const int span = 2 * p - 1;
+  auto waves = [&](int E, int NW, int MINB) {
+    const long long ctas = batch * ((span + E - 1) / E) * (long long)((q + NW - 1) / NW) * ((m + 31) / 32);
+    return (double)ctas / (148.0 * MINB);
+  };
   int v;
   if (span <= 4)
     v = 0;  // E=4
-  else if (dtype == COVGPU_C128 && p >= 32)
-    v = 2;  // E=16, NW=8, 1 CTA/SM
+  else if (dtype == COVGPU_C128)
+    v = (span > 8 && waves(16, 4, 2) >= 6.0) ? 6 : 7;
   else
-    v = 1;  // E=8, NW=8, 2 CTAs/SM
+    v = waves(8, 8, 2) >= 6.0 ? 1 : 7;
   if (const char* env = getenv("COVGPU_BULK_VARIANT")) {
     const int ev = atoi(env);
     if (ev >= 0 && ev < kNumBulkVariants) v = ev;
@@ -273,6 +281,8 @@ cudaError_t bulk_attrs() {
   if ((r = bulk_attr<T, 8, 16, 1>()) != cudaSuccess) e = r;
   if ((r = bulk_attr<T, 16, 8, 2>()) != cudaSuccess) e = r;
   if ((r = bulk_attr<T, 16, 16, 1>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 16, 4, 2>()) != cudaSuccess) e = r;
+  if ((r = bulk_attr<T, 8, 4, 2>()) != cudaSuccess) e = r;
   return e;
 }
 
@@ -340,6 +350,8 @@ void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream
     case 2: launch_bulk<T, 16, 8, 1>(pl, A, st); break;
     case 3: launch_bulk<T, 8, 16, 1>(pl, A, st); break;
     case 4: launch_bulk<T, 16, 8, 2>(pl, A, st); break;
+    case 6: launch_bulk<T, 16, 4, 2>(pl, A, st); break;
+    case 7: launch_bulk<T, 8, 4, 2>(pl, A, st); break;
     default: launch_bulk<T, 16, 16, 1>(pl, A, st);
   }
 }
@@ -592,7 +604,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   pr.PQ = p * q;
   pl->clean = (n >= 2LL * p - 2) && (m >= 2LL * q - 2) && q <= kMaxCleanQ;
   {
-    const int v = pick_bulk_variant(p, dtype);
+    const int v = pick_bulk_variant(n, m, p, q, batch, dtype);
     pl->bulk_variant = v;
     if (const char* nt = getenv("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
     pl->E = kBulkVariants[v].E;
@@ -935,10 +947,10 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
   return COVGPU_OK;
 }
 
-int covgpu_bulk_geometry(int32_t p, int32_t q, int32_t dtype, int32_t* lags, int32_t* warps) {
-  (void)q;
-  if (p < 1 || !lags || !warps) return fail(COVGPU_EINVAL, "bad arguments");
-  const int v = pick_bulk_variant(p, dtype);
+int covgpu_bulk_geometry(int64_t batch, int64_t n, int64_t m, int32_t p, int32_t q, int32_t dtype,
+                         int32_t* lags, int32_t* warps) {
+  if (p < 1 || q < 1 || batch < 1 || !lags || !warps) return fail(COVGPU_EINVAL, "bad arguments");
+  const int v = pick_bulk_variant(n, m, p, q, batch, dtype);
   *lags = kBulkVariants[v].E;
   *warps = kBulkVariants[v].NW;
   return COVGPU_OK;

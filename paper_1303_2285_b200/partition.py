@@ -23,21 +23,27 @@ from .core import WindowSpec
 __all__ = ["bulk_geometry", "work_units", "partition_classes", "shard_cost"]
 
 
-def bulk_geometry(p: int, fp64: bool = True) -> tuple[int, int]:
+def bulk_geometry(p: int, fp64: bool = True, n: int = 2048, m: int = 2048, q: int = 64,
+                  batch: int = 1) -> tuple[int, int]:
     """(row lags, column lags) per bulk CTA — mirrors covgpu.cu pick_bulk_variant
     (checked against covgpu_bulk_geometry in tests)."""
     span = 2 * p - 1
+
+    def waves(e, nw, minb):
+        ctas = batch * ((span + e - 1) // e) * ((q + nw - 1) // nw) * ((m + 31) // 32)
+        return ctas / (148.0 * minb)
+
     if span <= 4:
         return 4, 8
-    if fp64 and p >= 32:
-        return 16, 8
-    return 8, 8
+    if fp64:
+        return (16, 4) if span > 8 and waves(16, 4, 2) >= 6.0 else (8, 4)
+    return (8, 8) if waves(8, 8, 2) >= 6.0 else (8, 4)
 
 
 def work_units(n: int, m: int, window: WindowSpec, fp64: bool = True):
     """[(class ids, cost)] per bulk unit in launch order."""
     p, q = window.p, window.q
-    lags, warps = bulk_geometry(p, fp64)
+    lags, warps = bulk_geometry(p, fp64, n, m, q)
     units = []
     for drg in range((2 * p - 1 + lags - 1) // lags):
         dr0 = -(p - 1) + drg * lags

@@ -103,12 +103,14 @@ def test_partition_units_match_library_geometry():
 
     lib = _native.lib()
     e, nw = ctypes.c_int32(), ctypes.c_int32()
-    for p in (1, 2, 3, 4, 5, 8, 16, 31, 32, 64, 100):
+    for n, m, p, q, batch in [(32, 32, 4, 4, 1), (256, 256, 16, 16, 1), (512, 512, 32, 32, 1),
+                              (128, 128, 8, 16, 1024), (2048, 2048, 64, 64, 1), (300, 700, 100, 9, 1),
+                              (20, 20, 1, 1, 1), (50, 60, 3, 2, 7), (64, 64, 5, 31, 1)]:
         for fp64 in (True, False):
-            rc = lib.covgpu_bulk_geometry(p, 4, _native.C128 if fp64 else _native.C64,
+            rc = lib.covgpu_bulk_geometry(batch, n, m, p, q, _native.C128 if fp64 else _native.C64,
                                           ctypes.byref(e), ctypes.byref(nw))
             assert rc == 0
-            assert (e.value, nw.value) == bulk_geometry(p, fp64), (p, fp64)
+            assert (e.value, nw.value) == bulk_geometry(p, fp64, n, m, q, batch), (n, m, p, q, fp64)
 
 
 def test_counters_closed_form():
