@@ -51,6 +51,9 @@ struct BulkCfg {
   static constexpr size_t smem_tma = stages * stage_bytes + 2 * 8 * BULK_MAX_STAGES;  // + mbarriers
 };
 
+// (A packed-FP32 variant with 2 FFMA2 (fma.rn.f32x2) per lag was measured
+// slower on B200: cfg4 bulk 1.12 vs 0.88 ms; FFMA2 loops peak at 54-59 TF/s
+// against 65.6 TF/s for FFMA — tools/ffma2.cu.)
 // acc[e] += x * conj(y[(tt+e) % E]) for every lag, in four passes that each
 // keep one x component in the same operand slot, so consecutive FMAs can read
 // it from the operand-reuse cache (three distinct 64-bit sources per DFMA

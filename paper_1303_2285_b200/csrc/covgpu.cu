@@ -134,6 +134,7 @@ struct covgpu_plan {
   void* hR = nullptr;
   size_t hA_bytes = 0, hR_bytes = 0;
   std::mutex host_mu;
+  std::mutex exec_mu;  // executes mutate plan state (tensor-map cache, timing events)
 };
 
 namespace {
@@ -203,6 +204,7 @@ struct BulkVariant {
 };
 constexpr BulkVariant kBulkVariants[] = {
     {4, 8, 2}, {8, 8, 2}, {16, 8, 1}, {8, 16, 1}, {16, 8, 2}, {16, 16, 1}, {16, 4, 2}, {8, 4, 2},
+    {16, 4, 3}, {8, 4, 4},
 };
 constexpr int kNumBulkVariants = sizeof(kBulkVariants) / sizeof(kBulkVariants[0]);
 
@@ -283,6 +285,10 @@ cudaError_t bulk_attrs() {
   if ((r = bulk_attr<T, 16, 16, 1>()) != cudaSuccess) e = r;
   if ((r = bulk_attr<T, 16, 4, 2>()) != cudaSuccess) e = r;
   if ((r = bulk_attr<T, 8, 4, 2>()) != cudaSuccess) e = r;
+  if constexpr (sizeof(T) == 4) {  // FP32-only variants (FP64 tiles do not fit 3-4 CTAs/SM)
+    if ((r = bulk_attr<T, 16, 4, 3>()) != cudaSuccess) e = r;
+    if ((r = bulk_attr<T, 8, 4, 4>()) != cudaSuccess) e = r;
+  }
   return e;
 }
 
@@ -352,6 +358,20 @@ void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream
     case 4: launch_bulk<T, 16, 8, 2>(pl, A, st); break;
     case 6: launch_bulk<T, 16, 4, 2>(pl, A, st); break;
     case 7: launch_bulk<T, 8, 4, 2>(pl, A, st); break;
+    case 8:
+      if constexpr (sizeof(T) == 4) {
+        launch_bulk<T, 16, 4, 3>(pl, A, st);
+        break;
+      }
+      launch_bulk<T, 16, 4, 2>(pl, A, st);
+      break;
+    case 9:
+      if constexpr (sizeof(T) == 4) {
+        launch_bulk<T, 8, 4, 4>(pl, A, st);
+        break;
+      }
+      launch_bulk<T, 8, 4, 2>(pl, A, st);
+      break;
     default: launch_bulk<T, 16, 16, 1>(pl, A, st);
   }
 }
@@ -782,6 +802,7 @@ int covgpu_plan_execute(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_
   if (layout < COVGPU_DENSE || layout > COVGPU_COMPACT) return fail(COVGPU_EINVAL, "unknown layout");
   CUDA_TRY(cudaSetDevice(pl->device));
   cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(pl->exec_mu);
   if (pl->dtype == COVGPU_C128) return launch_all<double>(pl, A_dev, R_dev, layout, scale, st);
   return launch_all<float>(pl, A_dev, R_dev, layout, scale, st);
 }
@@ -829,9 +850,10 @@ static int cached_plan(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     *out = it->second;
     return COVGPU_OK;
   }
-  if (g_cache.size() >= 16) {
-    for (auto& kv : g_cache) covgpu_plan_destroy(kv.second);
-    g_cache.clear();
+  if (g_cache.size() >= 32) {  // evict one entry (cudaFree waits for its in-flight work)
+    auto victim = g_cache.begin();
+    covgpu_plan_destroy(victim->second);
+    g_cache.erase(victim);
   }
   int rc = covgpu_plan_create(out, device, batch, n, m, p, q, dtype, ids, nids);
   if (rc) return rc;
