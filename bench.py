@@ -218,7 +218,7 @@ def main() -> None:
     tdt = torch.complex128 if w.dtype == "c128" else torch.complex64
     ids = None
     if world > 1:
-        ids = partition_classes(w.n, w.m, win, world)[rank]
+        ids = partition_classes(w.n, w.m, win, world, fp64=(w.dtype == "c128"))[rank]
     plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, class_ids=ids, device=dev)
     layout = args.layout if world == 1 else "compact"
     host_a = make_input(w) if rank == 0 else None
@@ -231,9 +231,11 @@ def main() -> None:
     # roofline denominator: FMA pipe measured on this GPU (not in MEASURED_PEAKS.json)
     peak = probe_fma_peak(local, fp64=(w.dtype == "c128"), seconds=1.5)
 
+    a_real = torch.view_as_real(a)  # collectives on the real view (no complex dtypes in NCCL)
+
     def step():
         if world > 1:
-            dist.broadcast(a, src=0)
+            dist.broadcast(a_real, src=0)
         plan.execute(a, out, layout)
 
     for _ in range(max(args.warmup, 0)):

@@ -3,9 +3,10 @@
 // k_finalize_v (default, P <= 128): lanes own diagonal positions v; the warp
 // walks u = 0 .. qu-1 carrying every edge row's full_i(u) in registers
 // (full_i(u+1) = full_i(u) - pL_i[u] + pR_i[u]) and G(u) (G(u+1) = G(u) -
-// CColL[u] + CColR[u]); at each u the whole column of slots is
-//   S(v,u) = G(u) + suffix_{i>=v} fullT_i(u) + prefix_{t<v} fullB_t(u),
-// two segmented warp scans.  Classes with pv <= 16 pack 32/W snapshots per
+// CColL[u] + CColR[u]); at each u the whole column of slots follows the
+// diagonal-segment recurrence S(0,u) = G(u) + sum_i fullT_i(u),
+// S(v+1,u) = S(v,u) - fullT_v(u) + fullB_v(u): one segmented warp scan plus
+// one reduction per column.  Classes with pv <= 16 pack 32/W snapshots per
 // warp (W = pow2ceil(pv)-lane segments).  Corner reads come from the
 // transposed corner blocks (k_corners), so lanes read consecutive addresses.
 //
@@ -121,11 +122,11 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   for (int j = li; j < ac; j += W) acc = cadd(acc, cl[j]);
   double2 G = seg_sum(acc, W);
 
-  // edge-row state: lane owns v = li + k*W
+  // edge-row state: lane owns the contiguous rows v = li*KR + k
   double2 fT[KR], fB[KR];
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
-    const int v = li + k * W;
+    const int v = li * KR + k;
     fT[k] = fB[k] = make_double2(0.0, 0.0);
     if (v < ar) {
       for (int g = 0; g < nseg; ++g) {
@@ -137,28 +138,24 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const bool zero_im = (c.d == 0);
   const long long rb = (long long)b * r_bstride;
   for (int u = 0; u < qu; ++u) {
-    double2 sufT[KR], preB[KR];
-    double2 carry = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int k = KR - 1; k >= 0; --k) {
-      double2 tot;
-      const double2 s = seg_suffix_incl(fT[k], li, W, &tot);
-      sufT[k] = cadd(s, carry);
-      carry = cadd(carry, tot);
-    }
-    carry = make_double2(0.0, 0.0);
+    // the diagonal-segment walk along v:  S(0) = G + sum_i fullT_i,
+    // S(v+1) = S(v) - fullT_v + fullB_v  (drop the leaving edge row, add the
+    // entering one) — one exclusive scan of (fB - fT) plus one reduction of fT
+    double2 d[KR], tsum = make_double2(0.0, 0.0), run = make_double2(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
-      double2 tot;
-      const double2 s = seg_prefix_excl(fB[k], li, W, &tot);
-      preB[k] = cadd(s, carry);
-      carry = cadd(carry, tot);
+      d[k] = run;  // in-lane exclusive prefix
+      run = cadd(run, csub(fB[k], fT[k]));
+      tsum = cadd(tsum, fT[k]);
     }
+    double2 tot;
+    const double2 base = seg_prefix_excl(run, li, W, &tot);
+    const double2 s0 = cadd(G, seg_sum(tsum, W));
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
-      const int v = li + k * W;
+      const int v = li * KR + k;
       if (active && v < pv) {
-        const double2 sv = cadd(G, cadd(sufT[k], preB[k]));
+        const double2 sv = cadd(s0, cadd(base, d[k]));
         // compact slot (u-major, then v): lanes write consecutive addresses;
         // k_expand turns it into the dense / packed layout with coalesced stores
         C2 val;
@@ -175,7 +172,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
       const C2* BR = Cb + 3 * cstride;
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
-        const int v = li + k * W;
+        const int v = li * KR + k;
         if (v < ar) {
           const long long o1 = (long long)u * Sx + v + c.s1;
           const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
