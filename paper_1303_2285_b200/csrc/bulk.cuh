@@ -336,7 +336,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   if (w == NW) {  // producer warp: keep the ring full
     if (lane == 0) {
       for (int k = 0; k < total; ++k) {
-        if (k >= S) mbar_wait(&empty[k % S], ((k - S) / S) & 1);
+        if (k >= S) mbar_wait_sleep(&empty[k % S], ((k - S) / S) & 1);
         issue(k);
       }
     }

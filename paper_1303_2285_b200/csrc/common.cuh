@@ -173,6 +173,15 @@ __device__ inline void mbar_wait(uint64_t* bar, unsigned parity) {
   while (!mbar_try(bar, parity)) {
   }
 }
+// waiting loop for a warp that is usually early (the TMA producer): back off
+// so its polling does not take issue slots from the compute warps
+__device__ inline void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+  unsigned ns = 32;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 512 ? ns * 2 : 512;
+  }
+}
 // 3-D tensor tile -> SMEM, completion counted on `bar` (bytes)
 __device__ inline void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(

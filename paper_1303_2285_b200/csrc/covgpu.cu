@@ -379,7 +379,8 @@ void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream
 template <typename T, int D>
 void launch_edge(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   const Problem& pr = pl->pr;
-  if (pl->edge_tma && ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0)) {
+  if (pl->edge_tma && ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0) &&
+      EdgeCfg<T, D>::stages(pl->S, pl->r2g) >= 2) {
     using Cfg = EdgeCfg<T, D>;
     if (pl->etmap_ptr != (const void*)A) {
       CUtensorMap mx, my;

@@ -131,7 +131,15 @@ struct EdgeCfg {
   // TMA destinations must be 128-byte aligned: Y starts at xoff
   __host__ __device__ static size_t xoff(int S) { return (xbytes(S) + 127) / 128 * 128; }
   __host__ __device__ static size_t stage(int S, int R2G) { return (xoff(S) + ybytes(R2G) + 127) / 128 * 128; }
-  __host__ __device__ static size_t smem(int S, int R2G) { return EDGE_STAGES * stage(S, R2G) + 8 * EDGE_STAGES; }
+  // ring depth that fits the SMEM budget (0: TMA variant unusable for this S)
+  __host__ __device__ static int stages(int S, int R2G) {
+    const size_t st = stage(S, R2G);
+    const int n = (int)((200 * 1024 - 8 * EDGE_STAGES) / st);
+    return n < 2 ? 0 : (n > EDGE_STAGES ? EDGE_STAGES : n);
+  }
+  __host__ __device__ static size_t smem(int S, int R2G) {
+    return stages(S, R2G) * stage(S, R2G) + 8 * EDGE_STAGES;
+  }
 };
 
 template <typename T, int D>
@@ -146,7 +154,8 @@ __global__ void __launch_bounds__((EDGE_WARPS + 1) * 32, 1)
   extern __shared__ __align__(128) unsigned char esm[];
   const size_t xb = Cfg::xbytes(S), yb = Cfg::ybytes(R2G), sb = Cfg::stage(S, R2G);
   const size_t xo = Cfg::xoff(S);
-  uint64_t* full = reinterpret_cast<uint64_t*>(esm + EDGE_STAGES * sb);
+  const int NS = Cfg::stages(S, R2G);
+  uint64_t* full = reinterpret_cast<uint64_t*>(esm + Cfg::stages(S, R2G) * sb);
   long long t = blockIdx.x;
   const int seg = (int)(t % nseg);
   t /= nseg;
@@ -195,13 +204,13 @@ __global__ void __launch_bounds__((EDGE_WARPS + 1) * 32, 1)
     return;
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < EDGE_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_mbarrier_init();
   }
   __syncthreads();
   __shared__ uint64_t emptyb[EDGE_STAGES];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < EDGE_STAGES; ++s) mbar_init(&emptyb[s], EDGE_WARPS);
+    for (int s = 0; s < NS; ++s) mbar_init(&emptyb[s], EDGE_WARPS);
     fence_mbarrier_init();
   }
   __syncthreads();
@@ -209,8 +218,8 @@ __global__ void __launch_bounds__((EDGE_WARPS + 1) * 32, 1)
   if (w == EDGE_WARPS) {  // producer
     if (lane == 0) {
       for (int k = 0; k < nchunks; ++k) {
-        const int s = k % EDGE_STAGES;
-        if (k >= EDGE_STAGES) mbar_wait(&emptyb[s], ((k - EDGE_STAGES) / EDGE_STAGES) & 1);
+        const int s = k % NS;
+        if (k >= NS) mbar_wait_sleep(&emptyb[s], ((k - NS) / NS) & 1);
         const int c0 = cs + k * CW;
         unsigned char* st = esm + s * sb;
         mbar_expect_tx(&full[s], (unsigned)(xb + yb));
@@ -225,8 +234,8 @@ __global__ void __launch_bounds__((EDGE_WARPS + 1) * 32, 1)
 #pragma unroll
   for (int d = 0; d < D; ++d) ar[d] = ai[d] = yr[d] = yi[d] = (T)0;
   for (int k = 0; k < nchunks; ++k) {
-    const int s = k % EDGE_STAGES;
-    mbar_wait(&full[s], (k / EDGE_STAGES) & 1);
+    const int s = k % NS;
+    mbar_wait(&full[s], (k / NS) & 1);
     const C2* X = reinterpret_cast<const C2*>(esm + s * sb) + r1l * XW;
     const C2* Y = reinterpret_cast<const C2*>(esm + s * sb + xo) + r2l * YW;
     if (valid) {

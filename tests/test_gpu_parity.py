@@ -370,3 +370,51 @@ def test_exact_algebraic_properties(cuda):
     cnt_c = (torch.minimum(cj, torch.tensor(m - q, device=cuda)) - torch.clamp(cj - q + 1, min=0) + 1)
     tr = ((a.abs() ** 2) * cnt_r[:, None] * cnt_c[None, :]).sum() / w.k
     assert abs(r.diagonal().real.sum().item() - tr.item()) <= 1e-12 * tr.item()
+
+
+@pytest.mark.parametrize("n,m,p,q,batch,dt", [
+    (300, 20, 130, 2, 1, np.complex128),    # P > 128: warp-per-class finalize
+    (70, 66, 20, 9, 3, np.complex128),      # TMA edge kernel (strip >= 16) with batch
+    (70, 66, 20, 9, 5, np.complex64),       # same, FP32, even M (TMA bulk)
+    (61, 45, 17, 6, 2, np.complex64),       # odd M complex64: cp.async bulk, generic edge
+    (40, 37, 25, 7, 3, np.complex128),      # unclean rows (N < 2P-2): SAT path with batch
+    (33, 90, 4, 50, 2, np.complex128),      # unclean columns (M < 2Q-2)
+    (50, 50, 1, 1, 4, np.complex128),       # 1x1 window
+])
+def test_paths_batched_vs_oracle(cuda, n, m, p, q, batch, dt):
+    rng = np.random.default_rng(n * 7 + m * 13 + p + q)
+    stack = (rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m))).astype(dt)
+    got = estimate_batch_tensor(stack, WindowSpec(p, q)).cpu().numpy()
+    tol = TOL64 if dt == np.complex128 else TOL32
+    for b in range(batch):
+        assert_hermitian(got[b])
+        ref = co.covariance(stack[b].astype(np.complex128), p, q)
+        assert co.rel_frobenius(got[b].astype(np.complex128), ref) <= tol, b
+
+
+def test_batched_layouts_and_subsets(cuda):
+    """packed / compact layouts and class subsets with batch > 1 agree bit for
+    bit with the dense result."""
+    from paper_1303_2285_b200 import _native
+    from paper_1303_2285_b200.engine import _run
+    from paper_1303_2285_b200.partition import partition_classes
+
+    rng = np.random.default_rng(5)
+    stack = torch.as_tensor(rng.standard_normal((3, 64, 48)) + 1j * rng.standard_normal((3, 64, 48)),
+                            device=cuda)
+    win = WindowSpec(18, 7)
+    dense = _run(stack, win)
+    packed = _run(stack, win, layout=_native.PACKED)
+    r, c = torch.triu_indices(win.stack_size, win.stack_size, device=cuda)
+    assert torch.equal(packed, dense[:, r, c])
+    acc = torch.zeros_like(dense)
+    for ids in partition_classes(64, 48, win, 3):
+        acc += _run(stack, win, class_ids=ids)
+    assert torch.equal(acc, dense)
+
+
+def test_capacity_guard(cuda):
+    """Packed triangle beyond 2^31-1 entries is refused before any allocation
+    (core.py:147-151)."""
+    with pytest.raises(ValueError):
+        estimate_tensor(torch.zeros((1, 65536), dtype=torch.complex128, device=cuda), WindowSpec(1, 65536))
