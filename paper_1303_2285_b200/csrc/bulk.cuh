@@ -217,6 +217,25 @@ __device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int n
     if (!(g.valid & (1u << e))) continue;  // warp-uniform
     const int cid = cls_slot[class_index(g.dr0 + e, g.dc, P, Q)];
     double2 v = make_double2((double)ar[e], (double)ai[e]);
+    if constexpr (sizeof(T) == 4) {
+      // FP32: the 32-lane butterfly in FP32 (half the shuffles of FP64)
+      float sr = (lane_ok && core) ? (float)ar[e] : 0.f, si = (lane_ok && core) ? (float)ai[e] : 0.f;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, off);
+        si += __shfl_xor_sync(0xffffffffu, si, off);
+      }
+      if (lane_ok && !core) {
+        const ClassDesc& cd = cls[cid];
+        const int ac = cd.qu - 1;
+        const long long idx = c1 < left_end ? c1 : (long long)ac + (c1 - right_beg);
+        ccol[((long long)g.b * tot_ccol + cd.ccol_off + idx) * nrs + g.rs] = v;
+      }
+      if (lane == 0)
+        ccpart[((long long)g.b * nclasses + cid) * ncb * nrs + g.cb * nrs + g.rs] =
+            make_double2((double)sr, (double)si);
+      continue;
+    }
     if (lane_ok && !core) {
       const ClassDesc& cd = cls[cid];
       const int ac = cd.qu - 1;

@@ -179,7 +179,7 @@ __device__ inline void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
   unsigned ns = 32;
   while (!mbar_try(bar, parity)) {
     __nanosleep(ns);
-    ns = ns < 512 ? ns * 2 : 512;
+    ns = ns < 2048 ? ns * 2 : 2048;
   }
 }
 // 3-D tensor tile -> SMEM, completion counted on `bar` (bytes)
