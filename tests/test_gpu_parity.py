@@ -445,3 +445,24 @@ def test_random_shapes_fuzz(cuda):
             worst[dt] = max(worst[dt], err)
             assert err <= (TOL64 if dt == np.complex128 else TOL32), (it, n, m, p, q, batch, dt, err)
     print(f"fuzz worst relF: c128 {worst[np.complex128]:.2e}, c64 {worst[np.complex64]:.2e}")
+
+
+def test_integration_md_option_a(cuda, golden):
+    """The ctypes binding shown in INTEGRATION.md (Option A): host buffers,
+    scale 1.0 -> the reference's own unnormalised packed triangle."""
+    import ctypes
+
+    from paper_1303_2285_b200 import _native
+
+    lib = ctypes.CDLL(str(_native.lib_path()))
+    lib.covgpu_estimate_host.argtypes = [
+        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
+        ctypes.c_int]
+    a = np.ascontiguousarray(make_input("cfg1"), dtype=np.complex128)
+    out = np.zeros(16 * 17 // 2, dtype=np.complex128)
+    rc = lib.covgpu_estimate_host(a.ctypes.data, 1, 32, 32, 4, 4, 0, 1, 1.0, out.ctypes.data, 0)
+    assert rc == 0
+    assert co.rel_frobenius(out, golden["cfg1_packed"]) <= 1e-13
+    bad = lib.covgpu_estimate_host(a.ctypes.data, 1, 32, 32, 40, 4, 0, 1, 1.0, out.ctypes.data, 0)
+    assert bad == -1  # COVGPU_EINVAL -> ValueError in the binding
