@@ -135,6 +135,15 @@ struct covgpu_plan {
   size_t hA_bytes = 0, hR_bytes = 0;
   std::mutex host_mu;
   std::mutex exec_mu;  // executes mutate plan state (tensor-map cache, timing events)
+  // pipelined host path for batches: sub-batch plans, streams and buffers
+  static constexpr int kPipeSlots = 3;
+  covgpu_plan* pipe[kPipeSlots] = {};
+  covgpu_plan* pipe_tail = nullptr;
+  long long pipe_sub = 0, pipe_tail_b = 0;
+  cudaStream_t pipe_stream[kPipeSlots] = {};
+  void* pipe_A[kPipeSlots] = {};
+  void* pipe_R[kPipeSlots] = {};
+  size_t pipe_Ab = 0, pipe_Rb = 0;
 };
 
 namespace {
@@ -169,7 +178,31 @@ int dalloc(X** p, size_t count, long long* acc) {
   return COVGPU_OK;
 }
 
+void plan_free(covgpu_plan* pl);
+void plan_free_pipe(covgpu_plan* pl) {
+  for (int k = 0; k < covgpu_plan::kPipeSlots; ++k) {
+    if (pl->pipe[k]) {
+      plan_free(pl->pipe[k]);
+      delete pl->pipe[k];
+      pl->pipe[k] = nullptr;
+    }
+    if (pl->pipe_stream[k]) cudaStreamDestroy(pl->pipe_stream[k]);
+    pl->pipe_stream[k] = nullptr;
+    cudaFree(pl->pipe_A[k]);
+    cudaFree(pl->pipe_R[k]);
+    pl->pipe_A[k] = pl->pipe_R[k] = nullptr;
+  }
+  if (pl->pipe_tail) {
+    plan_free(pl->pipe_tail);
+    delete pl->pipe_tail;
+    pl->pipe_tail = nullptr;
+  }
+  pl->pipe_sub = pl->pipe_tail_b = 0;
+  pl->pipe_Ab = pl->pipe_Rb = 0;
+}
+
 void plan_free(covgpu_plan* pl) {
+  plan_free_pipe(pl);
   for (auto& e : pl->ev)
     if (e) cudaEventDestroy(e);
   if (pl->host_stream) cudaStreamDestroy(pl->host_stream);
@@ -928,6 +961,81 @@ int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tfl
   return COVGPU_OK;
 }
 
+// Batched host path: the batch is cut into sub-batches that flow through
+// kPipeSlots streams, so the H2D of one sub-batch, the kernels of another and
+// the D2H of a third overlap (full-duplex PCIe copy engines + SMs).  Each
+// slot owns its sub-batch plan (workspaces are per plan) and device buffers.
+static int execute_host_pipelined(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
+                                  double scale) {
+  const Problem& pr = pl->pr;
+  const size_t esz = pl->dtype == COVGPU_C128 ? 16 : 8;
+  const long long B = pl->batch;
+  const long long nch = std::min<long long>(16, B);
+  const long long sub = (B + nch - 1) / nch;
+  const long long tail = B - (B - 1) / sub * sub;  // size of the last sub-batch
+  long long r_per_b;
+  if (layout == COVGPU_DENSE)
+    r_per_b = (long long)pr.PQ * pr.PQ;
+  else if (layout == COVGPU_PACKED)
+    r_per_b = (long long)pr.PQ * (pr.PQ + 1) / 2;
+  else
+    r_per_b = pl->compact_elems;
+  const size_t a_per_b = (size_t)pr.N * pr.M * esz;
+  std::vector<int32_t> ids;
+  for (const auto& c : pl->h_cls) ids.push_back(c.uc);
+  const bool all = (long long)ids.size() == covgpu_num_classes(pr.P, pr.Q);
+  auto make = [&](covgpu_plan** dst, long long nb) -> int {
+    return covgpu_plan_create(dst, pl->device, nb, pr.N, pr.M, pr.P, pr.Q, pl->dtype,
+                              all ? nullptr : ids.data(), all ? 0 : (int32_t)ids.size());
+  };
+  if (pl->pipe_sub != sub || (tail != sub && pl->pipe_tail_b != tail)) {
+    plan_free_pipe(pl);
+    for (int k = 0; k < covgpu_plan::kPipeSlots; ++k) {
+      int rc = make(&pl->pipe[k], sub);
+      if (rc) return rc;
+      CUDA_TRY(cudaStreamCreateWithFlags(&pl->pipe_stream[k], cudaStreamNonBlocking));
+    }
+    if (tail != sub) {
+      int rc = make(&pl->pipe_tail, tail);
+      if (rc) return rc;
+    }
+    pl->pipe_sub = sub;
+    pl->pipe_tail_b = tail;
+  }
+  const size_t ab = (size_t)sub * a_per_b, rb = (size_t)sub * r_per_b * esz;
+  if (pl->pipe_Ab < ab || pl->pipe_Rb < rb) {
+    for (int k = 0; k < covgpu_plan::kPipeSlots; ++k) {
+      cudaFree(pl->pipe_A[k]);
+      cudaFree(pl->pipe_R[k]);
+      pl->pipe_A[k] = pl->pipe_R[k] = nullptr;
+    }
+    pl->pipe_Ab = pl->pipe_Rb = 0;
+    for (int k = 0; k < covgpu_plan::kPipeSlots; ++k) {
+      CUDA_TRY(cudaMalloc(&pl->pipe_A[k], ab));
+      CUDA_TRY(cudaMalloc(&pl->pipe_R[k], rb));
+    }
+    pl->pipe_Ab = ab;
+    pl->pipe_Rb = rb;
+  }
+  const char* ah = static_cast<const char*>(A_host);
+  char* rh = static_cast<char*>(R_host);
+  int c = 0;
+  for (long long b0 = 0; b0 < B; b0 += sub, ++c) {
+    const long long nb = std::min(sub, B - b0);
+    const int k = c % covgpu_plan::kPipeSlots;
+    covgpu_plan* sp = nb == sub ? pl->pipe[k] : pl->pipe_tail;
+    cudaStream_t st = pl->pipe_stream[k];
+    CUDA_TRY(cudaMemcpyAsync(pl->pipe_A[k], ah + (size_t)b0 * a_per_b, (size_t)nb * a_per_b,
+                             cudaMemcpyHostToDevice, st));
+    const int rc = covgpu_plan_execute(sp, pl->pipe_A[k], pl->pipe_R[k], layout, scale, st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(rh + (size_t)b0 * r_per_b * esz, pl->pipe_R[k],
+                             (size_t)nb * r_per_b * esz, cudaMemcpyDeviceToHost, st));
+  }
+  for (int k = 0; k < covgpu_plan::kPipeSlots; ++k) CUDA_TRY(cudaStreamSynchronize(pl->pipe_stream[k]));
+  return COVGPU_OK;
+}
+
 int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
                              double scale) {
   if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
@@ -946,6 +1054,7 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
     r_elems = pl->batch * pl->compact_elems;
   const size_t r_bytes = (size_t)r_elems * esz;
   std::lock_guard<std::mutex> lk(pl->host_mu);
+  if (pl->batch >= 8) return execute_host_pipelined(pl, A_host, R_host, layout, scale);
   if (!pl->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->host_stream, cudaStreamNonBlocking));
   if (pl->hA_bytes < a_bytes) {
     cudaFree(pl->hA);
