@@ -83,6 +83,7 @@ struct covgpu_plan {
   int NW = 8;         // column lags (warps) per bulk CTA
   int bulk_variant = 0;
   bool use_tma = true;          // COVGPU_NO_TMA=1 forces the cp.async bulk kernel
+  bool no_direct = false;       // COVGPU_NO_DIRECT=1: always finalize via compact + expand
   bool used_tma = false;
   const void* tmap_ptr = nullptr;  // A the cached tensor maps describe
   CUtensorMap tmx{}, tmy{};
@@ -529,19 +530,34 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     const unsigned blocks = (unsigned)((pl->ntasks + FIN_WARPS - 1) / FIN_WARPS);
     // finalize into the compact layout (R itself, or the plan's scratch),
     // then expand to dense / packed with coalesced stores
-    C2* cdst = layout == COVGPU_COMPACT ? R : (C2*)pl->d_slots;
-#define FINV(KR)                                                                                 \
-  k_finalize_v<T, KR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                       \
+    // dense R small enough to stay in L2: write it directly from the walk (the
+    // scattered diagonal stores merge in L2); otherwise finalize into the
+    // compact layout and expand with coalesced stores
+    const double dense_bytes = (double)B * pr.PQ * pr.PQ * sizeof(C2);
+    const bool direct = layout == COVGPU_DENSE && dense_bytes <= 48.0 * (1 << 20) && pr.P >= 16 &&
+                        !pl->no_direct;
+    C2* cdst = (layout == COVGPU_COMPACT || direct) ? R : (C2*)pl->d_slots;
+    const long long rstride = direct ? (long long)pr.PQ * pr.PQ : pl->compact_elems;
+#define FINV(KR, DIR)                                                                           \
+  k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                 \
       (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses,           \
       pl->ncb * pl->nrs, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
-      pl->nseg, cdst, pl->compact_elems, scale)
-    switch (pl->fin_kr) {
-      case 1: FINV(1); break;
-      case 2: FINV(2); break;
-      default: FINV(4);
+      pl->nseg, cdst, rstride, scale)
+    if (direct) {
+      switch (pl->fin_kr) {
+        case 1: FINV(1, true); break;
+        case 2: FINV(2, true); break;
+        default: FINV(4, true);
+      }
+    } else {
+      switch (pl->fin_kr) {
+        case 1: FINV(1, false); break;
+        case 2: FINV(2, false); break;
+        default: FINV(4, false);
+      }
     }
 #undef FINV
-    if (layout != COVGPU_COMPACT) {
+    if (layout != COVGPU_COMPACT && !direct) {
       ++launches;
       mark();
       const long long per = layout == COVGPU_DENSE ? (long long)pr.PQ * pr.PQ
@@ -661,6 +677,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const int v = pick_bulk_variant(n, m, p, q, batch, dtype);
     pl->bulk_variant = v;
     if (const char* nt = getenv("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
+    if (const char* nd = getenv("COVGPU_NO_DIRECT")) pl->no_direct = atoi(nd) != 0;
     pl->E = kBulkVariants[v].E;
     pl->NW = kBulkVariants[v].NW;
   }

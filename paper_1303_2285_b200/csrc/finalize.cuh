@@ -86,7 +86,7 @@ __device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* tot
 }
 
 // task = (class, snapshot group); W = min(32, pow2ceil(pv)) lanes per snapshot
-template <typename T, int KR>
+template <typename T, int KR, bool DIRECT>
 __global__ void __launch_bounds__(FIN_WARPS * 32)
     k_finalize_v(const typename CT<T>::c* __restrict__ corners, Problem pr,
                  const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
@@ -156,12 +156,18 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
       const int v = li * KR + k;
       if (active && v < pv) {
         const double2 sv = cadd(s0, cadd(base, d[k]));
-        // compact slot (u-major, then v): lanes write consecutive addresses;
-        // k_expand turns it into the dense / packed layout with coalesced stores
-        C2 val;
-        val.x = (T)(sv.x * scale);
-        val.y = (T)(zero_im ? 0.0 : sv.y * scale);
-        R[rb + c.slot_off + (long long)u * pv + v] = val;
+        if constexpr (DIRECT) {
+          // dense R straight from the walk (16-byte elements: the scattered
+          // diagonal stores merge in L2 well enough to beat a separate expand)
+          write_slot<T>(R, COVGPU_DENSE, rb, c, pr, v, u, sv.x * scale, zero_im ? 0.0 : sv.y * scale);
+        } else {
+          // compact slot (u-major, then v): lanes write consecutive addresses;
+          // k_expand turns it into the dense / packed layout with coalesced stores
+          C2 val;
+          val.x = (T)(sv.x * scale);
+          val.y = (T)(zero_im ? 0.0 : sv.y * scale);
+          R[rb + c.slot_off + (long long)u * pv + v] = val;
+        }
       }
     }
     if (u < ac) {
