@@ -44,18 +44,23 @@ L2_FLUSH_BYTES = 256 << 20
 
 
 def products(w):
-    """(UM, bulk-kernel products, edge-row products, corner products) per snapshot."""
+    """(UM, bulk-kernel products, edge-row products, corner products,
+    core products) per snapshot.  bulk = core rows x all columns (the
+    CUDA-core bulk kernel); core = core rows x core columns (the tensor-core
+    kernel; the edge columns then come from the CUDA-core kernel)."""
     from paper_1303_2285_b200.combinations import um_count, unique_combinations
     from paper_1303_2285_b200.core import WindowSpec
 
     n, m, p, q = w.n, w.m, w.p, w.q
-    bulk = edge = corner = 0
+    bulk = edge = corner = core = 0
     for c in unique_combinations(WindowSpec(p, q)):
         ar, ac = p - abs(c.dr) - 1, q - c.dc - 1
-        bulk += (n - 2 * p + 2 + abs(c.dr)) * (m - c.dc)
+        rows = n - 2 * p + 2 + abs(c.dr)
+        bulk += rows * (m - c.dc)
+        core += rows * (m - 2 * q + 2 + c.dc)
         edge += 2 * ar * (m - 2 * q + 2 + c.dc)
         corner += 4 * ar * ac
-    return um_count(n, m, p, q), bulk, edge, corner
+    return um_count(n, m, p, q), bulk, edge, corner, core
 
 
 def cpu_reference(w, budget_s: float, seed: int = 0):
@@ -205,7 +210,7 @@ def main() -> None:
 
     from paper_1303_2285_b200.core import WindowSpec
     from paper_1303_2285_b200.partition import partition_classes, shard_cost
-    from paper_1303_2285_b200.plan import Plan, probe_fma_peak
+    from paper_1303_2285_b200.plan import Plan, probe_dmma_peak, probe_fma_peak
     from paper_1303_2285_b200.workloads import make_input, workload
 
     torch.cuda.set_device(local)
@@ -228,8 +233,10 @@ def main() -> None:
     out = plan.alloc_output(layout)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
-    # roofline denominator: FMA pipe measured on this GPU (not in MEASURED_PEAKS.json)
+    # roofline denominators: FMA pipe / FP64 tensor cores measured on this GPU
+    # (MEASURED_PEAKS.json carries only bf16 and HBM)
     peak = probe_fma_peak(local, fp64=(w.dtype == "c128"), seconds=1.5)
+    peak_dmma = probe_dmma_peak(local, seconds=1.0) if w.dtype == "c128" else None
 
     a_real = torch.view_as_real(a)  # collectives on the real view (no complex dtypes in NCCL)
 
@@ -271,24 +278,42 @@ def main() -> None:
         torch.cuda.synchronize(dev)
         plan.execute(a, out, layout)
         kern.append(plan.kernel_times())
+    knames = plan.kernel_names()
     plan.set_timing(False)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item()) / args.steps
 
-    um, bulk_p, edge_p, corner_p = products(w)
+    um, bulk_p, edge_p, corner_p, core_p = products(w)
     entries = float(w.pq) ** 2 * w.batch
     value = entries / (ms * 1e-3)
     flops = 8.0 * um * w.batch
     kt = np.array(kern) if kern and all(len(k) == len(kern[0]) for k in kern) else None
     kernel_ms = {}
     if kt is not None and kt.size:
-        for name, col in zip(["bulk", "edge_rows", "finalize", "expand"], kt.mean(axis=0)):
+        for name, col in zip(knames, kt.mean(axis=0)):
             kernel_ms[name] = float(col)
     shard_frac = 1.0 if ids is None else shard_cost(w.n, w.m, win, ids) / um
     roof = None
-    if "bulk" in kernel_ms and kernel_ms["bulk"] > 0:
+    if kernel_ms.get("bulk_dmma", 0) > 0:
+        # dominant kernel on the FP64 tensor cores: core products x 8 flops
+        achieved = 8.0 * core_p * w.batch / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12
+        traffic = None
+        prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
+        if prof.exists():
+            try:
+                traffic = json.loads(prof.read_text()).get("bulk_dmma_dram_bytes_per_launch")
+            except (ValueError, OSError):
+                traffic = None
+        roof = {"bound": "fp64-tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
+                "frac": achieved / peak_dmma, "traffic": traffic, "kernel": "k_bulk_dmma",
+                "peak_source": "DMMA-loop probe (mma.sync m8n8k4 f64) measured on this GPU in this "
+                "run (MEASURED_PEAKS.json has no FP64 figure)",
+                "algorithmic_flops_per_launch": 8.0 * core_p * w.batch,
+                "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
+                "fma_loop_peak": peak}
+    elif "bulk" in kernel_ms and kernel_ms["bulk"] > 0:
         achieved = 8.0 * bulk_p * w.batch * shard_frac / (kernel_ms["bulk"] * 1e-3) / 1e12
         traffic = None
         prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"

@@ -100,6 +100,11 @@ int covgpu_plan_set_timing(covgpu_plan_t plan, int32_t enable);
  * (bulk, edge rows, finalize); waits for it.  Returns the count written. */
 int32_t covgpu_plan_kernel_times(covgpu_plan_t plan, float* ms, int32_t max_n);
 
+/* Comma-separated kernel names of those intervals ("bulk_dmma,edge_cols,
+ * edge_rows,finalize,expand" or "bulk,edge_rows,finalize,expand" ...) into
+ * buf (NUL-terminated, truncated to len).  Returns the count. */
+int32_t covgpu_plan_kernel_names(covgpu_plan_t plan, char* buf, int32_t len);
+
 int covgpu_plan_destroy(covgpu_plan_t plan);
 
 /* One-shot estimate on device buffers (plan cached per shape internally). */
@@ -123,6 +128,10 @@ int covgpu_plan_execute_host(covgpu_plan_t plan, const void* A_host, void* R_hos
  * throughput in TFLOP/s, measured for about `seconds` on `device` — the
  * roofline denominator of the covariance kernels. */
 int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tflops);
+
+/* Bench utility: FP64 tensor-core (DMMA) throughput in TFLOP/s — the
+ * roofline denominator of the tensor-core bulk kernel (complex128). */
+int covgpu_probe_dmma_peak(int device, double seconds, double* tflops);
 
 /* Bulk-kernel work unit of a shape: `lags` row lags x `warps` column lags
  * per CTA.  The partitioner shards classes in whole units. */

@@ -50,6 +50,7 @@ _SIGS = {
     "covgpu_plan_launches": (_i32, [_vp]),
     "covgpu_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
     "covgpu_plan_kernel_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), _i32]),
+    "covgpu_plan_kernel_names": (_i32, [_vp, ctypes.c_char_p, _i32]),
     "covgpu_plan_destroy": (ctypes.c_int, [_vp]),
     "covgpu_estimate": (
         ctypes.c_int,
@@ -61,6 +62,7 @@ _SIGS = {
     ),
     "covgpu_plan_execute_host": (ctypes.c_int, [_vp, _vp, _vp, _i32, _dbl]),
     "covgpu_probe_fma_peak": (ctypes.c_int, [ctypes.c_int, _i32, _dbl, ctypes.POINTER(_dbl)]),
+    "covgpu_probe_dmma_peak": (ctypes.c_int, [ctypes.c_int, _dbl, ctypes.POINTER(_dbl)]),
     "covgpu_bulk_geometry": (ctypes.c_int, [_i64, _i64, _i64, _i32, _i32, _i32, _p32, _p32]),
     "covgpu_scatter_compact": (
         ctypes.c_int, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _p32, _i32, _vp, _vp]),

@@ -79,9 +79,12 @@ struct BulkGeom {
   unsigned valid;  // selected lags of this warp
 };
 
+// ncb_l + ncb_r > 0 (edge-only mode, next to the tensor-core core sums):
+// the grid covers only the first ncb_l and last ncb_r column blocks, the
+// blocks holding edge columns.
 template <int E, int NW, int RC>
 __device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, int ncb, int nrs,
-                                     const int* __restrict__ cls_slot) {
+                                     const int* __restrict__ cls_slot, int ncb_l = 0, int ncb_r = 0) {
   BulkGeom g;
   long long t = blockIdx.x;
   g.rs = (int)(t % nrs);  // row segment (small problems split the row walk)
@@ -120,6 +123,15 @@ __device__ inline BulkGeom bulk_geom(const Problem& pr, int n_drg, int n_dcb, in
     g.rlo = lo;
   }
   g.nchunks = g.rhi >= g.rlo ? (g.rhi - g.rlo + RC) / RC : 0;
+  if (ncb_l + ncb_r > 0) {
+    if (g.cb >= ncb_l) g.cb = (pr.M + 31) / 32 - ncb_r + (g.cb - ncb_l);
+    // skip CTAs without an edge column: left edge c1 < Q-1-dc, right edge
+    // M-Q+1 <= c1 < M-dc (widest for the CTA's smallest lag dc_base)
+    const int c0 = g.cb * 32, dcb0 = g.dc_base;
+    const bool left = c0 < Q - 1 - dcb0;
+    const bool right = c0 + 31 >= pr.M - Q + 1 && dcb0 < Q - 1;
+    if (!left && !right) g.valid = 0;
+  }
   g.col0 = g.cb * 32;
   g.ycol0 = g.col0 + g.dc_base;
   return g;
@@ -204,7 +216,7 @@ __device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int n
                                      const int* __restrict__ cls_slot,
                                      const ClassDesc* __restrict__ cls, double2* __restrict__ ccpart,
                                      double2* __restrict__ ccol, long long tot_ccol, const T* ar,
-                                     const T* ai) {
+                                     const T* ai, bool edge_only = false) {
   const int lane = threadIdx.x & 31;
   const int M = pr.M, Q = pr.Q, P = pr.P;
   const int c1 = g.col0 + lane;
@@ -217,6 +229,15 @@ __device__ inline void bulk_epilogue(const BulkGeom& g, const Problem& pr, int n
     if (!(g.valid & (1u << e))) continue;  // warp-uniform
     const int cid = cls_slot[class_index(g.dr0 + e, g.dc, P, Q)];
     double2 v = make_double2((double)ar[e], (double)ai[e]);
+    if (edge_only) {  // core sums come from the tensor-core kernel
+      if (lane_ok && !core) {
+        const ClassDesc& cd = cls[cid];
+        const int ac = cd.qu - 1;
+        const long long idx = c1 < left_end ? c1 : (long long)ac + (c1 - right_beg);
+        ccol[((long long)g.b * tot_ccol + cd.ccol_off + idx) * nrs + g.rs] = v;
+      }
+      continue;
+    }
     if constexpr (sizeof(T) == 4) {
       // FP32: the 32-lane butterfly in FP32 (half the shuffles of FP64)
       float sr = (lane_ok && core) ? (float)ar[e] : 0.f, si = (lane_ok && core) ? (float)ai[e] : 0.f;
@@ -316,7 +337,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     k_bulk_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                Problem pr, int n_drg, int n_dcb, int ncb, int nrs, int nclasses, int B, int nsnap,
                const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
-               double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol) {
+               double2* __restrict__ ccpart, double2* __restrict__ ccol, long long tot_ccol,
+               int ncb_l, int ncb_r) {
   // one CTA walks `nsnap` consecutive snapshots back to back: the TMA ring
   // keeps streaming across snapshot boundaries, accumulators and the lag
   // window restart, and the epilogue of one snapshot overlaps the next
@@ -328,7 +350,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage_bytes);
   uint64_t* empty = full + S;
-  BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, nrs, cls_slot);  // g.b = snapshot group
+  BulkGeom g = bulk_geom<E, NW, RC>(pr, n_drg, n_dcb, ncb, nrs, cls_slot, ncb_l, ncb_r);  // g.b = snapshot group
   const int b0 = g.b * nsnap;
   const int nb = min(nsnap, B - b0);
   if (!__syncthreads_or(g.valid != 0) || nb <= 0) return;  // CTA-uniform
@@ -380,7 +402,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, MINB)
     }
     if (g.valid) {  // snapshot done
       g.b = b0 + bi;
-      bulk_epilogue<T, E>(g, pr, nclasses, ncb, nrs, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai);
+      bulk_epilogue<T, E>(g, pr, nclasses, ncb, nrs, cls_slot, cls, ccpart, ccol, tot_ccol, ar, ai,
+                          ncb_l + ncb_r > 0);
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) ar[e] = ai[e] = (T)0;

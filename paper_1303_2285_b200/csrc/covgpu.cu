@@ -45,6 +45,7 @@
 #include "edge.cuh"
 #include "finalize.cuh"
 #include "general.cuh"
+#include "mma.cuh"
 #include "probe.cuh"
 
 using namespace covgpu;
@@ -86,7 +87,16 @@ struct covgpu_plan {
   bool no_direct = false;       // COVGPU_NO_DIRECT=1: always finalize via compact + expand
   bool used_tma = false;
   const void* tmap_ptr = nullptr;  // A the cached tensor maps describe
+  const void* tmap_kernel = nullptr;  // ... for this bulk kernel instance (box sizes)
   CUtensorMap tmx{}, tmy{};
+  // FP64 tensor-core core sums (mma.cuh); CUDA-core bulk then covers only
+  // the ncb_l + ncb_r column blocks that hold edge columns
+  bool use_mma = false;
+  int mma_dc = 64, n_drt = 0, n_dct = 0, mma_g = 0;
+  int ncb_l = 0, ncb_r = 0;
+  int edge_variant = 0;
+  const void* mtmap_ptr = nullptr;
+  CUtensorMap mtmx{}, mtmy{};
   // edge-row kernel TMA variant (strips of >= 16 rows)
   bool edge_tma = false;
   int r2g = 1, n_r2g = 1;
@@ -125,6 +135,7 @@ struct covgpu_plan {
   // optional per-kernel timing of the last execute (events on its stream)
   bool timing = false;
   cudaEvent_t ev[8] = {};
+  const char* ev_name[8] = {};  // kernel timed by the interval ending at ev[i]
   int nev = 0;
   // side stream for the edge-row / corner kernels (overlap with the bulk)
   cudaStream_t side_stream = nullptr;
@@ -292,13 +303,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-// A as a {2M, N, B} tensor of reals with a {bw, bh, 1} box
+// A as a {2M, N, B} tensor of reals with a {bw, bh, 1} box.  width > 0: only
+// `width` complex columns are in bounds (the rest read as zeros); col0 shifts
+// the origin to complex column col0.
 bool make_tmap(CUtensorMap* map, const void* A, bool fp64, long long B, long long N, long long M,
-               int box_w, int box_h) {
+               int box_w, int box_h, long long width = -1, long long col0 = 0) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   const cuuint64_t esz = fp64 ? 8 : 4;
-  const cuuint64_t dims[3] = {(cuuint64_t)(2 * M), (cuuint64_t)N, (cuuint64_t)B};
+  if (width <= 0) width = M;
+  A = (const char*)A + 2 * col0 * esz;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * width), (cuuint64_t)N, (cuuint64_t)B};
   const cuuint64_t strides[2] = {(cuuint64_t)(2 * M) * esz, (cuuint64_t)(2 * M * N) * esz};
   const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -334,6 +349,12 @@ cudaError_t set_attrs() {
     if ((r = cudaFuncSetAttribute(k_finalize<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       e = r;
+    if ((r = cudaFuncSetAttribute(k_bulk_dmma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)MmaCfg<32>::smem)) != cudaSuccess)
+      e = r;
+    if ((r = cudaFuncSetAttribute(k_bulk_dmma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)MmaCfg<64>::smem)) != cudaSuccess)
+      e = r;
     if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       e = r;
@@ -342,23 +363,30 @@ cudaError_t set_attrs() {
   return once;
 }
 
+// ncb_l + ncb_r > 0: edge-only mode (TMA kernel only; the caller checked
+// that the tensor maps can be made)
 template <typename T, int E, int NW, int MINB>
-void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
+void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st, int ncb_l = 0,
+                 int ncb_r = 0) {
   using Cfg = BulkCfg<T, E, NW, MINB>;
-  const long long units = (long long)pl->n_drg * pl->n_dcb * pl->ncb * pl->nrs;  // CTAs per snapshot
+  const int n_drg = (2 * pl->pr.P - 1 + E - 1) / E, n_dcb = (pl->pr.Q + NW - 1) / NW;
+  const int ncb = ncb_l + ncb_r > 0 ? ncb_l + ncb_r : pl->ncb;
+  const long long units = (long long)n_drg * n_dcb * ncb * pl->nrs;  // CTAs per snapshot
   const long long blocks = pl->batch * units;
   const Problem& pr = pl->pr;
   // TMA needs 16-byte aligned rows: always for complex128, even M for complex64
   const bool tma_ok = pl->use_tma &&
                       ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0);
   if (tma_ok) {
-    if (pl->tmap_ptr != (const void*)A) {
+    const void* kfn = (const void*)k_bulk_tma<T, E, NW, MINB>;
+    if (pl->tmap_ptr != (const void*)A || pl->tmap_kernel != kfn) {
       CUtensorMap mx, my;
       if (make_tmap(&mx, A, sizeof(T) == 8, pl->batch, pr.N, pr.M, 2 * Cfg::XW, Cfg::RC) &&
           make_tmap(&my, A, sizeof(T) == 8, pl->batch, pr.N, pr.M, 2 * Cfg::YW, Cfg::YR)) {
         pl->tmx = mx;
         pl->tmy = my;
         pl->tmap_ptr = A;
+        pl->tmap_kernel = kfn;
       } else {
         pl->tmap_ptr = nullptr;
       }
@@ -370,44 +398,72 @@ void launch_bulk(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
       nsnap = std::min<long long>(nsnap, pl->batch);
       const long long groups = (pl->batch + nsnap - 1) / nsnap;
       k_bulk_tma<T, E, NW, MINB><<<(unsigned)(groups * units), (NW + 1) * 32, Cfg::smem_tma, st>>>(
-          pl->tmx, pl->tmy, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nrs, pl->nclasses, (int)pl->batch,
-          (int)nsnap, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
+          pl->tmx, pl->tmy, pr, n_drg, n_dcb, ncb, pl->nrs, pl->nclasses, (int)pl->batch,
+          (int)nsnap, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, ncb_l, ncb_r);
       pl->used_tma = true;
       return;
     }
   }
   pl->used_tma = false;
   k_bulk<T, E, NW, MINB><<<(unsigned)blocks, NW * 32, Cfg::smem, st>>>(
-      A, pr, pl->n_drg, pl->n_dcb, pl->ncb, pl->nrs, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart,
+      A, pr, n_drg, n_dcb, ncb, pl->nrs, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart,
       pl->d_ccol, pl->tot_ccol);
 }
 
 template <typename T>
-void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
-  switch (pl->bulk_variant) {
-    case 0: launch_bulk<T, 4, 8, 2>(pl, A, st); break;
-    case 1: launch_bulk<T, 8, 8, 2>(pl, A, st); break;
-    case 2: launch_bulk<T, 16, 8, 1>(pl, A, st); break;
-    case 3: launch_bulk<T, 8, 16, 1>(pl, A, st); break;
-    case 4: launch_bulk<T, 16, 8, 2>(pl, A, st); break;
-    case 6: launch_bulk<T, 16, 4, 2>(pl, A, st); break;
-    case 7: launch_bulk<T, 8, 4, 2>(pl, A, st); break;
+void launch_bulk_variant(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st, int variant,
+                         int ncb_l = 0, int ncb_r = 0) {
+  switch (variant) {
+    case 0: launch_bulk<T, 4, 8, 2>(pl, A, st, ncb_l, ncb_r); break;
+    case 1: launch_bulk<T, 8, 8, 2>(pl, A, st, ncb_l, ncb_r); break;
+    case 2: launch_bulk<T, 16, 8, 1>(pl, A, st, ncb_l, ncb_r); break;
+    case 3: launch_bulk<T, 8, 16, 1>(pl, A, st, ncb_l, ncb_r); break;
+    case 4: launch_bulk<T, 16, 8, 2>(pl, A, st, ncb_l, ncb_r); break;
+    case 6: launch_bulk<T, 16, 4, 2>(pl, A, st, ncb_l, ncb_r); break;
+    case 7: launch_bulk<T, 8, 4, 2>(pl, A, st, ncb_l, ncb_r); break;
     case 8:
       if constexpr (sizeof(T) == 4) {
-        launch_bulk<T, 16, 4, 3>(pl, A, st);
+        launch_bulk<T, 16, 4, 3>(pl, A, st, ncb_l, ncb_r);
         break;
       }
-      launch_bulk<T, 16, 4, 2>(pl, A, st);
+      launch_bulk<T, 16, 4, 2>(pl, A, st, ncb_l, ncb_r);
       break;
     case 9:
       if constexpr (sizeof(T) == 4) {
-        launch_bulk<T, 8, 4, 4>(pl, A, st);
+        launch_bulk<T, 8, 4, 4>(pl, A, st, ncb_l, ncb_r);
         break;
       }
-      launch_bulk<T, 8, 4, 2>(pl, A, st);
+      launch_bulk<T, 8, 4, 2>(pl, A, st, ncb_l, ncb_r);
       break;
-    default: launch_bulk<T, 16, 16, 1>(pl, A, st);
+    default: launch_bulk<T, 16, 16, 1>(pl, A, st, ncb_l, ncb_r);
   }
+}
+
+// FP64 tensor-core core sums; false when the tensor maps cannot describe A
+// (the caller then runs the CUDA-core bulk over every column block)
+template <int DC>
+bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
+  using Cfg = MmaCfg<DC>;
+  const Problem& pr = pl->pr;
+  if ((uintptr_t)A % 16 != 0) return false;
+  if (pl->mtmap_ptr != (const void*)A) {
+    CUtensorMap mx, my;
+    const long long w = pr.M - pr.Q + 1;
+    if (make_tmap(&mx, A, true, pl->batch, pr.N, pr.M, 2 * MMA_XP, MMA_XR, w, 0) &&
+        make_tmap(&my, A, true, pl->batch, pr.N, pr.M, 2 * Cfg::YP, MMA_RC, w, pr.Q - 1)) {
+      pl->mtmx = mx;
+      pl->mtmy = my;
+      pl->mtmap_ptr = A;
+    } else {
+      pl->mtmap_ptr = nullptr;
+      return false;
+    }
+  }
+  const long long blocks = pl->batch * (long long)pl->n_drt * pl->n_dct * pl->mma_g;
+  k_bulk_dmma<DC><<<(unsigned)blocks, (MMA_WARPS + 1) * 32, Cfg::smem, st>>>(
+      pl->mtmx, pl->mtmy, pr, pl->n_drt, pl->n_dct, pl->mma_g, pl->nclasses, pl->d_cls_slot,
+      pl->d_ccpart);
+  return true;
 }
 
 template <typename T, int D>
@@ -489,8 +545,11 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
 
   CUDA_TRY(set_attrs());
   pl->nev = 0;
-  auto mark = [&]() {
-    if (pl->timing && pl->nev < 8) cudaEventRecord(pl->ev[pl->nev++], st);
+  auto mark = [&](const char* name) {
+    if (pl->timing && pl->nev < 8) {
+      pl->ev_name[pl->nev] = name;
+      cudaEventRecord(pl->ev[pl->nev++], st);
+    }
   };
   // The edge-row and corner kernels do not depend on the bulk kernel: run
   // them on a side stream so they fill the SMs the bulk kernel's last wave
@@ -502,10 +561,24 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(es, pl->ev_fork, 0));
   }
-  mark();
-  launch_bulk_variant<T>(pl, A, st);
+  mark("start");
+  // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
+  // bulk over every column block (which also yields the edge-column sums)
+  bool mma = false;
+  if constexpr (sizeof(T) == 8) {
+    if (pl->use_mma)
+      mma = pl->mma_dc == 32 ? launch_dmma<32>(pl, (const double2*)A, st)
+                             : launch_dmma<64>(pl, (const double2*)A, st);
+  }
+  if (!mma) launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
+  const int npart = mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
-  mark();
+  mark(mma ? "bulk_dmma" : "bulk");
+  if (mma) {  // edge-column sums: CUDA-core bulk on the edge column blocks
+    launch_bulk_variant<T>(pl, A, es, pl->edge_variant, pl->ncb_l, pl->ncb_r);
+    ++launches;
+    mark("edge_cols");
+  }
   if (pl->S > 0) {
     switch (pl->D) {
       case 4: launch_edge<T, 4>(pl, A, es); break;
@@ -513,7 +586,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       default: launch_edge<T, 16>(pl, A, es);
     }
     ++launches;
-    mark();
+    mark("edge_rows");
   }
   if (pl->fin_kr > 0) {
     const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
@@ -541,7 +614,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
 #define FINV(KR, DIR)                                                                           \
   k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                 \
       (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses,           \
-      pl->ncb * pl->nrs, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
+      npart, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
       pl->nseg, cdst, rstride, scale)
     if (direct) {
       switch (pl->fin_kr) {
@@ -559,7 +632,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
 #undef FINV
     if (layout != COVGPU_COMPACT && !direct) {
       ++launches;
-      mark();
+      mark("finalize");
       const long long per = layout == COVGPU_DENSE ? (long long)pr.PQ * pr.PQ
                                                    : (long long)pr.PQ * (pr.PQ + 1) / 2;
       const long long tot = per * B;
@@ -569,12 +642,13 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   } else {
     const long long ntasks = (long long)B * pl->nclasses;
     k_finalize<T><<<(unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS), FIN_WARPS * 32, pl->fin_smem, st>>>(
-        A, pr, pl->d_cls, pl->nclasses, pl->ncb * pl->nrs, pl->nrs, pl->d_ccpart, pl->d_ccol,
+        A, pr, pl->d_cls, pl->nclasses, npart, pl->nrs, pl->d_ccpart, pl->d_ccol,
         pl->tot_ccol, pl->d_rc, pl->tot_rc, pl->nseg, pl->d_slots, pl->tot_slots, R, layout,
         r_bstride, scale, ntasks, pr.Q);
   }
   ++launches;
-  mark();
+  mark(pl->nev >= 1 && pl->ev_name[pl->nev - 1] && !strcmp(pl->ev_name[pl->nev - 1], "finalize") ? "expand"
+                                                                                                  : "finalize");
   CUDA_TRY(cudaGetLastError());
   pl->launches = launches;
   return COVGPU_OK;
@@ -698,6 +772,32 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     r = 1;  // (ccol would need a pre-reduction over segments before the finalize)
     pl->nrs = (int)std::max(1LL, std::min(r, std::min(max_split, 16LL)));
   }
+  {
+    // FP64 tensor cores for the core sums: complex128, all classes (class
+    // subsets — shards — keep the CUDA-core bulk, whose work units follow
+    // the selection), windows wide enough to fill the 32-lag x DC tiles and
+    // edge column blocks that stay a small share of the columns
+    const int ncb_l = (q - 2) / 32 + 1;
+    const int ncb_r = pl->ncb - (int)((m - q + 1) / 32);
+    bool ok = dtype == COVGPU_C128 && pl->clean && class_ids == nullptr && p >= 16 && q >= 24 &&
+              p <= FINV_MAX_P && q >= 2 && ncb_l + ncb_r <= pl->ncb / 2 && pl->use_tma;
+    if (const char* nm = getenv("COVGPU_NO_MMA")) ok = ok && atoi(nm) == 0;
+    if (ok) {
+      pl->use_mma = true;
+      pl->mma_dc = q <= 32 ? 32 : 64;
+      pl->n_drt = (2 * p - 1 + MMA_DR - 1) / MMA_DR;
+      pl->n_dct = (q + pl->mma_dc - 1) / pl->mma_dc;
+      // one wave of 2 CTAs/SM; each CTA a contiguous run of >= 2 chunks
+      const long long tiles = batch * (long long)pl->n_drt * pl->n_dct;
+      const long long chunks = (long long)((n + MMA_RC - 1) / MMA_RC + 2) * ((m - q + 1 + MMA_W - 1) / MMA_W);
+      long long g = std::max(1LL, (2LL * 148 + tiles - 1) / tiles);
+      g = std::min(g, std::max(1LL, chunks / 2));
+      pl->mma_g = (int)g;
+      pl->ncb_l = ncb_l;
+      pl->ncb_r = ncb_r;
+      pl->edge_variant = pick_bulk_variant(n, 32LL * (ncb_l + ncb_r), p, q, batch, dtype);
+    }
+  }
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
   pl->edge_tma = pl->S >= 16 && pl->use_tma;
@@ -774,7 +874,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     return rc;
   }
   if (pl->clean) {
-    if ((rc = dalloc(&pl->d_ccpart, (size_t)batch * nc * pl->ncb * pl->nrs, &ws)) ||
+    const size_t npart = (size_t)std::max(pl->ncb * pl->nrs, pl->use_mma ? pl->mma_g : 0);
+    if ((rc = dalloc(&pl->d_ccpart, (size_t)batch * nc * npart, &ws)) ||
         (rc = dalloc(&pl->d_ccol, (size_t)(batch * std::max(pl->tot_ccol, 1LL) * pl->nrs), &ws)) ||
         (rc = dalloc(&pl->d_rc, (size_t)(batch * std::max(pl->tot_rc, 1LL) * pl->nseg), &ws)) ||
         (rc = dalloc(&pl->d_slots, (size_t)(batch * std::max(pl->tot_slots, 1LL)), &ws))) {
@@ -883,6 +984,18 @@ int32_t covgpu_plan_kernel_times(covgpu_plan_t pl, float* ms, int32_t max_n) {
   return n;
 }
 
+int32_t covgpu_plan_kernel_names(covgpu_plan_t pl, char* buf, int32_t len) {
+  if (!pl || !buf || len < 1) return fail(COVGPU_EINVAL, "plan or buffer is NULL");
+  std::string s;
+  int n = 0;
+  for (int i = 1; i < pl->nev; ++i, ++n) {
+    if (i > 1) s += ",";
+    s += pl->ev_name[i] ? pl->ev_name[i] : "?";
+  }
+  std::snprintf(buf, (size_t)len, "%s", s.c_str());
+  return n;
+}
+
 int covgpu_plan_destroy(covgpu_plan_t pl) {
   if (!pl) return COVGPU_OK;
   cudaSetDevice(pl->device);
@@ -935,7 +1048,9 @@ int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m
   return covgpu_plan_execute_host(pl, A_host, R_host, layout, scale);
 }
 
-int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tflops) {
+namespace {
+// kind 0: FP64 FMA loop, 1: FP32 FMA loop, 2: FP64 DMMA loop
+int probe_peak(int device, int kind, double seconds, double* tflops) {
   if (!tflops) return fail(COVGPU_EINVAL, "tflops is NULL");
   CUDA_TRY(cudaSetDevice(device));
   cudaDeviceProp prop;
@@ -948,7 +1063,9 @@ int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tfl
   cudaEventCreate(&e1);
   auto run = [&](int iters) -> float {
     cudaEventRecord(e0);
-    if (dtype == COVGPU_C128)
+    if (kind == 2)
+      k_dmma_probe<<<blocks, threads>>>((double*)out, iters, 0.999999);
+    else if (kind == 0)
       k_fma_probe<double><<<blocks, threads>>>((double*)out, iters, 0.999999);
     else
       k_fma_probe<float><<<blocks, threads>>>((float*)out, iters, 0.999999f);
@@ -973,9 +1090,20 @@ int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tfl
   cudaEventDestroy(e1);
   cudaFree(out);
   if (e != cudaSuccess) return fail(COVGPU_ECUDA, cudaGetErrorString(e));
-  const double flops = 2.0 * 64.0 * (double)iters * blocks * threads;  // 64 FMA / iter
+  // FMA loop: 64 FMA per thread-iteration; DMMA loop: 8 x 256 FMA per warp-iteration
+  const double fma_per = kind == 2 ? 8.0 * 256.0 / 32.0 : 64.0;
+  const double flops = 2.0 * fma_per * (double)iters * blocks * threads;
   *tflops = flops / (best * 1e-3) / 1e12;
   return COVGPU_OK;
+}
+}  // namespace
+
+int covgpu_probe_fma_peak(int device, int32_t dtype, double seconds, double* tflops) {
+  return probe_peak(device, dtype == COVGPU_C128 ? 0 : 1, seconds, tflops);
+}
+
+int covgpu_probe_dmma_peak(int device, double seconds, double* tflops) {
+  return probe_peak(device, 2, seconds, tflops);
 }
 
 // Batched host path: the batch is cut into sub-batches that flow through

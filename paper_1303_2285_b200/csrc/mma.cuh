@@ -1,0 +1,239 @@
+// K1 on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64) — complex128 only.
+//
+// The core sums of every class are one GEMM.  For row lag dr and column lag
+// dc, CC(dr, dc) = sum over core rows r1 and core columns c of
+//     A[r1, c] * conj(A[r1 + dr, c + dc]).
+// Index the K dimension by (r2, c), r2 = r1 + dr the second element's row:
+//     CC[dr, dc] = sum_{r2, c} X[r2 - dr, c] * conj(Y[r2, c + dc])
+// is a (lags x lags) = (K-long) x (K-long)^T product whose A operand
+// (m = dr, k = c) is a row-Toeplitz gather of A's rows and whose B operand
+// (k = c, n = dc) is a Toeplitz gather of one row — both read straight from
+// the SMEM tiles, nothing is materialised.  The class's core restriction
+// splits into position-only masks that TMA applies for free:
+//   * core columns: c <= M-Q (X tensor map is M-Q+1 columns wide; the
+//     out-of-bounds columns are zero-filled) and c + dc >= Q-1 (Y tensor map
+//     starts at column Q-1; negative coordinates are zero-filled);
+//   * core rows: max(r1, r2) >= P-1 and min(r1, r2) <= N-P, which holds for
+//     every lag when r2 is in [P-1, N-P]; the few head / tail rows outside
+//     zero the A fragment of the lags they do not belong to.
+// Complex arithmetic = 4 real DMMAs per 8x8x4 tile: Re += xr*yr + xi*yi,
+// Im += xi*yr - xr*yi.
+//
+// CTA = (snapshot, 32-lag tile, DC-lag tile, split p of G): 4 compute warps as
+// 2 (16 lags) x 2 (DC/2 lags) warp tiles and one TMA producer warp.  The
+// CTA's K range is a contiguous run of (16-row x 32-column) chunks of the
+// tile's rows x columns, split evenly over the G CTAs of the tile; each
+// chunk is one TMA stage: X = the 47 first-element rows x 36 columns the 16
+// rows' 32 lags touch, Y = the 16 second-element rows x (32+DC) columns.  The
+// CTA writes its 32 x DC partial sums to the class's partial slot p; the
+// finalize adds the G partials in order, so the result is deterministic.
+// Edge-column sums CCol come from the CUDA-core kernel restricted to the
+// column blocks holding edge columns (bulk.cuh, edge-only mode).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace covgpu {
+
+constexpr int MMA_DR = 32;                   // row lags per CTA
+constexpr int MMA_RC = 16;                   // second-element rows per chunk
+constexpr int MMA_W = 32;                    // first-element columns per chunk
+constexpr int MMA_XP = 36;                   // X row pitch (complex): 576 B = 64 mod 128
+constexpr int MMA_XR = MMA_RC + MMA_DR - 1;  // X rows per chunk
+constexpr int MMA_STAGES = 2;
+constexpr int MMA_WARPS = 4;  // compute warps (+1 producer)
+
+template <int DC>
+struct MmaCfg {
+  static constexpr int NT = DC / 16;     // 8-wide lag tiles per warp (2 warps across DC)
+  static constexpr int YP = MMA_W + DC;  // Y row pitch (complex); W + DC - 1 used
+  static constexpr size_t xbytes = 16 * (size_t)MMA_XR * MMA_XP;
+  static constexpr size_t xoff = (xbytes + 127) / 128 * 128;
+  static constexpr size_t ybytes = 16 * (size_t)MMA_RC * YP;
+  static constexpr size_t stage = xoff + (ybytes + 127) / 128 * 128;
+  static constexpr size_t smem = MMA_STAGES * stage + 64;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// One k-step (4 columns at one second-element row): fragments from SMEM,
+// 4 passes of 2*NT independent DMMAs (dependent tiles 2*NT DMMAs apart).
+template <int NT>
+__device__ __forceinline__ void mma_kstep(const double2* __restrict__ xa0, const double2* __restrict__ xa1,
+                                          const double2* __restrict__ yb, bool on0, bool on1,
+                                          double (&cr)[2][NT][2], double (&ci)[2][NT][2]) {
+  double2 a[2];
+  a[0] = *xa0;
+  a[1] = *xa1;
+  if (!on0) a[0] = make_double2(0.0, 0.0);
+  if (!on1) a[1] = make_double2(0.0, 0.0);
+  double2 bv[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) bv[j] = yb[8 * j];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].x, bv[j].x);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].y, bv[j].x);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].y, bv[j].y);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double nx = -a[i].x;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma(ci[i][j][0], ci[i][j][1], nx, bv[j].y);
+  }
+}
+
+// The MMA_RC rows of one chunk.  MASKED: head / tail rows, lags whose core
+// rows exclude the row see a zero A fragment.  FULL: all MMA_W columns.
+template <int NT, int YP, bool MASKED, bool FULL>
+__device__ __forceinline__ void mma_rows(const double2* __restrict__ X, const double2* __restrict__ Y,
+                                         int xrow0, int kq, int ycol0, int nks, int R, int dra,
+                                         const Problem& pr, double (&cr)[2][NT][2],
+                                         double (&ci)[2][NT][2]) {
+  const int P = pr.P, N = pr.N;
+#pragma unroll 1
+  for (int tr = 0; tr < MMA_RC; ++tr) {
+    const double2* xa0 = X + (tr + xrow0) * MMA_XP + kq;
+    const double2* xa1 = xa0 - 8 * MMA_XP;  // lags + 8: rows - 8
+    const double2* yb = Y + tr * YP + ycol0;
+    bool on0 = true, on1 = true;
+    if constexpr (MASKED) {
+      const int r2 = R + tr, r1a = r2 - dra, r1b = r1a - 8;
+      on0 = max(r1a, r2) >= P - 1 && min(r1a, r2) <= N - P;
+      on1 = max(r1b, r2) >= P - 1 && min(r1b, r2) <= N - P;
+    }
+    if constexpr (FULL) {
+#pragma unroll
+      for (int ks = 0; ks < MMA_W / 4; ++ks)
+        mma_kstep<NT>(xa0 + 4 * ks, xa1 + 4 * ks, yb + 4 * ks, on0, on1, cr, ci);
+    } else {
+#pragma unroll 1
+      for (int ks = 0; ks < nks; ++ks)
+        mma_kstep<NT>(xa0 + 4 * ks, xa1 + 4 * ks, yb + 4 * ks, on0, on1, cr, ci);
+    }
+  }
+}
+
+// The X tile of a chunk at rows [R, R+MMA_RC) starts MMA_DR-1 rows above R - dr0.
+template <int DC>
+__global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
+    k_bulk_dmma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
+                Problem pr, int n_drt, int n_dct, int G, int nclasses,
+                const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+  using Cfg = MmaCfg<DC>;
+  constexpr int NT = Cfg::NT, YP = Cfg::YP, S = MMA_STAGES;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage);
+  uint64_t* empty = full + S;
+  long long t = blockIdx.x;
+  const int p = (int)(t % G);
+  t /= G;
+  const int dct = (int)(t % n_dct);
+  t /= n_dct;
+  const int drt = (int)(t % n_drt);
+  const int b = (int)(t / n_drt);
+  const int P = pr.P, Q = pr.Q, N = pr.N, M = pr.M;
+  const int dr0 = -(P - 1) + drt * MMA_DR;
+  const int dc0 = dct * DC;
+  const int drmax = min(dr0 + MMA_DR - 1, P - 1);
+  // second-element rows where at least one lag of the tile has core rows
+  const int rlo = max(0, P - 1 + min(dr0, 0));
+  const int rhi = min(N - 1, N - P + max(drmax, 0));
+  const int nrc = (rhi - rlo + MMA_RC) / MMA_RC;
+  const int xcols = M - Q + 1;  // first-element columns of core products
+  const int ncbk = (xcols + MMA_W - 1) / MMA_W;
+  const long long nch = (long long)nrc * ncbk;
+  const long long q0 = nch * p / G, q1 = nch * (p + 1) / G;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MMA_WARPS);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (w == MMA_WARPS) {  // producer
+    if (lane == 0) {
+      for (long long k = 0; k < q1 - q0; ++k) {
+        const int s = (int)(k % S);
+        if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
+        const long long q = q0 + k;
+        const int R = rlo + (int)(q / ncbk) * MMA_RC;
+        const int C0 = (int)(q % ncbk) * MMA_W;
+        unsigned char* st = smraw + s * Cfg::stage;
+        mbar_expect_tx(&full[s], (unsigned)(Cfg::xbytes + Cfg::ybytes));
+        tma_load_3d(st, &tmx, 2 * C0, R - dr0 - (MMA_DR - 1), b, &full[s]);
+        tma_load_3d(st + Cfg::xoff, &tmy, 2 * (C0 + dc0 - (Q - 1)), R, b, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int wm = w & 1, wn = w >> 1;
+  const int m = lane >> 2, kq = lane & 3;
+  double cr[2][NT][2], ci[2][NT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  // this lane's A rows: lag dr0 + 16 wm + 8 i + m -> X tile row tr + 31 - 16 wm - 8 i - m
+  const int xrow0 = MMA_DR - 1 - 16 * wm - m;
+  const int ycol0 = kq + wn * (DC / 2) + m;
+
+  for (long long k = 0; k < q1 - q0; ++k) {
+    const int s = (int)(k % S);
+    mbar_wait(&full[s], (int)((k / S) & 1));
+    const long long q = q0 + k;
+    const int R = rlo + (int)(q / ncbk) * MMA_RC;
+    const int C0 = (int)(q % ncbk) * MMA_W;
+    const int nks = min(MMA_W, xcols - C0 + 3) / 4;
+    const double2* X = reinterpret_cast<const double2*>(smraw + s * Cfg::stage);
+    const double2* Y = reinterpret_cast<const double2*>(smraw + s * Cfg::stage + Cfg::xoff);
+    const bool masked = R < P - 1 || R + MMA_RC - 1 > N - P;
+    const int dra = dr0 + 16 * wm + m;
+    if (nks == MMA_W / 4) {
+      if (!masked)
+        mma_rows<NT, YP, false, true>(X, Y, xrow0, kq, ycol0, nks, R, dra, pr, cr, ci);
+      else
+        mma_rows<NT, YP, true, true>(X, Y, xrow0, kq, ycol0, nks, R, dra, pr, cr, ci);
+    } else {
+      mma_rows<NT, YP, true, false>(X, Y, xrow0, kq, ycol0, nks, R, dra, pr, cr, ci);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // epilogue: C fragment (m, 2 kq + e) of tile (i, j) = lag (dr, dc)
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int dr = dr0 + 16 * wm + 8 * i + m;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int dc = dc0 + wn * (DC / 2) + 8 * j + 2 * kq + e;
+        if (dr > P - 1 || dc >= Q || !in_uc(dr, dc, P, Q)) continue;
+        const int cid = cls_slot[class_index(dr, dc, P, Q)];
+        if (cid < 0) continue;
+        ccpart[((long long)b * nclasses + cid) * G + p] = make_double2(cr[i][j][e], ci[i][j][e]);
+      }
+  }
+}
+
+}  // namespace covgpu

@@ -12,7 +12,7 @@ import torch
 from . import _native
 from .core import WindowSpec
 
-__all__ = ["Plan", "probe_fma_peak", "LAYOUTS"]
+__all__ = ["Plan", "probe_fma_peak", "probe_dmma_peak", "LAYOUTS"]
 
 LAYOUTS = {"dense": _native.DENSE, "packed": _native.PACKED, "compact": _native.COMPACT}
 _DT = {torch.complex128: _native.C128, torch.complex64: _native.C64}
@@ -76,6 +76,18 @@ class Plan:
             _native.check(n, "kernel_times")
         return [float(buf[i]) for i in range(n)]
 
+    def kernel_names(self) -> list[str]:
+        """Names of the kernel_times() intervals of the last timed execute."""
+        buf = ctypes.create_string_buffer(256)
+        n = self.lib.covgpu_plan_kernel_names(self.handle, buf, 256)
+        if n < 0:
+            _native.check(n, "kernel_names")
+        return buf.value.decode().split(",") if n > 0 else []
+
+    def kernel_timing(self) -> dict:
+        """{kernel name: ms} of the last timed execute."""
+        return dict(zip(self.kernel_names(), self.kernel_times()))
+
     @property
     def launches(self) -> int:
         return int(self.lib.covgpu_plan_launches(self.handle))
@@ -103,4 +115,14 @@ def probe_fma_peak(device: int = 0, fp64: bool = True, seconds: float = 1.0) -> 
     rc = lib.covgpu_probe_fma_peak(device, _native.C128 if fp64 else _native.C64, seconds,
                                    ctypes.byref(out))
     _native.check(rc, "covgpu_probe_fma_peak")
+    return float(out.value)
+
+
+def probe_dmma_peak(device: int = 0, seconds: float = 1.0) -> float:
+    """Measured FP64 tensor-core (DMMA) peak (TFLOP/s) — the roofline
+    denominator of the tensor-core bulk kernel."""
+    lib = _native.lib()
+    out = ctypes.c_double()
+    rc = lib.covgpu_probe_dmma_peak(device, seconds, ctypes.byref(out))
+    _native.check(rc, "covgpu_probe_dmma_peak")
     return float(out.value)

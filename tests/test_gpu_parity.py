@@ -489,3 +489,43 @@ def test_pipelined_host_path_bitwise(cuda):
                 r, c = torch.triu_indices(30, 30)
                 assert torch.equal(out.reshape(batch, -1), ref[:, r, c])
         plan.close()
+
+
+@pytest.mark.parametrize("n,m,p,q,batch", [
+    (300, 400, 20, 40, 1),   # Q=40 in a 64-lag tile, ragged last column block
+    (257, 600, 33, 70, 1),   # Q > 64: two lag tiles across dc; 3 tiles across dr
+    (200, 256, 16, 24, 3),   # smallest gated window, batch of 3
+    (515, 515, 32, 32, 2),   # N, M not multiples of the 16-row / 32-column chunks
+])
+def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, monkeypatch):
+    """complex128 core sums on the FP64 tensor cores (k_bulk_dmma) against the
+    Gram cross-check and against the CUDA-core bulk kernel of the same shape."""
+    from oracle.gpu_naive import covariance_gram
+    from paper_1303_2285_b200.plan import Plan
+
+    rng = np.random.default_rng(n * 7 + m)
+    a = torch.as_tensor(rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m)),
+                        device=cuda)
+    win = WindowSpec(p, q)
+    plan = Plan(n, m, win, batch=batch, dtype=torch.complex128, device=cuda)
+    plan.set_timing(True)
+    got = plan.alloc_output()
+    plan.execute(a, got)
+    got = got.reshape(batch, p * q, p * q)
+    assert "bulk_dmma" in plan.kernel_names()
+    plan.close()
+    monkeypatch.setenv("COVGPU_NO_MMA", "1")
+    plan2 = Plan(n, m, win, batch=batch, dtype=torch.complex128, device=cuda)
+    plan2.set_timing(True)
+    ref_cc = plan2.alloc_output()
+    plan2.execute(a, ref_cc)
+    ref_cc = ref_cc.reshape(batch, p * q, p * q)
+    assert "bulk_dmma" not in plan2.kernel_names()
+    plan2.close()
+    for b in range(batch):
+        assert_hermitian(got[b].cpu().numpy())
+        ref = covariance_gram(a[b], p, q)
+        err = (torch.linalg.norm(got[b] - ref) / torch.linalg.norm(ref)).item()
+        err_cc = (torch.linalg.norm(got[b] - ref_cc[b]) / torch.linalg.norm(ref_cc[b])).item()
+        assert err <= TOL64, err
+        assert err_cc <= 1e-13, err_cc

@@ -154,8 +154,9 @@ def test_bench_work_decomposition_sums_to_um():
     from paper_1303_2285_b200.workloads import WORKLOADS
 
     for w in WORKLOADS.values():
-        um, b, e, c = bench.products(w)
+        um, b, e, c, core = bench.products(w)
         assert um == b + e + c
+        assert 0 < core <= b  # tensor-core core products: core rows x core columns
 
 
 def test_c_oracle_matches_numpy_oracle():

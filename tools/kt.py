@@ -23,5 +23,6 @@ for name in sys.argv[1:]:
         kt = plan.kernel_times()
         acc = kt if acc is None else [x + y for x, y in zip(acc, kt)]
     kt = [x / reps for x in acc]
+    names = plan.kernel_names()
     print(f"{name} variant={os.environ.get('COVGPU_BULK_VARIANT','default')}: " +
-          " ".join(f"{x:.3f}" for x in kt) + f"  total {sum(kt):.3f} ms", flush=True)
+          " ".join(f"{k}={x:.3f}" for k, x in zip(names, kt)) + f"  total {sum(kt):.3f} ms", flush=True)
