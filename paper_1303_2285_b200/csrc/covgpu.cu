@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -97,6 +98,14 @@ struct covgpu_plan {
   int edge_variant = 0;
   const void* mtmap_ptr = nullptr;
   CUtensorMap mtmx{}, mtmy{};
+  // edge-column sums on the tensor cores too (Q <= 65): items x ecm_g CTAs
+  bool use_ecm = false;
+  int ecm_g = 1;
+  long long ecm_items = 0;
+  double2* d_ecm_part = nullptr;
+  unsigned* d_ecm_tickets = nullptr;
+  const void* ecm_ptr = nullptr;
+  CUtensorMap ecm_tm{};
   // edge-row kernel TMA variant (strips of >= 16 rows)
   bool edge_tma = false;
   int r2g = 1, n_r2g = 1;
@@ -233,6 +242,8 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_corners);
   cudaFree(pl->d_tasks);
   cudaFree(pl->d_uc_off);
+  cudaFree(pl->d_ecm_part);
+  cudaFree(pl->d_ecm_tickets);
 }
 
 int pick_lags(int span) {
@@ -355,6 +366,9 @@ cudaError_t set_attrs() {
     if ((r = cudaFuncSetAttribute(k_bulk_dmma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)MmaCfg<64>::smem)) != cudaSuccess)
       e = r;
+    if ((r = cudaFuncSetAttribute(k_edge_cols_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ECM_SMEM)) != cudaSuccess)
+      e = r;
     if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       e = r;
@@ -466,6 +480,25 @@ bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   return true;
 }
 
+// edge-column sums on the tensor cores; false when the tensor map fails
+bool launch_edge_cols_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
+  const Problem& pr = pl->pr;
+  if (pl->ecm_ptr != (const void*)A) {
+    CUtensorMap tm;
+    if (!make_tmap(&tm, A, true, pl->batch, pr.N, pr.M, 2 * ECM_PITCH, ECM_RC)) {
+      pl->ecm_ptr = nullptr;
+      return false;
+    }
+    pl->ecm_tm = tm;
+    pl->ecm_ptr = A;
+  }
+  const long long blocks = pl->ecm_items * pl->ecm_g;
+  k_edge_cols_dmma<<<(unsigned)blocks, (MMA_WARPS + 1) * 32, ECM_SMEM, st>>>(
+      pl->ecm_tm, pr, pl->ecm_g, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, pl->d_ecm_part,
+      pl->d_ecm_tickets);
+  return true;
+}
+
 template <typename T, int D>
 void launch_edge(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   const Problem& pr = pl->pr;
@@ -574,8 +607,9 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   const int npart = mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
   mark(mma ? "bulk_dmma" : "bulk");
-  if (mma) {  // edge-column sums: CUDA-core bulk on the edge column blocks
-    launch_bulk_variant<T>(pl, A, es, pl->edge_variant, pl->ncb_l, pl->ncb_r);
+  if (mma) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
+    if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es)))
+      launch_bulk_variant<T>(pl, A, es, pl->edge_variant, pl->ncb_l, pl->ncb_r);
     ++launches;
     mark("edge_cols");
   }
@@ -796,6 +830,31 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->ncb_l = ncb_l;
       pl->ncb_r = ncb_r;
       pl->edge_variant = pick_bulk_variant(n, 32LL * (ncb_l + ncb_r), p, q, batch, dtype);
+      // (the 8x8 tile map of the strip Gram needs >= 7 tile rows to keep the
+      // 4 warps balanced: cfg5 edge columns 0.647 -> 0.337 ms, but cfg3
+      // (Q=32) 0.037 -> 0.074 ms)
+      bool ecm = q >= 50 && q <= 65;
+      if (const char* ne = getenv("COVGPU_NO_MMA_EDGE")) ecm = ecm && atoi(ne) == 0;
+      if (ecm) {
+        // items (snapshot, strip, dr) x G row splits: pick G in [1, 16] for
+        // the best fill of 2 CTAs/SM waves (>= 2 chunks of 16 rows per CTA)
+        pl->use_ecm = true;
+        pl->ecm_items = batch * 2LL * (2 * p - 1);
+        const long long rows = n - 2LL * p + 2;
+        int best_g = 1;
+        double best = 0.0;
+        for (int g = 1; g <= 16; ++g) {
+          if (g > 1 && rows / ECM_RC / g < 2) break;
+          const double ctas = (double)pl->ecm_items * g;
+          const double waves = std::ceil(ctas / 296.0);
+          const double eff = ctas / (waves * 296.0);
+          if (eff > best + 0.02) {
+            best = eff;
+            best_g = g;
+          }
+        }
+        pl->ecm_g = best_g;
+      }
     }
   }
   pl->S = p - 1;
@@ -872,6 +931,17 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   if ((rc = dalloc(&pl->d_cls, nc, &ws)) || (rc = dalloc(&pl->d_cls_slot, (size_t)nuc, &ws))) {
     plan_free(pl.get());
     return rc;
+  }
+  if (pl->use_ecm && pl->ecm_g > 1) {
+    if ((rc = dalloc(&pl->d_ecm_part, (size_t)(pl->ecm_items * pl->ecm_g * ECM_PART), &ws)) ||
+        (rc = dalloc(&pl->d_ecm_tickets, (size_t)pl->ecm_items, &ws))) {
+      plan_free(pl.get());
+      return rc;
+    }
+    if (cudaMemset(pl->d_ecm_tickets, 0, sizeof(unsigned) * (size_t)pl->ecm_items) != cudaSuccess) {
+      plan_free(pl.get());
+      return fail(COVGPU_ECUDA, "ticket reset");
+    }
   }
   if (pl->clean) {
     const size_t npart = (size_t)std::max(pl->ncb * pl->nrs, pl->use_mma ? pl->mma_g : 0);

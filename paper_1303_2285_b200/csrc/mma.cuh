@@ -236,4 +236,182 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
   }
 }
 
+// ---- edge-column sums on the tensor cores ------------------------------------
+// For lag dr and one edge strip of Q-1 columns starting at o (left: o = 0;
+// right: o = M-Q+1), the edge-column sums
+//     CCol(dr, dc)[c1] = sum_{core rows} x[r2-dr, o+c1] * conj(y[r2, o+c1+dc]),
+// c1 + dc <= Q-2, are the upper triangle (e = c1 + dc >= c1) of the strip's
+// lag-dr cross Gram  G[c1, e] = sum_{r2} X[r2-dr, o+c1] conj(Y[r2, o+e]) — a
+// GEMM with K = the class's core rows r2 in [P-1+min(dr,0), N-P+max(dr,0)].
+// 8x8 tiles (ti, tj), tj >= ti, of the <= 64-column strip: warp w owns tile
+// rows w and 7-w (9 tiles).  CTA = (snapshot, strip, dr, row split g of G);
+// each chunk stages 16 rows of X (shifted by dr) and Y, 66-complex pitch
+// (4 rows x 2 columns of a fragment phase hit distinct banks).  With G > 1
+// the last CTA of an item (ticket counter, self-resetting) adds the G
+// partial tiles in slot order — deterministic — and writes CCol.
+constexpr int ECM_RC = 16;
+constexpr int ECM_PITCH = 66;
+constexpr int ECM_STAGES = 3;
+constexpr size_t ECM_TILE = 16 * (size_t)ECM_RC * ECM_PITCH;
+constexpr size_t ECM_STAGE = 2 * ECM_TILE;
+constexpr size_t ECM_SMEM = ECM_STAGES * ECM_STAGE + 64;
+constexpr int ECM_SLOTS = 9;
+constexpr int ECM_PART = MMA_WARPS * ECM_SLOTS * 2 * 32;  // double2 per CTA partial
+
+struct EcmItem {
+  int b, side, dr, lo, hi, o;
+};
+
+__device__ __forceinline__ EcmItem ecm_item(long long item, const Problem& pr) {
+  EcmItem it;
+  const int span = 2 * pr.P - 1;
+  it.dr = (int)(item % span) - (pr.P - 1);
+  it.side = (int)((item / span) % 2);
+  it.b = (int)(item / (2LL * span));
+  it.lo = pr.P - 1 + min(it.dr, 0);
+  it.hi = pr.N - pr.P + max(it.dr, 0);
+  it.o = it.side ? pr.M - pr.Q + 1 : 0;
+  return it;
+}
+
+template <int W>
+__device__ __forceinline__ void ecm_consume(const unsigned char* smraw, uint64_t* full, uint64_t* empty,
+                                            int nchunks, int R0, int hi, int nt, double (&cr)[ECM_SLOTS][2],
+                                            double (&ci)[ECM_SLOTS][2]) {
+  const int lane = threadIdx.x & 31, m = lane >> 2, kq = lane & 3;
+#pragma unroll
+  for (int sl = 0; sl < ECM_SLOTS; ++sl) cr[sl][0] = cr[sl][1] = ci[sl][0] = ci[sl][1] = 0.0;
+  constexpr int NB = 8 - W;  // B tiles tj in [W, 8)
+  for (int k = 0; k < nchunks; ++k) {
+    const int s = k % ECM_STAGES;
+    mbar_wait(&full[s], (k / ECM_STAGES) & 1);
+    const double2* X = reinterpret_cast<const double2*>(smraw + s * ECM_STAGE);
+    const double2* Y = X + ECM_TILE / 16;
+    const int R = R0 + k * ECM_RC;
+#pragma unroll 1
+    for (int kk = 0; kk < ECM_RC / 4; ++kk) {
+      const int row = 4 * kk + kq;
+      const bool on = R + row <= hi;
+      double2 a0 = X[row * ECM_PITCH + 8 * W + m], a1 = X[row * ECM_PITCH + 8 * (7 - W) + m];
+      if (!on) a0 = a1 = make_double2(0.0, 0.0);
+      const double na0 = -a0.x, na1 = -a1.x;
+      double2 bv[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) bv[j] = Y[row * ECM_PITCH + 8 * (W + j) + m];
+      // slot sl: (W, W+sl) for sl < NB, else (7-W, 7-W + sl-NB) = B index 7-2W + sl-NB
+#define ECM_PASS(ACC, AX, BX)                                              \
+  _Pragma("unroll") for (int sl = 0; sl < ECM_SLOTS; ++sl) {               \
+    const int bj = sl < NB ? sl : 7 - 2 * W + (sl - NB);                   \
+    if (W + bj < nt) {                                                     \
+      const double2& av = sl < NB ? a0 : a1;                               \
+      dmma(ACC[sl][0], ACC[sl][1], AX, BX);                                \
+    }                                                                      \
+  }
+      ECM_PASS(cr, av.x, bv[bj].x)
+      ECM_PASS(ci, av.y, bv[bj].x)
+      ECM_PASS(cr, av.y, bv[bj].y)
+      ECM_PASS(ci, (sl < NB ? na0 : na1), bv[bj].y)
+#undef ECM_PASS
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+__global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
+    k_edge_cols_dmma(const __grid_constant__ CUtensorMap tms, Problem pr, int G,
+                     const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
+                     double2* __restrict__ ccol, long long tot_ccol, double2* __restrict__ part,
+                     unsigned* __restrict__ tickets) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ECM_STAGES * ECM_STAGE);
+  uint64_t* empty = full + ECM_STAGES;
+  __shared__ int s_last;
+  const long long item = blockIdx.x / G;
+  const int g = (int)(blockIdx.x % G);
+  const EcmItem it = ecm_item(item, pr);
+  const int P = pr.P, Q = pr.Q;
+  const int nrc = (it.hi - it.lo + ECM_RC) / ECM_RC;
+  const int c0 = nrc * g / G, c1 = nrc * (g + 1) / G;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ECM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MMA_WARPS);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+  if (w == MMA_WARPS) {  // producer
+    if (lane == 0) {
+      for (int k = 0; k < c1 - c0; ++k) {
+        const int s = k % ECM_STAGES;
+        if (k >= ECM_STAGES) mbar_wait_sleep(&empty[s], ((k - ECM_STAGES) / ECM_STAGES) & 1);
+        const int R = it.lo + (c0 + k) * ECM_RC;
+        unsigned char* st = smraw + s * ECM_STAGE;
+        mbar_expect_tx(&full[s], (unsigned)ECM_STAGE);
+        tma_load_3d(st, &tms, 2 * it.o, R - it.dr, it.b, &full[s]);
+        tma_load_3d(st + ECM_TILE, &tms, 2 * it.o, R, it.b, &full[s]);
+      }
+    }
+    return;
+  }
+  const int nt = (Q - 1 + 7) / 8;
+  const int R0 = it.lo + c0 * ECM_RC;
+  double cr[ECM_SLOTS][2], ci[ECM_SLOTS][2];
+  switch (w) {
+    case 0: ecm_consume<0>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci); break;
+    case 1: ecm_consume<1>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci); break;
+    case 2: ecm_consume<2>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci); break;
+    default: ecm_consume<3>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci);
+  }
+  if (G > 1) {
+    double2* mine = part + (item * G + g) * ECM_PART + (long long)w * ECM_SLOTS * 64;
+#pragma unroll
+    for (int sl = 0; sl < ECM_SLOTS; ++sl)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) mine[(sl * 2 + e) * 32 + lane] = make_double2(cr[sl][e], ci[sl][e]);
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(MMA_WARPS * 32));
+    if (threadIdx.x == 0) s_last = atomicAdd(&tickets[item], 1u) == (unsigned)(G - 1);
+    asm volatile("bar.sync 1, %0;" ::"n"(MMA_WARPS * 32));
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int sl = 0; sl < ECM_SLOTS; ++sl)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double sr = 0.0, si = 0.0;
+        for (int gg = 0; gg < G; ++gg) {
+          const double2 v = __ldcg(part + (item * G + gg) * ECM_PART + (long long)w * ECM_SLOTS * 64 +
+                                   (sl * 2 + e) * 32 + lane);
+          sr += v.x;
+          si += v.y;
+        }
+        cr[sl][e] = sr;
+        ci[sl][e] = si;
+      }
+    if (threadIdx.x == 0) tickets[item] = 0u;  // ready for the next execute
+  }
+  // CCol entries: C fragment (m, 2 kq + e) of slot tile (ti, tj)
+  const int m = lane >> 2, kq = lane & 3;
+#pragma unroll
+  for (int sl = 0; sl < ECM_SLOTS; ++sl) {
+    const int nb = 8 - w;
+    const int ti = sl < nb ? w : 7 - w;
+    const int tj = sl < nb ? w + sl : 7 - w + (sl - nb);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c1c = 8 * ti + m, ec = 8 * tj + 2 * kq + e;
+      const int dc = ec - c1c;
+      if (c1c >= Q - 1 || ec > Q - 2 || dc < 0 || !in_uc(it.dr, dc, P, Q)) continue;
+      const int cid = cls_slot[class_index(it.dr, dc, P, Q)];
+      if (cid < 0) continue;
+      const ClassDesc& cd = cls[cid];
+      const long long idx = it.side ? (long long)(cd.qu - 1) + c1c : c1c;
+      ccol[(long long)it.b * tot_ccol + cd.ccol_off + idx] = make_double2(cr[sl][e], ci[sl][e]);
+    }
+  }
+}
+
 }  // namespace covgpu
