@@ -106,6 +106,11 @@ struct covgpu_plan {
   unsigned* d_ecm_tickets = nullptr;
   const void* ecm_ptr = nullptr;
   CUtensorMap ecm_tm{};
+  // edge-row sums on the tensor cores (P <= 65)
+  bool use_erm = false;
+  int erm_dct = 1;
+  const void* erm_ptr = nullptr;
+  CUtensorMap erm_tmx{}, erm_tmy{};
   // edge-row kernel TMA variant (strips of >= 16 rows)
   bool edge_tma = false;
   int r2g = 1, n_r2g = 1;
@@ -369,6 +374,9 @@ cudaError_t set_attrs() {
     if ((r = cudaFuncSetAttribute(k_edge_cols_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ECM_SMEM)) != cudaSuccess)
       e = r;
+    if ((r = cudaFuncSetAttribute(k_edge_rows_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ERM_SMEM)) != cudaSuccess)
+      e = r;
     if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       e = r;
@@ -499,9 +507,34 @@ bool launch_edge_cols_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   return true;
 }
 
+// edge-row sums on the tensor cores; false when the tensor maps fail
+bool launch_edge_rows_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
+  const Problem& pr = pl->pr;
+  if ((uintptr_t)A % 16 != 0) return false;
+  if (pl->erm_ptr != (const void*)A) {
+    CUtensorMap mx, my;
+    if (!make_tmap(&mx, A, true, pl->batch, pr.N, pr.M, 2 * MMA_XP, ERM_XR, pr.M - pr.Q + 1, 0) ||
+        !make_tmap(&my, A, true, pl->batch, pr.N, pr.M, 2 * ERM_YP, 1)) {
+      pl->erm_ptr = nullptr;
+      return false;
+    }
+    pl->erm_tmx = mx;
+    pl->erm_tmy = my;
+    pl->erm_ptr = A;
+  }
+  const long long blocks = pl->batch * 2LL * pl->S * pl->erm_dct * pl->nseg;
+  k_edge_rows_dmma<<<(unsigned)blocks, (ERM_WARPS + 1) * 32, ERM_SMEM, st>>>(
+      pl->erm_tmx, pl->erm_tmy, pr, pl->erm_dct, pl->nseg, pl->d_cls_slot, pl->d_cls, pl->d_rc,
+      pl->tot_rc);
+  return true;
+}
+
 template <typename T, int D>
 void launch_edge(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   const Problem& pr = pl->pr;
+  if constexpr (sizeof(T) == 8) {
+    if (pl->use_erm && launch_edge_rows_dmma(pl, (const double2*)A, st)) return;
+  }
   if (pl->edge_tma && ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0) &&
       EdgeCfg<T, D>::stages(pl->S, pl->r2g) >= 2) {
     using Cfg = EdgeCfg<T, D>;
@@ -880,6 +913,21 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     pl->nseg = (int)std::max(1LL, std::min(seg, 16LL));
   }
 
+  if (pl->use_mma && p >= 48 && p <= 65) {  // the 64-row strip tile: P-1 in [47, 64]
+    bool erm = true;
+    if (const char* ne = getenv("COVGPU_NO_MMA_EDGE")) erm = atoi(ne) == 0;
+    if (erm) {
+      // CTA = (snapshot, strip, r2, lag tile, column segment): >= ~3 waves of
+      // 2 CTAs/SM with >= 2 column chunks per segment
+      pl->use_erm = true;
+      pl->erm_dct = (q + ERM_DC - 1) / ERM_DC;
+      const long long per = batch * 2LL * (p - 1) * pl->erm_dct;
+      const long long chunks = (m - q + 1 + MMA_W - 1) / MMA_W;
+      long long seg = std::max(1LL, (3LL * 296 + per - 1) / per);
+      seg = std::min(seg, std::max(1LL, chunks / 2));
+      pl->nseg = (int)std::min(seg, 16LL);
+    }
+  }
   const int nuc = (int)covgpu_num_classes(p, q);
   std::vector<char> sel(nuc, class_ids ? 0 : 1);
   if (class_ids) {

@@ -414,4 +414,133 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
   }
 }
 
+// ---- edge-row sums on the tensor cores ----------------------------------------
+// K2's RC' (edge.cuh) for one strip (top: rows [0, P-1); bottom: [N-P+1, N))
+// and one second-element row r2 of it: for every first-element row r1 of the
+// strip and lag dc,
+//     RC'(r1, r2, dc) = sum_{c=0}^{M-Q} x[r1, c] * conj(y[r2, c + dc])
+// — a (strip rows x lags) GEMM with K = columns, A operand = the strip's
+// rows (plain tile), B operand = the Toeplitz gather of row r2 (as in the
+// core kernel).  The X tensor map is M-Q+1 columns wide (zero-filled beyond).
+// CTA = (snapshot, strip, r2, DC-lag tile, column segment g of nseg): 4 warps
+// as 2 (32 rows) x 2 (32 lags); the segment partials land in RC's nseg slots
+// and the finalize adds them in order.
+constexpr int ERM_XR = 64;  // strip rows per tile (P-1 <= 64)
+constexpr int ERM_DC = 64;
+constexpr int ERM_WARPS = 8;  // 2 (32 rows) x 4 (16 lags) warp tiles
+constexpr int ERM_YP = MMA_W + ERM_DC;
+constexpr size_t ERM_XBYTES = 16 * (size_t)ERM_XR * MMA_XP;
+constexpr size_t ERM_YBYTES = 16 * (size_t)ERM_YP;
+constexpr size_t ERM_STAGE = ERM_XBYTES + (ERM_YBYTES + 127) / 128 * 128;
+constexpr int ERM_STAGES = 2;
+constexpr size_t ERM_SMEM = ERM_STAGES * ERM_STAGE + 64;
+
+__global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 2)
+    k_edge_rows_dmma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
+                     Problem pr, int n_dct, int nseg, const int* __restrict__ cls_slot,
+                     const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ERM_STAGES * ERM_STAGE);
+  uint64_t* empty = full + ERM_STAGES;
+  const int P = pr.P, Q = pr.Q, S = P - 1;
+  long long t = blockIdx.x;
+  const int seg = (int)(t % nseg);
+  t /= nseg;
+  const int dct = (int)(t % n_dct);
+  t /= n_dct;
+  const int r2 = (int)(t % S);
+  t /= S;
+  const int strip = (int)(t % 2);
+  const int b = (int)(t / 2);
+  const int base = strip ? pr.bh : 0;
+  const int dc0 = dct * ERM_DC;
+  const int xcols = pr.M - Q + 1;
+  const int ncbk = (xcols + MMA_W - 1) / MMA_W;
+  const int k0 = ncbk * seg / nseg, k1 = ncbk * (seg + 1) / nseg;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ERM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ERM_WARPS);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+  if (w == ERM_WARPS) {  // producer
+    if (lane == 0) {
+      for (int k = 0; k < k1 - k0; ++k) {
+        const int s = k % ERM_STAGES;
+        if (k >= ERM_STAGES) mbar_wait_sleep(&empty[s], ((k - ERM_STAGES) / ERM_STAGES) & 1);
+        const int C0 = (k0 + k) * MMA_W;
+        unsigned char* st = smraw + s * ERM_STAGE;
+        mbar_expect_tx(&full[s], (unsigned)(ERM_XBYTES + ERM_YBYTES));
+        tma_load_3d(st, &tmx, 2 * C0, base, b, &full[s]);
+        tma_load_3d(st + ERM_XBYTES, &tmy, 2 * (C0 + dc0), base + r2, b, &full[s]);
+      }
+    }
+    return;
+  }
+  const int wm = w & 1, wn = w >> 1, m = lane >> 2, kq = lane & 3;
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  for (int k = 0; k < k1 - k0; ++k) {
+    const int s = k % ERM_STAGES;
+    mbar_wait(&full[s], (k / ERM_STAGES) & 1);
+    const double2* X = reinterpret_cast<const double2*>(smraw + s * ERM_STAGE) + (32 * wm + m) * MMA_XP + kq;
+    const double2* Y = reinterpret_cast<const double2*>(smraw + s * ERM_STAGE + ERM_XBYTES) + kq + 16 * wn + m;
+    const int nks = min(MMA_W, xcols - (k0 + k) * MMA_W + 3) / 4;
+#pragma unroll 1
+    for (int ks = 0; ks < nks; ++ks) {
+      double2 a[4], bv[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = X[8 * i * MMA_XP + 4 * ks];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[j] = Y[8 * j + 4 * ks];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].x, bv[j].x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].y, bv[j].x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].y, bv[j].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double nx = -a[i].x;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], nx, bv[j].y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // RC' of pane row min(r1, r2) (strip-relative) of class (r2 - r1, dc)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r1 = 32 * wm + 8 * i + m;
+    if (r1 >= S) continue;
+    const int dr = r2 - r1;
+    const int row = min(r1, r2);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int dc = dc0 + 16 * wn + 8 * j + 2 * kq + e;
+        if (dc >= Q || !in_uc(dr, dc, P, Q)) continue;
+        const int cid = cls_slot[class_index(dr, dc, P, Q)];
+        if (cid < 0) continue;
+        const ClassDesc& cd = cls[cid];
+        const int kk = strip ? cd.pv - 1 + row : row;
+        rc[((long long)b * tot_rc + cd.rc_off + kk) * nseg + seg] = make_double2(cr[i][j][e], ci[i][j][e]);
+      }
+  }
+}
+
 }  // namespace covgpu
