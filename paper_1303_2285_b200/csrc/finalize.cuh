@@ -137,7 +137,42 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   }
   const bool zero_im = (c.d == 0);
   const long long rb = (long long)b * r_bstride;
+  const C2* TL = Cb;
+  const C2* TR = Cb + cstride;
+  const C2* BL = Cb + 2 * cstride;
+  const C2* BR = Cb + 3 * cstride;
   for (int u = 0; u < qu; ++u) {
+    // KR == 1: this column's corner / edge-column reads go out first, so
+    // their latency overlaps the scan and the slot stores below (cfg3
+    // finalize 0.058 -> 0.050 ms); with KR >= 2 the extra live registers cost
+    // more occupancy than the overlap gains (cfg5 0.242 -> 0.277 ms), so the
+    // reads stay next to their use
+    const bool upd = u < ac;
+    C2 q[1][8];
+    double2 clr = make_double2(0.0, 0.0), cll = make_double2(0.0, 0.0);
+    auto load_corners = [&]() {
+#pragma unroll
+      for (int k = 0; k < 1; ++k) {
+        const int v = li * KR + k;
+        if (v < ar) {
+          const long long o1 = (long long)u * Sx + v + c.s1;
+          const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
+          q[k][0] = TR[o1];
+          q[k][1] = TR[o2];
+          q[k][2] = TL[o1];
+          q[k][3] = TL[o2];
+          q[k][4] = BR[o1];
+          q[k][5] = BR[o2];
+          q[k][6] = BL[o1];
+          q[k][7] = BL[o2];
+        }
+      }
+      clr = cl[ac + u];
+      cll = cl[u];
+    };
+    if constexpr (KR == 1) {
+      if (upd) load_corners();
+    }
     // the diagonal-segment walk along v:  S(0) = G + sum_i fullT_i,
     // S(v+1) = S(v) - fullT_v + fullB_v  (drop the leaving edge row, add the
     // entering one) — one exclusive scan of (fB - fT) plus one reduction of fT
@@ -170,23 +205,27 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
         }
       }
     }
-    if (u < ac) {
+    if (upd) {
       // corner products of column u (left) and bw+u (right), each formed once
-      const C2* TL = Cb;
-      const C2* TR = Cb + cstride;
-      const C2* BL = Cb + 2 * cstride;
-      const C2* BR = Cb + 3 * cstride;
-#pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const int v = li * KR + k;
-        if (v < ar) {
-          const long long o1 = (long long)u * Sx + v + c.s1;
-          const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
-          fT[k] = cadd(fT[k], csub(cmulconj<T>(TR[o1], TR[o2]), cmulconj<T>(TL[o1], TL[o2])));
-          fB[k] = cadd(fB[k], csub(cmulconj<T>(BR[o1], BR[o2]), cmulconj<T>(BL[o1], BL[o2])));
+      if constexpr (KR == 1) {
+        if (li < ar) {
+          fT[0] = cadd(fT[0], csub(cmulconj<T>(q[0][0], q[0][1]), cmulconj<T>(q[0][2], q[0][3])));
+          fB[0] = cadd(fB[0], csub(cmulconj<T>(q[0][4], q[0][5]), cmulconj<T>(q[0][6], q[0][7])));
         }
+        G = cadd(G, csub(clr, cll));
+      } else {
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const int v = li * KR + k;
+          if (v < ar) {
+            const long long o1 = (long long)u * Sx + v + c.s1;
+            const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
+            fT[k] = cadd(fT[k], csub(cmulconj<T>(TR[o1], TR[o2]), cmulconj<T>(TL[o1], TL[o2])));
+            fB[k] = cadd(fB[k], csub(cmulconj<T>(BR[o1], BR[o2]), cmulconj<T>(BL[o1], BL[o2])));
+          }
+        }
+        G = cadd(G, csub(cl[ac + u], cl[u]));
       }
-      G = cadd(G, csub(cl[ac + u], cl[u]));
     }
   }
 }
