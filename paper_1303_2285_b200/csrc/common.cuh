@@ -182,6 +182,20 @@ __device__ inline void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
     ns = ns < 2048 ? ns * 2 : 2048;
   }
 }
+// Wait until the band counter written by the host path's copy stream
+// (cuStreamWriteValue32 after each band's H2D copy) reaches `need`
+// (wrap-safe), then order the TMA (async proxy) reads after it.
+__device__ inline void wait_band(const unsigned* flag, unsigned need) {
+  unsigned ns = 64;
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - need) >= 0) break;
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : 1024;
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 // 3-D tensor tile -> SMEM, completion counted on `bar` (bytes)
 __device__ inline void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(

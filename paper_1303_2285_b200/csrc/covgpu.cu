@@ -107,6 +107,15 @@ struct covgpu_plan {
   const void* ecm_ptr = nullptr;
   CUtensorMap ecm_tm{};
   // edge-row sums on the tensor cores (P <= 65)
+  // host path streaming A in row bands (batch 1, tensor-core path): the
+  // copy stream bumps *d_band_flag after each band; k_bulk_dmma waits on it,
+  // the side-stream kernels wait for ev_h2d (the whole of A)
+  bool band_wait = false;
+  unsigned* d_band_flag = nullptr;
+  unsigned band_base = 0;
+  int band_rows = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_h2d = nullptr;
   bool use_erm = false;
   int erm_dct = 1;
   const void* erm_ptr = nullptr;
@@ -248,6 +257,9 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_tasks);
   cudaFree(pl->d_uc_off);
   cudaFree(pl->d_ecm_part);
+  cudaFree(pl->d_band_flag);
+  if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
+  if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
   cudaFree(pl->d_ecm_tickets);
 }
 
@@ -484,7 +496,7 @@ bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   const long long blocks = pl->batch * (long long)pl->n_drt * pl->n_dct * pl->mma_g;
   k_bulk_dmma<DC><<<(unsigned)blocks, (MMA_WARPS + 1) * 32, Cfg::smem, st>>>(
       pl->mtmx, pl->mtmy, pr, pl->n_drt, pl->n_dct, pl->mma_g, pl->nclasses, pl->d_cls_slot,
-      pl->d_ccpart);
+      pl->d_ccpart, pl->band_wait ? pl->d_band_flag : nullptr, pl->band_base, pl->band_rows);
   return true;
 }
 
@@ -627,6 +639,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(es, pl->ev_fork, 0));
   }
+  if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(es, pl->ev_h2d, 0));
   mark("start");
   // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
   // bulk over every column block (which also yields the edge-column sums)
@@ -636,7 +649,10 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       mma = pl->mma_dc == 32 ? launch_dmma<32>(pl, (const double2*)A, st)
                              : launch_dmma<64>(pl, (const double2*)A, st);
   }
-  if (!mma) launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
+  if (!mma) {
+    if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
+    launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
+  }
   const int npart = mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
   mark(mma ? "bulk_dmma" : "bulk");
@@ -1299,6 +1315,41 @@ static int execute_host_pipelined(covgpu_plan_t pl, const void* A_host, void* R_
   return COVGPU_OK;
 }
 
+// cuStreamWriteValue32 through the runtime's driver entry point (no -lcuda)
+static PFN_cuStreamWriteValue32_v11070 stream_write_value() {
+  static PFN_cuStreamWriteValue32_v11070 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+  }();
+  return fn;
+}
+
+// Stream A in row bands?  Single snapshot on the tensor-core path, A large
+// enough for the overlap to matter, the driver's stream write available.
+// Sets up the copy stream, band flag and event on first use.
+static bool stream_a_in_bands(covgpu_plan* pl, size_t a_bytes) {
+  if (!pl->use_mma || pl->batch != 1 || a_bytes < (8u << 20) || !stream_write_value()) return false;
+  if (const char* e = getenv("COVGPU_NO_BAND_H2D"))
+    if (atoi(e) != 0) return false;
+  if (!pl->d_band_flag) {
+    if (cudaMalloc(&pl->d_band_flag, sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(pl->d_band_flag, 0, sizeof(unsigned)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&pl->ev_h2d, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    pl->band_base = 0;
+  }
+  // ~16 bands, at least 64 rows each
+  pl->band_rows = std::max(64, (pl->pr.N + 15) / 16);
+  return true;
+}
+
 int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
                              double scale) {
   if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
@@ -1334,8 +1385,33 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
     pl->hR_bytes = r_bytes;
   }
   cudaStream_t st = pl->host_stream;
-  CUDA_TRY(cudaMemcpyAsync(pl->hA, A_host, a_bytes, cudaMemcpyHostToDevice, st));
-  int rc = covgpu_plan_execute(pl, pl->hA, pl->hR, layout, scale, st);
+  int rc;
+  if (stream_a_in_bands(pl, a_bytes)) {
+    // A in row bands on the copy stream, overlapped with the tensor-core
+    // bulk kernel (which waits per chunk for the band it reads)
+    const int nb = (pr.N + pl->band_rows - 1) / pl->band_rows;
+    const size_t row_bytes = (size_t)pr.M * esz;
+    auto wv = stream_write_value();
+    const unsigned base = pl->band_base;
+    for (int k = 0; k < nb; ++k) {
+      const int r0 = k * pl->band_rows, r1 = std::min(pr.N, r0 + pl->band_rows);
+      CUDA_TRY(cudaMemcpyAsync((char*)pl->hA + r0 * row_bytes, (const char*)A_host + r0 * row_bytes,
+                               (r1 - r0) * row_bytes, cudaMemcpyHostToDevice, pl->copy_stream));
+      if (wv(pl->copy_stream, (CUdeviceptr)pl->d_band_flag, base + (unsigned)k + 1u, 0) != CUDA_SUCCESS)
+        return fail(COVGPU_ECUDA, "cuStreamWriteValue32");
+    }
+    CUDA_TRY(cudaEventRecord(pl->ev_h2d, pl->copy_stream));
+    pl->band_wait = true;
+    rc = covgpu_plan_execute(pl, pl->hA, pl->hR, layout, scale, st);
+    pl->band_wait = false;
+    pl->band_base = base + (unsigned)nb;
+    // every later use of hA on `st` (the next execute's copies run on the
+    // copy stream) must follow this execute
+    if (!rc) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(pl->hA, A_host, a_bytes, cudaMemcpyHostToDevice, st));
+    rc = covgpu_plan_execute(pl, pl->hA, pl->hR, layout, scale, st);
+  }
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(R_host, pl->hR, r_bytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

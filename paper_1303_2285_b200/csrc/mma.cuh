@@ -21,8 +21,10 @@
 //
 // CTA = (snapshot, 32-lag tile, DC-lag tile, split p of G): 4 compute warps as
 // 2 (16 lags) x 2 (DC/2 lags) warp tiles and one TMA producer warp.  The
-// CTA's K range is a contiguous run of (16-row x 32-column) chunks of the
-// tile's rows x columns, split evenly over the G CTAs of the tile; each
+// tile's (16-row x 32-column) chunks, row-major, are dealt round-robin to
+// its G CTAs (chunks p, p+G, ...), so all CTAs sweep A top to bottom
+// together — which lets the host path stream A in row bands while the kernel
+// runs (band_flag: the producer waits for the band a chunk needs); each
 // chunk is one TMA stage: X = the 47 first-element rows x 36 columns the 16
 // rows' 32 lags touch, Y = the 16 second-element rows x (32+DC) columns.  The
 // CTA writes its 32 x DC partial sums to the class's partial slot p; the
@@ -132,7 +134,8 @@ template <int DC>
 __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
     k_bulk_dmma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                 Problem pr, int n_drt, int n_dct, int G, int nclasses,
-                const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+                const int* __restrict__ cls_slot, double2* __restrict__ ccpart,
+                const unsigned* __restrict__ band_flag, unsigned band_base, int band_rows) {
   using Cfg = MmaCfg<DC>;
   constexpr int NT = Cfg::NT, YP = Cfg::YP, S = MMA_STAGES;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
   const int xcols = M - Q + 1;  // first-element columns of core products
   const int ncbk = (xcols + MMA_W - 1) / MMA_W;
   const long long nch = (long long)nrc * ncbk;
-  const long long q0 = nch * p / G, q1 = nch * (p + 1) / G;
+  const long long nmine = p < nch ? (nch - p + G - 1) / G : 0;  // chunks p, p+G, ...
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -170,12 +173,16 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
 
   if (w == MMA_WARPS) {  // producer
     if (lane == 0) {
-      for (long long k = 0; k < q1 - q0; ++k) {
+      for (long long k = 0; k < nmine; ++k) {
         const int s = (int)(k % S);
         if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
-        const long long q = q0 + k;
+        const long long q = p + k * G;
         const int R = rlo + (int)(q / ncbk) * MMA_RC;
         const int C0 = (int)(q % ncbk) * MMA_W;
+        if (band_flag) {  // A still streaming in: wait for the last row this chunk reads
+          const int rneed = min(N - 1, R + MMA_RC - 1 + max(-dr0, 0));
+          wait_band(band_flag, band_base + (unsigned)(rneed / band_rows) + 1u);
+        }
         unsigned char* st = smraw + s * Cfg::stage;
         mbar_expect_tx(&full[s], (unsigned)(Cfg::xbytes + Cfg::ybytes));
         tma_load_3d(st, &tmx, 2 * C0, R - dr0 - (MMA_DR - 1), b, &full[s]);
@@ -196,10 +203,10 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
   const int xrow0 = MMA_DR - 1 - 16 * wm - m;
   const int ycol0 = kq + wn * (DC / 2) + m;
 
-  for (long long k = 0; k < q1 - q0; ++k) {
+  for (long long k = 0; k < nmine; ++k) {
     const int s = (int)(k % S);
     mbar_wait(&full[s], (int)((k / S) & 1));
-    const long long q = q0 + k;
+    const long long q = p + k * G;
     const int R = rlo + (int)(q / ncbk) * MMA_RC;
     const int C0 = (int)(q % ncbk) * MMA_W;
     const int nks = min(MMA_W, xcols - C0 + 3) / 4;

@@ -529,3 +529,26 @@ def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, monkey
         err_cc = (torch.linalg.norm(got[b] - ref_cc[b]) / torch.linalg.norm(ref_cc[b])).item()
         assert err <= TOL64, err
         assert err_cc <= 1e-13, err_cc
+
+
+def test_host_path_streams_a_in_bands_bitwise(cuda):
+    """Single-snapshot host path on the tensor-core kernels: A is copied in
+    row bands while k_bulk_dmma runs (band counter written by the copy
+    stream); R must equal the device-resident result bit for bit, twice in a
+    row (the band counter carries over between executes)."""
+    from paper_1303_2285_b200.plan import Plan
+
+    n = m = 1024
+    p = q = 64
+    rng = np.random.default_rng(5)
+    a = torch.from_numpy(rng.standard_normal((1, n, m)) + 1j * rng.standard_normal((1, n, m))).pin_memory()
+    win = WindowSpec(p, q)
+    plan = Plan(n, m, win, dtype=torch.complex128, device=cuda)
+    dev = plan.alloc_output("packed")
+    plan.execute(a.to(cuda), dev, "packed")
+    out = torch.empty(plan.output_elems("packed"), dtype=torch.complex128).pin_memory()
+    for _ in range(2):
+        out.zero_()
+        plan.execute_host(a, out, "packed")
+        assert torch.equal(out, dev.cpu())
+    plan.close()
