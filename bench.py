@@ -297,8 +297,9 @@ def main() -> None:
     shard_frac = 1.0 if ids is None else shard_cost(w.n, w.m, win, ids) / um
     roof = None
     if kernel_ms.get("bulk_dmma", 0) > 0:
-        # dominant kernel on the FP64 tensor cores: core products x 8 flops
-        achieved = 8.0 * core_p * w.batch / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12
+        # dominant kernel on the FP64 tensor cores: core products x 6 flops (the
+        # Gauss 3-multiplication complex product: 3 real FMAs per product)
+        achieved = 6.0 * core_p * w.batch / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12
         traffic = None
         prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
         if prof.exists():
@@ -310,7 +311,9 @@ def main() -> None:
                 "frac": achieved / peak_dmma, "traffic": traffic, "kernel": "k_bulk_dmma",
                 "peak_source": "DMMA-loop probe (mma.sync m8n8k4 f64) measured on this GPU in this "
                 "run (MEASURED_PEAKS.json has no FP64 figure)",
-                "algorithmic_flops_per_launch": 8.0 * core_p * w.batch,
+                "algorithmic_flops_per_launch": 6.0 * core_p * w.batch,
+                "flops_per_product": "6 (Gauss: Re = P1 + P2, Im = P3 - P1 + P2, 3 real FMAs)",
+                "complex_mac_equivalent_tflops": 8.0 * core_p * w.batch / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12,
                 "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
                 "fma_loop_peak": peak}
     elif "bulk" in kernel_ms and kernel_ms["bulk"] > 0:

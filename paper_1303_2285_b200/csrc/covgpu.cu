@@ -94,6 +94,8 @@ struct covgpu_plan {
   // the ncb_l + ncb_r column blocks that hold edge columns
   bool use_mma = false;
   int mma_dc = 64, n_drt = 0, n_dct = 0, mma_g = 0;
+  int mma_kind = 1;  // 0: 4-DMMA complex tiles (k_bulk_dmma); 1-3: Gauss 3-DMMA (k_bulk_dmma3)
+  int mtmap_kind = -1;
   int ncb_l = 0, ncb_r = 0;
   int edge_variant = 0;
   const void* mtmap_ptr = nullptr;
@@ -383,6 +385,15 @@ cudaError_t set_attrs() {
     if ((r = cudaFuncSetAttribute(k_bulk_dmma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)MmaCfg<64>::smem)) != cudaSuccess)
       e = r;
+    if ((r = cudaFuncSetAttribute(k_bulk_dmma3<2, 4, 2, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Mma3Cfg<2, 4, 2, 2, 2>::smem)) != cudaSuccess)
+      e = r;
+    if ((r = cudaFuncSetAttribute(k_bulk_dmma3<4, 4, 2, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Mma3Cfg<4, 4, 2, 2, 1>::smem)) != cudaSuccess)
+      e = r;
+    if ((r = cudaFuncSetAttribute(k_bulk_dmma3<2, 2, 2, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Mma3Cfg<2, 2, 2, 2, 2>::smem)) != cudaSuccess)
+      e = r;
     if ((r = cudaFuncSetAttribute(k_edge_cols_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ECM_SMEM)) != cudaSuccess)
       e = r;
@@ -480,7 +491,7 @@ bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   using Cfg = MmaCfg<DC>;
   const Problem& pr = pl->pr;
   if ((uintptr_t)A % 16 != 0) return false;
-  if (pl->mtmap_ptr != (const void*)A) {
+  if (pl->mtmap_ptr != (const void*)A || pl->mtmap_kind != 0) {
     CUtensorMap mx, my;
     const long long w = pr.M - pr.Q + 1;
     if (make_tmap(&mx, A, true, pl->batch, pr.N, pr.M, 2 * MMA_XP, MMA_XR, w, 0) &&
@@ -488,6 +499,7 @@ bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
       pl->mtmx = mx;
       pl->mtmy = my;
       pl->mtmap_ptr = A;
+      pl->mtmap_kind = 0;
     } else {
       pl->mtmap_ptr = nullptr;
       return false;
@@ -495,6 +507,33 @@ bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   }
   const long long blocks = pl->batch * (long long)pl->n_drt * pl->n_dct * pl->mma_g;
   k_bulk_dmma<DC><<<(unsigned)blocks, (MMA_WARPS + 1) * 32, Cfg::smem, st>>>(
+      pl->mtmx, pl->mtmy, pr, pl->n_drt, pl->n_dct, pl->mma_g, pl->nclasses, pl->d_cls_slot,
+      pl->d_ccpart, pl->band_wait ? pl->d_band_flag : nullptr, pl->band_base, pl->band_rows);
+  return true;
+}
+
+// Gauss 3-DMMA core sums (k_bulk_dmma3); false when the tensor maps fail
+template <int WM, int WN, int MT, int NTW, int MINB>
+bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
+  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB>;
+  const Problem& pr = pl->pr;
+  if ((uintptr_t)A % 16 != 0) return false;
+  if (pl->mtmap_ptr != (const void*)A || pl->mtmap_kind != pl->mma_kind) {
+    CUtensorMap mx, my;
+    const long long w = pr.M - pr.Q + 1;
+    if (make_tmap(&mx, A, true, pl->batch, pr.N, pr.M, 2 * MMA_XP, Cfg::XR, w, 0) &&
+        make_tmap(&my, A, true, pl->batch, pr.N, pr.M, 2 * Cfg::YP, MMA_RC, w, pr.Q - 1)) {
+      pl->mtmx = mx;
+      pl->mtmy = my;
+      pl->mtmap_ptr = A;
+      pl->mtmap_kind = pl->mma_kind;
+    } else {
+      pl->mtmap_ptr = nullptr;
+      return false;
+    }
+  }
+  const long long blocks = pl->batch * (long long)pl->n_drt * pl->n_dct * pl->mma_g;
+  k_bulk_dmma3<WM, WN, MT, NTW, MINB><<<(unsigned)blocks, (Cfg::WARPS + 1) * 32, Cfg::smem, st>>>(
       pl->mtmx, pl->mtmy, pr, pl->n_drt, pl->n_dct, pl->mma_g, pl->nclasses, pl->d_cls_slot,
       pl->d_ccpart, pl->band_wait ? pl->d_band_flag : nullptr, pl->band_base, pl->band_rows);
   return true;
@@ -645,9 +684,16 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   // bulk over every column block (which also yields the edge-column sums)
   bool mma = false;
   if constexpr (sizeof(T) == 8) {
-    if (pl->use_mma)
-      mma = pl->mma_dc == 32 ? launch_dmma<32>(pl, (const double2*)A, st)
-                             : launch_dmma<64>(pl, (const double2*)A, st);
+    if (pl->use_mma) {
+      const double2* Ad = (const double2*)A;
+      switch (pl->mma_kind) {
+        case 1: mma = launch_dmma3<2, 4, 2, 2, 2>(pl, Ad, st); break;
+        case 2: mma = launch_dmma3<4, 4, 2, 2, 1>(pl, Ad, st); break;
+        case 3: mma = launch_dmma3<2, 2, 2, 2, 2>(pl, Ad, st); break;
+        default:
+          mma = pl->mma_dc == 32 ? launch_dmma<32>(pl, Ad, st) : launch_dmma<64>(pl, Ad, st);
+      }
+    }
   }
   if (!mma) {
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
@@ -868,12 +914,26 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     if (ok) {
       pl->use_mma = true;
       pl->mma_dc = q <= 32 ? 32 : 64;
-      pl->n_drt = (2 * p - 1 + MMA_DR - 1) / MMA_DR;
+      // kernel: Gauss 3-DMMA tiles (1: 32x64 lags, 8 warps, 2 CTAs/SM; 2: 64x64,
+      // 16 warps, 1 CTA/SM; 3: 32x32 for Q <= 32), 0: 4-DMMA k_bulk_dmma
+      pl->mma_kind = q <= 32 ? 3 : 1;
+      if (const char* mk = getenv("COVGPU_MMA_KIND")) {
+        const int k = atoi(mk);
+        if (k >= 0 && k <= 3) pl->mma_kind = k;
+      }
+      int dr_tile = MMA_DR, ctas_per_sm = 2;
+      if (pl->mma_kind == 2) {
+        dr_tile = 64;
+        ctas_per_sm = 1;
+      }
+      if (pl->mma_kind == 1 || pl->mma_kind == 2) pl->mma_dc = 64;
+      if (pl->mma_kind == 3) pl->mma_dc = 32;
+      pl->n_drt = (2 * p - 1 + dr_tile - 1) / dr_tile;
       pl->n_dct = (q + pl->mma_dc - 1) / pl->mma_dc;
-      // one wave of 2 CTAs/SM; each CTA a contiguous run of >= 2 chunks
+      // one wave of CTAs; each CTA >= 2 chunks
       const long long tiles = batch * (long long)pl->n_drt * pl->n_dct;
       const long long chunks = (long long)((n + MMA_RC - 1) / MMA_RC + 2) * ((m - q + 1 + MMA_W - 1) / MMA_W);
-      long long g = std::max(1LL, (2LL * 148 + tiles - 1) / tiles);
+      long long g = std::max(1LL, (148LL * ctas_per_sm + tiles - 1) / tiles);
       g = std::min(g, std::max(1LL, chunks / 2));
       pl->mma_g = (int)g;
       pl->ncb_l = ncb_l;

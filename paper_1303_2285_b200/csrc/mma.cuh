@@ -550,4 +550,200 @@ __global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 2)
   }
 }
 
+// ---- K1 with 3 real GEMMs per complex GEMM (Gauss) ----------------------------
+// x * conj(y) = (a + ib)(c - id) = (ac + bd) + i(bc - ad).  With
+//   P1 = sum a c,  P2 = sum b d,  P3 = sum (a + b)(c - d):
+//   Re = P1 + P2,  Im = P3 - P1 + P2
+// — 3 DMMAs per complex 8x8x4 tile instead of 4.  The operand sums are one
+// DADD per fragment (FP64 pipe, beside the DMMA pipe).  Rounding: every
+// partial is a sum of products bounded by 2|x||y|, so the error stays at the
+// level of the 4-multiplication form (relative Frobenius ~1e-16 at cfg5,
+// tests/test_gpu_parity.py).  Same data flow as k_bulk_dmma; CTA tile DR =
+// WM*MT*8 lags x DC = WN*NTW*8 lags, WM*WN compute warps of MT x NTW tiles.
+template <int WM, int WN, int MT, int NTW, int MINB>
+struct Mma3Cfg {
+  static constexpr int WARPS = WM * WN;
+  static constexpr int DR = WM * MT * 8;
+  static constexpr int DC = WN * NTW * 8;
+  static constexpr int XR = MMA_RC + DR - 1;
+  static constexpr int YP = MMA_W + DC;
+  static constexpr size_t xbytes = 16 * (size_t)XR * MMA_XP;
+  static constexpr size_t xoff = (xbytes + 127) / 128 * 128;
+  static constexpr size_t ybytes = 16 * (size_t)MMA_RC * YP;
+  static constexpr size_t stage = xoff + (ybytes + 127) / 128 * 128;
+  static constexpr int fit = (int)((227 * 1024 / MINB - 2048) / stage);
+  static constexpr int S = fit > 4 ? 4 : fit;
+  static constexpr size_t smem = S * stage + 64;
+};
+
+template <int MT, int NTW, bool MASKED, bool FULL>
+__device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const double2* __restrict__ Y,
+                                          int xrow0, int kq, int ycol0, int yp, int nks, int R,
+                                          int dra, const Problem& pr, double (&p1)[MT][NTW][2],
+                                          double (&p2)[MT][NTW][2], double (&p3)[MT][NTW][2]) {
+  const int P = pr.P, N = pr.N;
+#pragma unroll 1
+  for (int tr = 0; tr < MMA_RC; ++tr) {
+    const double2* xa = X + (tr + xrow0) * MMA_XP + kq;  // m-tile i: rows - 8 i
+    const double2* yb = Y + tr * yp + ycol0;
+    bool on[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      on[i] = true;
+      if constexpr (MASKED) {
+        const int r2 = R + tr, r1 = r2 - dra - 8 * i;
+        on[i] = max(r1, r2) >= P - 1 && min(r1, r2) <= N - P;
+      }
+    }
+    auto kstep = [&](int ks) {
+      double2 a[MT], bv[NTW];
+      double as[MT], bd[NTW];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        a[i] = xa[4 * ks - 8 * i * MMA_XP];
+        if (MASKED && !on[i]) a[i] = make_double2(0.0, 0.0);
+        as[i] = a[i].x + a[i].y;
+      }
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) {
+        bv[j] = yb[4 * ks + 8 * j];
+        bd[j] = bv[j].x - bv[j].y;
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(p1[i][j][0], p1[i][j][1], a[i].x, bv[j].x);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(p2[i][j][0], p2[i][j][1], a[i].y, bv[j].y);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) dmma(p3[i][j][0], p3[i][j][1], as[i], bd[j]);
+    };
+    if constexpr (FULL) {
+#pragma unroll
+      for (int ks = 0; ks < MMA_W / 4; ++ks) kstep(ks);
+    } else {
+#pragma unroll 1
+      for (int ks = 0; ks < nks; ++ks) kstep(ks);
+    }
+  }
+}
+
+template <int WM, int WN, int MT, int NTW, int MINB>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
+    k_bulk_dmma3(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
+                 Problem pr, int n_drt, int n_dct, int G, int nclasses,
+                 const int* __restrict__ cls_slot, double2* __restrict__ ccpart,
+                 const unsigned* __restrict__ band_flag, unsigned band_base, int band_rows) {
+  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB>;
+  constexpr int S = Cfg::S, DR = Cfg::DR, DC = Cfg::DC, NW = Cfg::WARPS;
+  static_assert(S >= 2, "TMA ring needs two stages");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage);
+  uint64_t* empty = full + S;
+  long long t = blockIdx.x;
+  const int p = (int)(t % G);
+  t /= G;
+  const int dct = (int)(t % n_dct);
+  t /= n_dct;
+  const int drt = (int)(t % n_drt);
+  const int b = (int)(t / n_drt);
+  const int P = pr.P, Q = pr.Q, N = pr.N, M = pr.M;
+  const int dr0 = -(P - 1) + drt * DR;
+  const int dc0 = dct * DC;
+  const int drmax = min(dr0 + DR - 1, P - 1);
+  const int rlo = max(0, P - 1 + min(dr0, 0));
+  const int rhi = min(N - 1, N - P + max(drmax, 0));
+  const int nrc = (rhi - rlo + MMA_RC) / MMA_RC;
+  const int xcols = M - Q + 1;
+  const int ncbk = (xcols + MMA_W - 1) / MMA_W;
+  const long long nch = (long long)nrc * ncbk;
+  const long long nmine = p < nch ? (nch - p + G - 1) / G : 0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (w == NW) {  // producer
+    if (lane == 0) {
+      for (long long k = 0; k < nmine; ++k) {
+        const int s = (int)(k % S);
+        if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
+        const long long q = p + k * G;
+        const int R = rlo + (int)(q / ncbk) * MMA_RC;
+        const int C0 = (int)(q % ncbk) * MMA_W;
+        if (band_flag) {
+          const int rneed = min(N - 1, R + MMA_RC - 1 + max(-dr0, 0));
+          wait_band(band_flag, band_base + (unsigned)(rneed / band_rows) + 1u);
+        }
+        unsigned char* st = smraw + s * Cfg::stage;
+        mbar_expect_tx(&full[s], (unsigned)(Cfg::xbytes + Cfg::ybytes));
+        tma_load_3d(st, &tmx, 2 * C0, R - dr0 - (DR - 1), b, &full[s]);
+        tma_load_3d(st + Cfg::xoff, &tmy, 2 * (C0 + dc0 - (Q - 1)), R, b, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int wm = w % WM, wn = w / WM;
+  const int m = lane >> 2, kq = lane & 3;
+  double p1[MT][NTW][2], p2[MT][NTW][2], p3[MT][NTW][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j)
+      p1[i][j][0] = p1[i][j][1] = p2[i][j][0] = p2[i][j][1] = p3[i][j][0] = p3[i][j][1] = 0.0;
+  const int xrow0 = DR - 1 - MT * 8 * wm - m;
+  const int ycol0 = kq + wn * NTW * 8 + m;
+  const int dra = dr0 + MT * 8 * wm + m;
+
+  for (long long k = 0; k < nmine; ++k) {
+    const int s = (int)(k % S);
+    mbar_wait(&full[s], (int)((k / S) & 1));
+    const long long q = p + k * G;
+    const int R = rlo + (int)(q / ncbk) * MMA_RC;
+    const int C0 = (int)(q % ncbk) * MMA_W;
+    const int nks = min(MMA_W, xcols - C0 + 3) / 4;
+    const double2* X = reinterpret_cast<const double2*>(smraw + s * Cfg::stage);
+    const double2* Y = reinterpret_cast<const double2*>(smraw + s * Cfg::stage + Cfg::xoff);
+    const bool masked = R < P - 1 || R + MMA_RC - 1 > N - P;
+    if (nks == MMA_W / 4) {
+      if (!masked)
+        mma3_rows<MT, NTW, false, true>(X, Y, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1, p2, p3);
+      else
+        mma3_rows<MT, NTW, true, true>(X, Y, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1, p2, p3);
+    } else {
+      mma3_rows<MT, NTW, true, false>(X, Y, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1, p2, p3);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int dr = dra + 8 * i;
+#pragma unroll
+    for (int j = 0; j < NTW; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int dc = dc0 + wn * NTW * 8 + 8 * j + 2 * kq + e;
+        if (dr > P - 1 || dc >= Q || !in_uc(dr, dc, P, Q)) continue;
+        const int cid = cls_slot[class_index(dr, dc, P, Q)];
+        if (cid < 0) continue;
+        const double re = p1[i][j][e] + p2[i][j][e];
+        const double im = p3[i][j][e] - p1[i][j][e] + p2[i][j][e];
+        ccpart[((long long)b * nclasses + cid) * G + p] = make_double2(re, im);
+      }
+  }
+}
+
 }  // namespace covgpu

@@ -354,14 +354,18 @@ def test_cfg4_all_snapshots_against_gpu_gram(cuda):
 
 
 def test_exact_algebraic_properties(cuda):
-    """Size-independent identities at cfg5 size: R(2A) = 4 R(A) and
-    R(conj A) = conj R(A), both bit for bit; trace = weighted |A|^2 sum."""
+    """Size-independent identities at cfg5 size: R(2A) = 4 R(A) bit for bit
+    (power-of-two scaling is exact in every operation, including the Gauss
+    operand sums of the tensor-core kernel); R(conj A) = conj R(A) to 1e-15
+    (the 3-multiplication form rounds (a-b)(c+d) and (a+b)(c-d) differently,
+    so this one is not bitwise); trace = weighted |A|^2 sum."""
     w = workload("cfg5")
     a = torch.as_tensor(make_input(w), device=cuda)
     win = WindowSpec(w.p, w.q)
     r = estimate_tensor(a, win)
     assert torch.equal(estimate_tensor(2 * a, win), 4 * r)
-    assert torch.equal(estimate_tensor(a.conj().resolve_conj(), win), r.conj())
+    rc = estimate_tensor(a.conj().resolve_conj(), win)
+    assert (torch.linalg.norm(rc - r.conj()) / torch.linalg.norm(r)).item() <= 1e-15
     # trace: element (i, j) lies in cnt_r(i) * cnt_c(j) windows
     n, m, p, q = w.n, w.m, w.p, w.q
     ri = torch.arange(n, device=cuda)
