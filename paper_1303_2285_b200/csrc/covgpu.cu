@@ -994,12 +994,12 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     if (const char* ne = getenv("COVGPU_NO_MMA_EDGE")) erm = atoi(ne) == 0;
     if (erm) {
       // CTA = (snapshot, strip, r2, lag tile, column segment): >= ~3 waves of
-      // 2 CTAs/SM with >= 2 column chunks per segment
+      // 1 CTA/SM with >= 2 column chunks per segment
       pl->use_erm = true;
       pl->erm_dct = (q + ERM_DC - 1) / ERM_DC;
       const long long per = batch * 2LL * (p - 1) * pl->erm_dct;
       const long long chunks = (m - q + 1 + MMA_W - 1) / MMA_W;
-      long long seg = std::max(1LL, (3LL * 296 + per - 1) / per);
+      long long seg = std::max(1LL, (3LL * 148 + per - 1) / per);
       seg = std::min(seg, std::max(1LL, chunks / 2));
       pl->nseg = (int)std::min(seg, 16LL);
     }

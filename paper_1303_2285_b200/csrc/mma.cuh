@@ -283,12 +283,13 @@ __device__ __forceinline__ EcmItem ecm_item(long long item, const Problem& pr) {
 
 template <int W>
 __device__ __forceinline__ void ecm_consume(const unsigned char* smraw, uint64_t* full, uint64_t* empty,
-                                            int nchunks, int R0, int hi, int nt, double (&cr)[ECM_SLOTS][2],
-                                            double (&ci)[ECM_SLOTS][2]) {
+                                            int nchunks, int R0, int hi, int nt, double (&p1)[ECM_SLOTS][2],
+                                            double (&p2)[ECM_SLOTS][2], double (&p3)[ECM_SLOTS][2]) {
   const int lane = threadIdx.x & 31, m = lane >> 2, kq = lane & 3;
 #pragma unroll
-  for (int sl = 0; sl < ECM_SLOTS; ++sl) cr[sl][0] = cr[sl][1] = ci[sl][0] = ci[sl][1] = 0.0;
-  constexpr int NB = 8 - W;  // B tiles tj in [W, 8)
+  for (int sl = 0; sl < ECM_SLOTS; ++sl)
+    p1[sl][0] = p1[sl][1] = p2[sl][0] = p2[sl][1] = p3[sl][0] = p3[sl][1] = 0.0;
+  constexpr int NB = 8 - W;  // slots (W, W+sl) for sl < NB, then (7-W, 7-W + sl-NB)
   for (int k = 0; k < nchunks; ++k) {
     const int s = k % ECM_STAGES;
     mbar_wait(&full[s], (k / ECM_STAGES) & 1);
@@ -301,24 +302,22 @@ __device__ __forceinline__ void ecm_consume(const unsigned char* smraw, uint64_t
       const bool on = R + row <= hi;
       double2 a0 = X[row * ECM_PITCH + 8 * W + m], a1 = X[row * ECM_PITCH + 8 * (7 - W) + m];
       if (!on) a0 = a1 = make_double2(0.0, 0.0);
-      const double na0 = -a0.x, na1 = -a1.x;
-      double2 bv[NB];
+      const double s0 = a0.x + a0.y, s1 = a1.x + a1.y;
+      // Gauss form per slot: P1 += a.x b.x, P2 += a.y b.y, P3 += (a.x+a.y)(b.x-b.y);
+      // B fragments loaded per slot (keeps registers for 2 CTAs/SM)
 #pragma unroll
-      for (int j = 0; j < NB; ++j) bv[j] = Y[row * ECM_PITCH + 8 * (W + j) + m];
-      // slot sl: (W, W+sl) for sl < NB, else (7-W, 7-W + sl-NB) = B index 7-2W + sl-NB
-#define ECM_PASS(ACC, AX, BX)                                              \
-  _Pragma("unroll") for (int sl = 0; sl < ECM_SLOTS; ++sl) {               \
-    const int bj = sl < NB ? sl : 7 - 2 * W + (sl - NB);                   \
-    if (W + bj < nt) {                                                     \
-      const double2& av = sl < NB ? a0 : a1;                               \
-      dmma(ACC[sl][0], ACC[sl][1], AX, BX);                                \
-    }                                                                      \
-  }
-      ECM_PASS(cr, av.x, bv[bj].x)
-      ECM_PASS(ci, av.y, bv[bj].x)
-      ECM_PASS(cr, av.y, bv[bj].y)
-      ECM_PASS(ci, (sl < NB ? na0 : na1), bv[bj].y)
-#undef ECM_PASS
+      for (int sl = 0; sl < ECM_SLOTS; ++sl) {
+        const int tj = sl < NB ? W + sl : 7 - W + (sl - NB);
+        if (tj < nt) {
+          const double2 bv = Y[row * ECM_PITCH + 8 * tj + m];
+          const double bd = bv.x - bv.y;
+          const double2& av = sl < NB ? a0 : a1;
+          const double as = sl < NB ? s0 : s1;
+          dmma(p1[sl][0], p1[sl][1], av.x, bv.x);
+          dmma(p2[sl][0], p2[sl][1], av.y, bv.y);
+          dmma(p3[sl][0], p3[sl][1], as, bd);
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -366,11 +365,21 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
   const int nt = (Q - 1 + 7) / 8;
   const int R0 = it.lo + c0 * ECM_RC;
   double cr[ECM_SLOTS][2], ci[ECM_SLOTS][2];
-  switch (w) {
-    case 0: ecm_consume<0>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci); break;
-    case 1: ecm_consume<1>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci); break;
-    case 2: ecm_consume<2>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci); break;
-    default: ecm_consume<3>(smraw, full, empty, c1 - c0, R0, it.hi, nt, cr, ci);
+  {
+    double p1[ECM_SLOTS][2], p2[ECM_SLOTS][2], p3[ECM_SLOTS][2];
+    switch (w) {
+      case 0: ecm_consume<0>(smraw, full, empty, c1 - c0, R0, it.hi, nt, p1, p2, p3); break;
+      case 1: ecm_consume<1>(smraw, full, empty, c1 - c0, R0, it.hi, nt, p1, p2, p3); break;
+      case 2: ecm_consume<2>(smraw, full, empty, c1 - c0, R0, it.hi, nt, p1, p2, p3); break;
+      default: ecm_consume<3>(smraw, full, empty, c1 - c0, R0, it.hi, nt, p1, p2, p3);
+    }
+#pragma unroll
+    for (int sl = 0; sl < ECM_SLOTS; ++sl)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        cr[sl][e] = p1[sl][e] + p2[sl][e];
+        ci[sl][e] = p3[sl][e] - p1[sl][e] + p2[sl][e];
+      }
   }
   if (G > 1) {
     double2* mine = part + (item * G + g) * ECM_PART + (long long)w * ECM_SLOTS * 64;
@@ -434,15 +443,18 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
 // and the finalize adds them in order.
 constexpr int ERM_XR = 64;  // strip rows per tile (P-1 <= 64)
 constexpr int ERM_DC = 64;
-constexpr int ERM_WARPS = 8;  // 2 (32 rows) x 4 (16 lags) warp tiles
+constexpr int ERM_WM = 4, ERM_WN = 4;    // warp grid: rows x lags
+constexpr int ERM_WARPS = ERM_WM * ERM_WN;
+constexpr int ERM_MT = ERM_XR / 8 / ERM_WM;  // 8-row tiles per warp
+constexpr int ERM_NT = ERM_DC / 8 / ERM_WN;  // 8-lag tiles per warp
 constexpr int ERM_YP = MMA_W + ERM_DC;
 constexpr size_t ERM_XBYTES = 16 * (size_t)ERM_XR * MMA_XP;
 constexpr size_t ERM_YBYTES = 16 * (size_t)ERM_YP;
 constexpr size_t ERM_STAGE = ERM_XBYTES + (ERM_YBYTES + 127) / 128 * 128;
-constexpr int ERM_STAGES = 2;
+constexpr int ERM_STAGES = 4;
 constexpr size_t ERM_SMEM = ERM_STAGES * ERM_STAGE + 64;
 
-__global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 2)
+__global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 1)
     k_edge_rows_dmma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                      Problem pr, int n_dct, int nseg, const int* __restrict__ cls_slot,
                      const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc) {
@@ -487,65 +499,71 @@ __global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 2)
     }
     return;
   }
-  const int wm = w & 1, wn = w >> 1, m = lane >> 2, kq = lane & 3;
-  double cr[4][2][2], ci[4][2][2];
+  const int wm = w % ERM_WM, wn = w / ERM_WM, m = lane >> 2, kq = lane & 3;
+  constexpr int MT = ERM_MT, NT = ERM_NT;
+  double p1[MT][NT][2], p2[MT][NT][2], p3[MT][NT][2];  // Gauss form (see k_bulk_dmma3)
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j)
+      p1[i][j][0] = p1[i][j][1] = p2[i][j][0] = p2[i][j][1] = p3[i][j][0] = p3[i][j][1] = 0.0;
   for (int k = 0; k < k1 - k0; ++k) {
     const int s = k % ERM_STAGES;
     mbar_wait(&full[s], (k / ERM_STAGES) & 1);
-    const double2* X = reinterpret_cast<const double2*>(smraw + s * ERM_STAGE) + (32 * wm + m) * MMA_XP + kq;
-    const double2* Y = reinterpret_cast<const double2*>(smraw + s * ERM_STAGE + ERM_XBYTES) + kq + 16 * wn + m;
+    const double2* X =
+        reinterpret_cast<const double2*>(smraw + s * ERM_STAGE) + (8 * MT * wm + m) * MMA_XP + kq;
+    const double2* Y =
+        reinterpret_cast<const double2*>(smraw + s * ERM_STAGE + ERM_XBYTES) + kq + 8 * NT * wn + m;
     const int nks = min(MMA_W, xcols - (k0 + k) * MMA_W + 3) / 4;
 #pragma unroll 1
     for (int ks = 0; ks < nks; ++ks) {
-      double2 a[4], bv[2];
+      double2 a[MT], bv[NT];
+      double as[MT], bd[NT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = X[8 * i * MMA_XP + 4 * ks];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) bv[j] = Y[8 * j + 4 * ks];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].x, bv[j].x);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].y, bv[j].x);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].y, bv[j].y);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double nx = -a[i].x;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], nx, bv[j].y);
+      for (int i = 0; i < MT; ++i) {
+        a[i] = X[8 * i * MMA_XP + 4 * ks];
+        as[i] = a[i].x + a[i].y;
       }
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        bv[j] = Y[8 * j + 4 * ks];
+        bd[j] = bv[j].x - bv[j].y;
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(p1[i][j][0], p1[i][j][1], a[i].x, bv[j].x);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(p2[i][j][0], p2[i][j][1], a[i].y, bv[j].y);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(p3[i][j][0], p3[i][j][1], as[i], bd[j]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   // RC' of pane row min(r1, r2) (strip-relative) of class (r2 - r1, dc)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r1 = 32 * wm + 8 * i + m;
+  for (int i = 0; i < MT; ++i) {
+    const int r1 = 8 * MT * wm + 8 * i + m;
     if (r1 >= S) continue;
     const int dr = r2 - r1;
     const int row = min(r1, r2);
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int dc = dc0 + 16 * wn + 8 * j + 2 * kq + e;
+        const int dc = dc0 + 8 * NT * wn + 8 * j + 2 * kq + e;
         if (dc >= Q || !in_uc(dr, dc, P, Q)) continue;
         const int cid = cls_slot[class_index(dr, dc, P, Q)];
         if (cid < 0) continue;
         const ClassDesc& cd = cls[cid];
         const int kk = strip ? cd.pv - 1 + row : row;
-        rc[((long long)b * tot_rc + cd.rc_off + kk) * nseg + seg] = make_double2(cr[i][j][e], ci[i][j][e]);
+        rc[((long long)b * tot_rc + cd.rc_off + kk) * nseg + seg] =
+            make_double2(p1[i][j][e] + p2[i][j][e], p3[i][j][e] - p1[i][j][e] + p2[i][j][e]);
       }
   }
 }
