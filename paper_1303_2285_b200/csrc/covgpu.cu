@@ -993,14 +993,23 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     bool erm = true;
     if (const char* ne = getenv("COVGPU_NO_MMA_EDGE")) erm = atoi(ne) == 0;
     if (erm) {
-      // CTA = (snapshot, strip, r2, lag tile, column segment): >= ~3 waves of
-      // 1 CTA/SM with >= 2 column chunks per segment
+      // CTA = (snapshot, strip, r2, lag tile, column segment), 1 CTA/SM: the
+      // segment count with the best wave fill (>= 2 column chunks each;
+      // cfg5: 126 x 7 = 882 CTAs = 5.96 waves)
       pl->use_erm = true;
       pl->erm_dct = (q + ERM_DC - 1) / ERM_DC;
       const long long per = batch * 2LL * (p - 1) * pl->erm_dct;
       const long long chunks = (m - q + 1 + MMA_W - 1) / MMA_W;
-      long long seg = std::max(1LL, (3LL * 148 + per - 1) / per);
-      seg = std::min(seg, std::max(1LL, chunks / 2));
+      long long seg = 1;
+      double best = 0.0;
+      for (long long g = 1; g <= 16 && (g == 1 || chunks / g >= 2); ++g) {
+        const double ctas = (double)per * g, waves = std::ceil(ctas / 148.0);
+        const double eff = ctas / (waves * 148.0) * std::min(1.0, ctas / 444.0);
+        if (eff > best + 0.01) {
+          best = eff;
+          seg = g;
+        }
+      }
       pl->nseg = (int)std::min(seg, 16LL);
     }
   }
