@@ -573,12 +573,15 @@ __global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 1)
 //   P1 = sum a c,  P2 = sum b d,  P3 = sum (a + b)(c - d):
 //   Re = P1 + P2,  Im = P3 - P1 + P2
 // — 3 DMMAs per complex 8x8x4 tile instead of 4.  The operand sums are one
-// DADD per fragment (FP64 pipe, beside the DMMA pipe).  Rounding: every
+// DADD per fragment — on B200 DMMA and DADD share the FP64 datapath, so with
+// PREP the producer warp writes a+b / c-d for each landed stage into SMEM
+// once (instead of every warp recomputing them per fragment) and the compute
+// warps wait on a second per-stage barrier.  Rounding: every
 // partial is a sum of products bounded by 2|x||y|, so the error stays at the
 // level of the 4-multiplication form (relative Frobenius ~1e-16 at cfg5,
 // tests/test_gpu_parity.py).  Same data flow as k_bulk_dmma; CTA tile DR =
 // WM*MT*8 lags x DC = WN*NTW*8 lags, WM*WN compute warps of MT x NTW tiles.
-template <int WM, int WN, int MT, int NTW, int MINB>
+template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false>
 struct Mma3Cfg {
   static constexpr int WARPS = WM * WN;
   static constexpr int DR = WM * MT * 8;
@@ -588,22 +591,29 @@ struct Mma3Cfg {
   static constexpr size_t xbytes = 16 * (size_t)XR * MMA_XP;
   static constexpr size_t xoff = (xbytes + 127) / 128 * 128;
   static constexpr size_t ybytes = 16 * (size_t)MMA_RC * YP;
-  static constexpr size_t stage = xoff + (ybytes + 127) / 128 * 128;
+  static constexpr size_t yend = xoff + (ybytes + 127) / 128 * 128;
+  // PREP: a+b of every X element, c-d of every Y element (doubles)
+  static constexpr size_t xsoff = yend;
+  static constexpr size_t ydoff = xsoff + (8 * (size_t)XR * MMA_XP + 127) / 128 * 128;
+  static constexpr size_t stage = PREP ? ydoff + (8 * (size_t)MMA_RC * YP + 127) / 128 * 128 : yend;
   static constexpr int fit = (int)((227 * 1024 / MINB - 2048) / stage);
   static constexpr int S = fit > 4 ? 4 : fit;
-  static constexpr size_t smem = S * stage + 64;
+  static constexpr size_t smem = S * stage + 128;  // + full / empty / prepped barriers
 };
 
-template <int MT, int NTW, bool MASKED, bool FULL>
+template <int MT, int NTW, bool MASKED, bool FULL, bool PREP>
 __device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const double2* __restrict__ Y,
+                                          const double* __restrict__ Xs, const double* __restrict__ Yd,
                                           int xrow0, int kq, int ycol0, int yp, int nks, int R,
                                           int dra, const Problem& pr, double (&p1)[MT][NTW][2],
                                           double (&p2)[MT][NTW][2], double (&p3)[MT][NTW][2]) {
   const int P = pr.P, N = pr.N;
 #pragma unroll 1
   for (int tr = 0; tr < MMA_RC; ++tr) {
-    const double2* xa = X + (tr + xrow0) * MMA_XP + kq;  // m-tile i: rows - 8 i
-    const double2* yb = Y + tr * yp + ycol0;
+    const int xo = (tr + xrow0) * MMA_XP + kq;  // m-tile i: rows - 8 i
+    const int yo = tr * yp + ycol0;
+    const double2* xa = X + xo;
+    const double2* yb = Y + yo;
     bool on[MT];
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
@@ -619,13 +629,22 @@ __device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const d
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         a[i] = xa[4 * ks - 8 * i * MMA_XP];
-        if (MASKED && !on[i]) a[i] = make_double2(0.0, 0.0);
-        as[i] = a[i].x + a[i].y;
+        if constexpr (PREP)
+          as[i] = Xs[xo + 4 * ks - 8 * i * MMA_XP];
+        else
+          as[i] = a[i].x + a[i].y;
+        if (MASKED && !on[i]) {
+          a[i] = make_double2(0.0, 0.0);
+          as[i] = 0.0;
+        }
       }
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         bv[j] = yb[4 * ks + 8 * j];
-        bd[j] = bv[j].x - bv[j].y;
+        if constexpr (PREP)
+          bd[j] = Yd[yo + 4 * ks + 8 * j];
+        else
+          bd[j] = bv[j].x - bv[j].y;
       }
 #pragma unroll
       for (int i = 0; i < MT; ++i)
@@ -650,18 +669,19 @@ __device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const d
   }
 }
 
-template <int WM, int WN, int MT, int NTW, int MINB>
+template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_bulk_dmma3(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                  Problem pr, int n_drt, int n_dct, int G, int nclasses,
                  const int* __restrict__ cls_slot, double2* __restrict__ ccpart,
                  const unsigned* __restrict__ band_flag, unsigned band_base, int band_rows) {
-  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB>;
+  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB, PREP>;
   constexpr int S = Cfg::S, DR = Cfg::DR, DC = Cfg::DC, NW = Cfg::WARPS;
   static_assert(S >= 2, "TMA ring needs two stages");
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + S * Cfg::stage);
   uint64_t* empty = full + S;
+  uint64_t* prepped = empty + S;  // PREP: operand sums of the stage written
   long long t = blockIdx.x;
   const int p = (int)(t % G);
   t /= G;
@@ -686,11 +706,58 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
+      mbar_init(&prepped[s], 1);
     }
     fence_mbarrier_init();
   }
   __syncthreads();
 
+  if (w == NW && PREP) {  // producer: TMA issue + operand sums of landed stages
+    auto issue = [&](long long k) {
+      const int s = (int)(k % S);
+      if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
+      const long long q = p + k * G;
+      const int R = rlo + (int)(q / ncbk) * MMA_RC;
+      const int C0 = (int)(q % ncbk) * MMA_W;
+      if (band_flag) {
+        const int rneed = min(N - 1, R + MMA_RC - 1 + max(-dr0, 0));
+        wait_band(band_flag, band_base + (unsigned)(rneed / band_rows) + 1u);
+      }
+      unsigned char* st = smraw + s * Cfg::stage;
+      mbar_expect_tx(&full[s], (unsigned)(Cfg::xbytes + Cfg::ybytes));
+      tma_load_3d(st, &tmx, 2 * C0, R - dr0 - (DR - 1), b, &full[s]);
+      tma_load_3d(st + Cfg::xoff, &tmy, 2 * (C0 + dc0 - (Q - 1)), R, b, &full[s]);
+    };
+    long long issued = 0;
+    if (lane == 0)
+      for (; issued < nmine && issued < S - 1; ++issued) issue(issued);
+    for (long long k = 0; k < nmine; ++k) {
+      const int s = (int)(k % S);
+      mbar_wait(&full[s], (int)((k / S) & 1));
+      const unsigned char* st = smraw + s * Cfg::stage;
+      const double2* X = reinterpret_cast<const double2*>(st);
+      const double2* Y = reinterpret_cast<const double2*>(st + Cfg::xoff);
+      double* Xs = reinterpret_cast<double*>(smraw + s * Cfg::stage + Cfg::xsoff);
+      double* Yd = reinterpret_cast<double*>(smraw + s * Cfg::stage + Cfg::ydoff);
+#pragma unroll 4
+      for (int i = lane; i < Cfg::XR * MMA_XP; i += 32) {
+        const double2 v = X[i];
+        Xs[i] = v.x + v.y;
+      }
+#pragma unroll 4
+      for (int i = lane; i < MMA_RC * Cfg::YP; i += 32) {
+        const double2 v = Y[i];
+        Yd[i] = v.x - v.y;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&prepped[s]);
+        if (issued < nmine) issue(issued++);  // refill (waits for the slot's consumers)
+      }
+      __syncwarp();
+    }
+    return;
+  }
   if (w == NW) {  // producer
     if (lane == 0) {
       for (long long k = 0; k < nmine; ++k) {
@@ -726,21 +793,29 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
 
   for (long long k = 0; k < nmine; ++k) {
     const int s = (int)(k % S);
-    mbar_wait(&full[s], (int)((k / S) & 1));
+    if constexpr (PREP)
+      mbar_wait(&prepped[s], (int)((k / S) & 1));
+    else
+      mbar_wait(&full[s], (int)((k / S) & 1));
     const long long q = p + k * G;
     const int R = rlo + (int)(q / ncbk) * MMA_RC;
     const int C0 = (int)(q % ncbk) * MMA_W;
     const int nks = min(MMA_W, xcols - C0 + 3) / 4;
     const double2* X = reinterpret_cast<const double2*>(smraw + s * Cfg::stage);
     const double2* Y = reinterpret_cast<const double2*>(smraw + s * Cfg::stage + Cfg::xoff);
+    const double* Xs = reinterpret_cast<const double*>(smraw + s * Cfg::stage + Cfg::xsoff);
+    const double* Yd = reinterpret_cast<const double*>(smraw + s * Cfg::stage + Cfg::ydoff);
     const bool masked = R < P - 1 || R + MMA_RC - 1 > N - P;
     if (nks == MMA_W / 4) {
       if (!masked)
-        mma3_rows<MT, NTW, false, true>(X, Y, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1, p2, p3);
+        mma3_rows<MT, NTW, false, true, PREP>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
+                                              p2, p3);
       else
-        mma3_rows<MT, NTW, true, true>(X, Y, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1, p2, p3);
+        mma3_rows<MT, NTW, true, true, PREP>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
+                                             p2, p3);
     } else {
-      mma3_rows<MT, NTW, true, false>(X, Y, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1, p2, p3);
+      mma3_rows<MT, NTW, true, false, PREP>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
+                                            p2, p3);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
