@@ -398,6 +398,10 @@ cudaError_t set_attrs() {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)Mma3Cfg<4, 4, 2, 2, 1, true>::smem)) != cudaSuccess)
       e = r;
+    if ((r = cudaFuncSetAttribute(k_bulk_dmma3<2, 4, 2, 2, 2, true, 8>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Mma3Cfg<2, 4, 2, 2, 2, true, 8>::smem)) != cudaSuccess)
+      e = r;
     if ((r = cudaFuncSetAttribute(k_edge_cols_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ECM_SMEM)) != cudaSuccess)
       e = r;
@@ -517,16 +521,16 @@ bool launch_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
 }
 
 // Gauss 3-DMMA core sums (k_bulk_dmma3); false when the tensor maps fail
-template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false>
+template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false, int RC = MMA_RC>
 bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
-  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB, PREP>;
+  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB, PREP, RC>;
   const Problem& pr = pl->pr;
   if ((uintptr_t)A % 16 != 0) return false;
   if (pl->mtmap_ptr != (const void*)A || pl->mtmap_kind != pl->mma_kind) {
     CUtensorMap mx, my;
     const long long w = pr.M - pr.Q + 1;
     if (make_tmap(&mx, A, true, pl->batch, pr.N, pr.M, 2 * MMA_XP, Cfg::XR, w, 0) &&
-        make_tmap(&my, A, true, pl->batch, pr.N, pr.M, 2 * Cfg::YP, MMA_RC, w, pr.Q - 1)) {
+        make_tmap(&my, A, true, pl->batch, pr.N, pr.M, 2 * Cfg::YP, Cfg::RC, w, pr.Q - 1)) {
       pl->mtmx = mx;
       pl->mtmy = my;
       pl->mtmap_ptr = A;
@@ -537,7 +541,7 @@ bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
     }
   }
   const long long blocks = pl->batch * (long long)pl->n_drt * pl->n_dct * pl->mma_g;
-  k_bulk_dmma3<WM, WN, MT, NTW, MINB, PREP><<<(unsigned)blocks, (Cfg::WARPS + 1) * 32, Cfg::smem, st>>>(
+  k_bulk_dmma3<WM, WN, MT, NTW, MINB, PREP, RC><<<(unsigned)blocks, (Cfg::WARPS + 1) * 32, Cfg::smem, st>>>(
       pl->mtmx, pl->mtmy, pr, pl->n_drt, pl->n_dct, pl->mma_g, pl->nclasses, pl->d_cls_slot,
       pl->d_ccpart, pl->band_wait ? pl->d_band_flag : nullptr, pl->band_base, pl->band_rows);
   return true;
@@ -695,6 +699,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
         case 2: mma = launch_dmma3<4, 4, 2, 2, 1>(pl, Ad, st); break;
         case 3: mma = launch_dmma3<2, 2, 2, 2, 2>(pl, Ad, st); break;
         case 4: mma = launch_dmma3<4, 4, 2, 2, 1, true>(pl, Ad, st); break;
+        case 5: mma = launch_dmma3<2, 4, 2, 2, 2, true, 8>(pl, Ad, st); break;
         default:
           mma = pl->mma_dc == 32 ? launch_dmma<32>(pl, Ad, st) : launch_dmma<64>(pl, Ad, st);
       }
@@ -920,18 +925,20 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->use_mma = true;
       pl->mma_dc = q <= 32 ? 32 : 64;
       // kernel: Gauss 3-DMMA tiles (1: 32x64 lags, 8 warps, 2 CTAs/SM; 2: 64x64,
-      // 16 warps, 1 CTA/SM; 3: 32x32 for Q <= 32), 0: 4-DMMA k_bulk_dmma
-      pl->mma_kind = q <= 32 ? 3 : 1;
+      // 16 warps, 1 CTA/SM; 3: 32x32 for Q <= 32; 4: kind 2 + producer-warp
+      // operand sums (PREP); 5: kind 1 + PREP with 8-row chunks), 0: 4-DMMA k_bulk_dmma
+      // (cfg5 bulk: kind 0 7.06 ms, 1 5.74, 2 5.90, 4 5.75, 5 5.65)
+      pl->mma_kind = q <= 32 ? 3 : 5;
       if (const char* mk = getenv("COVGPU_MMA_KIND")) {
         const int k = atoi(mk);
-        if (k >= 0 && k <= 4) pl->mma_kind = k;
+        if (k >= 0 && k <= 5) pl->mma_kind = k;
       }
       int dr_tile = MMA_DR, ctas_per_sm = 2;
       if (pl->mma_kind == 2 || pl->mma_kind == 4) {
         dr_tile = 64;
         ctas_per_sm = 1;
       }
-      if (pl->mma_kind == 1 || pl->mma_kind == 2 || pl->mma_kind == 4) pl->mma_dc = 64;
+      if (pl->mma_kind == 1 || pl->mma_kind == 2 || pl->mma_kind == 4 || pl->mma_kind == 5) pl->mma_dc = 64;
       if (pl->mma_kind == 3) pl->mma_dc = 32;
       pl->n_drt = (2 * p - 1 + dr_tile - 1) / dr_tile;
       pl->n_dct = (q + pl->mma_dc - 1) / pl->mma_dc;

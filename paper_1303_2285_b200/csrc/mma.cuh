@@ -581,27 +581,28 @@ __global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 1)
 // level of the 4-multiplication form (relative Frobenius ~1e-16 at cfg5,
 // tests/test_gpu_parity.py).  Same data flow as k_bulk_dmma; CTA tile DR =
 // WM*MT*8 lags x DC = WN*NTW*8 lags, WM*WN compute warps of MT x NTW tiles.
-template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false>
+template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false, int RC_ = MMA_RC>
 struct Mma3Cfg {
+  static constexpr int RC = RC_;  // second-element rows per chunk
   static constexpr int WARPS = WM * WN;
   static constexpr int DR = WM * MT * 8;
   static constexpr int DC = WN * NTW * 8;
-  static constexpr int XR = MMA_RC + DR - 1;
+  static constexpr int XR = RC + DR - 1;
   static constexpr int YP = MMA_W + DC;
   static constexpr size_t xbytes = 16 * (size_t)XR * MMA_XP;
   static constexpr size_t xoff = (xbytes + 127) / 128 * 128;
-  static constexpr size_t ybytes = 16 * (size_t)MMA_RC * YP;
+  static constexpr size_t ybytes = 16 * (size_t)RC * YP;
   static constexpr size_t yend = xoff + (ybytes + 127) / 128 * 128;
   // PREP: a+b of every X element, c-d of every Y element (doubles)
   static constexpr size_t xsoff = yend;
   static constexpr size_t ydoff = xsoff + (8 * (size_t)XR * MMA_XP + 127) / 128 * 128;
-  static constexpr size_t stage = PREP ? ydoff + (8 * (size_t)MMA_RC * YP + 127) / 128 * 128 : yend;
+  static constexpr size_t stage = PREP ? ydoff + (8 * (size_t)RC * YP + 127) / 128 * 128 : yend;
   static constexpr int fit = (int)((227 * 1024 / MINB - 2048) / stage);
   static constexpr int S = fit > 4 ? 4 : fit;
   static constexpr size_t smem = S * stage + 128;  // + full / empty / prepped barriers
 };
 
-template <int MT, int NTW, bool MASKED, bool FULL, bool PREP>
+template <int MT, int NTW, bool MASKED, bool FULL, bool PREP, int RC>
 __device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const double2* __restrict__ Y,
                                           const double* __restrict__ Xs, const double* __restrict__ Yd,
                                           int xrow0, int kq, int ycol0, int yp, int nks, int R,
@@ -609,7 +610,7 @@ __device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const d
                                           double (&p2)[MT][NTW][2], double (&p3)[MT][NTW][2]) {
   const int P = pr.P, N = pr.N;
 #pragma unroll 1
-  for (int tr = 0; tr < MMA_RC; ++tr) {
+  for (int tr = 0; tr < RC; ++tr) {
     const int xo = (tr + xrow0) * MMA_XP + kq;  // m-tile i: rows - 8 i
     const int yo = tr * yp + ycol0;
     const double2* xa = X + xo;
@@ -669,13 +670,13 @@ __device__ __forceinline__ void mma3_rows(const double2* __restrict__ X, const d
   }
 }
 
-template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false>
+template <int WM, int WN, int MT, int NTW, int MINB, bool PREP = false, int RC = MMA_RC>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_bulk_dmma3(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                  Problem pr, int n_drt, int n_dct, int G, int nclasses,
                  const int* __restrict__ cls_slot, double2* __restrict__ ccpart,
                  const unsigned* __restrict__ band_flag, unsigned band_base, int band_rows) {
-  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB, PREP>;
+  using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB, PREP, RC>;
   constexpr int S = Cfg::S, DR = Cfg::DR, DC = Cfg::DC, NW = Cfg::WARPS;
   static_assert(S >= 2, "TMA ring needs two stages");
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -695,7 +696,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
   const int drmax = min(dr0 + DR - 1, P - 1);
   const int rlo = max(0, P - 1 + min(dr0, 0));
   const int rhi = min(N - 1, N - P + max(drmax, 0));
-  const int nrc = (rhi - rlo + MMA_RC) / MMA_RC;
+  const int nrc = (rhi - rlo + RC) / RC;
   const int xcols = M - Q + 1;
   const int ncbk = (xcols + MMA_W - 1) / MMA_W;
   const long long nch = (long long)nrc * ncbk;
@@ -717,10 +718,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       const int s = (int)(k % S);
       if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
       const long long q = p + k * G;
-      const int R = rlo + (int)(q / ncbk) * MMA_RC;
+      const int R = rlo + (int)(q / ncbk) * RC;
       const int C0 = (int)(q % ncbk) * MMA_W;
       if (band_flag) {
-        const int rneed = min(N - 1, R + MMA_RC - 1 + max(-dr0, 0));
+        const int rneed = min(N - 1, R + RC - 1 + max(-dr0, 0));
         wait_band(band_flag, band_base + (unsigned)(rneed / band_rows) + 1u);
       }
       unsigned char* st = smraw + s * Cfg::stage;
@@ -745,7 +746,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
         Xs[i] = v.x + v.y;
       }
 #pragma unroll 4
-      for (int i = lane; i < MMA_RC * Cfg::YP; i += 32) {
+      for (int i = lane; i < RC * Cfg::YP; i += 32) {
         const double2 v = Y[i];
         Yd[i] = v.x - v.y;
       }
@@ -764,10 +765,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
         const int s = (int)(k % S);
         if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
         const long long q = p + k * G;
-        const int R = rlo + (int)(q / ncbk) * MMA_RC;
+        const int R = rlo + (int)(q / ncbk) * RC;
         const int C0 = (int)(q % ncbk) * MMA_W;
         if (band_flag) {
-          const int rneed = min(N - 1, R + MMA_RC - 1 + max(-dr0, 0));
+          const int rneed = min(N - 1, R + RC - 1 + max(-dr0, 0));
           wait_band(band_flag, band_base + (unsigned)(rneed / band_rows) + 1u);
         }
         unsigned char* st = smraw + s * Cfg::stage;
@@ -798,23 +799,23 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     else
       mbar_wait(&full[s], (int)((k / S) & 1));
     const long long q = p + k * G;
-    const int R = rlo + (int)(q / ncbk) * MMA_RC;
+    const int R = rlo + (int)(q / ncbk) * RC;
     const int C0 = (int)(q % ncbk) * MMA_W;
     const int nks = min(MMA_W, xcols - C0 + 3) / 4;
     const double2* X = reinterpret_cast<const double2*>(smraw + s * Cfg::stage);
     const double2* Y = reinterpret_cast<const double2*>(smraw + s * Cfg::stage + Cfg::xoff);
     const double* Xs = reinterpret_cast<const double*>(smraw + s * Cfg::stage + Cfg::xsoff);
     const double* Yd = reinterpret_cast<const double*>(smraw + s * Cfg::stage + Cfg::ydoff);
-    const bool masked = R < P - 1 || R + MMA_RC - 1 > N - P;
+    const bool masked = R < P - 1 || R + RC - 1 > N - P;
     if (nks == MMA_W / 4) {
       if (!masked)
-        mma3_rows<MT, NTW, false, true, PREP>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
+        mma3_rows<MT, NTW, false, true, PREP, RC>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
                                               p2, p3);
       else
-        mma3_rows<MT, NTW, true, true, PREP>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
+        mma3_rows<MT, NTW, true, true, PREP, RC>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
                                              p2, p3);
     } else {
-      mma3_rows<MT, NTW, true, false, PREP>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
+      mma3_rows<MT, NTW, true, false, PREP, RC>(X, Y, Xs, Yd, xrow0, kq, ycol0, Cfg::YP, nks, R, dra, pr, p1,
                                             p2, p3);
     }
     __syncwarp();
