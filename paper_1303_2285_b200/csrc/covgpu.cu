@@ -919,7 +919,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const int ncb_l = (q - 2) / 32 + 1;
     const int ncb_r = pl->ncb - (int)((m - q + 1) / 32);
     bool ok = dtype == COVGPU_C128 && pl->clean && class_ids == nullptr && p >= 16 && q >= 24 &&
-              p <= FINV_MAX_P && q >= 2 && ncb_l + ncb_r <= pl->ncb / 2 && pl->use_tma;
+              p <= FINV_MAX_P && q >= 2 && ncb_l + ncb_r <= pl->ncb && pl->use_tma;
     if (const char* nm = getenv("COVGPU_NO_MMA")) ok = ok && atoi(nm) == 0;
     if (ok) {
       pl->use_mma = true;

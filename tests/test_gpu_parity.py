@@ -556,3 +556,36 @@ def test_host_path_streams_a_in_bands_bitwise(cuda):
         plan.execute_host(a, out, "packed")
         assert torch.equal(out, dev.cpu())
     plan.close()
+
+
+def test_tensor_core_path_fuzz(cuda):
+    """24 seeded random complex128 shapes inside the tensor-core gate (P >= 16,
+    Q >= 24, wide enough M): ragged chunk / column-block / lag-tile edges,
+    Q in and beyond one 64-lag tile, P above and below the tensor-core edge
+    kernels' ranges, batch 1-3 — against the Gram cross-check."""
+    from oracle.gpu_naive import covariance_gram
+    from paper_1303_2285_b200.plan import Plan
+
+    rng = np.random.default_rng(1303)
+    worst = 0.0
+    for it in range(24):
+        p = int(rng.integers(16, 49))
+        q = int(rng.integers(24, 49)) if it % 4 else int(rng.integers(50, 72))
+        n = int(rng.integers(2 * p, 2 * p + 160))
+        m = int(rng.integers(4 * q + 8, 4 * q + 200))
+        batch = int(rng.integers(1, 4))
+        a = torch.as_tensor(rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m)),
+                            device=cuda)
+        plan = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=torch.complex128, device=cuda)
+        plan.set_timing(True)
+        got = plan.alloc_output()
+        plan.execute(a, got)
+        assert "bulk_dmma" in plan.kernel_names(), (it, n, m, p, q)
+        plan.close()
+        got = got.reshape(batch, p * q, p * q)
+        for b in range(batch):
+            ref = covariance_gram(a[b], p, q)
+            err = (torch.linalg.norm(got[b] - ref) / torch.linalg.norm(ref)).item()
+            worst = max(worst, err)
+            assert err <= TOL64, (it, n, m, p, q, batch, err)
+    print(f"tensor-core fuzz worst relF {worst:.2e}")
