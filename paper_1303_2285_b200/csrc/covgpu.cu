@@ -1109,6 +1109,11 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         const long long ng = (batch + per - 1) / per;
         for (long long g = 0; g < ng; ++g) tasks.push_back(make_int2(ci, (int)g));
       }
+      // longest walks first (a warp's time ~ its qu column steps): the last
+      // wave then holds only short tasks
+      std::stable_sort(tasks.begin(), tasks.end(), [&](const int2& x, const int2& y) {
+        return pl->h_cls[x.x].qu > pl->h_cls[y.x].qu;
+      });
       pl->ntasks = (long long)tasks.size();
       const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
       const size_t cbytes = (size_t)batch * 4 * (size_t)std::max(p - 1, 0) * (size_t)std::max(q - 1, 0) * esz;
