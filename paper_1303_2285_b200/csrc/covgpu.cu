@@ -742,12 +742,11 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     const unsigned blocks = (unsigned)((pl->ntasks + FIN_WARPS - 1) / FIN_WARPS);
     // finalize into the compact layout (R itself, or the plan's scratch),
     // then expand to dense / packed with coalesced stores
-    // dense R small enough to stay in L2: write it directly from the walk (the
-    // scattered diagonal stores merge in L2); otherwise finalize into the
-    // compact layout and expand with coalesced stores
-    const double dense_bytes = (double)B * pr.PQ * pr.PQ * sizeof(C2);
-    const bool direct = layout == COVGPU_DENSE && dense_bytes <= 48.0 * (1 << 20) && pr.P >= 16 &&
-                        !pl->no_direct;
+    // dense R: write it directly from the walk (the scattered diagonal stores
+    // merge in L2; with longest-walk-first tasks this beats finalize into
+    // the compact layout + a coalesced expand: cfg5 0.325 -> 0.257 ms, cfg4
+    // 0.255 -> 0.249 ms); packed R goes through the compact layout + expand
+    const bool direct = layout == COVGPU_DENSE && !pl->no_direct;
     C2* cdst = (layout == COVGPU_COMPACT || direct) ? R : (C2*)pl->d_slots;
     const long long rstride = direct ? (long long)pr.PQ * pr.PQ : pl->compact_elems;
 #define FINV(KR, DIR)                                                                           \
