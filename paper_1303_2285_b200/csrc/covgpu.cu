@@ -745,15 +745,15 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     // dense R: write it directly from the walk (the scattered diagonal stores
     // merge in L2; with longest-walk-first tasks this beats finalize into
     // the compact layout + a coalesced expand: cfg5 0.325 -> 0.257 ms, cfg4
-    // 0.255 -> 0.249 ms); packed R goes through the compact layout + expand
-    const bool direct = layout == COVGPU_DENSE && !pl->no_direct;
+    // 0.255 -> 0.249 ms; packed: cfg4 0.224 -> 0.170 ms)
+    const bool direct = layout != COVGPU_COMPACT && !pl->no_direct;
     C2* cdst = (layout == COVGPU_COMPACT || direct) ? R : (C2*)pl->d_slots;
-    const long long rstride = direct ? (long long)pr.PQ * pr.PQ : pl->compact_elems;
+    const long long rstride = direct ? r_bstride : pl->compact_elems;
 #define FINV(KR, DIR)                                                                           \
   k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                 \
       (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses,           \
       npart, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
-      pl->nseg, cdst, rstride, scale)
+      pl->nseg, cdst, rstride, scale, direct ? layout : (int)COVGPU_COMPACT)
     if (direct) {
       switch (pl->fin_kr) {
         case 1: FINV(1, true); break;
@@ -1349,8 +1349,12 @@ static int execute_host_pipelined(covgpu_plan_t pl, const void* A_host, void* R_
   for (const auto& c : pl->h_cls) ids.push_back(c.uc);
   const bool all = (long long)ids.size() == covgpu_num_classes(pr.P, pr.Q);
   auto make = [&](covgpu_plan** dst, long long nb) -> int {
-    return covgpu_plan_create(dst, pl->device, nb, pr.N, pr.M, pr.P, pr.Q, pl->dtype,
-                              all ? nullptr : ids.data(), all ? 0 : (int32_t)ids.size());
+    const int rc = covgpu_plan_create(dst, pl->device, nb, pr.N, pr.M, pr.P, pr.Q, pl->dtype,
+                                      all ? nullptr : ids.data(), all ? 0 : (int32_t)ids.size());
+    // sub-batches overlapped on 3 streams: finalize into the compact layout
+    // and expand (measured: cfg4 e2e 3.0 ms vs 3.2 ms with the direct write)
+    if (!rc) (*dst)->no_direct = true;
+    return rc;
   };
   if (pl->pipe_sub != sub || (tail != sub && pl->pipe_tail_b != tail)) {
     plan_free_pipe(pl);

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
                  int nclasses, int ncb, int nrs, int B, const double2* __restrict__ ccpart,
                  const double2* __restrict__ ccol, long long tot_ccol, const double2* __restrict__ rc,
                  long long tot_rc, int nseg, typename CT<T>::c* __restrict__ R,
-                 long long r_bstride, double scale) {
+                 long long r_bstride, double scale, int dlayout) {
   // R: compact (class-major) output, r_bstride elements per snapshot
   using C2 = typename CT<T>::c;
   const int lane = threadIdx.x & 31;
@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
       if (active && v < pv) {
         const double2 sv = cadd(s0, cadd(base, d[k]));
         if constexpr (DIRECT) {
-          // dense R straight from the walk (16-byte elements: the scattered
-          // diagonal stores merge in L2 well enough to beat a separate expand)
-          write_slot<T>(R, COVGPU_DENSE, rb, c, pr, v, u, sv.x * scale, zero_im ? 0.0 : sv.y * scale);
+          // dense / packed R straight from the walk (the scattered diagonal
+          // stores merge in L2 well enough to beat a separate expand)
+          write_slot<T>(R, dlayout, rb, c, pr, v, u, sv.x * scale, zero_im ? 0.0 : sv.y * scale);
         } else {
           // compact slot (u-major, then v): lanes write consecutive addresses;
           // k_expand turns it into the dense / packed layout with coalesced stores
