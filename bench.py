@@ -196,6 +196,8 @@ def main() -> None:
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of CPU-baseline sample")
     ap.add_argument("--ref-budget", type=float, default=4.0, help="seconds per reference-arm step")
     ap.add_argument("--layout", default="dense", choices=["dense", "packed", "compact"])
+    ap.add_argument("--no-cuda-core", action="store_true",
+                    help="skip the CUDA-core (non-tensor-core) comparison steps")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -308,7 +310,8 @@ def main() -> None:
             except (ValueError, OSError):
                 traffic = None
         roof = {"bound": "fp64-tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
-                "frac": achieved / peak_dmma, "traffic": traffic, "kernel": "k_bulk_dmma",
+                "frac": achieved / peak_dmma, "traffic": traffic,
+                "kernel": "k_bulk_dmma" if os.environ.get("COVGPU_MMA_KIND") == "0" else "k_bulk_dmma3",
                 "peak_source": "DMMA-loop probe (mma.sync m8n8k4 f64) measured on this GPU in this "
                 "run (MEASURED_PEAKS.json has no FP64 figure)",
                 "algorithmic_flops_per_launch": 6.0 * core_p * w.batch,
@@ -346,6 +349,47 @@ def main() -> None:
         "roofline": roof,
         "clocks": clocks.summary(),
     }
+
+    # the CUDA-core path beside it (the north_star's FP64/FP32-pipe kernel;
+    # still the path for complex64 and class shards): same workload, a few
+    # steps, per-kernel events — reported, not the headline
+    if roof is not None and roof.get("kernel", "").startswith("k_bulk_dmma") and world == 1 \
+            and not args.no_cuda_core:
+        os.environ["COVGPU_NO_MMA"] = "1"
+        try:
+            cplan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, device=dev)
+        finally:
+            del os.environ["COVGPU_NO_MMA"]
+        cout = cplan.alloc_output(layout)
+        for _ in range(2):
+            cplan.execute(a, cout, layout)
+        torch.cuda.synchronize(dev)
+        tot = 0.0
+        nst = 5
+        for _ in range(nst):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            cplan.execute(a, cout, layout)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            tot += e0.elapsed_time(e1)
+        cplan.set_timing(True)
+        flush.fill_(1)
+        torch.cuda.synchronize(dev)
+        cplan.execute(a, cout, layout)
+        ck = dict(zip(cplan.kernel_names(), cplan.kernel_times()))
+        cplan.close()
+        cms = tot / nst
+        cach = 8.0 * bulk_p * w.batch / (ck["bulk"] * 1e-3) / 1e12 if ck.get("bulk") else None
+        line["cuda_core_path"] = {
+            "ms_per_step": cms, "value": entries / (cms * 1e-3), "kernel_ms": ck,
+            "bulk_achieved_tflops": cach,
+            "bulk_frac_of_fma_probe": cach / peak if cach else None,
+            "bulk_frac_of_nominal_fp64": cach / (148 * 64 * 2 * 1.965e9 / 1e12) if cach else None,
+            "note": "COVGPU_NO_MMA=1: core sums on the FP64 FMA pipe (k_bulk_tma), 8 flops per "
+                    "core-row product",
+        }
 
     # end to end through the C ABI with pinned host buffers
     if not args.no_e2e:
