@@ -105,6 +105,26 @@ int32_t covgpu_plan_kernel_times(covgpu_plan_t plan, float* ms, int32_t max_n);
  * buf (NUL-terminated, truncated to len).  Returns the count. */
 int32_t covgpu_plan_kernel_names(covgpu_plan_t plan, char* buf, int32_t len);
 
+/* Multi-GPU row bands (the core / edge sums are sums over rows and columns
+ * of A, so they split over the K dimension with one exchange: an all-reduce
+ * of the per-band sums; replaces the reference's per-class work split,
+ * engine.py:158-190, with a split that keeps every GPU on the tensor-core
+ * path).  sums_elems: complex128 values of the reduced-sums buffer
+ * [CC | CCol | RC'].  execute_sums: part `part` of `nparts` of every sum
+ * (rank = part); the caller all-reduces the buffers (sum).  finalize_sums:
+ * corners + diagonal-segment walk from the reduced sums for plan classes
+ * [class_lo, class_hi) (a sub-range writes its slots of the COMPACT layout;
+ * the full range may write DENSE / PACKED).  class_slot_offset: compact
+ * offset of a plan class (class_index == #classes: total).  Requires the
+ * complex128 tensor-core path (COVGPU_ECAPACITY otherwise). */
+int64_t covgpu_plan_sums_elems(covgpu_plan_t plan);
+int covgpu_plan_execute_sums(covgpu_plan_t plan, const void* A_dev, void* sums_dev, int32_t part,
+                             int32_t nparts, void* stream);
+int covgpu_plan_finalize_sums(covgpu_plan_t plan, const void* A_dev, const void* sums_dev, void* R_dev,
+                              int32_t layout, double scale, int32_t class_lo, int32_t class_hi,
+                              void* stream);
+int64_t covgpu_plan_class_slot_offset(covgpu_plan_t plan, int32_t class_index);
+
 int covgpu_plan_destroy(covgpu_plan_t plan);
 
 /* One-shot estimate on device buffers (plan cached per shape internally). */

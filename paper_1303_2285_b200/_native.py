@@ -51,6 +51,10 @@ _SIGS = {
     "covgpu_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
     "covgpu_plan_kernel_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), _i32]),
     "covgpu_plan_kernel_names": (_i32, [_vp, ctypes.c_char_p, _i32]),
+    "covgpu_plan_sums_elems": (_i64, [_vp]),
+    "covgpu_plan_execute_sums": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp]),
+    "covgpu_plan_finalize_sums": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _dbl, _i32, _i32, _vp]),
+    "covgpu_plan_class_slot_offset": (_i64, [_vp, _i32]),
     "covgpu_plan_destroy": (ctypes.c_int, [_vp]),
     "covgpu_estimate": (
         ctypes.c_int,

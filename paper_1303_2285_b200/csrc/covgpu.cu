@@ -113,6 +113,15 @@ struct covgpu_plan {
   // copy stream bumps *d_band_flag after each band; k_bulk_dmma waits on it,
   // the side-stream kernels wait for ev_h2d (the whole of A)
   bool band_wait = false;
+  // multi-GPU row bands (covgpu_plan_execute_sums): this execute computes
+  // part ks_part of ks_nparts of every sum and reduces them into ks_out
+  int ks_part = 0, ks_nparts = 1;
+  bool ks_failed = false;
+  double2* ks_out = nullptr;
+  // finalize from reduced sums for a class range: cached task list
+  int2* d_rtasks = nullptr;
+  long long n_rtasks = 0;
+  int rtask_lo = -1, rtask_hi = -1;
   unsigned* d_band_flag = nullptr;
   unsigned band_base = 0;
   int band_rows = 0;
@@ -150,6 +159,7 @@ struct covgpu_plan {
   double2* d_sat = nullptr;
   void* d_corners = nullptr;  // transposed corner blocks (k_corners)
   int2* d_tasks = nullptr;    // k_finalize_v tasks (class, snapshot group)
+  std::vector<int2> h_tasks;
   long long* d_uc_off = nullptr;  // compact offset per UC index (-1: not in shard)
   long long ntasks = 0;
   int fin_kr = 0;             // k_finalize_v rows per lane (0: wide finalize)
@@ -260,6 +270,7 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_uc_off);
   cudaFree(pl->d_ecm_part);
   cudaFree(pl->d_band_flag);
+  cudaFree(pl->d_rtasks);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
   cudaFree(pl->d_ecm_tickets);
@@ -543,7 +554,8 @@ bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   const long long blocks = pl->batch * (long long)pl->n_drt * pl->n_dct * pl->mma_g;
   k_bulk_dmma3<WM, WN, MT, NTW, MINB, PREP, RC><<<(unsigned)blocks, (Cfg::WARPS + 1) * 32, Cfg::smem, st>>>(
       pl->mtmx, pl->mtmy, pr, pl->n_drt, pl->n_dct, pl->mma_g, pl->nclasses, pl->d_cls_slot,
-      pl->d_ccpart, pl->band_wait ? pl->d_band_flag : nullptr, pl->band_base, pl->band_rows);
+      pl->d_ccpart, pl->band_wait ? pl->d_band_flag : nullptr, pl->band_base, pl->band_rows,
+      pl->ks_part, pl->ks_nparts);
   return true;
 }
 
@@ -562,7 +574,7 @@ bool launch_edge_cols_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   const long long blocks = pl->ecm_items * pl->ecm_g;
   k_edge_cols_dmma<<<(unsigned)blocks, (MMA_WARPS + 1) * 32, ECM_SMEM, st>>>(
       pl->ecm_tm, pr, pl->ecm_g, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, pl->d_ecm_part,
-      pl->d_ecm_tickets);
+      pl->d_ecm_tickets, pl->ks_part, pl->ks_nparts);
   return true;
 }
 
@@ -584,7 +596,7 @@ bool launch_edge_rows_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   const long long blocks = pl->batch * 2LL * pl->S * pl->erm_dct * pl->nseg;
   k_edge_rows_dmma<<<(unsigned)blocks, (ERM_WARPS + 1) * 32, ERM_SMEM, st>>>(
       pl->erm_tmx, pl->erm_tmy, pr, pl->erm_dct, pl->nseg, pl->d_cls_slot, pl->d_cls, pl->d_rc,
-      pl->tot_rc);
+      pl->tot_rc, pl->ks_part, pl->ks_nparts);
   return true;
 }
 
@@ -593,6 +605,11 @@ void launch_edge(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
   const Problem& pr = pl->pr;
   if constexpr (sizeof(T) == 8) {
     if (pl->use_erm && launch_edge_rows_dmma(pl, (const double2*)A, st)) return;
+  }
+  if (pl->ks_nparts > 1) {  // the CUDA-core edge-row kernels have no row bands
+    fail(COVGPU_ECUDA, "row-band sums: edge-row kernel unavailable");
+    pl->ks_failed = true;
+    return;
   }
   if (pl->edge_tma && ((uintptr_t)A % 16 == 0) && ((2LL * pr.M * sizeof(T)) % 16 == 0) &&
       EdgeCfg<T, D>::stages(pl->S, pl->r2g) >= 2) {
@@ -705,6 +722,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       }
     }
   }
+  if (!mma && pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: tensor-core kernel unavailable");
   if (!mma) {
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
     launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
@@ -713,8 +731,10 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   ++launches;
   mark(mma ? "bulk_dmma" : "bulk");
   if (mma) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
-    if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es)))
+    if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es))) {
+      if (pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: edge-column kernel unavailable");
       launch_bulk_variant<T>(pl, A, es, pl->edge_variant, pl->ncb_l, pl->ncb_r);
+    }
     ++launches;
     mark("edge_cols");
   }
@@ -726,6 +746,24 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     }
     ++launches;
     mark("edge_rows");
+  }
+  if (pl->ks_out) {
+    // row-band partial sums (multi-GPU): reduce the per-CTA / per-segment
+    // partials into [CC | CCol | RC'] and stop before the finalize
+    if (fork) {
+      CUDA_TRY(cudaEventRecord(pl->ev_join, es));
+      CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
+    }
+    const long long ncc = (long long)B * pl->nclasses, ncl = (long long)B * pl->tot_ccol,
+                    nrc = (long long)B * pl->tot_rc;
+    const long long tot = ncc + ncl + nrc;
+    k_reduce_sums<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_ccpart, npart, ncc, pl->d_ccol,
+                                                                ncl, pl->d_rc, pl->nseg, nrc, pl->ks_out);
+    ++launches;
+    mark("reduce_sums");
+    CUDA_TRY(cudaGetLastError());
+    pl->launches = launches;
+    return COVGPU_OK;
   }
   if (pl->fin_kr > 0) {
     const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
@@ -789,6 +827,77 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
                                                                                                   : "finalize");
   CUDA_TRY(cudaGetLastError());
   pl->launches = launches;
+  return COVGPU_OK;
+}
+
+// Finalize from reduced sums [CC | CCol | RC'] (covgpu_plan_finalize_sums):
+// corners + the diagonal-segment walk for classes [c_lo, c_hi) of the plan.
+template <typename T>
+int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, void* R_dev, int layout,
+                       double scale, int c_lo, int c_hi, cudaStream_t st) {
+  using C2 = typename CT<T>::c;
+  const Problem& pr = pl->pr;
+  const int B = (int)pl->batch;
+  if (!pl->clean || pl->fin_kr == 0)
+    return fail(COVGPU_ECAPACITY, "finalize from sums needs the clean path with P <= 128");
+  const bool full = c_lo == 0 && c_hi == pl->nclasses;
+  if (!full && layout != COVGPU_COMPACT)
+    return fail(COVGPU_EINVAL, "a class range finalizes into the compact layout");
+  const int2* tasks = pl->d_tasks;
+  long long ntasks = pl->ntasks;
+  if (!full) {
+    if (pl->rtask_lo != c_lo || pl->rtask_hi != c_hi) {
+      std::vector<int2> sub;
+      for (const int2& t : pl->h_tasks)
+        if (t.x >= c_lo && t.x < c_hi) sub.push_back(t);
+      cudaFree(pl->d_rtasks);
+      pl->d_rtasks = nullptr;
+      CUDA_TRY(cudaMalloc((void**)&pl->d_rtasks, sizeof(int2) * std::max<size_t>(sub.size(), 1)));
+      if (!sub.empty())
+        CUDA_TRY(cudaMemcpy(pl->d_rtasks, sub.data(), sizeof(int2) * sub.size(), cudaMemcpyHostToDevice));
+      pl->n_rtasks = (long long)sub.size();
+      pl->rtask_lo = c_lo;
+      pl->rtask_hi = c_hi;
+    }
+    tasks = pl->d_rtasks;
+    ntasks = pl->n_rtasks;
+  }
+  long long r_bstride;
+  if (layout == COVGPU_DENSE)
+    r_bstride = (long long)pr.PQ * pr.PQ;
+  else if (layout == COVGPU_PACKED)
+    r_bstride = (long long)pr.PQ * (pr.PQ + 1) / 2;
+  else
+    r_bstride = pl->compact_elems;
+  const C2* A = (const C2*)A_dev;
+  const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
+  if (nc > 0) k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, (C2*)pl->d_corners);
+  if (ntasks > 0) {
+    const double2* cc = sums;
+    const double2* cl = sums + (long long)B * pl->nclasses;
+    const double2* rc = cl + (long long)B * pl->tot_ccol;
+    const unsigned blocks = (unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS);
+    const bool direct = layout != COVGPU_COMPACT;
+#define FINS(KR, DIR)                                                                             \
+  k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                   \
+      (const C2*)pl->d_corners, pr, pl->d_cls, tasks, ntasks, pl->nclasses, 1, 1, B, cc, cl,      \
+      pl->tot_ccol, rc, pl->tot_rc, 1, (C2*)R_dev, r_bstride, scale, direct ? layout : (int)COVGPU_COMPACT)
+    if (direct) {
+      switch (pl->fin_kr) {
+        case 1: FINS(1, true); break;
+        case 2: FINS(2, true); break;
+        default: FINS(4, true);
+      }
+    } else {
+      switch (pl->fin_kr) {
+        case 1: FINS(1, false); break;
+        case 2: FINS(2, false); break;
+        default: FINS(4, false);
+      }
+    }
+#undef FINS
+  }
+  CUDA_TRY(cudaGetLastError());
   return COVGPU_OK;
 }
 
@@ -1114,6 +1223,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         return pl->h_cls[x.x].qu > pl->h_cls[y.x].qu;
       });
       pl->ntasks = (long long)tasks.size();
+      pl->h_tasks = tasks;
       const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
       const size_t cbytes = (size_t)batch * 4 * (size_t)std::max(p - 1, 0) * (size_t)std::max(q - 1, 0) * esz;
       std::vector<long long> uc_off(nuc, -1);
@@ -1201,6 +1311,59 @@ int32_t covgpu_plan_kernel_times(covgpu_plan_t pl, float* ms, int32_t max_n) {
   for (int i = 0; i + 1 < pl->nev && n < max_n; ++i, ++n)
     if (cudaEventElapsedTime(&ms[n], pl->ev[i], pl->ev[i + 1]) != cudaSuccess) ms[n] = -1.0f;
   return n;
+}
+
+int64_t covgpu_plan_sums_elems(covgpu_plan_t pl) {
+  if (!pl) return -1;
+  return pl->batch * ((long long)pl->nclasses + pl->tot_ccol + pl->tot_rc);
+}
+
+int covgpu_plan_execute_sums(covgpu_plan_t pl, const void* A_dev, void* sums_dev, int32_t part,
+                             int32_t nparts, void* stream) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  if (!A_dev || !sums_dev) return fail(COVGPU_EINVAL, "A and sums must be device pointers");
+  if (nparts < 1 || part < 0 || part >= nparts) return fail(COVGPU_EINVAL, "part must be in [0, nparts)");
+  if (!(pl->use_mma && pl->use_ecm && pl->use_erm && pl->mma_kind != 0))
+    return fail(COVGPU_ECAPACITY,
+                "row-band partial sums need the complex128 tensor-core path with tensor-core edge "
+                "kernels (all classes, P in [48, 65], Q in [50, 65])");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  std::lock_guard<std::mutex> lk(pl->exec_mu);
+  if ((uintptr_t)A_dev % 16 != 0) return fail(COVGPU_EINVAL, "A must be 16-byte aligned");
+  pl->ks_part = part;
+  pl->ks_nparts = nparts;
+  pl->ks_out = (double2*)sums_dev;
+  pl->ks_failed = false;
+  int rc = launch_all<double>(pl, A_dev, nullptr, COVGPU_COMPACT, 1.0, (cudaStream_t)stream);
+  if (!rc && pl->ks_failed) rc = COVGPU_ECUDA;
+  pl->ks_part = 0;
+  pl->ks_nparts = 1;
+  pl->ks_out = nullptr;
+  return rc;
+}
+
+int covgpu_plan_finalize_sums(covgpu_plan_t pl, const void* A_dev, const void* sums_dev, void* R_dev,
+                              int32_t layout, double scale, int32_t class_lo, int32_t class_hi,
+                              void* stream) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  if (!A_dev || !sums_dev || !R_dev) return fail(COVGPU_EINVAL, "A, sums and R must be device pointers");
+  if (layout < COVGPU_DENSE || layout > COVGPU_COMPACT) return fail(COVGPU_EINVAL, "unknown layout");
+  if (class_lo < 0 || class_hi > pl->nclasses || class_lo > class_hi)
+    return fail(COVGPU_EINVAL, "class range outside the plan");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  std::lock_guard<std::mutex> lk(pl->exec_mu);
+  CUDA_TRY(set_attrs());
+  if (pl->dtype == COVGPU_C128)
+    return finalize_from_sums<double>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale, class_lo,
+                                      class_hi, (cudaStream_t)stream);
+  return finalize_from_sums<float>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale, class_lo,
+                                   class_hi, (cudaStream_t)stream);
+}
+
+int64_t covgpu_plan_class_slot_offset(covgpu_plan_t pl, int32_t class_index) {
+  if (!pl || class_index < 0 || class_index > pl->nclasses) return -1;
+  if (class_index == pl->nclasses) return pl->compact_elems;
+  return pl->h_cls[class_index].slot_off;
 }
 
 int32_t covgpu_plan_kernel_names(covgpu_plan_t pl, char* buf, int32_t len) {

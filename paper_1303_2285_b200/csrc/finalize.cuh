@@ -413,4 +413,26 @@ __global__ void k_expand(const typename CT<T>::c* __restrict__ compact, long lon
   R[tid] = val;
 }
 
+// Reduce the partials of one execute into [CC | CCol | RC'] (one value per
+// class / edge column / edge row): CC over the bulk kernel's npart partials,
+// RC' over the edge-row kernel's nseg column segments, fixed order.
+__global__ void k_reduce_sums(const double2* __restrict__ ccpart, int npart, long long ncc,
+                              const double2* __restrict__ ccol, long long ncl,
+                              const double2* __restrict__ rc, int nseg, long long nrc,
+                              double2* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ncc) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int g = 0; g < npart; ++g) a = cadd(a, ccpart[t * npart + g]);
+    out[t] = a;
+  } else if (t < ncc + ncl) {
+    out[t] = ccol[t - ncc];
+  } else if (t < ncc + ncl + nrc) {
+    const long long r = t - ncc - ncl;
+    double2 a = make_double2(0.0, 0.0);
+    for (int g = 0; g < nseg; ++g) a = cadd(a, rc[r * nseg + g]);
+    out[t] = a;
+  }
+}
+
 }  // namespace covgpu

@@ -328,7 +328,7 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
     k_edge_cols_dmma(const __grid_constant__ CUtensorMap tms, Problem pr, int G,
                      const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
                      double2* __restrict__ ccol, long long tot_ccol, double2* __restrict__ part,
-                     unsigned* __restrict__ tickets) {
+                     unsigned* __restrict__ tickets, int kpart, int knparts) {
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ECM_STAGES * ECM_STAGE);
   uint64_t* empty = full + ECM_STAGES;
@@ -337,8 +337,10 @@ __global__ void __launch_bounds__((MMA_WARPS + 1) * 32, 2)
   const int g = (int)(blockIdx.x % G);
   const EcmItem it = ecm_item(item, pr);
   const int P = pr.P, Q = pr.Q;
-  const int nrc = (it.hi - it.lo + ECM_RC) / ECM_RC;
-  const int c0 = nrc * g / G, c1 = nrc * (g + 1) / G;
+  // multi-GPU row band kpart of knparts, then split g of G within it
+  const int nrc_all = (it.hi - it.lo + ECM_RC) / ECM_RC;
+  const int b_lo = nrc_all * kpart / knparts, nrc = nrc_all * (kpart + 1) / knparts - b_lo;
+  const int c0 = b_lo + nrc * g / G, c1 = b_lo + nrc * (g + 1) / G;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ECM_STAGES; ++s) {
@@ -457,7 +459,8 @@ constexpr size_t ERM_SMEM = ERM_STAGES * ERM_STAGE + 64;
 __global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 1)
     k_edge_rows_dmma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                      Problem pr, int n_dct, int nseg, const int* __restrict__ cls_slot,
-                     const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc) {
+                     const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc,
+                     int kpart, int knparts) {
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + ERM_STAGES * ERM_STAGE);
   uint64_t* empty = full + ERM_STAGES;
@@ -475,7 +478,9 @@ __global__ void __launch_bounds__((ERM_WARPS + 1) * 32, 1)
   const int dc0 = dct * ERM_DC;
   const int xcols = pr.M - Q + 1;
   const int ncbk = (xcols + MMA_W - 1) / MMA_W;
-  const int k0 = ncbk * seg / nseg, k1 = ncbk * (seg + 1) / nseg;
+  // multi-GPU: segment seg belongs to part seg % knparts; the others write zeros
+  const bool mine = seg % knparts == kpart;
+  const int k0 = ncbk * seg / nseg, k1 = mine ? ncbk * (seg + 1) / nseg : k0;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ERM_STAGES; ++s) {
@@ -675,7 +680,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     k_bulk_dmma3(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
                  Problem pr, int n_drt, int n_dct, int G, int nclasses,
                  const int* __restrict__ cls_slot, double2* __restrict__ ccpart,
-                 const unsigned* __restrict__ band_flag, unsigned band_base, int band_rows) {
+                 const unsigned* __restrict__ band_flag, unsigned band_base, int band_rows, int part,
+                 int nparts) {
+  // part / nparts: multi-GPU row bands — this launch covers row chunks
+  // [nrc*part/nparts, nrc*(part+1)/nparts) of every tile (partial sums)
   using Cfg = Mma3Cfg<WM, WN, MT, NTW, MINB, PREP, RC>;
   constexpr int S = Cfg::S, DR = Cfg::DR, DC = Cfg::DC, NW = Cfg::WARPS;
   static_assert(S >= 2, "TMA ring needs two stages");
@@ -696,7 +704,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
   const int drmax = min(dr0 + DR - 1, P - 1);
   const int rlo = max(0, P - 1 + min(dr0, 0));
   const int rhi = min(N - 1, N - P + max(drmax, 0));
-  const int nrc = (rhi - rlo + RC) / RC;
+  const int nrc_all = (rhi - rlo + RC) / RC;
+  const int rc_lo = (int)((long long)nrc_all * part / nparts);
+  const int nrc = (int)((long long)nrc_all * (part + 1) / nparts) - rc_lo;
+  const int rbase = rlo + rc_lo * RC;  // first row of this band
   const int xcols = M - Q + 1;
   const int ncbk = (xcols + MMA_W - 1) / MMA_W;
   const long long nch = (long long)nrc * ncbk;
@@ -718,7 +729,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       const int s = (int)(k % S);
       if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
       const long long q = p + k * G;
-      const int R = rlo + (int)(q / ncbk) * RC;
+      const int R = rbase + (int)(q / ncbk) * RC;
       const int C0 = (int)(q % ncbk) * MMA_W;
       if (band_flag) {
         const int rneed = min(N - 1, R + RC - 1 + max(-dr0, 0));
@@ -765,7 +776,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
         const int s = (int)(k % S);
         if (k >= S) mbar_wait_sleep(&empty[s], (int)(((k - S) / S) & 1));
         const long long q = p + k * G;
-        const int R = rlo + (int)(q / ncbk) * RC;
+        const int R = rbase + (int)(q / ncbk) * RC;
         const int C0 = (int)(q % ncbk) * MMA_W;
         if (band_flag) {
           const int rneed = min(N - 1, R + RC - 1 + max(-dr0, 0));
@@ -799,7 +810,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     else
       mbar_wait(&full[s], (int)((k / S) & 1));
     const long long q = p + k * G;
-    const int R = rlo + (int)(q / ncbk) * RC;
+    const int R = rbase + (int)(q / ncbk) * RC;
     const int C0 = (int)(q % ncbk) * MMA_W;
     const int nks = min(MMA_W, xcols - C0 + 3) / 4;
     const double2* X = reinterpret_cast<const double2*>(smraw + s * Cfg::stage);

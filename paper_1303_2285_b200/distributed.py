@@ -14,9 +14,18 @@ and batch snapshots are independent (``engine.py:219-255``).  So:
   contiguously across ranks; each rank returns its own (b, PQ, PQ) slice, and
   rank 0 can gather the full batch.
 
-The per-shard compute and the root-side scatter are injectable (``ShardOps``)
-so the orchestration can be tested on CPU with the gloo backend; the default
-ops are the CUDA library and there is no CPU fallback.
+* ``estimate_rowband`` — the single large estimate on the tensor-core path:
+  the sums the kernels accumulate (CC, edge-column and edge-row sums) are
+  sums over A's rows, so each rank computes one row band of every sum
+  (``covgpu_plan_execute_sums``), the bands meet in ONE all-reduce of the
+  [CC | CCol | RC'] buffer (16 MB at cfg5), and each rank finalizes a
+  contiguous, slot-balanced range of classes from the reduced sums
+  (``covgpu_plan_finalize_sums``); rank 0 gathers the compact ranges on
+  request.  Unlike class sharding, every rank keeps the tensor-core kernels.
+
+The per-shard compute and the root-side scatter are injectable (``ShardOps``,
+``BandOps``) so the orchestration can be tested on CPU with the gloo backend;
+the default ops are the CUDA library and there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -30,7 +39,8 @@ import torch.distributed as dist
 from .core import WindowSpec
 from .partition import partition_classes
 
-__all__ = ["ShardOps", "cuda_ops", "estimate_sharded", "estimate_batch_sharded", "shard_bounds"]
+__all__ = ["ShardOps", "cuda_ops", "estimate_sharded", "estimate_batch_sharded", "shard_bounds",
+           "BandOps", "cuda_band_ops", "estimate_rowband", "class_ranges"]
 
 
 @dataclass
@@ -180,3 +190,103 @@ def estimate_batch_sharded(stack: torch.Tensor | None, shape: tuple[int, int, in
         else:
             full = out
     return full, out, (lo, hi)
+
+
+@dataclass
+class BandOps:
+    # (window, N, M) -> compact offset of every class in UC order (+ total at the end)
+    slot_offsets: Callable
+    # (A (N,M), window, part, nparts) -> this band's reduced sums (1-D tensor)
+    compute_sums: Callable
+    # (A, window, all-reduced sums, class_lo, class_hi) -> compact slots of those classes
+    finalize_range: Callable
+    # (full compact tensor, window, N, M, dtype, device) -> dense R
+    expand_dense: Callable
+
+
+def cuda_band_ops() -> BandOps:
+    from .plan import Plan
+
+    cache = {}
+
+    def plan_for(a, window):
+        key = (a.shape[0], a.shape[1], window.p, window.q, a.dtype, a.device)
+        if key not in cache:
+            cache[key] = Plan(a.shape[0], a.shape[1], window, dtype=a.dtype, device=a.device)
+        return cache[key]
+
+    def slot_offsets(window, n, m):
+        a = torch.empty((n, m), dtype=torch.complex128, device=torch.device("cuda", torch.cuda.current_device()))
+        plan = plan_for(a, window)
+        return [plan.class_slot_offset(i) for i in range(plan.num_classes + 1)]
+
+    def compute_sums(a, window, part, nparts):
+        plan = plan_for(a, window)
+        sums = plan.alloc_sums()
+        return plan.execute_sums(a, sums, part, nparts)
+
+    def finalize_range(a, window, sums, lo, hi):
+        plan = plan_for(a, window)
+        full = torch.empty(plan.output_elems("compact"), dtype=a.dtype, device=a.device)
+        plan.finalize_sums(a, sums, full, "compact", lo, hi)
+        return full[plan.class_slot_offset(lo):plan.class_slot_offset(hi)]
+
+    def expand_dense(compact, window, n, m, dtype, device):
+        nuc = window.p * window.q + (window.p - 1) * (window.q - 1)
+        return cuda_ops().scatter_dense([compact], [list(range(nuc))], window, n, m, dtype, device)
+
+    return BandOps(slot_offsets, compute_sums, finalize_range, expand_dense)
+
+
+def class_ranges(offsets, world: int) -> list[tuple[int, int]]:
+    """Contiguous class ranges with about equal slot counts (the finalize's
+    work), one per rank, from the compact offsets (len = classes + 1)."""
+    nc = len(offsets) - 1
+    total = offsets[-1]
+    bounds = [0]
+    c = 0
+    for r in range(1, world):
+        target = total * r / world
+        while c < nc and offsets[c] < target:
+            c += 1
+        bounds.append(max(c, bounds[-1]))
+    bounds.append(nc)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def estimate_rowband(a: torch.Tensor | None, shape: tuple[int, int], window: WindowSpec,
+                     dtype=torch.complex128, device=None, gather: bool = False,
+                     ops: BandOps | None = None):
+    """Row-band estimate of one matrix across the process group (module
+    docstring).  `a` lives on rank 0.  Returns (dense R on rank 0 if `gather`
+    else None, this rank's compact slots, its class range)."""
+    ops = ops or cuda_band_ops()
+    rank, world = _world()
+    n, m = shape
+    window.validate_for(n, m)
+    if device is None:
+        device = a.device if (a is not None and rank == 0) else torch.device("cpu")
+    buf = a if rank == 0 else torch.empty((n, m), dtype=dtype, device=device)
+    if world > 1:
+        dist.broadcast(_r(buf), src=0)
+    sums = ops.compute_sums(buf, window, rank, world)
+    if world > 1:
+        dist.all_reduce(_r(sums))  # the one exchange: per-band sums -> full sums
+    offsets = ops.slot_offsets(window, n, m)
+    lo, hi = class_ranges(offsets, world)[rank]
+    comp = ops.finalize_range(buf, window, sums, lo, hi)
+    dense = None
+    if gather:
+        if world > 1:
+            width = max(offsets[h] - offsets[l] for l, h in class_ranges(offsets, world))
+            padded = torch.zeros(width, dtype=dtype, device=device)
+            padded[: comp.numel()] = comp
+            bucket = [torch.empty_like(padded) for _ in range(world)] if rank == 0 else None
+            dist.gather(_r(padded), [_r(x) for x in bucket] if rank == 0 else None, dst=0)
+            if rank == 0:
+                full = torch.cat([bucket[r][: offsets[h] - offsets[l]]
+                                  for r, (l, h) in enumerate(class_ranges(offsets, world))])
+                dense = ops.expand_dense(full, window, n, m, dtype, device)
+        else:
+            dense = ops.expand_dense(comp, window, n, m, dtype, device)
+    return dense, comp, (lo, hi)

@@ -66,6 +66,49 @@ class Plan:
         _native.check(rc, "covgpu_plan_execute_host")
         return out_host
 
+    # ---- multi-GPU row bands (include/covgpu.h: covgpu_plan_execute_sums) ----
+    def sums_elems(self) -> int:
+        """complex128 values of the reduced-sums buffer [CC | CCol | RC']."""
+        return int(self.lib.covgpu_plan_sums_elems(self.handle))
+
+    def alloc_sums(self) -> torch.Tensor:
+        return torch.zeros(self.sums_elems(), dtype=torch.complex128, device=self.device)
+
+    def execute_sums(self, a: torch.Tensor, sums: torch.Tensor, part: int = 0, nparts: int = 1,
+                     stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Part `part` of `nparts` row bands of every sum, reduced into `sums`."""
+        if sums.dtype != torch.complex128 or sums.numel() != self.sums_elems() or not sums.is_contiguous():
+            raise ValueError("sums buffer does not match the plan")
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.covgpu_plan_execute_sums(self.handle, ctypes.c_void_p(a.data_ptr()),
+                                               ctypes.c_void_p(sums.data_ptr()), part, nparts,
+                                               ctypes.c_void_p(st.cuda_stream))
+        _native.check(rc, "covgpu_plan_execute_sums")
+        return sums
+
+    def finalize_sums(self, a: torch.Tensor, sums: torch.Tensor, out: torch.Tensor,
+                      layout: str = "compact", class_lo: int = 0, class_hi: int | None = None,
+                      scale: float | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """R (or the compact slots of classes [class_lo, class_hi)) from reduced sums."""
+        hi = self.num_classes if class_hi is None else class_hi
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.covgpu_plan_finalize_sums(
+            self.handle, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(sums.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), LAYOUTS[layout], 1.0 / self.k if scale is None else scale,
+            class_lo, hi, ctypes.c_void_p(st.cuda_stream))
+        _native.check(rc, "covgpu_plan_finalize_sums")
+        return out
+
+    @property
+    def num_classes(self) -> int:
+        if self.class_ids is not None:
+            return len(set(self.class_ids))
+        return int(self.lib.covgpu_num_classes(self.window.p, self.window.q))
+
+    def class_slot_offset(self, i: int) -> int:
+        """Compact offset of plan class i (i == num_classes: total slots)."""
+        return int(self.lib.covgpu_plan_class_slot_offset(self.handle, i))
+
     def set_timing(self, enable: bool = True) -> None:
         _native.check(self.lib.covgpu_plan_set_timing(self.handle, int(enable)), "set_timing")
 

@@ -14,7 +14,15 @@ import torch.multiprocessing as mp
 
 from oracle import covoracle as co
 from paper_1303_2285_b200 import WindowSpec
-from paper_1303_2285_b200.distributed import ShardOps, estimate_batch_sharded, estimate_sharded, shard_bounds
+from paper_1303_2285_b200.distributed import (
+    BandOps,
+    ShardOps,
+    class_ranges,
+    estimate_batch_sharded,
+    estimate_rowband,
+    estimate_sharded,
+    shard_bounds,
+)
 from paper_1303_2285_b200.partition import partition_classes
 
 
@@ -45,6 +53,46 @@ def oracle_ops() -> ShardOps:
         return torch.stack([torch.from_numpy(co.covariance(x.numpy(), window.p, window.q)) for x in a])
 
     return ShardOps(compute_compact, scatter_dense, compute_batch)
+
+
+def oracle_band_ops() -> BandOps:
+    """Row-band ops on the CPU oracle.  A band's partial 'sums' here are the
+    unnormalised slot sums over a band of window-placement rows (linear in
+    the products, so the all-reduce of the bands is the full slot sums) in
+    compact (UC-major) order; finalizing a class range scales its slots by
+    1/K — the same orchestration as the CUDA ops, with oracle-defined sums."""
+
+    def slot_offsets(window, n, m):
+        offs = [0]
+        for dr, dc in co.unique_combinations(window.p, window.q):
+            offs.append(offs[-1] + (window.p - abs(dr)) * (window.q - dc))
+        return offs
+
+    def compute_sums(a, window, part, nparts):
+        arr = a.numpy()
+        n = arr.shape[0]
+        bh = n - window.p + 1
+        w0, w1 = bh * part // nparts, bh * (part + 1) // nparts
+        sub = arr[w0:w1 + window.p - 1]
+        parts = []
+        for dr, dc in co.unique_combinations(window.p, window.q):
+            if w1 > w0:
+                parts.append(co.class_slot_sums(sub, dr, dc, window.p, window.q))
+            else:
+                parts.append(np.zeros((window.p - abs(dr)) * (window.q - dc), dtype=np.complex128))
+        return torch.from_numpy(np.concatenate(parts))
+
+    def finalize_range(a, window, sums, lo, hi):
+        n, m = a.shape
+        k = (n - window.p + 1) * (m - window.q + 1)
+        offs = slot_offsets(window, n, m)
+        return sums[offs[lo]:offs[hi]] / k
+
+    def expand_dense(compact, window, n, m, dtype, device):
+        nuc = len(co.unique_combinations(window.p, window.q))
+        return oracle_ops().scatter_dense([compact], [list(range(nuc))], window, n, m, dtype, device)
+
+    return BandOps(slot_offsets, compute_sums, finalize_range, expand_dense)
 
 
 def _free_port():
@@ -80,6 +128,14 @@ def _worker(rank, world, port, results):
         if rank == 0:
             ref = np.stack([co.covariance(x, 3, 4) for x in stack.numpy()])
             out["batch_err"] = co.rel_frobenius(full.numpy(), ref)
+        # row bands: per-band sums, all-reduce, class-range finalize, gather
+        dense_b, comp_b, crange = estimate_rowband(a if rank == 0 else None, (n, m), WindowSpec(p, q),
+                                                   gather=True, ops=oracle_band_ops(),
+                                                   device=torch.device("cpu"))
+        out["band_range"] = crange
+        out["band_comp"] = comp_b.numpy()
+        if rank == 0:
+            out["band_err"] = co.rel_frobenius(dense_b.numpy(), co.covariance(a.numpy(), p, q))
         results[rank] = out
     finally:
         dist.destroy_process_group()
@@ -97,6 +153,11 @@ def test_two_rank_sharded_estimate():
     assert r0["ids"] == shards[0] and r1["ids"] == shards[1]
     assert set(r0["ids"]).isdisjoint(r1["ids"])
     assert r0["bounds"] == (0, 3) and r1["bounds"] == (3, 5)
+    # row bands: full R on the root, contiguous class ranges covering UC
+    assert r0["band_err"] <= 1e-13
+    nuc = len(co.unique_combinations(5, 4))
+    assert r0["band_range"][0] == 0 and r0["band_range"][1] == r1["band_range"][0]
+    assert r1["band_range"][1] == nuc
 
 
 def test_shard_bounds_cover_batch():
@@ -107,3 +168,15 @@ def test_shard_bounds_cover_batch():
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
             sizes = [hi - lo for lo, hi in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_class_ranges_balance_slots():
+    offs = [0]
+    for dr, dc in co.unique_combinations(64, 64):
+        offs.append(offs[-1] + (64 - abs(dr)) * (64 - dc))
+    for world in (1, 2, 3, 8):
+        rng = class_ranges(offs, world)
+        assert rng[0][0] == 0 and rng[-1][1] == len(offs) - 1
+        assert all(rng[i][1] == rng[i + 1][0] for i in range(world - 1))
+        loads = [offs[h] - offs[l] for l, h in rng]
+        assert max(loads) - min(loads) <= 2 * 64 * 64  # within one class of even

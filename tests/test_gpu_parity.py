@@ -589,3 +589,47 @@ def test_tensor_core_path_fuzz(cuda):
             worst = max(worst, err)
             assert err <= TOL64, (it, n, m, p, q, batch, err)
     print(f"tensor-core fuzz worst relF {worst:.2e}")
+
+
+def test_row_band_sums_and_class_range_finalize(cuda):
+    """Multi-GPU row-band mode on one GPU: the sums of 3 bands added together
+    (what the all-reduce does) finalize to R; one band matches the plain
+    execute to rounding (the CC partials are pre-reduced in a different
+    order); class-range finalizes tile the compact layout bit for bit."""
+    from paper_1303_2285_b200.distributed import class_ranges
+    from paper_1303_2285_b200.plan import Plan
+
+    n, m, p, q = 400, 420, 50, 56
+    rng = np.random.default_rng(77)
+    a = torch.as_tensor(rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m)), device=cuda)
+    win = WindowSpec(p, q)
+    plan = Plan(n, m, win, dtype=torch.complex128, device=cuda)
+    ref = plan.alloc_output()
+    plan.execute(a, ref)
+    ref_c = plan.alloc_output("compact")
+    plan.execute(a, ref_c, "compact")
+    # one band == the plain path up to the order of the CC partial sums
+    s1 = plan.execute_sums(a, plan.alloc_sums(), 0, 1)
+    got = plan.finalize_sums(a, s1, plan.alloc_output(), "dense")
+    assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= 1e-15
+    full_c = plan.finalize_sums(a, s1, plan.alloc_output("compact"), "compact")
+    assert (torch.linalg.norm(full_c - ref_c) / torch.linalg.norm(ref_c)).item() <= 1e-15
+    # three bands summed
+    tot = plan.alloc_sums()
+    for part in range(3):
+        tot += plan.execute_sums(a, plan.alloc_sums(), part, 3)
+    got3 = plan.finalize_sums(a, tot, plan.alloc_output(), "dense")
+    err = (torch.linalg.norm(got3 - ref) / torch.linalg.norm(ref)).item()
+    assert err <= 1e-14, err
+    # class ranges tile the compact layout
+    offs = [plan.class_slot_offset(i) for i in range(plan.num_classes + 1)]
+    comp = plan.alloc_output("compact", zero=True)
+    for lo, hi in class_ranges(offs, 3):
+        plan.finalize_sums(a, s1, comp, "compact", lo, hi)
+    assert torch.equal(comp, full_c)
+    plan.close()
+    # outside the tensor-core edge kernels' range the mode is refused
+    small = Plan(200, 240, WindowSpec(20, 30), dtype=torch.complex128, device=cuda)
+    with pytest.raises(ValueError):
+        small.execute_sums(a[:200, :240].contiguous(), small.alloc_sums(), 0, 2)
+    small.close()
