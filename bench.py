@@ -196,6 +196,8 @@ def main() -> None:
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of CPU-baseline sample")
     ap.add_argument("--ref-budget", type=float, default=4.0, help="seconds per reference-arm step")
     ap.add_argument("--layout", default="dense", choices=["dense", "packed", "compact"])
+    ap.add_argument("--rowband", action="store_true",
+                    help="use the multi-GPU row-band mode also at N=1 (testing)")
     ap.add_argument("--no-cuda-core", action="store_true",
                     help="skip the CUDA-core (non-tensor-core) comparison steps")
     args = ap.parse_args()
@@ -223,11 +225,21 @@ def main() -> None:
     w = workload(args.config)
     win = WindowSpec(w.p, w.q)
     tdt = torch.complex128 if w.dtype == "c128" else torch.complex64
+    # N > 1: row bands (every rank on the tensor-core path, one all-reduce of
+    # the per-band sums) where the shape allows, else class shards
+    rowband = (world > 1 or args.rowband) and w.dtype == "c128" and 48 <= w.p <= 65 \
+        and 50 <= w.q <= 65
     ids = None
-    if world > 1:
+    if world > 1 and not rowband:
         ids = partition_classes(w.n, w.m, win, world, fp64=(w.dtype == "c128"))[rank]
     plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, class_ids=ids, device=dev)
-    layout = args.layout if world == 1 else "compact"
+    layout = args.layout if world == 1 and not rowband else "compact"
+    if rowband:
+        from paper_1303_2285_b200.distributed import class_ranges
+
+        sums = plan.alloc_sums()
+        offsets = [plan.class_slot_offset(i) for i in range(plan.num_classes + 1)]
+        c_lo, c_hi = class_ranges(offsets, world)[rank]
     host_a = make_input(w) if rank == 0 else None
     a = torch.empty((w.batch, w.n, w.m), dtype=tdt, device=dev)
     if rank == 0:
@@ -245,7 +257,13 @@ def main() -> None:
     def step():
         if world > 1:
             dist.broadcast(a_real, src=0)
-        plan.execute(a, out, layout)
+        if rowband:
+            plan.execute_sums(a, sums, rank, world)
+            if world > 1:
+                dist.all_reduce(torch.view_as_real(sums))
+            plan.finalize_sums(a, sums, out, "compact", c_lo, c_hi)
+        else:
+            plan.execute(a, out, layout)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -269,7 +287,7 @@ def main() -> None:
         # short timed regions end before nvidia-smi's first samples: keep the
         # same load running (untimed) until ~0.6 s have been sampled
         while time.perf_counter() - t_start < 0.6:
-            plan.execute(a, out, layout)
+            step()
             torch.cuda.synchronize(dev)
     # per-kernel breakdown: separate steps with events between the launches
     # (kernels serialised on one stream for this, so intervals are per kernel)
@@ -278,7 +296,10 @@ def main() -> None:
     for _ in range(max(3, min(args.steps, 10))):
         flush.fill_(1)
         torch.cuda.synchronize(dev)
-        plan.execute(a, out, layout)
+        if rowband:
+            plan.execute_sums(a, sums, rank, world)
+        else:
+            plan.execute(a, out, layout)
         kern.append(plan.kernel_times())
     knames = plan.kernel_names()
     plan.set_timing(False)
@@ -297,11 +318,13 @@ def main() -> None:
         for name, col in zip(knames, kt.mean(axis=0)):
             kernel_ms[name] = float(col)
     shard_frac = 1.0 if ids is None else shard_cost(w.n, w.m, win, ids) / um
+    if rowband:
+        shard_frac = 1.0 / world
     roof = None
     if kernel_ms.get("bulk_dmma", 0) > 0:
         # dominant kernel on the FP64 tensor cores: core products x 6 flops (the
         # Gauss 3-multiplication complex product: 3 real FMAs per product)
-        achieved = 6.0 * core_p * w.batch / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12
+        achieved = 6.0 * core_p * w.batch * shard_frac / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12
         traffic = None
         prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
         if prof.exists():
@@ -314,9 +337,10 @@ def main() -> None:
                 "kernel": "k_bulk_dmma" if os.environ.get("COVGPU_MMA_KIND") == "0" else "k_bulk_dmma3",
                 "peak_source": "DMMA-loop probe (mma.sync m8n8k4 f64) measured on this GPU in this "
                 "run (MEASURED_PEAKS.json has no FP64 figure)",
-                "algorithmic_flops_per_launch": 6.0 * core_p * w.batch,
+                "algorithmic_flops_per_launch": 6.0 * core_p * w.batch * shard_frac,
                 "flops_per_product": "6 (Gauss: Re = P1 + P2, Im = P3 - P1 + P2, 3 real FMAs)",
-                "complex_mac_equivalent_tflops": 8.0 * core_p * w.batch / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12,
+                "complex_mac_equivalent_tflops": 8.0 * core_p * w.batch * shard_frac
+                / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12,
                 "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
                 "fma_loop_peak": peak}
     elif "bulk" in kernel_ms and kernel_ms["bulk"] > 0:
@@ -342,10 +366,12 @@ def main() -> None:
         "data": f"synthetic ({w.name}: seeded CN(0,1)/sinusoid inputs of BASELINE.json)",
         "config": {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
                    "input": w.dtype, "output": layout, "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"class-shard x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"row-band x{world}: per-band sums, one all-reduce of [CC|CCol|RC'] "
+                                   f"({sums.numel() * 16 / 2**20:.1f} MiB), class-range finalize")
+                   if rowband else (f"class-shard x{world}" if world > 1 else "single GPU")},
         "effective_gflops": flops / (ms * 1e-3) / 1e9,
         "kernel_ms": kernel_ms,
-        "gpu_launches": plan.launches * args.steps,
+        "gpu_launches": (plan.launches + (2 if rowband else 0)) * args.steps,
         "roofline": roof,
         "clocks": clocks.summary(),
     }
@@ -354,7 +380,7 @@ def main() -> None:
     # still the path for complex64 and class shards): same workload, a few
     # steps, per-kernel events — reported, not the headline
     if roof is not None and roof.get("kernel", "").startswith("k_bulk_dmma") and world == 1 \
-            and not args.no_cuda_core:
+            and not args.no_cuda_core and not rowband:
         os.environ["COVGPU_NO_MMA"] = "1"
         try:
             cplan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, device=dev)
@@ -392,7 +418,38 @@ def main() -> None:
         }
 
     # end to end through the C ABI with pinned host buffers
-    if not args.no_e2e:
+    if not args.no_e2e and rowband:
+        # end to end for row bands: rank 0's pinned host A -> device, broadcast,
+        # band sums, all-reduce, class-range finalize, D2H of the rank's range
+        a_host = torch.from_numpy(host_a if rank == 0 else make_input(w)).reshape(
+            w.batch, w.n, w.m).pin_memory()
+        lo_off, hi_off = offsets[c_lo], offsets[c_hi]
+        r_host = torch.empty(hi_off - lo_off, dtype=tdt).pin_memory()
+
+        def e2e_step():
+            if rank == 0:
+                a.copy_(a_host, non_blocking=True)
+            step()
+            r_host.copy_(out[lo_off:hi_off], non_blocking=True)
+            torch.cuda.synchronize(dev)
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        te = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        esz = r_host.element_size()
+        line["e2e"] = {"value": entries / float(te.item()), "unit": UNIT,
+                       "h2d_bytes_per_step": a_host.numel() * esz if rank == 0 else 0,
+                       "d2h_bytes_per_step": r_host.numel() * esz,
+                       "ms_per_step": float(te.item()) * 1e3,
+                       "path": "row bands: pinned H2D of A on rank 0, broadcast, execute_sums, all-reduce, "
+                               "finalize_sums (class range), D2H of the rank's compact range; wall clock"}
+    elif not args.no_e2e:
         e2e_layout = "packed" if world == 1 else "compact"
         a_host = torch.from_numpy(host_a if rank == 0 else make_input(w)).reshape(
             w.batch, w.n, w.m).pin_memory()
