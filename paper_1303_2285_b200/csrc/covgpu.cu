@@ -34,6 +34,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -48,6 +49,7 @@
 #include "general.cuh"
 #include "mma.cuh"
 #include "probe.cuh"
+#include "spectral.cuh"
 
 using namespace covgpu;
 
@@ -108,6 +110,12 @@ struct covgpu_plan {
   unsigned* d_ecm_tickets = nullptr;
   const void* ecm_ptr = nullptr;
   CUtensorMap ecm_tm{};
+  // spectral core sums (spectral.cuh): row FFTs of length L = 2^spec_logL,
+  // per-frequency row-lag correlation, output DFT; dr = 0 in the space domain
+  bool use_spec = false;
+  int spec_logL = 0, spec_L = 0, spec_nseg = 1, spec_nfb = 1, spec_ngrp = 1;
+  int spec_nrb = 0, spec_ncp = 1;
+  double2 *d_tw = nullptr, *d_fx = nullptr, *d_fy = nullptr, *d_gp = nullptr, *d_d0p = nullptr;
   // edge-row sums on the tensor cores (P <= 65)
   // host path streaming A in row bands (batch 1, tensor-core path): the
   // copy stream bumps *d_band_flag after each band; k_bulk_dmma waits on it,
@@ -169,8 +177,9 @@ struct covgpu_plan {
   int launches = 0;
   // optional per-kernel timing of the last execute (events on its stream)
   bool timing = false;
-  cudaEvent_t ev[8] = {};
-  const char* ev_name[8] = {};  // kernel timed by the interval ending at ev[i]
+  static constexpr int kMaxEv = 12;
+  cudaEvent_t ev[kMaxEv] = {};
+  const char* ev_name[kMaxEv] = {};  // kernel timed by the interval ending at ev[i]
   int nev = 0;
   // side stream for the edge-row / corner kernels (overlap with the bulk)
   cudaStream_t side_stream = nullptr;
@@ -274,6 +283,11 @@ void plan_free(covgpu_plan* pl) {
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
   cudaFree(pl->d_ecm_tickets);
+  cudaFree(pl->d_tw);
+  cudaFree(pl->d_fx);
+  cudaFree(pl->d_fy);
+  cudaFree(pl->d_gp);
+  cudaFree(pl->d_d0p);
 }
 
 int pick_lags(int span) {
@@ -422,6 +436,12 @@ cudaError_t set_attrs() {
     if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       e = r;
+    for (const void* fn : {(const void*)k_spec_dr0<double>, (const void*)k_spec_dr0<float>,
+                           (const void*)k_spec_fft<double>, (const void*)k_spec_fft<float>,
+                           (const void*)k_spec_dft})
+      if ((r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)) !=
+          cudaSuccess)
+        e = r;
     return e;
   }();
   return once;
@@ -559,6 +579,31 @@ bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   return true;
 }
 
+// spectral core sums (spectral.cuh) for band ks_part of ks_nparts: writes
+// the one CC partial per class (npart = 1)
+template <typename T>
+void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st,
+                     const std::function<void(const char*)>& mark) {
+  const Problem& pr = pl->pr;
+  const long long B = pl->batch;
+  const int L = pl->spec_L, part = pl->ks_part, nparts = pl->ks_nparts;
+  const int rows_lo = pr.P - 1, nrows = pr.N - 2 * pr.P + 2;
+  const int ra = rows_lo + (int)((long long)nrows * part / nparts);
+  const int rz = rows_lo + (int)((long long)nrows * (part + 1) / nparts) - 1;
+  k_spec_dr0<T><<<(unsigned)(B * pl->spec_nrb * pl->spec_ncp), SPEC_D0_W * 32, SPEC_D0_SMEM, st>>>(
+      A, pr, ra, rz, pl->spec_nrb, pl->spec_ncp, pl->d_d0p);
+  mark("spec_dr0");
+  k_spec_fft<T><<<(unsigned)(B * pr.N * 2), SPEC_FFT_THREADS, sizeof(double2) * L, st>>>(
+      A, pr, pl->spec_logL, pl->d_tw, pl->d_fx, pl->d_fy);
+  mark("spec_fft");
+  k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
+      pl->d_fx, pl->d_fy, pr, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts, pl->d_gp);
+  mark("spec_corr");
+  k_spec_dft<<<(unsigned)(B * (2 * pr.P - 1)), 256, sizeof(double2) * L, st>>>(
+      pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp, pl->d_tw, pr, L, pl->spec_nseg, pl->nclasses,
+      pl->d_cls_slot, pl->d_ccpart);
+}
+
 // edge-column sums on the tensor cores; false when the tensor map fails
 bool launch_edge_cols_dmma(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   const Problem& pr = pl->pr;
@@ -688,7 +733,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   CUDA_TRY(set_attrs());
   pl->nev = 0;
   auto mark = [&](const char* name) {
-    if (pl->timing && pl->nev < 8) {
+    if (pl->timing && pl->nev < covgpu_plan::kMaxEv) {
       pl->ev_name[pl->nev] = name;
       cudaEventRecord(pl->ev[pl->nev++], st);
     }
@@ -708,8 +753,14 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
   // bulk over every column block (which also yields the edge-column sums)
   bool mma = false;
+  if (pl->use_spec) {
+    if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
+    launch_spectral<T>(pl, A, st, mark);
+    launches += 3;
+    mma = true;
+  }
   if constexpr (sizeof(T) == 8) {
-    if (pl->use_mma) {
+    if (pl->use_mma && !mma) {
       const double2* Ad = (const double2*)A;
       switch (pl->mma_kind) {
         case 1: mma = launch_dmma3<2, 4, 2, 2, 2>(pl, Ad, st); break;
@@ -727,9 +778,9 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
     launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
   }
-  const int npart = mma ? pl->mma_g : pl->ncb * pl->nrs;
+  const int npart = pl->use_spec ? 1 : mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
-  mark(mma ? "bulk_dmma" : "bulk");
+  mark(pl->use_spec ? "spec_dft" : mma ? "bulk_dmma" : "bulk");
   if (mma) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
     if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es))) {
       if (pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: edge-column kernel unavailable");
@@ -1086,6 +1137,34 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       }
     }
   }
+  {
+    // spectral core sums: replaces the tensor-core core-sum kernel where its
+    // FFT length fits SMEM and the dr = 0 space-domain kernel covers Q
+    bool spec = pl->use_mma && q <= SPEC_D0_E * SPEC_D0_W;
+    int logL = 0;
+    while ((1LL << logL) < m) ++logL;
+    spec = spec && logL >= 5 && logL <= 13;
+    if (const char* ns = getenv("COVGPU_NO_SPECTRAL")) spec = spec && atoi(ns) == 0;
+    if (spec) {
+      pl->use_spec = true;
+      pl->spec_logL = logL;
+      pl->spec_L = 1 << logL;
+      pl->spec_ngrp = (2 * p - 1 + SPEC_E - 1) / SPEC_E;
+      pl->spec_nfb = (pl->spec_L + SPEC_CW * 32 - 1) / (SPEC_CW * 32);
+      // row segments: ~6 CTAs of 4 warps per SM, >= 4 windows of rows each
+      const long long per = batch * (long long)pl->spec_ngrp * pl->spec_nfb;
+      const long long rows = n - 2LL * p + 2 + SPEC_E;
+      long long seg = std::max(1LL, (148LL * 6 + per - 1) / per);
+      seg = std::min(seg, std::max(1LL, rows / (4LL * SPEC_E)));
+      pl->spec_nseg = (int)std::min(seg, 64LL);
+      const long long d0rows = n - 2LL * p + 2;
+      pl->spec_nrb = (int)((d0rows + SPEC_D0_RB - 1) / SPEC_D0_RB);
+      const long long nch = (m - q + 1 + SPEC_D0_CW - 1) / SPEC_D0_CW;
+      const long long d0per = batch * (long long)pl->spec_nrb;
+      long long cpn = std::max(1LL, (148LL * 4 + d0per - 1) / d0per);
+      pl->spec_ncp = (int)std::max(1LL, std::min(cpn, nch));
+    }
+  }
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
   pl->edge_tma = pl->S >= 16 && pl->use_tma;
@@ -1194,6 +1273,26 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     if (cudaMemset(pl->d_ecm_tickets, 0, sizeof(unsigned) * (size_t)pl->ecm_items) != cudaSuccess) {
       plan_free(pl.get());
       return fail(COVGPU_ECUDA, "ticket reset");
+    }
+  }
+  if (pl->use_spec) {
+    const size_t L = (size_t)pl->spec_L;
+    std::vector<double2> tw(L);
+    const long double pi2 = 6.283185307179586476925286766559L;
+    for (size_t j = 0; j < L; ++j) {
+      const long double a = -pi2 * (long double)j / (long double)L;
+      tw[j] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    if ((rc = dalloc(&pl->d_tw, L, &ws)) || (rc = dalloc(&pl->d_fx, (size_t)batch * n * L, &ws)) ||
+        (rc = dalloc(&pl->d_fy, (size_t)batch * n * L, &ws)) ||
+        (rc = dalloc(&pl->d_gp, (size_t)batch * pl->spec_nseg * (2 * p - 1) * L, &ws)) ||
+        (rc = dalloc(&pl->d_d0p, (size_t)batch * pl->spec_nrb * pl->spec_ncp * q, &ws))) {
+      plan_free(pl.get());
+      return rc;
+    }
+    if (cudaMemcpy(pl->d_tw, tw.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) != cudaSuccess) {
+      plan_free(pl.get());
+      return fail(COVGPU_ECUDA, "twiddle upload");
     }
   }
   if (pl->clean) {

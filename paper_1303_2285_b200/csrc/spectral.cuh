@@ -1,0 +1,364 @@
+// K1 in the frequency domain — the core sums CC(dr, dc) of every class at
+// once through FFTs along A's rows (FP64 arithmetic; complex128 or complex64
+// inputs).
+//
+// With x_r = row r of A restricted to the core first-element columns
+// c <= M-Q and y_r = row r restricted to the core second-element columns
+// c' >= Q-1 (the two position-only core-column masks of DESIGN.md §3),
+//     CC(dr, dc) = sum_{r2 in rows(dr)} sum_c x_{r2-dr}[c] conj(y_{r2}[c+dc]),
+// rows(dr) = [P-1, N-P+dr] for dr >= 0 and [P-1+dr, N-P] for dr < 0 (the core
+// rows).  For an FFT length L >= M (power of two) no circular wrap occurs
+// (c + dc <= M-1 < L), so with X_r = FFT_L(x_r), Y_r = FFT_L(y_r),
+// w = exp(-2 pi i / L):
+//     sum_c x_a[c] conj(y_b[c+dc]) = (1/L) sum_f X_a[f] conj(Y_b[f]) w^(f dc)
+// and therefore
+//     G(dr, f)   = sum_{r2 in rows(dr)} X_{r2-dr}[f] conj(Y_{r2}[f])     (k_spec_corr)
+//     CC(dr, dc) = (1/L) sum_f G(dr, f) w^(f dc)                         (k_spec_dft)
+// — the row-lag correlation is done per frequency, the column lags by one
+// short DFT per row lag.  Cost: 2N row FFTs (k_spec_fft) + (2P-1) L N complex
+// MACs + (2P-1) Q L for the DFT: cfg5 5.3e8 MACs against 3.1e10 core products
+// for the direct sums (mma.cuh).
+//
+// Accuracy: the FFT rounds at ~eps log2(L) of the row energy.  For dr != 0
+// the sum over r2 is incoherent and CC keeps ~1e-14 relative accuracy on
+// white noise; for dr = 0 the terms X_r conj(Y_r) are coherent (|X_r|^2 for
+// the shared columns), so the dr = 0 classes — Q of them, 1/(2P-1) of the
+// core products — are summed directly in the space domain (k_spec_dr0).
+// Every sum runs in a fixed order: results are bitwise reproducible.
+#pragma once
+
+#include "common.cuh"
+
+namespace covgpu {
+
+constexpr int SPEC_FFT_THREADS = 256;
+constexpr int SPEC_E = 16;        // row lags per k_spec_corr thread
+constexpr int SPEC_CW = 4;        // warps (32-frequency columns) per k_spec_corr CTA
+constexpr int SPEC_D0_E = 16;     // column lags per k_spec_dr0 warp
+constexpr int SPEC_D0_W = 4;      // warps per k_spec_dr0 CTA (lag groups)
+constexpr int SPEC_D0_RB = 32;    // rows per k_spec_dr0 CTA (one per lane)
+constexpr int SPEC_D0_CW = 32;    // columns per k_spec_dr0 chunk
+constexpr int SPEC_D0_PITCH = SPEC_D0_CW + SPEC_D0_E * SPEC_D0_W;  // 96 -> +1 below (odd)
+constexpr int SPEC_D0_TP = SPEC_D0_PITCH + 1;  // odd pitch in 16-byte units: conflict-free LDS.128
+constexpr size_t SPEC_D0_SMEM = 2 * sizeof(double2) * SPEC_D0_RB * SPEC_D0_TP;
+
+template <typename C2>
+__device__ __forceinline__ double2 widen2(C2 v) {
+  return make_double2((double)v.x, (double)v.y);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// Row FFTs: CTA = (snapshot b, row r, which): which 0 -> X_r (columns
+// c <= M-Q), 1 -> Y_r (columns c >= Q-1), zero-padded to L = 2^logL.
+// Iterative radix-2 DIT in shared memory after a bit-reversed load; twiddles
+// tw[j] = exp(-2 pi i j / L) from the host (long double, correctly rounded).
+template <typename T>
+__global__ void __launch_bounds__(SPEC_FFT_THREADS)
+    k_spec_fft(const typename CT<T>::c* __restrict__ A, Problem pr, int logL, const double2* __restrict__ tw,
+               double2* __restrict__ FX, double2* __restrict__ FY) {
+  extern __shared__ double2 sbuf[];
+  const int L = 1 << logL;
+  long long t = blockIdx.x;
+  const int which = (int)(t & 1);
+  t >>= 1;
+  const int N = pr.N, M = pr.M, Q = pr.Q;
+  const int r = (int)(t % N);
+  const long long b = t / N;
+  const typename CT<T>::c* row = A + (b * N + r) * (long long)M;
+  const int clo = which ? Q - 1 : 0, chi = which ? M - 1 : M - Q;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (i >= clo && i <= chi) v = widen2(row[i]);
+    sbuf[__brev((unsigned)i) >> (32 - logL)] = v;
+  }
+  __syncthreads();
+  for (int s = 1; s <= logL; ++s) {
+    const int half = 1 << (s - 1);
+    const int tstride = L >> s;
+    for (int k = threadIdx.x; k < (L >> 1); k += blockDim.x) {
+      const int j = k & (half - 1);
+      const int i0 = ((k >> (s - 1)) << s) + j;
+      const int i1 = i0 + half;
+      const double2 w = tw[j * tstride];
+      const double2 u = sbuf[i0];
+      const double2 v = cmul(sbuf[i1], w);
+      sbuf[i0] = make_double2(u.x + v.x, u.y + v.y);
+      sbuf[i1] = make_double2(u.x - v.x, u.y - v.y);
+    }
+    __syncthreads();
+  }
+  double2* out = (which ? FY : FX) + (b * N + r) * (long long)L;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) out[i] = sbuf[i];
+}
+
+__device__ __forceinline__ int spec_lo(int dr, int P) { return P - 1 + min(dr, 0); }
+__device__ __forceinline__ int spec_hi(int dr, int P, int N) { return N - P + max(dr, 0); }
+
+// acc[e] += X_{r2 - dr0 - e} conj(y) for the E lags: the X rows sit in a
+// rotating register window (slot (tt + E - 1 - e) % E holds row r2 - dr0 - e
+// at step tt).  Grouped by the y component so consecutive FMAs share it.
+template <int E>
+__device__ __forceinline__ void spec_mac(int tt, double2 y, const double* wr, const double* wi, double* ar,
+                                         double* ai) {
+  const double ny = -y.y;
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = fma(wr[(tt + E - 1 - e) % E], y.x, ar[e]);
+#pragma unroll
+  for (int e = 0; e < E; ++e) ai[e] = fma(wi[(tt + E - 1 - e) % E], y.x, ai[e]);
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = fma(wi[(tt + E - 1 - e) % E], y.y, ar[e]);
+#pragma unroll
+  for (int e = 0; e < E; ++e) ai[e] = fma(wr[(tt + E - 1 - e) % E], ny, ai[e]);
+}
+
+// Per-frequency row-lag correlation G(dr, f), partial over row segments.
+// CTA = (snapshot b, row segment, 128-frequency block, lag group of E row
+// lags; the lag group varies fastest so the CTAs reading the same X / Y rows
+// run together and share them in L2); lane = frequency.  The row range of
+// the group (union of its lags' core rows) is cut into nparts bands (multi-GPU
+// row bands) x nseg segments; rows where every lag is active run without
+// predicates.
+template <int E>
+__global__ void __launch_bounds__(SPEC_CW * 32, 2)
+    k_spec_corr(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, int L, int nfb,
+                int ngrp, int nseg, int part, int nparts, double2* __restrict__ Gp) {
+  long long t = blockIdx.x;
+  const int g = (int)(t % ngrp);
+  t /= ngrp;
+  const int fb = (int)(t % nfb);
+  t /= nfb;
+  const int seg = (int)(t % nseg);
+  const long long b = t / nseg;
+  const int f = (fb * SPEC_CW + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
+  if (f >= L) return;
+  const int P = pr.P, N = pr.N;
+  const int nlag = 2 * P - 1;
+  const int dr0 = -(P - 1) + g * E;
+  const int drl = min(dr0 + E - 1, P - 1);
+  const int rlo = spec_lo(dr0, P), rhi = spec_hi(drl, P, N);
+  const int nr = rhi - rlo + 1;
+  const int pieces = nparts * nseg, idx = part * nseg + seg;
+  const int a = rlo + (int)((long long)nr * idx / pieces);
+  const int z = rlo + (int)((long long)nr * (idx + 1) / pieces) - 1;  // last row (inclusive)
+  const int blo = spec_lo(drl, P), bhi = min(spec_hi(dr0, P, N), z);  // every lag active
+  const double2* fx = FX + b * N * (long long)L + f;
+  const double2* fy = FY + b * N * (long long)L + f;
+
+  double ar[E], ai[E], wr[E], wi[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = ai[e] = wr[e] = wi[e] = 0.0;
+  // window: slot k holds X row (a - dr0) - (E - 1) + k for k < E - 1
+  {
+    const int t0 = a - dr0;
+#pragma unroll
+    for (int k = 0; k < E - 1; ++k) {
+      const int row = t0 - (E - 1) + k;
+      if (row >= 0 && row < N) {
+        const double2 v = fx[(long long)row * L];
+        wr[k] = v.x;
+        wi[k] = v.y;
+      }
+    }
+  }
+  for (int rb = a; rb <= z; rb += E) {
+    const int t0 = rb - dr0;
+    if (rb >= blo && rb + E - 1 <= bhi) {
+      const double2* px = fx + (long long)t0 * L;
+      const double2* py = fy + (long long)rb * L;
+#pragma unroll
+      for (int tt = 0; tt < E; ++tt) {
+        const double2 xn = px[(long long)tt * L];
+        const double2 y = py[(long long)tt * L];
+        wr[(tt + E - 1) % E] = xn.x;
+        wi[(tt + E - 1) % E] = xn.y;
+        spec_mac<E>(tt, y, wr, wi, ar, ai);
+      }
+    } else {
+#pragma unroll
+      for (int tt = 0; tt < E; ++tt) {
+        const int r2 = rb + tt, row = t0 + tt;
+        double2 xn = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+        if (row >= 0 && row < N) xn = fx[(long long)row * L];
+        if (r2 <= z) y = fy[(long long)r2 * L];
+        wr[(tt + E - 1) % E] = xn.x;
+        wi[(tt + E - 1) % E] = xn.y;
+        const double ny = -y.y;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int dr = dr0 + e;
+          const bool on = r2 >= spec_lo(dr, P) && r2 <= spec_hi(dr, P, N);
+          const double yx = on ? y.x : 0.0, yy = on ? y.y : 0.0, nyy = on ? ny : 0.0;
+          const int s = (tt + E - 1 - e) % E;
+          ar[e] = fma(wr[s], yx, ar[e]);
+          ai[e] = fma(wi[s], yx, ai[e]);
+          ar[e] = fma(wi[s], yy, ar[e]);
+          ai[e] = fma(wr[s], nyy, ai[e]);
+        }
+      }
+    }
+  }
+  double2* out = Gp + (b * nseg + seg) * (long long)nlag * L + f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int dr = dr0 + e;
+    if (dr <= P - 1) out[(long long)(dr + P - 1) * L] = make_double2(ar[e], ai[e]);
+  }
+}
+
+// dr = 0 core sums in the space domain (Q <= 64):
+//     CC(0, dc) = sum_{r in [P-1, N-P]} sum_{c <= M-Q, c+dc >= Q-1} A[r,c] conj(A[r,c+dc]).
+// CTA = (snapshot b, block of 32 rows, column part cp): lane = row, warp w =
+// column lags [16w, 16w+16); chunks of 32 first-element columns plus the
+// 63-column lag halo are staged in SMEM by cp.async (double buffer, odd row
+// pitch: the 32 lanes' LDS.128 hit distinct banks), and each thread walks its
+// row with the 16 second elements in a rotating register window (2 LDS per
+// 16 complex MACs).  Partials per (row block, column part) are summed in a
+// fixed order by k_spec_dft.
+template <typename T>
+__global__ void __launch_bounds__(SPEC_D0_W * 32)
+    k_spec_dr0(const typename CT<T>::c* __restrict__ A, Problem pr, int row_a, int row_z, int nrb, int ncp,
+               double2* __restrict__ D0p) {
+  using C2 = typename CT<T>::c;
+  constexpr int E = SPEC_D0_E, TP = SPEC_D0_TP, CW = SPEC_D0_CW, TW = SPEC_D0_PITCH;
+  extern __shared__ __align__(16) unsigned char d0raw[];
+  C2* tile = reinterpret_cast<C2*>(d0raw);
+  long long t = blockIdx.x;
+  const int cp = (int)(t % ncp);
+  t /= ncp;
+  const int rb = (int)(t % nrb);
+  const long long b = t / nrb;
+  const int N = pr.N, M = pr.M, Q = pr.Q;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = row_a + rb * SPEC_D0_RB;
+  const int xcols = M - Q + 1;
+  const int nch_all = (xcols + CW - 1) / CW;
+  const int ch_a = (int)((long long)nch_all * cp / ncp), ch_z = (int)((long long)nch_all * (cp + 1) / ncp);
+  const int dc0 = w * E;  // first column lag of this warp
+  const C2* Ab = A + b * N * (long long)M;
+  auto load = [&](int ch, int buf) {
+    const int cc = ch * CW;  // tile column 0 = A column cc
+    C2* dst = tile + buf * SPEC_D0_RB * TP;
+    for (int i = threadIdx.x; i < SPEC_D0_RB * TW; i += blockDim.x) {
+      const int rr = i / TW, cq = i % TW;
+      const int r = r0 + rr, c = cc + cq;
+      const bool ok = r <= row_z && c < M;
+      cp_async_elem<sizeof(C2)>(dst + rr * TP + cq, ok ? Ab + (long long)r * M + c : Ab, ok);
+    }
+    cp_async_commit();
+  };
+  double ar[E], ai[E], yr[E], yi[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = ai[e] = yr[e] = yi[e] = 0.0;
+  const bool live = r0 <= row_z && ch_a < ch_z;
+  const bool active = dc0 < Q;
+  if (live) load(ch_a, 0);
+  for (int ch = ch_a; live && ch < ch_z; ++ch) {
+    const int buf = (ch - ch_a) & 1;
+    if (ch + 1 < ch_z) {
+      load(ch + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (active) {
+      const C2* row = tile + buf * SPEC_D0_RB * TP + lane * TP;
+      const int c0 = ch * CW;
+      const int ncols = min(CW, xcols - c0);
+      // x column c0 + j at tile column j; y column c0 + j + dc0 + e at tile column j + dc0 + e
+#pragma unroll
+      for (int e = 0; e < E - 1; ++e) {
+        const double2 v = c0 + dc0 + e >= Q - 1 ? widen2(row[dc0 + e]) : make_double2(0.0, 0.0);
+        yr[e] = v.x;
+        yi[e] = v.y;
+      }
+      if (ncols == CW && c0 >= Q - 1) {
+#pragma unroll
+        for (int t0 = 0; t0 < CW; t0 += E) {
+#pragma unroll
+          for (int tt = 0; tt < E; ++tt) {
+            const double2 yn = widen2(row[t0 + tt + dc0 + E - 1]);
+            const double2 x = widen2(row[t0 + tt]);
+            yr[(tt + E - 1) % E] = yn.x;
+            yi[(tt + E - 1) % E] = yn.y;
+            cmac_all<double, E>(tt, x, yr, yi, ar, ai);
+          }
+        }
+      } else {
+        for (int t0 = 0; t0 < CW; t0 += E) {
+#pragma unroll
+          for (int tt = 0; tt < E; ++tt) {
+            const int j = t0 + tt;
+            const int col = c0 + j + dc0 + E - 1;
+            const double2 yn = col >= Q - 1 ? widen2(row[j + dc0 + E - 1]) : make_double2(0.0, 0.0);
+            const double2 x = j < ncols ? widen2(row[j]) : make_double2(0.0, 0.0);
+            yr[(tt + E - 1) % E] = yn.x;
+            yi[(tt + E - 1) % E] = yn.y;
+            cmac_all<double, E>(tt, x, yr, yi, ar, ai);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!active) return;
+  // rows past row_z and lags past Q-1 hold exact zeros; fixed-order lane sums
+  double2* out = D0p + (b * nrb + rb) * (long long)ncp * Q + (long long)cp * Q;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const double2 s = warp_sum(make_double2(ar[e], ai[e]));
+    if (lane == 0 && dc0 + e < Q) out[dc0 + e] = s;
+  }
+}
+
+// CC(dr, dc) = (1/L) sum_f G(dr, f) w^(f dc) for dr != 0 (G summed over the
+// row segments in order), and the ordered sum of the space-domain partials
+// for dr = 0.  CTA = (snapshot b, row lag dr); warp = column lags dc, lanes =
+// frequencies, fixed-order butterfly.  Writes the classes' CC slot (one
+// partial: npart = 1 for the finalize).
+__global__ void __launch_bounds__(256)
+    k_spec_dft(const double2* __restrict__ Gp, const double2* __restrict__ D0p, int nd0,
+               const double2* __restrict__ tw, Problem pr, int L, int nseg, int nclasses,
+               const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+  extern __shared__ double2 sg[];
+  const int P = pr.P, Q = pr.Q;
+  const int nlag = 2 * P - 1;
+  const int li = (int)(blockIdx.x % nlag);
+  const long long b = blockIdx.x / nlag;
+  const int dr = li - (P - 1);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (dr == 0) {
+    for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
+      double2 s = make_double2(0.0, 0.0);
+      const double2* p = D0p + b * (long long)nd0 * Q + dc;
+      for (int k = 0; k < nd0; ++k) s = cadd(s, p[(long long)k * Q]);
+      const int cid = cls_slot[class_index(0, dc, P, Q)];
+      if (cid >= 0) ccpart[b * nclasses + cid] = s;
+    }
+    return;
+  }
+  for (int f = threadIdx.x; f < L; f += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int sgm = 0; sgm < nseg; ++sgm) s = cadd(s, Gp[((b * nseg + sgm) * nlag + li) * (long long)L + f]);
+    sg[f] = s;
+  }
+  __syncthreads();
+  const double inv = 1.0 / (double)L;
+  for (int dc = (dr < 0 ? 1 : 0) + w; dc < Q; dc += nw) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int f = lane; f < L; f += 32) {
+      const double2 v = cmul(sg[f], tw[(int)(((long long)f * dc) & (L - 1))]);
+      acc = cadd(acc, v);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const int cid = cls_slot[class_index(dr, dc, P, Q)];
+      if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(acc.x * inv, acc.y * inv);
+    }
+  }
+}
+
+}  // namespace covgpu

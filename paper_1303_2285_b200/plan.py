@@ -113,8 +113,8 @@ class Plan:
         _native.check(self.lib.covgpu_plan_set_timing(self.handle, int(enable)), "set_timing")
 
     def kernel_times(self) -> list[float]:
-        buf = (ctypes.c_float * 8)()
-        n = self.lib.covgpu_plan_kernel_times(self.handle, buf, 8)
+        buf = (ctypes.c_float * 12)()
+        n = self.lib.covgpu_plan_kernel_times(self.handle, buf, 12)
         if n < 0:
             _native.check(n, "kernel_times")
         return [float(buf[i]) for i in range(n)]

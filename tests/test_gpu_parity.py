@@ -501,9 +501,11 @@ def test_pipelined_host_path_bitwise(cuda):
     (200, 256, 16, 24, 3),   # smallest gated window, batch of 3
     (515, 515, 32, 32, 2),   # N, M not multiples of the 16-row / 32-column chunks
 ])
-def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, monkeypatch):
-    """complex128 core sums on the FP64 tensor cores (k_bulk_dmma) against the
-    Gram cross-check and against the CUDA-core bulk kernel of the same shape."""
+@pytest.mark.parametrize("spectral", [False, True])
+def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, spectral, monkeypatch):
+    """complex128 core sums on the FP64 tensor cores (k_bulk_dmma) or in the
+    frequency domain (spectral.cuh, Q <= 64) against the Gram cross-check and
+    against the CUDA-core bulk kernel of the same shape."""
     from oracle.gpu_naive import covariance_gram
     from paper_1303_2285_b200.plan import Plan
 
@@ -511,12 +513,17 @@ def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, monkey
     a = torch.as_tensor(rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m)),
                         device=cuda)
     win = WindowSpec(p, q)
+    if not spectral:
+        monkeypatch.setenv("COVGPU_NO_SPECTRAL", "1")
     plan = Plan(n, m, win, batch=batch, dtype=torch.complex128, device=cuda)
+    monkeypatch.delenv("COVGPU_NO_SPECTRAL", raising=False)
     plan.set_timing(True)
     got = plan.alloc_output()
     plan.execute(a, got)
     got = got.reshape(batch, p * q, p * q)
-    assert "bulk_dmma" in plan.kernel_names()
+    names = plan.kernel_names()
+    assert ("spec_dft" in names) == (spectral and q <= 64), names
+    assert ("bulk_dmma" in names) == (not spectral or q > 64), names
     plan.close()
     monkeypatch.setenv("COVGPU_NO_MMA", "1")
     plan2 = Plan(n, m, win, batch=batch, dtype=torch.complex128, device=cuda)
