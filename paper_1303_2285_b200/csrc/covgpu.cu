@@ -116,6 +116,11 @@ struct covgpu_plan {
   int spec_logL = 0, spec_L = 0, spec_nseg = 1, spec_nfb = 1, spec_ngrp = 1;
   int spec_nrb = 0, spec_ncp = 1;
   double2 *d_tw = nullptr, *d_fx = nullptr, *d_fy = nullptr, *d_gp = nullptr, *d_d0p = nullptr;
+  // spectral edge sums: column FFTs of length Lr = 2^spec_logLr (CCol), the
+  // unmasked strip-row spectra (RC')
+  bool spec_edges = false;
+  int spec_logLr = 0;
+  double2 *d_twr = nullptr, *d_fc = nullptr, *d_fy0 = nullptr;
   // edge-row sums on the tensor cores (P <= 65)
   // host path streaming A in row bands (batch 1, tensor-core path): the
   // copy stream bumps *d_band_flag after each band; k_bulk_dmma waits on it,
@@ -288,6 +293,9 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_fy);
   cudaFree(pl->d_gp);
   cudaFree(pl->d_d0p);
+  cudaFree(pl->d_twr);
+  cudaFree(pl->d_fc);
+  cudaFree(pl->d_fy0);
 }
 
 int pick_lags(int span) {
@@ -437,8 +445,7 @@ cudaError_t set_attrs() {
                                   200 * 1024)) != cudaSuccess)
       e = r;
     for (const void* fn : {(const void*)k_spec_dr0<double>, (const void*)k_spec_dr0<float>,
-                           (const void*)k_spec_fft<double>, (const void*)k_spec_fft<float>,
-                           (const void*)k_spec_dft})
+                          })
       if ((r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)) !=
           cudaSuccess)
         e = r;
@@ -579,8 +586,55 @@ bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   return true;
 }
 
+// Spectral kernels are instantiated for FFT lengths 2^6 .. 2^12; SPEC_LOGL
+// dispatches a launch on the runtime log2 length (SMEM attribute set once per
+// instantiation: up to (L + L/8) complex values).
+template <typename K>
+void spec_attr(K* fn, int logL) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    done = true;
+  }
+  (void)logL;
+}
+#define SPEC_LOGL(lg, KERNEL, GRID, ...)                                                        \
+  do {                                                                                          \
+    switch (lg) {                                                                               \
+      case 6: SPEC_LAUNCH(6, KERNEL, GRID, __VA_ARGS__); break;                                 \
+      case 7: SPEC_LAUNCH(7, KERNEL, GRID, __VA_ARGS__); break;                                 \
+      case 8: SPEC_LAUNCH(8, KERNEL, GRID, __VA_ARGS__); break;                                 \
+      case 9: SPEC_LAUNCH(9, KERNEL, GRID, __VA_ARGS__); break;                                 \
+      case 10: SPEC_LAUNCH(10, KERNEL, GRID, __VA_ARGS__); break;                               \
+      case 11: SPEC_LAUNCH(11, KERNEL, GRID, __VA_ARGS__); break;                               \
+      default: SPEC_LAUNCH(12, KERNEL, GRID, __VA_ARGS__);                                      \
+    }                                                                                           \
+  } while (0)
+#define SPEC_LAUNCH(LG, KERNEL, GRID, ...)                                                     \
+  do {                                                                                          \
+    auto fn_ = KERNEL<LG>();                                                                    \
+    spec_attr(fn_, LG);                                                                         \
+    fn_<<<(unsigned)(GRID), spec_threads<LG>(), sizeof(double2) * ((1 << LG) + (1 << LG) / 8), st>>>( \
+        __VA_ARGS__);                                                                           \
+  } while (0)
+
+template <typename T>
+struct SpecK {
+  template <int LG>
+  static auto fft() { return &k_spec_fft<T, LG>; }
+  template <int LG>
+  static auto colfft() { return &k_spec_colfft<T, LG>; }
+  template <int LG>
+  static auto dft() { return &k_spec_dft<LG>; }
+  template <int LG>
+  static auto ccol() { return &k_spec_ccol<LG>; }
+  template <int LG>
+  static auto rc() { return &k_spec_rc<LG>; }
+};
+
 // spectral core sums (spectral.cuh) for band ks_part of ks_nparts: writes
-// the one CC partial per class (npart = 1)
+// the one CC partial per class (npart = 1); with spec_edges also the
+// edge-column sums CCol and edge-row sums RC' (one segment)
 template <typename T>
 void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st,
                      const std::function<void(const char*)>& mark) {
@@ -590,18 +644,28 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   const int rows_lo = pr.P - 1, nrows = pr.N - 2 * pr.P + 2;
   const int ra = rows_lo + (int)((long long)nrows * part / nparts);
   const int rz = rows_lo + (int)((long long)nrows * (part + 1) / nparts) - 1;
+  const int S = pr.P - 1, S1 = pr.Q - 1;
   k_spec_dr0<T><<<(unsigned)(B * pl->spec_nrb * pl->spec_ncp), SPEC_D0_W * 32, SPEC_D0_SMEM, st>>>(
       A, pr, ra, rz, pl->spec_nrb, pl->spec_ncp, pl->d_d0p);
   mark("spec_dr0");
-  k_spec_fft<T><<<(unsigned)(B * pr.N * 2), SPEC_FFT_THREADS, sizeof(double2) * L, st>>>(
-      A, pr, pl->spec_logL, pl->d_tw, pl->d_fx, pl->d_fy);
+  SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->d_tw, pl->d_fx, pl->d_fy);
+  if (pl->spec_edges)
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->d_tw, pl->d_fx, pl->d_fy0);
   mark("spec_fft");
   k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
       pl->d_fx, pl->d_fy, pr, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts, pl->d_gp);
   mark("spec_corr");
-  k_spec_dft<<<(unsigned)(B * (2 * pr.P - 1)), 256, sizeof(double2) * L, st>>>(
-      pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp, pl->d_tw, pr, L, pl->spec_nseg, pl->nclasses,
-      pl->d_cls_slot, pl->d_ccpart);
+  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp,
+            pl->d_tw, pr, pl->spec_nseg, pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
+  if (pl->spec_edges) {
+    mark("spec_dft");
+    SPEC_LOGL(pl->spec_logLr, SpecK<T>::template colfft, B * 2 * 4 * S1, A, pr, pl->d_twr, pl->d_fc);
+    SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * 2 * (long long)S1 * S1, pl->d_fc, pr, pl->d_twr,
+              pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+    mark("spec_ccol");
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr, pl->d_tw,
+              pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+  }
 }
 
 // edge-column sums on the tensor cores; false when the tensor map fails
@@ -756,7 +820,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->use_spec) {
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
     launch_spectral<T>(pl, A, st, mark);
-    launches += 3;
+    launches += pl->spec_edges ? 7 : 3;
     mma = true;
   }
   if constexpr (sizeof(T) == 8) {
@@ -780,8 +844,8 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   }
   const int npart = pl->use_spec ? 1 : mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
-  mark(pl->use_spec ? "spec_dft" : mma ? "bulk_dmma" : "bulk");
-  if (mma) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
+  mark(pl->use_spec ? (pl->spec_edges ? "spec_rc" : "spec_dft") : mma ? "bulk_dmma" : "bulk");
+  if (mma && !pl->spec_edges) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
     if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es))) {
       if (pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: edge-column kernel unavailable");
       launch_bulk_variant<T>(pl, A, es, pl->edge_variant, pl->ncb_l, pl->ncb_r);
@@ -789,7 +853,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     ++launches;
     mark("edge_cols");
   }
-  if (pl->S > 0) {
+  if (pl->S > 0 && !pl->spec_edges) {
     switch (pl->D) {
       case 4: launch_edge<T, 4>(pl, A, es); break;
       case 8: launch_edge<T, 8>(pl, A, es); break;
@@ -1143,7 +1207,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     bool spec = pl->use_mma && q <= SPEC_D0_E * SPEC_D0_W;
     int logL = 0;
     while ((1LL << logL) < m) ++logL;
-    spec = spec && logL >= 5 && logL <= 13;
+    spec = spec && logL >= 6 && logL <= 12;  // instantiated FFT lengths
     if (const char* ns = getenv("COVGPU_NO_SPECTRAL")) spec = spec && atoi(ns) == 0;
     if (spec) {
       pl->use_spec = true;
@@ -1210,6 +1274,18 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         }
       }
       pl->nseg = (int)std::min(seg, 16LL);
+    }
+  }
+  if (pl->use_spec) {
+    // edge sums in the frequency domain too: column FFTs of length >= N
+    int logLr = 0;
+    while ((1LL << logLr) < n) ++logLr;
+    bool se = logLr >= 6 && logLr <= 12 && p >= 2 && q >= 2;
+    if (const char* ne = getenv("COVGPU_NO_SPECTRAL_EDGES")) se = se && atoi(ne) == 0;
+    if (se) {
+      pl->spec_edges = true;
+      pl->spec_logLr = logLr;
+      pl->nseg = 1;  // RC' in one piece
     }
   }
   const int nuc = (int)covgpu_num_classes(p, q);
@@ -1293,6 +1369,24 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     if (cudaMemcpy(pl->d_tw, tw.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) != cudaSuccess) {
       plan_free(pl.get());
       return fail(COVGPU_ECUDA, "twiddle upload");
+    }
+    if (pl->spec_edges) {
+      const size_t Lr = (size_t)1 << pl->spec_logLr;
+      std::vector<double2> twr(Lr);
+      for (size_t j = 0; j < Lr; ++j) {
+        const long double a = -pi2 * (long double)j / (long double)Lr;
+        twr[j] = make_double2((double)cosl(a), (double)sinl(a));
+      }
+      if ((rc = dalloc(&pl->d_twr, Lr, &ws)) ||
+          (rc = dalloc(&pl->d_fc, (size_t)batch * 8 * (q - 1) * Lr, &ws)) ||
+          (rc = dalloc(&pl->d_fy0, (size_t)batch * 2 * (p - 1) * L, &ws))) {
+        plan_free(pl.get());
+        return rc;
+      }
+      if (cudaMemcpy(pl->d_twr, twr.data(), sizeof(double2) * Lr, cudaMemcpyHostToDevice) != cudaSuccess) {
+        plan_free(pl.get());
+        return fail(COVGPU_ECUDA, "twiddle upload");
+      }
     }
   }
   if (pl->clean) {

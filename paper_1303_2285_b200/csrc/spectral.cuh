@@ -31,7 +31,6 @@
 
 namespace covgpu {
 
-constexpr int SPEC_FFT_THREADS = 256;
 constexpr int SPEC_E = 16;        // row lags per k_spec_corr thread
 constexpr int SPEC_CW = 4;        // warps (32-frequency columns) per k_spec_corr CTA
 constexpr int SPEC_D0_E = 16;     // column lags per k_spec_dr0 warp
@@ -51,47 +50,304 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 
-// Row FFTs: CTA = (snapshot b, row r, which): which 0 -> X_r (columns
-// c <= M-Q), 1 -> Y_r (columns c >= Q-1), zero-padded to L = 2^logL.
-// Iterative radix-2 DIT in shared memory after a bit-reversed load; twiddles
-// tw[j] = exp(-2 pi i j / L) from the host (long double, correctly rounded).
-template <typename T>
-__global__ void __launch_bounds__(SPEC_FFT_THREADS)
-    k_spec_fft(const typename CT<T>::c* __restrict__ A, Problem pr, int logL, const double2* __restrict__ tw,
+// In-register R-point forward DFTs (w = exp(-2 pi i / R)).
+__device__ __forceinline__ double2 cadd2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }  // a * (-i)
+
+template <int R>
+__device__ __forceinline__ void dft_small(double2* u);
+template <>
+__device__ __forceinline__ void dft_small<2>(double2* u) {
+  const double2 a = u[0], b = u[1];
+  u[0] = cadd2(a, b);
+  u[1] = csub2(a, b);
+}
+template <>
+__device__ __forceinline__ void dft_small<4>(double2* u) {
+  const double2 t0 = cadd2(u[0], u[2]), t1 = csub2(u[0], u[2]);
+  const double2 t2 = cadd2(u[1], u[3]), t3 = mul_mi(csub2(u[1], u[3]));
+  u[0] = cadd2(t0, t2);
+  u[2] = csub2(t0, t2);
+  u[1] = cadd2(t1, t3);
+  u[3] = csub2(t1, t3);
+}
+template <>
+__device__ __forceinline__ void dft_small<8>(double2* u) {
+  constexpr double c = 0.70710678118654752440;  // sqrt(1/2)
+  double2 e[4] = {u[0], u[2], u[4], u[6]}, o[4] = {u[1], u[3], u[5], u[7]};
+  dft_small<4>(e);
+  dft_small<4>(o);
+  // o[k] *= w8^k: w8 = (c, -c), w8^2 = -i, w8^3 = (-c, -c)
+  const double2 o1 = make_double2(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x));
+  const double2 o2 = mul_mi(o[2]);
+  const double2 o3 = make_double2(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y));
+  u[0] = cadd2(e[0], o[0]);
+  u[4] = csub2(e[0], o[0]);
+  u[1] = cadd2(e[1], o1);
+  u[5] = csub2(e[1], o1);
+  u[2] = cadd2(e[2], o2);
+  u[6] = csub2(e[2], o2);
+  u[3] = cadd2(e[3], o3);
+  u[7] = csub2(e[3], o3);
+}
+
+// SMEM index with one pad element per 8: the strided Stockham stores hit
+// distinct 16-byte bank groups
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+
+// One radix-R Stockham pass (autosort, no bit reversal): item i of L/R,
+// k = i mod p (p = product of the radices already applied):
+//     u_r = in[i + r L/R] * w_L^(r k L/(pR)),  DFT_R(u),  out[(i - k) R + k + r p] = u_r.
+// blockDim >= L/8, so a thread holds at most 8 values; in place in SMEM with
+// a barrier between the reads and the writes.  The first pass reads its input
+// through `ld(idx)` (global memory, coalesced), the last pass hands the
+// natural-order spectrum to `st(idx, v)`.
+template <int LOGL, int R, int P0, class Load, class Store>
+__device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict__ tw, const Load& ld,
+                                          const Store& st) {
+  constexpr int L = 1 << LOGL, T = L / R, NTHR = L / 8 > 32 ? L / 8 : 32;
+  constexpr int IPT = (T + NTHR - 1) / NTHR;
+  constexpr bool first = P0 == 1, last = P0 * R == L;
+  double2 u[IPT][R];
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
+    const int i = threadIdx.x + it * NTHR;
+    if (i < T) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int idx = i + r * T;
+        if constexpr (first)
+          u[it][r] = ld(idx);
+        else
+          u[it][r] = sb[fpad(idx)];
+      }
+    }
+  }
+  if constexpr (!first) __syncthreads();
+  constexpr int tws = L / (P0 * R);
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
+    const int i = threadIdx.x + it * NTHR;
+    if (i < T) {
+      const int k = i & (P0 - 1);
+      if (k) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) u[it][r] = cmul(u[it][r], tw[r * k * tws]);
+      }
+      dft_small<R>(u[it]);
+      const int j = i * R - k * (R - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int idx = j + r * P0;
+        if constexpr (last)
+          st(idx, u[it][r]);
+        else
+          sb[fpad(idx)] = u[it][r];
+      }
+    }
+  }
+  if constexpr (!last) __syncthreads();
+}
+
+// The whole forward FFT of length 2^LOGL: radix-8 passes, then one radix-4 /
+// radix-2 pass.  tw[j] = exp(-2 pi i j / L) (host-made, long double).
+template <int LOGL, int P0 = 1, class Load, class Store>
+__device__ __forceinline__ void spec_fft_block(double2* sb, const double2* __restrict__ tw, const Load& ld,
+                                               const Store& st) {
+  constexpr int done = P0 == 1 ? 0 : __builtin_ctz(P0);
+  constexpr int rem = LOGL - done;
+  if constexpr (rem > 0) {
+    constexpr int lr = rem >= 3 ? 3 : rem;
+    spec_pass<LOGL, (1 << lr), P0>(sb, tw, ld, st);
+    spec_fft_block<LOGL, (P0 << lr)>(sb, tw, ld, st);
+  }
+}
+
+template <int LOGL>
+constexpr int spec_threads() {
+  return (1 << LOGL) / 8 > 32 ? (1 << LOGL) / 8 : 32;
+}
+
+// Row FFTs.  mode 0: CTA = (snapshot b, row r, which): which 0 -> X_r
+// (columns c <= M-Q), 1 -> Y_r (columns c >= Q-1).  mode 1 (edge rows):
+// CTA = (b, strip row s of 2(P-1)) -> Y0_s, the unmasked row of the top
+// strip [0, P-1) / bottom strip [N-P+1, N).  Zero-padded to L = 2^LOGL.
+template <typename T, int LOGL>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
+    k_spec_fft(const typename CT<T>::c* __restrict__ A, Problem pr, int mode, const double2* __restrict__ tw,
                double2* __restrict__ FX, double2* __restrict__ FY) {
   extern __shared__ double2 sbuf[];
-  const int L = 1 << logL;
+  constexpr int L = 1 << LOGL;
   long long t = blockIdx.x;
-  const int which = (int)(t & 1);
-  t >>= 1;
-  const int N = pr.N, M = pr.M, Q = pr.Q;
-  const int r = (int)(t % N);
-  const long long b = t / N;
-  const typename CT<T>::c* row = A + (b * N + r) * (long long)M;
-  const int clo = which ? Q - 1 : 0, chi = which ? M - 1 : M - Q;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    double2 v = make_double2(0.0, 0.0);
-    if (i >= clo && i <= chi) v = widen2(row[i]);
-    sbuf[__brev((unsigned)i) >> (32 - logL)] = v;
+  const int N = pr.N, M = pr.M, Q = pr.Q, S = pr.P - 1;
+  int r, clo, chi;
+  long long orow;
+  double2* out;
+  if (mode == 0) {
+    const int which = (int)(t & 1);
+    t >>= 1;
+    r = (int)(t % N);
+    const long long b = t / N;
+    clo = which ? Q - 1 : 0;
+    chi = which ? M - 1 : M - Q;
+    orow = b * N + r;
+    out = (which ? FY : FX) + orow * L;
+    orow = b * N + r;
+  } else {
+    const int sr = (int)(t % (2 * S));
+    const long long b = t / (2 * S);
+    r = sr < S ? sr : N - S + (sr - S);
+    clo = 0;
+    chi = M - 1;
+    orow = b * N + r;
+    out = FY + (b * 2 * S + sr) * (long long)L;
   }
-  __syncthreads();
-  for (int s = 1; s <= logL; ++s) {
-    const int half = 1 << (s - 1);
-    const int tstride = L >> s;
-    for (int k = threadIdx.x; k < (L >> 1); k += blockDim.x) {
-      const int j = k & (half - 1);
-      const int i0 = ((k >> (s - 1)) << s) + j;
-      const int i1 = i0 + half;
-      const double2 w = tw[j * tstride];
-      const double2 u = sbuf[i0];
-      const double2 v = cmul(sbuf[i1], w);
-      sbuf[i0] = make_double2(u.x + v.x, u.y + v.y);
-      sbuf[i1] = make_double2(u.x - v.x, u.y - v.y);
-    }
+  const typename CT<T>::c* row = A + orow * (long long)M;
+  spec_fft_block<LOGL>(
+      sbuf, tw, [&](int idx) { return (idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0); },
+      [&](int idx, double2 v) { out[idx] = v; });
+}
+
+// Column FFTs of the edge-column strips (left: columns [0, Q-1), right:
+// [M-Q+1, M)), four row-masked versions each: v0 x+ = rows [0, N-P],
+// v1 y+ = rows [P-1, N-1] (row lags dr >= 0), v2 x- = rows [P-1, N-1],
+// v3 y- = rows [0, N-P] (dr < 0).  CTA = (b, side, version, strip column j);
+// FC[((b*2 + side)*4 + v)*(Q-1) + j][0 .. Lr).
+template <typename T, int LOGL>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
+    k_spec_colfft(const typename CT<T>::c* __restrict__ A, Problem pr, const double2* __restrict__ tw,
+                  double2* __restrict__ FC) {
+  extern __shared__ double2 sbuf[];
+  constexpr int L = 1 << LOGL;
+  const int N = pr.N, M = pr.M, P = pr.P, Q = pr.Q;
+  long long t = blockIdx.x;
+  const int j = (int)(t % (Q - 1));
+  t /= Q - 1;
+  const int v = (int)(t % 4);
+  t /= 4;
+  const int side = (int)(t % 2);
+  const long long b = t / 2;
+  const int col = side ? M - Q + 1 + j : j;
+  const int rlo = (v == 1 || v == 2) ? P - 1 : 0;
+  const int rhi = (v == 1 || v == 2) ? N - 1 : N - P;
+  const typename CT<T>::c* base = A + b * N * (long long)M + col;
+  double2* out = FC + (((b * 2 + side) * 4 + v) * (Q - 1) + j) * (long long)L;
+  spec_fft_block<LOGL>(
+      sbuf, tw,
+      [&](int idx) {
+        return (idx >= rlo && idx <= rhi) ? widen2(base[(long long)idx * M]) : make_double2(0.0, 0.0);
+      },
+      [&](int idx, double2 v2) { out[idx] = v2; });
+}
+
+// Edge-column sums CCol from the column spectra: for strip side, sign and
+// column pair (c1, e = c1 + dc), e <= Q-2,
+//     CCol(dr, dc)[c1] = (1/Lr) sum_f Xc1[f] conj(Ye[f]) w^(f dr),
+// dr in [0, P) from the + versions (index dr), dr in (-P, 0) from the -
+// versions (index Lr + dr).  CTA = (b, side, sign, c1, e); pairs with e < c1
+// (and e == c1 for sign -) exit; in multi-GPU row-band mode pair q belongs
+// to part q mod nparts (the others write zeros: the bands are summed).
+template <int LOGL>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
+    k_spec_ccol(const double2* __restrict__ FC, Problem pr, const double2* __restrict__ tw,
+                const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls, double2* __restrict__ ccol,
+                long long tot_ccol, int part, int nparts) {
+  extern __shared__ double2 sbuf[];
+  constexpr int L = 1 << LOGL;
+  const int P = pr.P, Q = pr.Q, S1 = Q - 1;
+  long long t = blockIdx.x;
+  const int e = (int)(t % S1);
+  t /= S1;
+  const int c1 = (int)(t % S1);
+  t /= S1;
+  const int sign = (int)(t % 2);
+  t /= 2;
+  const int side = (int)(t % 2);
+  const long long b = t / 2;
+  if (e < c1 || (sign == 1 && e == c1)) return;
+  const int dc = e - c1;
+  const bool mine = ((long long)c1 * S1 + e) % nparts == part;
+  const double2* fx = FC + (((b * 2 + side) * 4 + 2 * sign) * S1 + c1) * (long long)L;
+  const double2* fy = FC + (((b * 2 + side) * 4 + 2 * sign + 1) * S1 + e) * (long long)L;
+  if (mine) {
+    spec_fft_block<LOGL>(
+        sbuf, tw,
+        [&](int idx) {
+          const double2 x = fx[idx], y = fy[idx];
+          return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
+        },
+        [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
     __syncthreads();
   }
-  double2* out = (which ? FY : FX) + (b * N + r) * (long long)L;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) out[i] = sbuf[i];
+  const double inv = 1.0 / (double)L;
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    const int dr = sign ? -(k + 1) : k;
+    if (!in_uc(dr, dc, P, Q)) continue;
+    const int cid = cls_slot[class_index(dr, dc, P, Q)];
+    if (cid < 0 || (sign && k + 1 > P - 1)) continue;
+    double2 v = make_double2(0.0, 0.0);
+    if (mine) {
+      const double2 s = sbuf[fpad(sign ? L + dr : dr)];
+      v = make_double2(s.x * inv, s.y * inv);
+    }
+    const ClassDesc& cd = cls[cid];
+    const long long idx = side ? (long long)(cd.qu - 1) + c1 : c1;
+    ccol[b * tot_ccol + cd.ccol_off + idx] = v;
+  }
+}
+
+// Edge-row sums RC' from the row spectra: for strip rows (i1, i2) (first
+// element row base + i1, second base + i2, dr = i2 - i1),
+//     RC'(dr, dc) of pane row min(i1, i2) = (1/L) sum_f X_{base+i1}[f] conj(Y0_{i2}[f]) w^(f dc)
+// (X masked to the slot-0 box columns [0, M-Q], Y0 unmasked).  CTA = (b,
+// strip, i1, i2); multi-GPU: pair q belongs to part q mod nparts.  RC' has one
+// segment here (nseg = 1).
+template <int LOGL>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
+    k_spec_rc(const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr,
+              const double2* __restrict__ tw, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
+              double2* __restrict__ rc, long long tot_rc, int part, int nparts) {
+  extern __shared__ double2 sbuf[];
+  constexpr int L = 1 << LOGL;
+  const int N = pr.N, P = pr.P, Q = pr.Q, S = P - 1;
+  long long t = blockIdx.x;
+  const int i2 = (int)(t % S);
+  t /= S;
+  const int i1 = (int)(t % S);
+  t /= S;
+  const int strip = (int)(t % 2);
+  const long long b = t / 2;
+  const int dr = i2 - i1;
+  const int base = strip ? N - S : 0;
+  const bool mine = ((long long)i1 * S + i2) % nparts == part;
+  const double2* fx = FX + (b * N + base + i1) * (long long)L;
+  const double2* fy = FY0 + (b * 2 * S + strip * S + i2) * (long long)L;
+  if (mine) {
+    spec_fft_block<LOGL>(
+        sbuf, tw,
+        [&](int idx) {
+          const double2 x = fx[idx], y = fy[idx];
+          return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
+        },
+        [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
+    __syncthreads();
+  }
+  const double inv = 1.0 / (double)L;
+  const int i = min(i1, i2);
+  for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
+    if (!in_uc(dr, dc, P, Q)) continue;
+    const int cid = cls_slot[class_index(dr, dc, P, Q)];
+    if (cid < 0) continue;
+    const ClassDesc& cd = cls[cid];
+    const int k = strip ? (cd.pv - 1) + i : i;
+    double2 v = make_double2(0.0, 0.0);
+    if (mine) {
+      const double2 s = sbuf[fpad(dc)];
+      v = make_double2(s.x * inv, s.y * inv);
+    }
+    rc[b * tot_rc + cd.rc_off + k] = v;
+  }
 }
 
 __device__ __forceinline__ int spec_lo(int dr, int P) { return P - 1 + min(dr, 0); }
@@ -314,22 +570,23 @@ __global__ void __launch_bounds__(SPEC_D0_W * 32)
   }
 }
 
-// CC(dr, dc) = (1/L) sum_f G(dr, f) w^(f dc) for dr != 0 (G summed over the
-// row segments in order), and the ordered sum of the space-domain partials
-// for dr = 0.  CTA = (snapshot b, row lag dr); warp = column lags dc, lanes =
-// frequencies, fixed-order butterfly.  Writes the classes' CC slot (one
-// partial: npart = 1 for the finalize).
-__global__ void __launch_bounds__(256)
+// CC(dr, dc) = (1/L) sum_f G(dr, f) w^(f dc) for dr != 0: one forward FFT of
+// G(dr, .) (summed over the row segments in order) per row lag, outputs
+// dc in [0, Q); for dr = 0 the ordered sum of the space-domain partials.
+// CTA = (snapshot b, row lag dr).  Writes the classes' CC slot (one partial:
+// npart = 1 for the finalize).
+template <int LOGL>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_dft(const double2* __restrict__ Gp, const double2* __restrict__ D0p, int nd0,
-               const double2* __restrict__ tw, Problem pr, int L, int nseg, int nclasses,
+               const double2* __restrict__ tw, Problem pr, int nseg, int nclasses,
                const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
-  extern __shared__ double2 sg[];
+  extern __shared__ double2 sbuf[];
+  constexpr int L = 1 << LOGL;
   const int P = pr.P, Q = pr.Q;
   const int nlag = 2 * P - 1;
   const int li = (int)(blockIdx.x % nlag);
   const long long b = blockIdx.x / nlag;
   const int dr = li - (P - 1);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (dr == 0) {
     for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
       double2 s = make_double2(0.0, 0.0);
@@ -340,24 +597,22 @@ __global__ void __launch_bounds__(256)
     }
     return;
   }
-  for (int f = threadIdx.x; f < L; f += blockDim.x) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int sgm = 0; sgm < nseg; ++sgm) s = cadd(s, Gp[((b * nseg + sgm) * nlag + li) * (long long)L + f]);
-    sg[f] = s;
-  }
+  const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
+  const long long sstride = (long long)nlag * L;
+  spec_fft_block<LOGL>(
+      sbuf, tw,
+      [&](int idx) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int sg = 0; sg < nseg; ++sg) s = cadd(s, g[sg * sstride + idx]);
+        return s;
+      },
+      [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
   __syncthreads();
   const double inv = 1.0 / (double)L;
-  for (int dc = (dr < 0 ? 1 : 0) + w; dc < Q; dc += nw) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int f = lane; f < L; f += 32) {
-      const double2 v = cmul(sg[f], tw[(int)(((long long)f * dc) & (L - 1))]);
-      acc = cadd(acc, v);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const int cid = cls_slot[class_index(dr, dc, P, Q)];
-      if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(acc.x * inv, acc.y * inv);
-    }
+  for (int dc = (dr < 0 ? 1 : 0) + threadIdx.x; dc < Q; dc += blockDim.x) {
+    const int cid = cls_slot[class_index(dr, dc, P, Q)];
+    const double2 s = sbuf[fpad(dc)];
+    if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(s.x * inv, s.y * inv);
   }
 }
 

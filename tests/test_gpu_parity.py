@@ -565,7 +565,7 @@ def test_host_path_streams_a_in_bands_bitwise(cuda):
     plan.close()
 
 
-def test_tensor_core_path_fuzz(cuda):
+def test_tensor_core_path_fuzz(cuda, monkeypatch):
     """24 seeded random complex128 shapes inside the tensor-core gate (P >= 16,
     Q >= 24, wide enough M): ragged chunk / column-block / lag-tile edges,
     Q in and beyond one 64-lag tile, P above and below the tensor-core edge
@@ -583,11 +583,19 @@ def test_tensor_core_path_fuzz(cuda):
         batch = int(rng.integers(1, 4))
         a = torch.as_tensor(rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m)),
                             device=cuda)
+        spectral = it % 2 == 1  # odd draws: frequency-domain sums where Q <= 64
+        if not spectral:
+            monkeypatch.setenv("COVGPU_NO_SPECTRAL", "1")
         plan = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=torch.complex128, device=cuda)
+        monkeypatch.delenv("COVGPU_NO_SPECTRAL", raising=False)
         plan.set_timing(True)
         got = plan.alloc_output()
         plan.execute(a, got)
-        assert "bulk_dmma" in plan.kernel_names(), (it, n, m, p, q)
+        names = plan.kernel_names()
+        if spectral and q <= 64:
+            assert "spec_corr" in names and "spec_rc" in names, (it, n, m, p, q, names)
+        else:
+            assert "bulk_dmma" in names, (it, n, m, p, q, names)
         plan.close()
         got = got.reshape(batch, p * q, p * q)
         for b in range(batch):
