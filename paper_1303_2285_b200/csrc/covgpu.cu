@@ -116,6 +116,9 @@ struct covgpu_plan {
   int spec_logL = 0, spec_L = 0, spec_nseg = 1, spec_nfb = 1, spec_ngrp = 1;
   int spec_nrb = 0, spec_ncp = 1;
   double2 *d_tw = nullptr, *d_fx = nullptr, *d_fy = nullptr, *d_gp = nullptr, *d_d0p = nullptr;
+  SpecLayout spec_lay{};
+  bool spec_smem = false;  // k_spec_corr_smem (P <= 64) instead of the L2-fed k_spec_corr
+  int spec_stages = 2;
   // spectral edge sums: column FFTs of length Lr = 2^spec_logLr (CCol), the
   // unmasked strip-row spectra (RC')
   bool spec_edges = false;
@@ -586,6 +589,28 @@ bool launch_dmma3(covgpu_plan* pl, const double2* A, cudaStream_t st) {
   return true;
 }
 
+// Pass-major twiddle table of an FFT of length 2^logL (spectral.cuh,
+// spec_tw_off): w_{pR}^(r k) in long double, rounded once.
+std::vector<double2> spec_twiddles(int logL) {
+  std::vector<double2> t((size_t)1 << logL, make_double2(0.0, 0.0));
+  const long double pi2 = 6.283185307179586476925286766559L;
+  int p = 1, rem = logL;
+  while (rem > 0) {
+    const int lr = rem >= 3 ? 3 : rem, R = 1 << lr;
+    if (p > 1) {
+      const int off = spec_tw_off(logL, p);
+      for (int r = 1; r < R; ++r)
+        for (int k = 0; k < p; ++k) {
+          const long double a = -pi2 * (long double)(r * k) / (long double)(p * R);
+          t[(size_t)off + (size_t)(r - 1) * p + k] = make_double2((double)cosl(a), (double)sinl(a));
+        }
+    }
+    p <<= lr;
+    rem -= lr;
+  }
+  return t;
+}
+
 // Spectral kernels are instantiated for FFT lengths 2^6 .. 2^12; SPEC_LOGL
 // dispatches a launch on the runtime log2 length (SMEM attribute set once per
 // instantiation: up to (L + L/8) complex values).
@@ -648,12 +673,44 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   k_spec_dr0<T><<<(unsigned)(B * pl->spec_nrb * pl->spec_ncp), SPEC_D0_W * 32, SPEC_D0_SMEM, st>>>(
       A, pr, ra, rz, pl->spec_nrb, pl->spec_ncp, pl->d_d0p);
   mark("spec_dr0");
-  SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->d_tw, pl->d_fx, pl->d_fy);
+  SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
+            pl->d_fy);
   if (pl->spec_edges)
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->d_tw, pl->d_fx, pl->d_fy0);
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
+              pl->d_fy0);
   mark("spec_fft");
-  k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
-      pl->d_fx, pl->d_fy, pr, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts, pl->d_gp);
+  if (pl->spec_smem) {
+    const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
+    const unsigned blocks = (unsigned)(B * pl->spec_lay.nfb * pl->spec_nseg);
+#define SPEC_CORR(NG)                                                                                   \
+  case NG: {                                                                                            \
+    static bool attr = false;                                                                           \
+    if (!attr) {                                                                                        \
+      cudaFuncSetAttribute(k_spec_corr_smem<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
+      attr = true;                                                                                      \
+    }                                                                                                   \
+    k_spec_corr_smem<NG><<<blocks, NG * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay,       \
+                                                            pl->spec_nseg, part, nparts, pl->spec_stages, \
+                                                            pl->d_gp);                                  \
+  } break
+    switch (pl->spec_ngrp) {
+      SPEC_CORR(2); SPEC_CORR(3); SPEC_CORR(4); SPEC_CORR(5); SPEC_CORR(6); SPEC_CORR(7);
+      default: {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_spec_corr_smem<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+          attr = true;
+        }
+        k_spec_corr_smem<8><<<blocks, 8 * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, pl->spec_nseg,
+                                                         part, nparts, pl->spec_stages, pl->d_gp);
+      }
+    }
+#undef SPEC_CORR
+  } else {
+    k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
+        pl->d_fx, pl->d_fy, pr, pl->spec_lay, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts,
+        pl->d_gp);
+  }
   mark("spec_corr");
   SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp,
             pl->d_tw, pr, pl->spec_nseg, pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
@@ -663,7 +720,8 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * 2 * (long long)S1 * S1, pl->d_fc, pr, pl->d_twr,
               pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
     mark("spec_ccol");
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr, pl->d_tw,
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+              pl->spec_lay, pl->d_tw,
               pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
   }
 }
@@ -1221,6 +1279,29 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       long long seg = std::max(1LL, (148LL * 6 + per - 1) / per);
       seg = std::min(seg, std::max(1LL, rows / (4LL * SPEC_E)));
       pl->spec_nseg = (int)std::min(seg, 64LL);
+      pl->spec_lay.nfb = pl->spec_L / 32;
+      pl->spec_lay.padr = p - 1 + SC_RC;
+      pl->spec_lay.np = (int)n + 2 * pl->spec_lay.padr;
+      const size_t stb = spec_corr_stage_bytes(p);
+      pl->spec_smem = pl->spec_ngrp <= 8 && 2 * stb + 64 <= SC_SMEM_BUDGET;
+      if (const char* nsm = getenv("COVGPU_SPEC_NO_SMEM")) pl->spec_smem = pl->spec_smem && atoi(nsm) == 0;
+      if (pl->spec_smem) {
+        pl->spec_stages = (int)std::min<size_t>(4, SC_SMEM_BUDGET / (stb + 16));
+        // row segments: whole waves of 1-CTA/SM blocks, >= 4 chunks per segment
+        const long long per2 = batch * (long long)pl->spec_lay.nfb;
+        const long long nch = (n + SC_RC - 1) / SC_RC;
+        int best = 1;
+        double best_eff = 0.0;
+        for (int sg = 1; sg <= 32 && (sg == 1 || nch / sg >= 4); ++sg) {
+          const double ctas = (double)per2 * sg, waves = std::ceil(ctas / 148.0);
+          const double eff = ctas / (waves * 148.0) * std::min(1.0, ctas / 296.0);
+          if (eff > best_eff + 0.01) {
+            best_eff = eff;
+            best = sg;
+          }
+        }
+        pl->spec_nseg = best;
+      }
       const long long d0rows = n - 2LL * p + 2;
       pl->spec_nrb = (int)((d0rows + SPEC_D0_RB - 1) / SPEC_D0_RB);
       const long long nch = (m - q + 1 + SPEC_D0_CW - 1) / SPEC_D0_CW;
@@ -1353,30 +1434,24 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   }
   if (pl->use_spec) {
     const size_t L = (size_t)pl->spec_L;
-    std::vector<double2> tw(L);
-    const long double pi2 = 6.283185307179586476925286766559L;
-    for (size_t j = 0; j < L; ++j) {
-      const long double a = -pi2 * (long double)j / (long double)L;
-      tw[j] = make_double2((double)cosl(a), (double)sinl(a));
-    }
-    if ((rc = dalloc(&pl->d_tw, L, &ws)) || (rc = dalloc(&pl->d_fx, (size_t)batch * n * L, &ws)) ||
-        (rc = dalloc(&pl->d_fy, (size_t)batch * n * L, &ws)) ||
+    const std::vector<double2> tw = spec_twiddles(pl->spec_logL);
+    const size_t fxe = (size_t)batch * pl->spec_lay.nfb * pl->spec_lay.np * 32;
+    if ((rc = dalloc(&pl->d_tw, L, &ws)) || (rc = dalloc(&pl->d_fx, fxe, &ws)) ||
+        (rc = dalloc(&pl->d_fy, fxe, &ws)) ||
         (rc = dalloc(&pl->d_gp, (size_t)batch * pl->spec_nseg * (2 * p - 1) * L, &ws)) ||
         (rc = dalloc(&pl->d_d0p, (size_t)batch * pl->spec_nrb * pl->spec_ncp * q, &ws))) {
       plan_free(pl.get());
       return rc;
     }
-    if (cudaMemcpy(pl->d_tw, tw.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemset(pl->d_fx, 0, sizeof(double2) * fxe) != cudaSuccess ||
+        cudaMemset(pl->d_fy, 0, sizeof(double2) * fxe) != cudaSuccess ||
+        cudaMemcpy(pl->d_tw, tw.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) != cudaSuccess) {
       plan_free(pl.get());
       return fail(COVGPU_ECUDA, "twiddle upload");
     }
     if (pl->spec_edges) {
       const size_t Lr = (size_t)1 << pl->spec_logLr;
-      std::vector<double2> twr(Lr);
-      for (size_t j = 0; j < Lr; ++j) {
-        const long double a = -pi2 * (long double)j / (long double)Lr;
-        twr[j] = make_double2((double)cosl(a), (double)sinl(a));
-      }
+      const std::vector<double2> twr = spec_twiddles(pl->spec_logLr);
       if ((rc = dalloc(&pl->d_twr, Lr, &ws)) ||
           (rc = dalloc(&pl->d_fc, (size_t)batch * 8 * (q - 1) * Lr, &ws)) ||
           (rc = dalloc(&pl->d_fy0, (size_t)batch * 2 * (p - 1) * L, &ws))) {

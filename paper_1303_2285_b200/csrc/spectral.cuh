@@ -96,6 +96,22 @@ __device__ __forceinline__ void dft_small<8>(double2* u) {
 // distinct 16-byte bank groups
 __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
 
+// Twiddle table, pass-major: for each pass after the first (p = product of
+// the earlier radices, radix R) the entries w_{pR}^(r k), r in [1, R),
+// k in [0, p), at [(r-1) p + k] — consecutive lanes (consecutive k) read
+// consecutive entries.  spec_tw_off(logL, p) = offset of the pass; the same
+// walk builds the table on the host (spec_twiddles).
+__host__ __device__ constexpr int spec_tw_off(int logL, int P0) {
+  int off = 0, p = 1, rem = logL;
+  while (p < P0) {
+    const int lr = rem >= 3 ? 3 : rem;
+    if (p > 1) off += ((1 << lr) - 1) * p;
+    p <<= lr;
+    rem -= lr;
+  }
+  return off;
+}
+
 // One radix-R Stockham pass (autosort, no bit reversal): item i of L/R,
 // k = i mod p (p = product of the radices already applied):
 //     u_r = in[i + r L/R] * w_L^(r k L/(pR)),  DFT_R(u),  out[(i - k) R + k + r p] = u_r.
@@ -125,7 +141,7 @@ __device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict
     }
   }
   if constexpr (!first) __syncthreads();
-  constexpr int tws = L / (P0 * R);
+  const double2* __restrict__ twp = tw + spec_tw_off(LOGL, P0);
 #pragma unroll
   for (int it = 0; it < IPT; ++it) {
     const int i = threadIdx.x + it * NTHR;
@@ -133,7 +149,7 @@ __device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict
       const int k = i & (P0 - 1);
       if (k) {
 #pragma unroll
-        for (int r = 1; r < R; ++r) u[it][r] = cmul(u[it][r], tw[r * k * tws]);
+        for (int r = 1; r < R; ++r) u[it][r] = cmul(u[it][r], twp[(r - 1) * P0 + k]);
       }
       dft_small<R>(u[it]);
       const int j = i * R - k * (R - 1);
@@ -151,7 +167,7 @@ __device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict
 }
 
 // The whole forward FFT of length 2^LOGL: radix-8 passes, then one radix-4 /
-// radix-2 pass.  tw[j] = exp(-2 pi i j / L) (host-made, long double).
+// radix-2 pass.  tw = the pass-major twiddle table (spec_tw_off).
 template <int LOGL, int P0 = 1, class Load, class Store>
 __device__ __forceinline__ void spec_fft_block(double2* sb, const double2* __restrict__ tw, const Load& ld,
                                                const Store& st) {
@@ -169,14 +185,26 @@ constexpr int spec_threads() {
   return (1 << LOGL) / 8 > 32 ? (1 << LOGL) / 8 : 32;
 }
 
+// Row spectra X_r, Y_r live f-block-major: [b][f / 32][PADR + r][f % 32],
+// with PADR zero rows above and below every block (never written), so that
+// a run of rows of one 32-frequency block is one contiguous bulk copy.
+struct SpecLayout {
+  int nfb;   // 32-frequency blocks (L / 32)
+  int padr;  // zero rows above and below
+  int np;    // rows per block: N + 2 padr
+  __host__ __device__ long long at(long long b, int r, int f) const {
+    return ((b * nfb + (f >> 5)) * np + padr + r) * 32LL + (f & 31);
+  }
+};
+
 // Row FFTs.  mode 0: CTA = (snapshot b, row r, which): which 0 -> X_r
 // (columns c <= M-Q), 1 -> Y_r (columns c >= Q-1).  mode 1 (edge rows):
 // CTA = (b, strip row s of 2(P-1)) -> Y0_s, the unmasked row of the top
 // strip [0, P-1) / bottom strip [N-P+1, N).  Zero-padded to L = 2^LOGL.
 template <typename T, int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_fft(const typename CT<T>::c* __restrict__ A, Problem pr, int mode, const double2* __restrict__ tw,
-               double2* __restrict__ FX, double2* __restrict__ FY) {
+    k_spec_fft(const typename CT<T>::c* __restrict__ A, Problem pr, int mode, SpecLayout lay,
+               const double2* __restrict__ tw, double2* __restrict__ FX, double2* __restrict__ FY) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   long long t = blockIdx.x;
@@ -192,8 +220,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     clo = which ? Q - 1 : 0;
     chi = which ? M - 1 : M - Q;
     orow = b * N + r;
-    out = (which ? FY : FX) + orow * L;
-    orow = b * N + r;
+    out = (which ? FY : FX) + lay.at(b, r, 0);
   } else {
     const int sr = (int)(t % (2 * S));
     const long long b = t / (2 * S);
@@ -201,12 +228,13 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     clo = 0;
     chi = M - 1;
     orow = b * N + r;
-    out = FY + (b * 2 * S + sr) * (long long)L;
+    out = FY + (b * 2 * S + sr) * (long long)L;  // row-major (mode 1 stride: 32 per block)
   }
   const typename CT<T>::c* row = A + orow * (long long)M;
+  const long long fstride = mode == 0 ? (long long)lay.np * 32 : 32;  // next 32-frequency block
   spec_fft_block<LOGL>(
       sbuf, tw, [&](int idx) { return (idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0); },
-      [&](int idx, double2 v) { out[idx] = v; });
+      [&](int idx, double2 v) { out[(idx >> 5) * fstride + (idx & 31)] = v; });
 }
 
 // Column FFTs of the edge-column strips (left: columns [0, Q-1), right:
@@ -305,7 +333,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // segment here (nseg = 1).
 template <int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_rc(const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr,
+    k_spec_rc(const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr, SpecLayout lay,
               const double2* __restrict__ tw, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
               double2* __restrict__ rc, long long tot_rc, int part, int nparts) {
   extern __shared__ double2 sbuf[];
@@ -321,13 +349,14 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const int dr = i2 - i1;
   const int base = strip ? N - S : 0;
   const bool mine = ((long long)i1 * S + i2) % nparts == part;
-  const double2* fx = FX + (b * N + base + i1) * (long long)L;
+  const double2* fx = FX + lay.at(b, base + i1, 0);
+  const long long fxs = (long long)lay.np * 32;
   const double2* fy = FY0 + (b * 2 * S + strip * S + i2) * (long long)L;
   if (mine) {
     spec_fft_block<LOGL>(
         sbuf, tw,
         [&](int idx) {
-          const double2 x = fx[idx], y = fy[idx];
+          const double2 x = fx[(idx >> 5) * fxs + (idx & 31)], y = fy[idx];
           return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
         },
         [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
@@ -379,7 +408,8 @@ __device__ __forceinline__ void spec_mac(int tt, double2 y, const double* wr, co
 // predicates.
 template <int E>
 __global__ void __launch_bounds__(SPEC_CW * 32, 2)
-    k_spec_corr(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, int L, int nfb,
+    k_spec_corr(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay, int L,
+                int nfb,
                 int ngrp, int nseg, int part, int nparts, double2* __restrict__ Gp) {
   long long t = blockIdx.x;
   const int g = (int)(t % ngrp);
@@ -400,8 +430,9 @@ __global__ void __launch_bounds__(SPEC_CW * 32, 2)
   const int a = rlo + (int)((long long)nr * idx / pieces);
   const int z = rlo + (int)((long long)nr * (idx + 1) / pieces) - 1;  // last row (inclusive)
   const int blo = spec_lo(drl, P), bhi = min(spec_hi(dr0, P, N), z);  // every lag active
-  const double2* fx = FX + b * N * (long long)L + f;
-  const double2* fy = FY + b * N * (long long)L + f;
+  // rows of one 32-frequency block are 32 apart (SpecLayout)
+  const double2* fx = FX + lay.at(b, 0, f);
+  const double2* fy = FY + lay.at(b, 0, f);
 
   double ar[E], ai[E], wr[E], wi[E];
 #pragma unroll
@@ -413,7 +444,7 @@ __global__ void __launch_bounds__(SPEC_CW * 32, 2)
     for (int k = 0; k < E - 1; ++k) {
       const int row = t0 - (E - 1) + k;
       if (row >= 0 && row < N) {
-        const double2 v = fx[(long long)row * L];
+        const double2 v = fx[(long long)row * 32];
         wr[k] = v.x;
         wi[k] = v.y;
       }
@@ -422,12 +453,12 @@ __global__ void __launch_bounds__(SPEC_CW * 32, 2)
   for (int rb = a; rb <= z; rb += E) {
     const int t0 = rb - dr0;
     if (rb >= blo && rb + E - 1 <= bhi) {
-      const double2* px = fx + (long long)t0 * L;
-      const double2* py = fy + (long long)rb * L;
+      const double2* px = fx + (long long)t0 * 32;
+      const double2* py = fy + (long long)rb * 32;
 #pragma unroll
       for (int tt = 0; tt < E; ++tt) {
-        const double2 xn = px[(long long)tt * L];
-        const double2 y = py[(long long)tt * L];
+        const double2 xn = px[(long long)tt * 32];
+        const double2 y = py[(long long)tt * 32];
         wr[(tt + E - 1) % E] = xn.x;
         wi[(tt + E - 1) % E] = xn.y;
         spec_mac<E>(tt, y, wr, wi, ar, ai);
@@ -437,8 +468,8 @@ __global__ void __launch_bounds__(SPEC_CW * 32, 2)
       for (int tt = 0; tt < E; ++tt) {
         const int r2 = rb + tt, row = t0 + tt;
         double2 xn = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
-        if (row >= 0 && row < N) xn = fx[(long long)row * L];
-        if (r2 <= z) y = fy[(long long)r2 * L];
+        if (row >= 0 && row < N) xn = fx[(long long)row * 32];
+        if (r2 <= z) y = fy[(long long)r2 * 32];
         wr[(tt + E - 1) % E] = xn.x;
         wi[(tt + E - 1) % E] = xn.y;
         const double ny = -y.y;
@@ -461,6 +492,145 @@ __global__ void __launch_bounds__(SPEC_CW * 32, 2)
   for (int e = 0; e < E; ++e) {
     const int dr = dr0 + e;
     if (dr <= P - 1) out[(long long)(dr + P - 1) * L] = make_double2(ar[e], ai[e]);
+  }
+}
+
+// The same correlation with the rows staged in SMEM (P <= 64): CTA = (b,
+// 32-frequency block, row segment), NG compute warps = the 16-lag groups of
+// all 2P-1 lags (so the X / Y rows are read from L2 once per CTA instead of
+// once per lag group) + one producer warp.  Per chunk of SC_RC second-element
+// rows R.., the producer bulk-copies (cp.async.bulk, mbarrier ring) the
+// contiguous runs Y rows [R, R+SC_RC) and X rows [R-(P-1), R+SC_RC+P-2) of the
+// f-block (zero pad rows cover the ends); warp g walks the chunk with its 16
+// X rows in a rotating register window (2 LDS.128 per 16 complex MACs).
+constexpr int SC_RC = 32;
+constexpr size_t SC_SMEM_BUDGET = 220 * 1024;
+
+__host__ __device__ inline size_t spec_corr_stage_bytes(int P) {
+  return sizeof(double2) * 32 * (size_t)(2 * SC_RC + 2 * P - 2);
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NG>
+__global__ void __launch_bounds__(NG * 32, 1)
+    k_spec_corr_smem(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay,
+                     int nseg, int part, int nparts, int stages, double2* __restrict__ Gp) {
+  constexpr int E = SPEC_E;
+  extern __shared__ __align__(128) unsigned char scraw[];
+  const int P = pr.P, N = pr.N;
+  const int nlag = 2 * P - 1, XR = SC_RC + 2 * P - 2;
+  const size_t stage_bytes = spec_corr_stage_bytes(P);
+  uint64_t* full = reinterpret_cast<uint64_t*>(scraw + stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  long long t = blockIdx.x;
+  const int seg = (int)(t % nseg);
+  t /= nseg;
+  const int fb = (int)(t % lay.nfb);
+  const long long b = t / lay.nfb;
+  const int nch = (N + SC_RC - 1) / SC_RC;
+  const int pieces = nparts * nseg, idx = part * nseg + seg;
+  const int ca = (int)((long long)nch * idx / pieces), cz = (int)((long long)nch * (idx + 1) / pieces);
+  const int nk = cz - ca;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* fxb = FX + ((b * lay.nfb + fb) * lay.np + lay.padr) * 32LL;  // row 0 of the block
+  const double2* fyb = FY + ((b * lay.nfb + fb) * lay.np + lay.padr) * 32LL;
+  // thread 0 is also the producer (keeps 2 warps per SM sub-partition: the
+  // register budget of 8 warps is 255 per thread, 9 warps would cap it at 168)
+  auto issue = [&](int k) {
+    const int s = k % stages;
+    if (k >= stages) mbar_wait(&empty[s], ((k - stages) / stages) & 1);
+    const int R = (ca + k) * SC_RC;
+    unsigned char* st = scraw + s * stage_bytes;
+    mbar_expect_tx(&full[s], (unsigned)stage_bytes);
+    bulk_g2s(st, fyb + (long long)R * 32, (unsigned)(sizeof(double2) * 32 * SC_RC), &full[s]);
+    bulk_g2s(st + sizeof(double2) * 32 * SC_RC, fxb + (long long)(R - (P - 1)) * 32,
+             (unsigned)(sizeof(double2) * 32 * XR), &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NG);
+    }
+    fence_mbarrier_init();
+    for (int k = 0; k < stages - 1 && k < nk; ++k) issue(k);
+  }
+  __syncthreads();
+  const int dr0 = -(P - 1) + w * E;
+  const int drl = min(dr0 + E - 1, P - 1);
+  const int glo = spec_lo(dr0, P), ghi = spec_hi(drl, P, N);   // rows where some lag is active
+  const int blo = spec_lo(drl, P), bhi = spec_hi(dr0, P, N);   // rows where every lag is active
+  double ar[E], ai[E], wr[E], wi[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) ar[e] = ai[e] = wr[e] = wi[e] = 0.0;
+  const int xoff = (P - 1) - dr0;  // stage X row of (r2 = R + j, lag e) = j + xoff - e
+  for (int k = 0; k < nk; ++k) {
+    if (threadIdx.x == 0 && k + stages - 1 < nk) issue(k + stages - 1);
+    const int s = k % stages;
+    mbar_wait(&full[s], (k / stages) & 1);
+    const int R = (ca + k) * SC_RC;
+    const double2* Y = reinterpret_cast<const double2*>(scraw + s * stage_bytes) + lane;
+    const double2* X = Y + 32 * SC_RC;
+    if (R + SC_RC - 1 >= glo && R <= ghi && dr0 <= P - 1) {
+      // window: slot kk holds X row (xoff - (E-1) + kk) for kk < E-1 (clamped: those rows only feed
+      // lags past P-1 when negative)
+#pragma unroll
+      for (int kk = 0; kk < E - 1; ++kk) {
+        const double2 v = X[max(xoff - (E - 1) + kk, 0) * 32];
+        wr[kk] = v.x;
+        wi[kk] = v.y;
+      }
+#pragma unroll 1
+      for (int j0 = 0; j0 < SC_RC; j0 += E) {
+        const int rb = R + j0;
+        if (rb >= blo && rb + E - 1 <= bhi) {
+#pragma unroll
+          for (int tt = 0; tt < E; ++tt) {
+            const double2 xn = X[(j0 + tt + xoff) * 32];
+            const double2 y = Y[(j0 + tt) * 32];
+            wr[(tt + E - 1) % E] = xn.x;
+            wi[(tt + E - 1) % E] = xn.y;
+            spec_mac<E>(tt, y, wr, wi, ar, ai);
+          }
+        } else {
+#pragma unroll
+          for (int tt = 0; tt < E; ++tt) {
+            const int r2 = rb + tt;
+            const double2 xn = X[(j0 + tt + xoff) * 32];
+            const double2 y = Y[(j0 + tt) * 32];
+            wr[(tt + E - 1) % E] = xn.x;
+            wi[(tt + E - 1) % E] = xn.y;
+            const double ny = -y.y;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int dr = dr0 + e;
+              const bool on = r2 >= spec_lo(dr, P) && r2 <= spec_hi(dr, P, N);
+              const double yx = on ? y.x : 0.0, yy = on ? y.y : 0.0, nyy = on ? ny : 0.0;
+              const int sl = (tt + E - 1 - e) % E;
+              ar[e] = fma(wr[sl], yx, ar[e]);
+              ai[e] = fma(wi[sl], yx, ai[e]);
+              ar[e] = fma(wi[sl], yy, ar[e]);
+              ai[e] = fma(wr[sl], nyy, ai[e]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  const int f = fb * 32 + lane;
+  double2* out = Gp + (b * nseg + seg) * (long long)nlag * (lay.nfb * 32) + f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int dr = dr0 + e;
+    if (dr <= P - 1) out[(long long)(dr + P - 1) * (lay.nfb * 32)] = make_double2(ar[e], ai[e]);
   }
 }
 
