@@ -321,43 +321,78 @@ def main() -> None:
     if rowband:
         shard_frac = 1.0 / world
     roof = None
-    if kernel_ms.get("bulk_dmma", 0) > 0:
-        # dominant kernel on the FP64 tensor cores: core products x 6 flops (the
-        # Gauss 3-multiplication complex product: 3 real FMAs per product)
-        achieved = 6.0 * core_p * w.batch * shard_frac / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12
-        traffic = None
+    hbm_peak = None
+    try:
+        hbm_peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        hbm_peak = 7672.0  # B200_PROFILING.md fallback
+    n, m, p, q, B = w.n, w.m, w.p, w.q, w.batch
+    esz_in = 16 if w.dtype == "c128" else 8
+    L = 1
+    while L < m:
+        L *= 2
+    per_kernel = {}
+
+    def fp_roof(name, flops, note, pk=None, pk_src=None):
+        ms_k = kernel_ms[name]
+        ach = flops / (ms_k * 1e-3) / 1e12
+        pk = peak if pk is None else pk
+        return {"bound": "fp64" if w.dtype == "c128" or name.startswith("spec") else "fp32",
+                "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                "algorithmic_flops_per_launch": flops, "work": note,
+                "peak_source": pk_src or "FMA-loop probe (operand-reuse DFMA/FFMA pattern) measured on this "
+                "GPU in this run (MEASURED_PEAKS.json has no FP64/FP32 figure)",
+                "nominal_peak": 148 * (64 if w.dtype == "c128" or name.startswith("spec") else 128) * 2
+                * 1.965e9 / 1e12}
+
+    def hbm_roof(name, nbytes, note):
+        ach = nbytes / (kernel_ms[name] * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "algorithmic_bytes_per_launch": nbytes, "work": note,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"}
+
+    sf = shard_frac
+    for name in kernel_ms:
+        if kernel_ms[name] <= 0:
+            continue
+        if name == "spec_corr":
+            macs = sum((n - 2 * p + 2 + abs(dr)) for dr in range(-(p - 1), p) if dr != 0) * L * B * sf
+            per_kernel[name] = fp_roof(name, 8.0 * macs, "8 flops x sum over row lags dr != 0 of "
+                                       "|core rows(dr)| x L frequencies (complex MAC per row, frequency, lag)")
+        elif name == "spec_dr0":
+            macs = (n - 2 * p + 2) * sum(m - 2 * q + 2 + dc for dc in range(q)) * B * sf
+            per_kernel[name] = fp_roof(name, 8.0 * macs, "8 flops x core products of the dr = 0 classes")
+        elif name == "spec_fft":
+            nb = (2 * n * m * esz_in + 2 * n * L * 16 + 2 * (p - 1) * (m * esz_in + L * 16)) * B
+            per_kernel[name] = hbm_roof(name, nb, "A read twice + the X / Y row spectra written "
+                                        "(+ the unmasked edge-row spectra)")
+        elif name == "bulk_dmma":
+            per_kernel[name] = fp_roof(name, 6.0 * core_p * B * sf,
+                                       "6 flops (Gauss 3 real FMAs) x core products", pk=peak_dmma,
+                                       pk_src="DMMA-loop probe (mma.sync m8n8k4 f64) measured on this GPU "
+                                       "in this run")
+            per_kernel[name]["bound"] = "fp64-tensor"
+        elif name == "bulk":
+            per_kernel[name] = fp_roof(name, 8.0 * bulk_p * B * sf, "8 flops x core-row products")
+        elif name in ("finalize", "expand"):
+            nbytes = float(w.pq) ** 2 * esz_in * B * sf if layout == "dense" else None
+            if nbytes:
+                per_kernel[name] = hbm_roof(name, nbytes, "dense R written once (the walk's reads of "
+                                            "the per-class sums are L2-resident and not counted)")
+    if per_kernel:
+        dom = max(per_kernel, key=lambda k: kernel_ms[k])
+        roof = dict(per_kernel[dom])
+        roof["kernel"] = {"spec_corr": "k_spec_corr_smem", "spec_dr0": "k_spec_dr0", "spec_fft": "k_spec_fft",
+                          "bulk_dmma": "k_bulk_dmma3", "bulk": "k_bulk_tma", "finalize": "k_finalize_v",
+                          "expand": "k_expand"}.get(dom, dom)
+        roof["share_of_step"] = kernel_ms[dom] / max(sum(kernel_ms.values()), 1e-12)
+        roof["traffic"] = None
         prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
         if prof.exists():
             try:
-                traffic = json.loads(prof.read_text()).get("bulk_dmma_dram_bytes_per_launch")
+                roof["traffic"] = json.loads(prof.read_text()).get(f"{dom}_dram_bytes_per_launch")
             except (ValueError, OSError):
-                traffic = None
-        roof = {"bound": "fp64-tensor", "achieved": achieved, "peak": peak_dmma, "unit": "TFLOP/s",
-                "frac": achieved / peak_dmma, "traffic": traffic,
-                "kernel": "k_bulk_dmma" if os.environ.get("COVGPU_MMA_KIND") == "0" else "k_bulk_dmma3",
-                "peak_source": "DMMA-loop probe (mma.sync m8n8k4 f64) measured on this GPU in this "
-                "run (MEASURED_PEAKS.json has no FP64 figure)",
-                "algorithmic_flops_per_launch": 6.0 * core_p * w.batch * shard_frac,
-                "flops_per_product": "6 (Gauss: Re = P1 + P2, Im = P3 - P1 + P2, 3 real FMAs)",
-                "complex_mac_equivalent_tflops": 8.0 * core_p * w.batch * shard_frac
-                / (kernel_ms["bulk_dmma"] * 1e-3) / 1e12,
-                "nominal_peak": 148 * 64 * 2 * 1.965e9 / 1e12,
-                "fma_loop_peak": peak}
-    elif "bulk" in kernel_ms and kernel_ms["bulk"] > 0:
-        achieved = 8.0 * bulk_p * w.batch * shard_frac / (kernel_ms["bulk"] * 1e-3) / 1e12
-        traffic = None
-        prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
-        if prof.exists():
-            try:
-                traffic = json.loads(prof.read_text()).get("bulk_dram_bytes_per_launch")
-            except (ValueError, OSError):
-                traffic = None
-        roof = {"bound": "fp64" if w.dtype == "c128" else "fp32", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_bulk", "peak_source": "FMA-loop probe measured on this GPU in this run "
-                "(MEASURED_PEAKS.json has no FP64/FP32 figure)",
-                "algorithmic_flops_per_launch": 8.0 * bulk_p * w.batch * shard_frac,
-                "nominal_peak": 148 * (64 if w.dtype == "c128" else 128) * 2 * 1.965e9 / 1e12}
+                pass
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -370,28 +405,33 @@ def main() -> None:
                                    f"({sums.numel() * 16 / 2**20:.1f} MiB), class-range finalize")
                    if rowband else (f"class-shard x{world}" if world > 1 else "single GPU")},
         "effective_gflops": flops / (ms * 1e-3) / 1e9,
+        "effective_gflops_note": "8 x UM (the paper's unique products) / step time; the spectral path "
+                                 "does fewer flops than that, so this is not a hardware rate",
         "kernel_ms": kernel_ms,
+        "kernel_roofline": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac")}
+                            for k, v in per_kernel.items()},
         "gpu_launches": (plan.launches + (2 if rowband else 0)) * args.steps,
         "roofline": roof,
         "clocks": clocks.summary(),
     }
 
-    # the CUDA-core path beside it (the north_star's FP64/FP32-pipe kernel;
-    # still the path for complex64 and class shards): same workload, a few
-    # steps, per-kernel events — reported, not the headline
-    if roof is not None and roof.get("kernel", "").startswith("k_bulk_dmma") and world == 1 \
-            and not args.no_cuda_core and not rowband:
-        os.environ["COVGPU_NO_MMA"] = "1"
+    # the earlier paths beside it, same workload, a few steps, per-kernel
+    # events — reported, not the headline: the FP64 tensor-core core sums
+    # (COVGPU_NO_SPECTRAL) and the north_star's CUDA-core recurrence kernels
+    # (COVGPU_NO_MMA: also the path of shapes outside the spectral gates)
+    def side_path(env):
+        for k, v in env.items():
+            os.environ[k] = v
         try:
             cplan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, device=dev)
         finally:
-            del os.environ["COVGPU_NO_MMA"]
+            for k in env:
+                del os.environ[k]
         cout = cplan.alloc_output(layout)
         for _ in range(2):
             cplan.execute(a, cout, layout)
         torch.cuda.synchronize(dev)
-        tot = 0.0
-        nst = 5
+        tot, nst = 0.0, 5
         for _ in range(nst):
             flush.fill_(1)
             torch.cuda.synchronize(dev)
@@ -406,15 +446,27 @@ def main() -> None:
         cplan.execute(a, cout, layout)
         ck = dict(zip(cplan.kernel_names(), cplan.kernel_times()))
         cplan.close()
-        cms = tot / nst
+        return tot / nst, ck
+
+    if world == 1 and not args.no_cuda_core and not rowband and "spec_corr" in kernel_ms:
+        tms, tk = side_path({"COVGPU_NO_SPECTRAL": "1"})
+        tach = 6.0 * core_p * w.batch / (tk["bulk_dmma"] * 1e-3) / 1e12 if tk.get("bulk_dmma") else None
+        line["tensor_core_path"] = {
+            "ms_per_step": tms, "value": entries / (tms * 1e-3), "kernel_ms": tk,
+            "bulk_dmma_achieved_tflops": tach,
+            "bulk_dmma_frac_of_dmma_probe": tach / peak_dmma if tach and peak_dmma else None,
+            "note": "COVGPU_NO_SPECTRAL=1: core sums as Toeplitz GEMMs on the FP64 tensor cores "
+                    "(k_bulk_dmma3, 6 flops per core product), edge sums on DMMA too"}
+    if world == 1 and not args.no_cuda_core and not rowband and w.dtype == "c128":
+        cms, ck = side_path({"COVGPU_NO_MMA": "1", "COVGPU_NO_SPECTRAL": "1"})
         cach = 8.0 * bulk_p * w.batch / (ck["bulk"] * 1e-3) / 1e12 if ck.get("bulk") else None
         line["cuda_core_path"] = {
             "ms_per_step": cms, "value": entries / (cms * 1e-3), "kernel_ms": ck,
             "bulk_achieved_tflops": cach,
             "bulk_frac_of_fma_probe": cach / peak if cach else None,
             "bulk_frac_of_nominal_fp64": cach / (148 * 64 * 2 * 1.965e9 / 1e12) if cach else None,
-            "note": "COVGPU_NO_MMA=1: core sums on the FP64 FMA pipe (k_bulk_tma), 8 flops per "
-                    "core-row product",
+            "note": "COVGPU_NO_MMA=1 COVGPU_NO_SPECTRAL=1: core sums on the FP64 FMA pipe (k_bulk_tma), "
+                    "8 flops per core-row product",
         }
 
     # end to end through the C ABI with pinned host buffers
