@@ -225,14 +225,16 @@ def main() -> None:
     w = workload(args.config)
     win = WindowSpec(w.p, w.q)
     tdt = torch.complex128 if w.dtype == "c128" else torch.complex64
-    # N > 1: row bands (every rank on the tensor-core path, one all-reduce of
-    # the per-band sums) where the shape allows, else class shards
-    rowband = (world > 1 or args.rowband) and w.dtype == "c128" and 48 <= w.p <= 65 \
-        and 50 <= w.q <= 65
+    # N > 1: row bands (every rank on the spectral / tensor-core sums of its
+    # band, one all-reduce of the per-band sums) where the plan supports them,
+    # else class shards
+    plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, device=dev)
+    rowband = (world > 1 or args.rowband) and plan.supports_rowband
     ids = None
     if world > 1 and not rowband:
+        plan.close()
         ids = partition_classes(w.n, w.m, win, world, fp64=(w.dtype == "c128"))[rank]
-    plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, class_ids=ids, device=dev)
+        plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, class_ids=ids, device=dev)
     layout = args.layout if world == 1 and not rowband else "compact"
     if rowband:
         from paper_1303_2285_b200.distributed import class_ranges

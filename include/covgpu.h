@@ -92,6 +92,17 @@ int64_t covgpu_plan_workspace_bytes(covgpu_plan_t plan);
 int32_t covgpu_plan_num_groups(covgpu_plan_t plan);
 int32_t covgpu_plan_launches(covgpu_plan_t plan);
 
+/* Which sum kernels the plan runs (bit flags): COVGPU_PATH_SPECTRAL — the
+ * core / edge sums in the frequency domain (row and column FFTs, per-frequency
+ * row-lag correlation); COVGPU_PATH_TENSOR — the core sums as Toeplitz GEMMs
+ * on the FP64 tensor cores; neither — the CUDA-core recurrence kernels;
+ * COVGPU_PATH_ROWBAND — covgpu_plan_execute_sums is available.  Replaces the
+ * reference's backend query (backend.resolve_backend, backend.py:45-57). */
+#define COVGPU_PATH_SPECTRAL 1
+#define COVGPU_PATH_TENSOR 2
+#define COVGPU_PATH_ROWBAND 4
+int32_t covgpu_plan_path(covgpu_plan_t plan);
+
 /* Record CUDA events around every kernel of subsequent executes (on the
  * execute's stream) so covgpu_plan_kernel_times can report per-kernel times. */
 int covgpu_plan_set_timing(covgpu_plan_t plan, int32_t enable);
@@ -116,7 +127,8 @@ int32_t covgpu_plan_kernel_names(covgpu_plan_t plan, char* buf, int32_t len);
  * [class_lo, class_hi) (a sub-range writes its slots of the COMPACT layout;
  * the full range may write DENSE / PACKED).  class_slot_offset: compact
  * offset of a plan class (class_index == #classes: total).  Requires the
- * complex128 tensor-core path (COVGPU_ECAPACITY otherwise). */
+ * spectral path or the complex128 tensor-core path (COVGPU_PATH_ROWBAND;
+ * COVGPU_ECAPACITY otherwise). */
 int64_t covgpu_plan_sums_elems(covgpu_plan_t plan);
 int covgpu_plan_execute_sums(covgpu_plan_t plan, const void* A_dev, void* sums_dev, int32_t part,
                              int32_t nparts, void* stream);

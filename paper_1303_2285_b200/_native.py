@@ -48,6 +48,7 @@ _SIGS = {
     "covgpu_plan_workspace_bytes": (_i64, [_vp]),
     "covgpu_plan_num_groups": (_i32, [_vp]),
     "covgpu_plan_launches": (_i32, [_vp]),
+    "covgpu_plan_path": (_i32, [_vp]),
     "covgpu_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
     "covgpu_plan_kernel_times": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), _i32]),
     "covgpu_plan_kernel_names": (_i32, [_vp, ctypes.c_char_p, _i32]),

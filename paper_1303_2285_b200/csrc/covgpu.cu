@@ -74,6 +74,11 @@ __global__ void k_warm(int* p) {
 }
 
 constexpr int kMaxCleanQ = 4096;
+// direct core-sum work (batch (2P-1) Q N M) from which the spectral path is
+// the default (below it the direct kernels' fewer launches win; measured on
+// B200)
+constexpr double kSpecMinWork = 1e8;  // per snapshot; cfg2 (3.3e7): direct 0.065 vs spectral 0.098 ms,
+                                      // cfg4 (3.9e6 x 1024): 1.21 vs 2.04 ms; cfg3 (5.3e8): 0.225 vs 0.124 ms
 
 }  // namespace
 
@@ -1079,11 +1084,23 @@ struct PlanKey {
   long long batch, n, m;
   int p, q;
   std::vector<int32_t> ids;
+  std::string env;  // the COVGPU_* path switches the plan was made under
   bool operator<(const PlanKey& o) const {
-    return std::tie(device, dtype, batch, n, m, p, q, ids) <
-           std::tie(o.device, o.dtype, o.batch, o.n, o.m, o.p, o.q, o.ids);
+    return std::tie(device, dtype, batch, n, m, p, q, ids, env) <
+           std::tie(o.device, o.dtype, o.batch, o.n, o.m, o.p, o.q, o.ids, o.env);
   }
 };
+
+std::string path_env() {
+  std::string e;
+  for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT"}) {
+    const char* v = getenv(k);
+    e += v ? v : "-";
+    e += ',';
+  }
+  return e;
+}
 
 std::mutex g_cache_mu;
 std::map<PlanKey, covgpu_plan*> g_cache;
@@ -1260,21 +1277,35 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     }
   }
   {
-    // spectral core sums: replaces the tensor-core core-sum kernel where its
-    // FFT length fits SMEM and the dr = 0 space-domain kernel covers Q
-    bool spec = pl->use_mma && q <= SPEC_D0_E * SPEC_D0_W;
-    int logL = 0;
+    // spectral core and edge sums (spectral.cuh): any dtype and class
+    // selection, Q <= 64 (the dr = 0 space-domain kernel), FFT lengths
+    // 2^6 .. 2^12 along rows (>= M) and columns (>= N), the walk finalize
+    // (P <= FINV_MAX_P); small problems stay on the direct kernels (fewer
+    // launches) unless COVGPU_SPECTRAL=1
+    bool spec = pl->clean && p >= 2 && q >= 2 && q <= SPEC_D0_E * SPEC_D0_W && p <= FINV_MAX_P;
+    int logL = 6, logLr = 6;
     while ((1LL << logL) < m) ++logL;
-    spec = spec && logL >= 6 && logL <= 12;  // instantiated FFT lengths
+    while ((1LL << logLr) < n) ++logLr;
+    spec = spec && logL <= 12 && logLr <= 12;
+    const double direct_work = (2.0 * p - 1) * q * (double)n * (double)m;  // per snapshot
+    // (class shards: every shard would repeat the FFTs and the correlation of
+    // all lags — the multi-GPU split for this path is row bands)
+    bool want = direct_work >= kSpecMinWork && class_ids == nullptr;
+    if (const char* fs = getenv("COVGPU_SPECTRAL")) want = want || atoi(fs) != 0;
+    spec = spec && want;
     if (const char* ns = getenv("COVGPU_NO_SPECTRAL")) spec = spec && atoi(ns) == 0;
     if (spec) {
       pl->use_spec = true;
+      pl->spec_edges = true;
+      pl->spec_logLr = logLr;
       pl->spec_logL = logL;
       pl->spec_L = 1 << logL;
       pl->spec_ngrp = (2 * p - 1 + SPEC_E - 1) / SPEC_E;
       pl->spec_nfb = (pl->spec_L + SPEC_CW * 32 - 1) / (SPEC_CW * 32);
-      // row segments: ~6 CTAs of 4 warps per SM, >= 4 windows of rows each
-      const long long per = batch * (long long)pl->spec_ngrp * pl->spec_nfb;
+      // row segments: ~6 CTAs of 4 warps per SM, >= 4 windows of rows each.
+      // Every split below is chosen per snapshot (not from the batch size), so a
+      // snapshot's sums run in the same order alone or in a batch (bitwise equal)
+      const long long per = (long long)pl->spec_ngrp * pl->spec_nfb;
       const long long rows = n - 2LL * p + 2 + SPEC_E;
       long long seg = std::max(1LL, (148LL * 6 + per - 1) / per);
       seg = std::min(seg, std::max(1LL, rows / (4LL * SPEC_E)));
@@ -1288,7 +1319,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       if (pl->spec_smem) {
         pl->spec_stages = (int)std::min<size_t>(4, SC_SMEM_BUDGET / (stb + 16));
         // row segments: whole waves of 1-CTA/SM blocks, >= 4 chunks per segment
-        const long long per2 = batch * (long long)pl->spec_lay.nfb;
+        const long long per2 = (long long)pl->spec_lay.nfb;
         const long long nch = (n + SC_RC - 1) / SC_RC;
         int best = 1;
         double best_eff = 0.0;
@@ -1303,9 +1334,9 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         pl->spec_nseg = best;
       }
       const long long d0rows = n - 2LL * p + 2;
-      pl->spec_nrb = (int)((d0rows + SPEC_D0_RB - 1) / SPEC_D0_RB);
+      pl->spec_nrb = (int)std::max(1LL, (d0rows + SPEC_D0_RB - 1) / SPEC_D0_RB);  // N = 2P-2: no core rows
       const long long nch = (m - q + 1 + SPEC_D0_CW - 1) / SPEC_D0_CW;
-      const long long d0per = batch * (long long)pl->spec_nrb;
+      const long long d0per = (long long)pl->spec_nrb;
       long long cpn = std::max(1LL, (148LL * 4 + d0per - 1) / d0per);
       pl->spec_ncp = (int)std::max(1LL, std::min(cpn, nch));
     }
@@ -1357,18 +1388,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->nseg = (int)std::min(seg, 16LL);
     }
   }
-  if (pl->use_spec) {
-    // edge sums in the frequency domain too: column FFTs of length >= N
-    int logLr = 0;
-    while ((1LL << logLr) < n) ++logLr;
-    bool se = logLr >= 6 && logLr <= 12 && p >= 2 && q >= 2;
-    if (const char* ne = getenv("COVGPU_NO_SPECTRAL_EDGES")) se = se && atoi(ne) == 0;
-    if (se) {
-      pl->spec_edges = true;
-      pl->spec_logLr = logLr;
-      pl->nseg = 1;  // RC' in one piece
-    }
-  }
+  if (pl->use_spec) pl->nseg = 1;  // RC' in one piece (k_spec_rc)
   const int nuc = (int)covgpu_num_classes(p, q);
   std::vector<char> sel(nuc, class_ids ? 0 : 1);
   if (class_ids) {
@@ -1581,6 +1601,19 @@ int32_t covgpu_plan_kernel_times(covgpu_plan_t pl, float* ms, int32_t max_n) {
   return n;
 }
 
+static bool rowband_ok(const covgpu_plan* pl) {
+  return pl->use_spec || (pl->use_mma && pl->use_ecm && pl->use_erm && pl->mma_kind != 0);
+}
+
+int32_t covgpu_plan_path(covgpu_plan_t pl) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  int32_t f = 0;
+  if (pl->use_spec) f |= COVGPU_PATH_SPECTRAL;
+  else if (pl->use_mma) f |= COVGPU_PATH_TENSOR;
+  if (rowband_ok(pl)) f |= COVGPU_PATH_ROWBAND;
+  return f;
+}
+
 int64_t covgpu_plan_sums_elems(covgpu_plan_t pl) {
   if (!pl) return -1;
   return pl->batch * ((long long)pl->nclasses + pl->tot_ccol + pl->tot_rc);
@@ -1591,10 +1624,10 @@ int covgpu_plan_execute_sums(covgpu_plan_t pl, const void* A_dev, void* sums_dev
   if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
   if (!A_dev || !sums_dev) return fail(COVGPU_EINVAL, "A and sums must be device pointers");
   if (nparts < 1 || part < 0 || part >= nparts) return fail(COVGPU_EINVAL, "part must be in [0, nparts)");
-  if (!(pl->use_mma && pl->use_ecm && pl->use_erm && pl->mma_kind != 0))
+  if (!rowband_ok(pl))
     return fail(COVGPU_ECAPACITY,
-                "row-band partial sums need the complex128 tensor-core path with tensor-core edge "
-                "kernels (all classes, P in [48, 65], Q in [50, 65])");
+                "row-band partial sums need the spectral path or the complex128 tensor-core path with "
+                "tensor-core edge kernels (all classes, P in [48, 65], Q in [50, 65])");
   CUDA_TRY(cudaSetDevice(pl->device));
   std::lock_guard<std::mutex> lk(pl->exec_mu);
   if ((uintptr_t)A_dev % 16 != 0) return fail(COVGPU_EINVAL, "A must be 16-byte aligned");
@@ -1602,7 +1635,9 @@ int covgpu_plan_execute_sums(covgpu_plan_t pl, const void* A_dev, void* sums_dev
   pl->ks_nparts = nparts;
   pl->ks_out = (double2*)sums_dev;
   pl->ks_failed = false;
-  int rc = launch_all<double>(pl, A_dev, nullptr, COVGPU_COMPACT, 1.0, (cudaStream_t)stream);
+  int rc = pl->dtype == COVGPU_C128
+               ? launch_all<double>(pl, A_dev, nullptr, COVGPU_COMPACT, 1.0, (cudaStream_t)stream)
+               : launch_all<float>(pl, A_dev, nullptr, COVGPU_COMPACT, 1.0, (cudaStream_t)stream);
   if (!rc && pl->ks_failed) rc = COVGPU_ECUDA;
   pl->ks_part = 0;
   pl->ks_nparts = 1;
@@ -1656,7 +1691,7 @@ int covgpu_plan_destroy(covgpu_plan_t pl) {
 
 static int cached_plan(covgpu_plan_t* out, int device, int64_t batch, int64_t n, int64_t m,
                        int32_t p, int32_t q, int32_t dtype, const int32_t* ids, int32_t nids) {
-  PlanKey key{device, dtype, batch, n, m, p, q, {}};
+  PlanKey key{device, dtype, batch, n, m, p, q, {}, path_env()};
   if (ids) key.ids.assign(ids, ids + nids);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   auto it = g_cache.find(key);

@@ -66,6 +66,24 @@ class Plan:
         _native.check(rc, "covgpu_plan_execute_host")
         return out_host
 
+    # ---- which sum kernels run (include/covgpu.h: covgpu_plan_path) ----
+    PATH_SPECTRAL, PATH_TENSOR, PATH_ROWBAND = 1, 2, 4
+
+    @property
+    def path(self) -> int:
+        f = int(self.lib.covgpu_plan_path(self.handle))
+        if f < 0:
+            _native.check(f, "covgpu_plan_path")
+        return f
+
+    @property
+    def spectral(self) -> bool:
+        return bool(self.path & self.PATH_SPECTRAL)
+
+    @property
+    def supports_rowband(self) -> bool:
+        return bool(self.path & self.PATH_ROWBAND)
+
     # ---- multi-GPU row bands (include/covgpu.h: covgpu_plan_execute_sums) ----
     def sums_elems(self) -> int:
         """complex128 values of the reduced-sums buffer [CC | CCol | RC']."""

@@ -76,8 +76,13 @@ def test_single_window_is_outer_product(cuda):
     np.testing.assert_allclose(cov.numpy(), np.outer(v, v.conj()), rtol=1e-12, atol=1e-12)
 
 
-def test_c4_sweep(cuda, golden):
-    """All 200 seeded instances of the reference's criterion 4 (N, M <= 24)."""
+@pytest.mark.parametrize("spectral", [False, True])
+def test_c4_sweep(cuda, golden, spectral, monkeypatch):
+    """All 200 seeded instances of the reference's criterion 4 (N, M <= 24);
+    spectral=True forces the frequency-domain sums wherever they apply
+    (COVGPU_SPECTRAL=1: P, Q >= 2, Q <= 64, clean shapes)."""
+    if spectral:
+        monkeypatch.setenv("COVGPU_SPECTRAL", "1")
     worst = 0.0
     for i, (n, m, p, q, seed) in enumerate(c4_instances()):
         a = ref_random(n, m, seed)
@@ -424,13 +429,16 @@ def test_capacity_guard(cuda):
         estimate_tensor(torch.zeros((1, 65536), dtype=torch.complex128, device=cuda), WindowSpec(1, 65536))
 
 
-def test_random_shapes_fuzz(cuda):
+@pytest.mark.parametrize("spectral", [False, True])
+def test_random_shapes_fuzz(cuda, spectral, monkeypatch):
     """60 seeded random shapes across every kernel path (clean / SAT, TMA /
     cp.async, small / large lag groups, batch 1-3, both dtypes) against the
     C oracle port."""
     from oracle import covoracle_c
 
-    rng = np.random.default_rng(20261020)
+    rng = np.random.default_rng(20261020 + (7 if spectral else 0))
+    if spectral:
+        monkeypatch.setenv("COVGPU_SPECTRAL", "1")
     worst = {np.complex128: 0.0, np.complex64: 0.0}
     for it in range(60):
         n = int(rng.integers(1, 160))
@@ -513,10 +521,10 @@ def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, spectr
     a = torch.as_tensor(rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m)),
                         device=cuda)
     win = WindowSpec(p, q)
-    if not spectral:
-        monkeypatch.setenv("COVGPU_NO_SPECTRAL", "1")
+    monkeypatch.setenv("COVGPU_SPECTRAL" if spectral else "COVGPU_NO_SPECTRAL", "1")
     plan = Plan(n, m, win, batch=batch, dtype=torch.complex128, device=cuda)
     monkeypatch.delenv("COVGPU_NO_SPECTRAL", raising=False)
+    monkeypatch.delenv("COVGPU_SPECTRAL", raising=False)
     plan.set_timing(True)
     got = plan.alloc_output()
     plan.execute(a, got)
@@ -584,10 +592,10 @@ def test_tensor_core_path_fuzz(cuda, monkeypatch):
         a = torch.as_tensor(rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m)),
                             device=cuda)
         spectral = it % 2 == 1  # odd draws: frequency-domain sums where Q <= 64
-        if not spectral:
-            monkeypatch.setenv("COVGPU_NO_SPECTRAL", "1")
+        monkeypatch.setenv("COVGPU_SPECTRAL" if spectral else "COVGPU_NO_SPECTRAL", "1")
         plan = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=torch.complex128, device=cuda)
         monkeypatch.delenv("COVGPU_NO_SPECTRAL", raising=False)
+        monkeypatch.delenv("COVGPU_SPECTRAL", raising=False)
         plan.set_timing(True)
         got = plan.alloc_output()
         plan.execute(a, got)
@@ -648,3 +656,42 @@ def test_row_band_sums_and_class_range_finalize(cuda):
     with pytest.raises(ValueError):
         small.execute_sums(a[:200, :240].contiguous(), small.alloc_sums(), 0, 2)
     small.close()
+
+
+@pytest.mark.parametrize("n,m,p,q,batch,dt", [
+    (30, 40, 16, 21, 1, np.complex128),     # N = 2P-2: no core rows (dr = 0 kernel all zeros)
+    (70, 62, 9, 32, 2, np.complex128),      # M = 2Q-2: no core columns beyond the edges
+    (65, 129, 2, 2, 1, np.complex128),      # smallest window, FFT lengths 128 / 256 (M, N + padding)
+    (200, 300, 40, 64, 1, np.complex128),   # Q = 64: the dr = 0 kernel's full 4 warps
+    (257, 513, 70, 33, 1, np.complex128),   # P > 64: the L2-fed correlation kernel (9 lag groups)
+    (128, 128, 8, 16, 5, np.complex64),     # cfg4 shape, complex64 inputs (FP64 spectral arithmetic)
+    (100, 77, 12, 20, 3, np.complex64),
+])
+def test_spectral_path_vs_oracle(cuda, n, m, p, q, batch, dt, monkeypatch):
+    """The frequency-domain sums (spectral.cuh) forced on small and ragged
+    shapes against the C oracle; dense R exactly Hermitian."""
+    from oracle import covoracle_c
+    from paper_1303_2285_b200.plan import Plan
+
+    monkeypatch.setenv("COVGPU_SPECTRAL", "1")
+    rng = np.random.default_rng(n * 31 + m * 7 + p + q)
+    stack = (rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m))).astype(dt)
+    tdt = torch.complex128 if dt == np.complex128 else torch.complex64
+    plan = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=tdt, device=cuda)
+    assert plan.spectral and plan.supports_rowband
+    out = plan.alloc_output()
+    plan.execute(torch.as_tensor(stack, device=cuda), out)
+    got = out.reshape(batch, p * q, p * q).cpu().numpy()
+    plan.close()
+    if batch > 1:  # a snapshot's sums run in the same order alone and in a batch
+        single = Plan(n, m, WindowSpec(p, q), batch=1, dtype=tdt, device=cuda)
+        o1 = single.alloc_output()
+        single.execute(torch.as_tensor(stack[batch - 1:], device=cuda), o1)
+        assert np.array_equal(o1.reshape(p * q, p * q).cpu().numpy(), got[batch - 1])
+        single.close()
+    k = (n - p + 1) * (m - q + 1)
+    for b in range(batch):
+        assert_hermitian(got[b])
+        ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), p, q) / k
+        err = co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref)
+        assert err <= (TOL64 if dt == np.complex128 else TOL32), (b, err)

@@ -41,7 +41,7 @@ for name in sys.argv[1:] or ["cfg3", "cfg5"]:
     d = r_sp - r_ref
     relf = (torch.linalg.norm(d) / torch.linalg.norm(r_ref)).item()
     pq = w.p * w.q
-    R1, R2 = r_ref.view(pq, pq), r_sp.view(pq, pq)
+    R1, R2 = r_ref.view(-1, pq, pq)[0], r_sp.view(-1, pq, pq)[0]
     # per-diagonal (d = dc*P + dr) worst relative error of the diagonal's entries
     worst = 0.0
     for dd in range(0, pq, max(1, pq // 64)):
