@@ -197,6 +197,7 @@ struct covgpu_plan {
   // side stream for the edge-row / corner kernels (overlap with the bulk)
   cudaStream_t side_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_d0 = nullptr;  // spectral: dr = 0 sums (side stream) done
   // end-to-end host path: cached stream and device buffers
   cudaStream_t host_stream = nullptr;
   void* hA = nullptr;
@@ -278,6 +279,7 @@ void plan_free(covgpu_plan* pl) {
   if (pl->side_stream) cudaStreamDestroy(pl->side_stream);
   if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
   if (pl->ev_join) cudaEventDestroy(pl->ev_join);
+  if (pl->ev_d0) cudaEventDestroy(pl->ev_d0);
   cudaFree(pl->hA);
   cudaFree(pl->hR);
   cudaFree(pl->d_cls);
@@ -666,7 +668,7 @@ struct SpecK {
 // the one CC partial per class (npart = 1); with spec_edges also the
 // edge-column sums CCol and edge-row sums RC' (one segment)
 template <typename T>
-void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st,
+void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st, cudaStream_t es,
                      const std::function<void(const char*)>& mark) {
   const Problem& pr = pl->pr;
   const long long B = pl->batch;
@@ -675,8 +677,13 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   const int ra = rows_lo + (int)((long long)nrows * part / nparts);
   const int rz = rows_lo + (int)((long long)nrows * (part + 1) / nparts) - 1;
   const int S = pr.P - 1, S1 = pr.Q - 1;
-  k_spec_dr0<T><<<(unsigned)(B * pl->spec_nrb * pl->spec_ncp), SPEC_D0_W * 32, SPEC_D0_SMEM, st>>>(
+  // side stream (es): the dr = 0 sums and the edge-column sums depend only on
+  // A; main stream: row spectra -> correlation -> output FFT -> edge rows
+  k_spec_dr0<T><<<(unsigned)(B * pl->spec_nrb * pl->spec_ncp), SPEC_D0_W * 32, SPEC_D0_SMEM, es>>>(
       A, pr, ra, rz, pl->spec_nrb, pl->spec_ncp, pl->d_d0p);
+  if (es != st) {
+    cudaEventRecord(pl->ev_d0, es);
+  }
   mark("spec_dr0");
   SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
             pl->d_fy);
@@ -717,13 +724,19 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
         pl->d_gp);
   }
   mark("spec_corr");
+  if (es != st) cudaStreamWaitEvent(st, pl->ev_d0, 0);  // the output FFT kernel also sums the dr = 0 partials
   SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp,
             pl->d_tw, pr, pl->spec_nseg, pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
   if (pl->spec_edges) {
     mark("spec_dft");
-    SPEC_LOGL(pl->spec_logLr, SpecK<T>::template colfft, B * 2 * 4 * S1, A, pr, pl->d_twr, pl->d_fc);
-    SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * 2 * (long long)S1 * S1, pl->d_fc, pr, pl->d_twr,
-              pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+    {
+      cudaStream_t st_main = st;
+      st = es;  // SPEC_LOGL launches on `st`
+      SPEC_LOGL(pl->spec_logLr, SpecK<T>::template colfft, B * 2 * 4 * S1, A, pr, pl->d_twr, pl->d_fc);
+      SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * 2 * (long long)S1 * S1, pl->d_fc, pr,
+                pl->d_twr, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+      st = st_main;
+    }
     mark("spec_ccol");
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
               pl->spec_lay, pl->d_tw,
@@ -882,7 +895,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   bool mma = false;
   if (pl->use_spec) {
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
-    launch_spectral<T>(pl, A, st, mark);
+    launch_spectral<T>(pl, A, st, es, mark);
     launches += pl->spec_edges ? 7 : 3;
     mma = true;
   }
@@ -1546,7 +1559,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&pl->side_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&pl->ev_d0, cudaEventDisableTiming) != cudaSuccess) {
       plan_free(pl.get());
       return fail(COVGPU_ECUDA, "side stream");
     }
