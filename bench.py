@@ -9,13 +9,18 @@ A step = one full estimate of R for the configured workload (default cfg5:
 GPU).  `value` is dense R entries per second with A resident in HBM; every
 step is bracketed by a barrier and device syncs, timed with CUDA events on the
 launch stream, and L2 is flushed (256 MiB write) between steps.  Under
-torchrun the offset classes are sharded across ranks (strong scaling: total
-work fixed), A is broadcast from rank 0 inside the timed region over NCCL,
-and the time is the max over ranks.
+torchrun the sums are split into row bands (spectral / tensor-core plans:
+one all-reduce of the per-band sums, class-range finalize) or the offset
+classes are sharded (strong scaling: total work fixed), A is broadcast from
+rank 0 inside the timed region over NCCL, and the time is the max over ranks.
 
-Extra keys: `roofline` (bulk kernel = the dominant one: algorithmic FP64/FP32
-flops per launch / its CUDA-event duration, against the FMA peak measured on
-this GPU right before the run), `cpu_baseline` (the oracle's multithreaded
+Extra keys: `kernel_ms` / `kernel_roofline` (every kernel's CUDA-event time
+and its own roofline: FP64 kernels against the DFMA / DMMA loop probes
+measured on this GPU right before the run, memory-bound kernels against
+MEASURED_PEAKS.json's HBM figure, each with its algorithmic flops or bytes),
+`roofline` (the dominant kernel's entry), `tensor_core_path` /
+`cuda_core_path` (the same workload on the other two sum engines),
+`cpu_baseline` (the oracle's multithreaded
 C port of the reference's class kernel on this host's cores, bounded sample,
 extrapolated by product count), `e2e` (same metric through the C ABI with
 pinned HOST buffers: H2D of A + compute + D2H of the packed triangle, wall
