@@ -724,6 +724,10 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
         pl->d_gp);
   }
   mark("spec_corr");
+  if (pl->spec_nseg > 1) {  // row-segment partials -> segment 0, in order
+    const long long per_seg = (long long)(2 * pr.P - 1) * L, tot = B * per_seg;
+    k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, pl->spec_nseg, per_seg, tot);
+  }
   if (es != st) cudaStreamWaitEvent(st, pl->ev_d0, 0);  // the output FFT kernel also sums the dr = 0 partials
   SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp,
             pl->d_tw, pr, pl->spec_nseg, pl->nclasses, pl->d_cls_slot, pl->d_ccpart);

@@ -148,8 +148,23 @@ __device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict
     if (i < T) {
       const int k = i & (P0 - 1);
       if (k) {
+        // w^(rk) for r = 1..R-1 from at most two table reads (w^k, w^4k) and
+        // products of depth <= 2: fewer L1 wavefronts (the FFT kernels are
+        // LSU-bound), twiddle error <= ~3 ulp
+        double2 w[R];
+        w[1] = twp[k];
+        if constexpr (R >= 4) {
+          w[2] = cmul(w[1], w[1]);
+          w[3] = cmul(w[2], w[1]);
+        }
+        if constexpr (R == 8) {
+          w[4] = twp[3 * P0 + k];
+          w[5] = cmul(w[4], w[1]);
+          w[6] = cmul(w[4], w[2]);
+          w[7] = cmul(w[4], w[3]);
+        }
 #pragma unroll
-        for (int r = 1; r < R; ++r) u[it][r] = cmul(u[it][r], twp[(r - 1) * P0 + k]);
+        for (int r = 1; r < R; ++r) u[it][r] = cmul(u[it][r], w[r]);
       }
       dft_small<R>(u[it]);
       const int j = i * R - k * (R - 1);
@@ -756,8 +771,29 @@ __global__ void __launch_bounds__(SPEC_D0_W * 32)
   }
 }
 
+// G partials of the row segments summed in order into segment 0 (one thread
+// per (b, dr, f): the output FFT below then reads one value per frequency)
+__global__ void __launch_bounds__(256)
+    k_spec_gsum(double2* __restrict__ Gp, int nseg, long long per_seg, long long total) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const long long b = t / per_seg, e = t % per_seg;
+  double2* g = Gp + b * nseg * per_seg + e;
+  double2 v[8];
+  double2 s = g[0];
+  int sg = 1;
+  for (; sg + 8 <= nseg; sg += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = g[(sg + j) * per_seg];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = cadd(s, v[j]);
+  }
+  for (; sg < nseg; ++sg) s = cadd(s, g[sg * per_seg]);
+  g[0] = s;
+}
+
 // CC(dr, dc) = (1/L) sum_f G(dr, f) w^(f dc) for dr != 0: one forward FFT of
-// G(dr, .) (summed over the row segments in order) per row lag, outputs
+// G(dr, .) (segment 0 after k_spec_gsum) per row lag, outputs
 // dc in [0, Q); for dr = 0 the ordered sum of the space-domain partials.
 // CTA = (snapshot b, row lag dr).  Writes the classes' CC slot (one partial:
 // npart = 1 for the finalize).
@@ -774,24 +810,42 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const long long b = blockIdx.x / nlag;
   const int dr = li - (P - 1);
   if (dr == 0) {
-    for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
+    // ordered sum of the nd0 space-domain partials per dc: thread = (dc, chunk
+    // of the partials), chunks combined in order through SMEM
+    const int nch = max(1, (int)blockDim.x / Q);
+    for (int dc0 = 0; dc0 < Q; dc0 += blockDim.x) {
+      const int dc = dc0 + (int)threadIdx.x % Q, ch = (int)threadIdx.x / Q;
       double2 s = make_double2(0.0, 0.0);
-      const double2* p = D0p + b * (long long)nd0 * Q + dc;
-      for (int k = 0; k < nd0; ++k) s = cadd(s, p[(long long)k * Q]);
-      const int cid = cls_slot[class_index(0, dc, P, Q)];
-      if (cid >= 0) ccpart[b * nclasses + cid] = s;
+      if (dc < Q && ch < nch) {
+        const int k0 = (int)((long long)nd0 * ch / nch), k1 = (int)((long long)nd0 * (ch + 1) / nch);
+        const double2* p = D0p + b * (long long)nd0 * Q + dc;
+        int k = k0;
+        for (; k + 8 <= k1; k += 8) {
+          double2 v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = p[(long long)(k + j) * Q];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s = cadd(s, v[j]);
+        }
+        for (; k < k1; ++k) s = cadd(s, p[(long long)k * Q]);
+      }
+      if (ch < nch && dc < Q) sbuf[threadIdx.x] = s;
+      __syncthreads();
+      if (ch == 0 && dc < Q) {
+        double2 t = sbuf[threadIdx.x];
+        for (int c = 1; c < nch; ++c) t = cadd(t, sbuf[threadIdx.x + c * Q]);
+        const int cid = cls_slot[class_index(0, dc, P, Q)];
+        if (cid >= 0) ccpart[b * nclasses + cid] = t;
+      }
+      __syncthreads();
+      if (Q <= (int)blockDim.x) break;
     }
     return;
   }
   const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
-  const long long sstride = (long long)nlag * L;
   spec_fft_block<LOGL>(
       sbuf, tw,
-      [&](int idx) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int sg = 0; sg < nseg; ++sg) s = cadd(s, g[sg * sstride + idx]);
-        return s;
-      },
+      [&](int idx) { return g[idx]; },  // segment 0 holds the ordered sum (k_spec_gsum)
       [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
   __syncthreads();
   const double inv = 1.0 / (double)L;
