@@ -119,7 +119,7 @@ struct covgpu_plan {
   // per-frequency row-lag correlation, output DFT; dr = 0 in the space domain
   bool use_spec = false;
   int spec_logL = 0, spec_L = 0, spec_nseg = 1, spec_nfb = 1, spec_ngrp = 1;
-  int spec_nrb = 0, spec_ncp = 1;
+  int spec_nd0 = 0;  // dr = 0 per-row partials (core rows)
   double2 *d_tw = nullptr, *d_fx = nullptr, *d_fy = nullptr, *d_gp = nullptr, *d_d0p = nullptr;
   SpecLayout spec_lay{};
   bool spec_smem = false;  // k_spec_corr_smem (P <= 64) instead of the L2-fed k_spec_corr
@@ -454,11 +454,6 @@ cudaError_t set_attrs() {
     if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
       e = r;
-    for (const void* fn : {(const void*)k_spec_dr0<double>, (const void*)k_spec_dr0<float>,
-                          })
-      if ((r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)) !=
-          cudaSuccess)
-        e = r;
     return e;
   }();
   return once;
@@ -662,6 +657,8 @@ struct SpecK {
   static auto ccol() { return &k_spec_ccol<LG>; }
   template <int LG>
   static auto rc() { return &k_spec_rc<LG>; }
+  template <int LG>
+  static auto rowac() { return &k_spec_rowac<LG>; }
 };
 
 // spectral core sums (spectral.cuh) for band ks_part of ks_nparts: writes
@@ -677,20 +674,21 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   const int ra = rows_lo + (int)((long long)nrows * part / nparts);
   const int rz = rows_lo + (int)((long long)nrows * (part + 1) / nparts) - 1;
   const int S = pr.P - 1, S1 = pr.Q - 1;
-  // side stream (es): the dr = 0 sums and the edge-column sums depend only on
-  // A; main stream: row spectra -> correlation -> output FFT -> edge rows
-  k_spec_dr0<T><<<(unsigned)(B * pl->spec_nrb * pl->spec_ncp), SPEC_D0_W * 32, SPEC_D0_SMEM, es>>>(
-      A, pr, ra, rz, pl->spec_nrb, pl->spec_ncp, pl->d_d0p);
-  if (es != st) {
-    cudaEventRecord(pl->ev_d0, es);
-  }
-  mark("spec_dr0");
+  // side stream (es): the edge-column sums depend only on A; main stream:
+  // row spectra -> dr = 0 per-row transforms, correlation -> output FFT ->
+  // edge rows
   SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
             pl->d_fy);
   if (pl->spec_edges)
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
               pl->d_fy0);
   mark("spec_fft");
+  if (rz >= ra)
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr, pl->spec_lay,
+              pl->d_tw, ra, rz - ra + 1, rz - ra + 1, pl->d_d0p);
+  k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
+                                                     pl->d_cls_slot, pl->d_ccpart);
+  mark("spec_rowac");
   if (pl->spec_smem) {
     const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
     const unsigned blocks = (unsigned)(B * pl->spec_lay.nfb * pl->spec_nseg);
@@ -728,8 +726,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     const long long per_seg = (long long)(2 * pr.P - 1) * L, tot = B * per_seg;
     k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, pl->spec_nseg, per_seg, tot);
   }
-  if (es != st) cudaStreamWaitEvent(st, pl->ev_d0, 0);  // the output FFT kernel also sums the dr = 0 partials
-  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, pl->spec_nrb * pl->spec_ncp,
+  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, std::max(0, rz - ra + 1),
             pl->d_tw, pr, pl->spec_nseg, pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
   if (pl->spec_edges) {
     mark("spec_dft");
@@ -900,7 +897,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->use_spec) {
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
     launch_spectral<T>(pl, A, st, es, mark);
-    launches += pl->spec_edges ? 7 : 3;
+    launches += 8;  // rowac, fft x2, corr, gsum, dft, colfft, ccol, rc
     mma = true;
   }
   if constexpr (sizeof(T) == 8) {
@@ -1299,7 +1296,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     // 2^6 .. 2^12 along rows (>= M) and columns (>= N), the walk finalize
     // (P <= FINV_MAX_P); small problems stay on the direct kernels (fewer
     // launches) unless COVGPU_SPECTRAL=1
-    bool spec = pl->clean && p >= 2 && q >= 2 && q <= SPEC_D0_E * SPEC_D0_W && p <= FINV_MAX_P;
+    bool spec = pl->clean && p >= 2 && q >= 2 && q <= SPEC_MAX_Q && p <= FINV_MAX_P;
     int logL = 6, logLr = 6;
     while ((1LL << logL) < m) ++logL;
     while ((1LL << logLr) < n) ++logLr;
@@ -1351,11 +1348,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         pl->spec_nseg = best;
       }
       const long long d0rows = n - 2LL * p + 2;
-      pl->spec_nrb = (int)std::max(1LL, (d0rows + SPEC_D0_RB - 1) / SPEC_D0_RB);  // N = 2P-2: no core rows
-      const long long nch = (m - q + 1 + SPEC_D0_CW - 1) / SPEC_D0_CW;
-      const long long d0per = (long long)pl->spec_nrb;
-      long long cpn = std::max(1LL, (148LL * 4 + d0per - 1) / d0per);
-      pl->spec_ncp = (int)std::max(1LL, std::min(cpn, nch));
+      pl->spec_nd0 = (int)std::max(1LL, d0rows);  // N = 2P-2: no core rows
     }
   }
   pl->S = p - 1;
@@ -1476,7 +1469,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     if ((rc = dalloc(&pl->d_tw, L, &ws)) || (rc = dalloc(&pl->d_fx, fxe, &ws)) ||
         (rc = dalloc(&pl->d_fy, fxe, &ws)) ||
         (rc = dalloc(&pl->d_gp, (size_t)batch * pl->spec_nseg * (2 * p - 1) * L, &ws)) ||
-        (rc = dalloc(&pl->d_d0p, (size_t)batch * pl->spec_nrb * pl->spec_ncp * q, &ws))) {
+        (rc = dalloc(&pl->d_d0p, (size_t)batch * pl->spec_nd0 * q, &ws))) {
       plan_free(pl.get());
       return rc;
     }

@@ -22,8 +22,8 @@
 // Accuracy: the FFT rounds at ~eps log2(L) of the row energy.  For dr != 0
 // the sum over r2 is incoherent and CC keeps ~1e-14 relative accuracy on
 // white noise; for dr = 0 the terms X_r conj(Y_r) are coherent (|X_r|^2 for
-// the shared columns), so the dr = 0 classes — Q of them, 1/(2P-1) of the
-// core products — are summed directly in the space domain (k_spec_dr0).
+// the shared columns), so the dr = 0 classes are transformed row by row and
+// summed over rows in the space domain (k_spec_rowac).
 // Every sum runs in a fixed order: results are bitwise reproducible.
 #pragma once
 
@@ -33,13 +33,7 @@ namespace covgpu {
 
 constexpr int SPEC_E = 16;        // row lags per k_spec_corr thread
 constexpr int SPEC_CW = 4;        // warps (32-frequency columns) per k_spec_corr CTA
-constexpr int SPEC_D0_E = 16;     // column lags per k_spec_dr0 warp
-constexpr int SPEC_D0_W = 4;      // warps per k_spec_dr0 CTA (lag groups)
-constexpr int SPEC_D0_RB = 32;    // rows per k_spec_dr0 CTA (one per lane)
-constexpr int SPEC_D0_CW = 32;    // columns per k_spec_dr0 chunk
-constexpr int SPEC_D0_PITCH = SPEC_D0_CW + SPEC_D0_E * SPEC_D0_W;  // 96 -> +1 below (odd)
-constexpr int SPEC_D0_TP = SPEC_D0_PITCH + 1;  // odd pitch in 16-byte units: conflict-free LDS.128
-constexpr size_t SPEC_D0_SMEM = 2 * sizeof(double2) * SPEC_D0_RB * SPEC_D0_TP;
+constexpr int SPEC_MAX_Q = 512;   // edge-column pairs grow as Q^2
 
 template <typename C2>
 __device__ __forceinline__ double2 widen2(C2 v) {
@@ -665,109 +659,69 @@ __global__ void __launch_bounds__(NG * 32, 1)
   }
 }
 
-// dr = 0 core sums in the space domain (Q <= 64):
-//     CC(0, dc) = sum_{r in [P-1, N-P]} sum_{c <= M-Q, c+dc >= Q-1} A[r,c] conj(A[r,c+dc]).
-// CTA = (snapshot b, block of 32 rows, column part cp): lane = row, warp w =
-// column lags [16w, 16w+16); chunks of 32 first-element columns plus the
-// 63-column lag halo are staged in SMEM by cp.async (double buffer, odd row
-// pitch: the 32 lanes' LDS.128 hit distinct banks), and each thread walks its
-// row with the 16 second elements in a rotating register window (2 LDS per
-// 16 complex MACs).  Partials per (row block, column part) are summed in a
-// fixed order by k_spec_dft.
-template <typename T>
-__global__ void __launch_bounds__(SPEC_D0_W * 32)
-    k_spec_dr0(const typename CT<T>::c* __restrict__ A, Problem pr, int row_a, int row_z, int nrb, int ncp,
-               double2* __restrict__ D0p) {
-  using C2 = typename CT<T>::c;
-  constexpr int E = SPEC_D0_E, TP = SPEC_D0_TP, CW = SPEC_D0_CW, TW = SPEC_D0_PITCH;
-  extern __shared__ __align__(16) unsigned char d0raw[];
-  C2* tile = reinterpret_cast<C2*>(d0raw);
-  long long t = blockIdx.x;
-  const int cp = (int)(t % ncp);
-  t /= ncp;
-  const int rb = (int)(t % nrb);
-  const long long b = t / nrb;
-  const int N = pr.N, M = pr.M, Q = pr.Q;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r0 = row_a + rb * SPEC_D0_RB;
-  const int xcols = M - Q + 1;
-  const int nch_all = (xcols + CW - 1) / CW;
-  const int ch_a = (int)((long long)nch_all * cp / ncp), ch_z = (int)((long long)nch_all * (cp + 1) / ncp);
-  const int dc0 = w * E;  // first column lag of this warp
-  const C2* Ab = A + b * N * (long long)M;
-  auto load = [&](int ch, int buf) {
-    const int cc = ch * CW;  // tile column 0 = A column cc
-    C2* dst = tile + buf * SPEC_D0_RB * TP;
-    for (int i = threadIdx.x; i < SPEC_D0_RB * TW; i += blockDim.x) {
-      const int rr = i / TW, cq = i % TW;
-      const int r = r0 + rr, c = cc + cq;
-      const bool ok = r <= row_z && c < M;
-      cp_async_elem<sizeof(C2)>(dst + rr * TP + cq, ok ? Ab + (long long)r * M + c : Ab, ok);
-    }
-    cp_async_commit();
-  };
-  double ar[E], ai[E], yr[E], yi[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) ar[e] = ai[e] = yr[e] = yi[e] = 0.0;
-  const bool live = r0 <= row_z && ch_a < ch_z;
-  const bool active = dc0 < Q;
-  if (live) load(ch_a, 0);
-  for (int ch = ch_a; live && ch < ch_z; ++ch) {
-    const int buf = (ch - ch_a) & 1;
-    if (ch + 1 < ch_z) {
-      load(ch + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (active) {
-      const C2* row = tile + buf * SPEC_D0_RB * TP + lane * TP;
-      const int c0 = ch * CW;
-      const int ncols = min(CW, xcols - c0);
-      // x column c0 + j at tile column j; y column c0 + j + dc0 + e at tile column j + dc0 + e
-#pragma unroll
-      for (int e = 0; e < E - 1; ++e) {
-        const double2 v = c0 + dc0 + e >= Q - 1 ? widen2(row[dc0 + e]) : make_double2(0.0, 0.0);
-        yr[e] = v.x;
-        yi[e] = v.y;
-      }
-      if (ncols == CW && c0 >= Q - 1) {
-#pragma unroll
-        for (int t0 = 0; t0 < CW; t0 += E) {
-#pragma unroll
-          for (int tt = 0; tt < E; ++tt) {
-            const double2 yn = widen2(row[t0 + tt + dc0 + E - 1]);
-            const double2 x = widen2(row[t0 + tt]);
-            yr[(tt + E - 1) % E] = yn.x;
-            yi[(tt + E - 1) % E] = yn.y;
-            cmac_all<double, E>(tt, x, yr, yi, ar, ai);
-          }
-        }
-      } else {
-        for (int t0 = 0; t0 < CW; t0 += E) {
-#pragma unroll
-          for (int tt = 0; tt < E; ++tt) {
-            const int j = t0 + tt;
-            const int col = c0 + j + dc0 + E - 1;
-            const double2 yn = col >= Q - 1 ? widen2(row[j + dc0 + E - 1]) : make_double2(0.0, 0.0);
-            const double2 x = j < ncols ? widen2(row[j]) : make_double2(0.0, 0.0);
-            yr[(tt + E - 1) % E] = yn.x;
-            yi[(tt + E - 1) % E] = yn.y;
-            cmac_all<double, E>(tt, x, yr, yi, ar, ai);
-          }
-        }
-      }
-    }
+// dr = 0 core sums, one row at a time: for each core row r (both elements
+// on row r),
+//     CC_r(0, dc) = (1/L) sum_f X_r[f] conj(Y_r[f]) w^(f dc),   dc < Q,
+// one FFT per row; the rows are then added in the space domain (k_spec_dft,
+// in order).  Summing X_r conj(Y_r) over the rows first (as G does for
+// dr != 0) would add the rows' |X_r|^2 coherently and leave ~1e-12 relative
+// error at dc > 0 (numpy, cfg5); per row the error is ~eps log L of the row
+// energy and adds incoherently over rows (~1e-15 relative, numpy, cfg5).
+// CTA = (b, row r of the band [row_a, row_a + nrows)).
+template <int LOGL>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
+    k_spec_rowac(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay,
+                 const double2* __restrict__ tw, int row_a, int nrows, int nd0, double2* __restrict__ D0p) {
+  extern __shared__ double2 sbuf[];
+  constexpr int L = 1 << LOGL;
+  const int Q = pr.Q;
+  const int k = (int)(blockIdx.x % nrows);
+  const long long b = blockIdx.x / nrows;
+  const int r = row_a + k;
+  const double2* fx = FX + lay.at(b, r, 0);
+  const double2* fy = FY + lay.at(b, r, 0);
+  const long long fs = (long long)lay.np * 32;
+  spec_fft_block<LOGL>(
+      sbuf, tw,
+      [&](int idx) {
+        const long long o = (idx >> 5) * fs + (idx & 31);
+        const double2 x = fx[o], y = fy[o];
+        return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
+      },
+      [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
+  __syncthreads();
+  const double inv = 1.0 / (double)L;
+  double2* out = D0p + (b * nd0 + k) * (long long)Q;
+  for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
+    const double2 v = sbuf[fpad(dc)];
+    out[dc] = make_double2(v.x * inv, v.y * inv);
+  }
+}
+
+// CC(0, dc) = sum over the band's core rows of the per-row transforms
+// (k_spec_rowac): CTA = (b, dc), thread = a contiguous run of rows summed in
+// order, then a fixed-shape tree over the threads — deterministic.
+__global__ void __launch_bounds__(256)
+    k_spec_d0sum(const double2* __restrict__ D0p, int nd0, Problem pr, int nclasses,
+                 const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+  __shared__ double2 red[256];
+  const int Q = pr.Q;
+  const int dc = (int)(blockIdx.x % Q);
+  const long long b = blockIdx.x / Q;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int k0 = (int)((long long)nd0 * t / nt), k1 = (int)((long long)nd0 * (t + 1) / nt);
+  const double2* p = D0p + b * (long long)nd0 * Q + dc;
+  double2 s = make_double2(0.0, 0.0);
+  for (int k = k0; k < k1; ++k) s = cadd(s, p[(long long)k * Q]);
+  red[t] = s;
+  __syncthreads();
+  for (int h = nt / 2; h > 0; h >>= 1) {
+    if (t < h) red[t] = cadd(red[t], red[t + h]);
     __syncthreads();
   }
-  if (!active) return;
-  // rows past row_z and lags past Q-1 hold exact zeros; fixed-order lane sums
-  double2* out = D0p + (b * nrb + rb) * (long long)ncp * Q + (long long)cp * Q;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const double2 s = warp_sum(make_double2(ar[e], ai[e]));
-    if (lane == 0 && dc0 + e < Q) out[dc0 + e] = s;
+  if (t == 0) {
+    const int cid = cls_slot[class_index(0, dc, pr.P, Q)];
+    if (cid >= 0) ccpart[b * nclasses + cid] = red[0];
   }
 }
 
@@ -809,39 +763,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const int li = (int)(blockIdx.x % nlag);
   const long long b = blockIdx.x / nlag;
   const int dr = li - (P - 1);
-  if (dr == 0) {
-    // ordered sum of the nd0 space-domain partials per dc: thread = (dc, chunk
-    // of the partials), chunks combined in order through SMEM
-    const int nch = max(1, (int)blockDim.x / Q);
-    for (int dc0 = 0; dc0 < Q; dc0 += blockDim.x) {
-      const int dc = dc0 + (int)threadIdx.x % Q, ch = (int)threadIdx.x / Q;
-      double2 s = make_double2(0.0, 0.0);
-      if (dc < Q && ch < nch) {
-        const int k0 = (int)((long long)nd0 * ch / nch), k1 = (int)((long long)nd0 * (ch + 1) / nch);
-        const double2* p = D0p + b * (long long)nd0 * Q + dc;
-        int k = k0;
-        for (; k + 8 <= k1; k += 8) {
-          double2 v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = p[(long long)(k + j) * Q];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) s = cadd(s, v[j]);
-        }
-        for (; k < k1; ++k) s = cadd(s, p[(long long)k * Q]);
-      }
-      if (ch < nch && dc < Q) sbuf[threadIdx.x] = s;
-      __syncthreads();
-      if (ch == 0 && dc < Q) {
-        double2 t = sbuf[threadIdx.x];
-        for (int c = 1; c < nch; ++c) t = cadd(t, sbuf[threadIdx.x + c * Q]);
-        const int cid = cls_slot[class_index(0, dc, P, Q)];
-        if (cid >= 0) ccpart[b * nclasses + cid] = t;
-      }
-      __syncthreads();
-      if (Q <= (int)blockDim.x) break;
-    }
-    return;
-  }
+  if (dr == 0) return;  // k_spec_d0sum
   const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
   spec_fft_block<LOGL>(
       sbuf, tw,

@@ -512,7 +512,7 @@ def test_pipelined_host_path_bitwise(cuda):
 @pytest.mark.parametrize("spectral", [False, True])
 def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, spectral, monkeypatch):
     """complex128 core sums on the FP64 tensor cores (k_bulk_dmma) or in the
-    frequency domain (spectral.cuh, Q <= 64) against the Gram cross-check and
+    frequency domain (spectral.cuh) against the Gram cross-check and
     against the CUDA-core bulk kernel of the same shape."""
     from oracle.gpu_naive import covariance_gram
     from paper_1303_2285_b200.plan import Plan
@@ -530,8 +530,8 @@ def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, spectr
     plan.execute(a, got)
     got = got.reshape(batch, p * q, p * q)
     names = plan.kernel_names()
-    assert ("spec_dft" in names) == (spectral and q <= 64), names
-    assert ("bulk_dmma" in names) == (not spectral or q > 64), names
+    assert ("spec_dft" in names) == spectral, names
+    assert ("bulk_dmma" in names) == (not spectral), names
     plan.close()
     monkeypatch.setenv("COVGPU_NO_MMA", "1")
     plan2 = Plan(n, m, win, batch=batch, dtype=torch.complex128, device=cuda)
@@ -600,7 +600,7 @@ def test_tensor_core_path_fuzz(cuda, monkeypatch):
         got = plan.alloc_output()
         plan.execute(a, got)
         names = plan.kernel_names()
-        if spectral and q <= 64:
+        if spectral:
             assert "spec_corr" in names and "spec_rc" in names, (it, n, m, p, q, names)
         else:
             assert "bulk_dmma" in names, (it, n, m, p, q, names)
