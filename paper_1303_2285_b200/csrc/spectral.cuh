@@ -307,30 +307,31 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const bool mine = ((long long)c1 * S1 + e) % nparts == part;
   const double2* fx = FC + (((b * 2 + side) * 4 + 2 * sign) * S1 + c1) * (long long)L;
   const double2* fy = FC + (((b * 2 + side) * 4 + 2 * sign + 1) * S1 + e) * (long long)L;
+  const double inv = 1.0 / (double)L;
+  // CCol of class (dr, dc) at strip column c1 (zero where this part does not own the pair)
+  auto emit = [&](int dr, double2 v) {
+    if (!in_uc(dr, dc, P, Q)) return;
+    const int cid = cls_slot[class_index(dr, dc, P, Q)];
+    if (cid < 0) return;
+    const ClassDesc& cd = cls[cid];
+    const long long o = side ? (long long)(cd.qu - 1) + c1 : c1;
+    ccol[b * tot_ccol + cd.ccol_off + o] = v;
+  };
   if (mine) {
+    // the last pass hands over the natural-order outputs: only the P row lags
+    // of this sign are kept, stored straight to CCol (no SMEM round trip)
     spec_fft_block<LOGL>(
         sbuf, tw,
         [&](int idx) {
           const double2 x = fx[idx], y = fy[idx];
           return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
         },
-        [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
-    __syncthreads();
-  }
-  const double inv = 1.0 / (double)L;
-  for (int k = threadIdx.x; k < P; k += blockDim.x) {
-    const int dr = sign ? -(k + 1) : k;
-    if (!in_uc(dr, dc, P, Q)) continue;
-    const int cid = cls_slot[class_index(dr, dc, P, Q)];
-    if (cid < 0 || (sign && k + 1 > P - 1)) continue;
-    double2 v = make_double2(0.0, 0.0);
-    if (mine) {
-      const double2 s = sbuf[fpad(sign ? L + dr : dr)];
-      v = make_double2(s.x * inv, s.y * inv);
-    }
-    const ClassDesc& cd = cls[cid];
-    const long long idx = side ? (long long)(cd.qu - 1) + c1 : c1;
-    ccol[b * tot_ccol + cd.ccol_off + idx] = v;
+        [&](int idx, double2 v) {
+          const int dr = sign ? idx - L : idx;
+          if ((sign == 0 && idx < P) || (sign == 1 && dr > -P)) emit(dr, make_double2(v.x * inv, v.y * inv));
+        });
+  } else {
+    for (int k = threadIdx.x; k < P; k += blockDim.x) emit(sign ? -(k + 1) : k, make_double2(0.0, 0.0));
   }
 }
 
@@ -361,6 +362,16 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const double2* fx = FX + lay.at(b, base + i1, 0);
   const long long fxs = (long long)lay.np * 32;
   const double2* fy = FY0 + (b * 2 * S + strip * S + i2) * (long long)L;
+  const double inv = 1.0 / (double)L;
+  const int i = min(i1, i2);
+  auto emit = [&](int dc, double2 v) {
+    if (!in_uc(dr, dc, P, Q)) return;
+    const int cid = cls_slot[class_index(dr, dc, P, Q)];
+    if (cid < 0) return;
+    const ClassDesc& cd = cls[cid];
+    const int k = strip ? (cd.pv - 1) + i : i;
+    rc[b * tot_rc + cd.rc_off + k] = v;
+  };
   if (mine) {
     spec_fft_block<LOGL>(
         sbuf, tw,
@@ -368,23 +379,11 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
           const double2 x = fx[(idx >> 5) * fxs + (idx & 31)], y = fy[idx];
           return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
         },
-        [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
-    __syncthreads();
-  }
-  const double inv = 1.0 / (double)L;
-  const int i = min(i1, i2);
-  for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
-    if (!in_uc(dr, dc, P, Q)) continue;
-    const int cid = cls_slot[class_index(dr, dc, P, Q)];
-    if (cid < 0) continue;
-    const ClassDesc& cd = cls[cid];
-    const int k = strip ? (cd.pv - 1) + i : i;
-    double2 v = make_double2(0.0, 0.0);
-    if (mine) {
-      const double2 s = sbuf[fpad(dc)];
-      v = make_double2(s.x * inv, s.y * inv);
-    }
-    rc[b * tot_rc + cd.rc_off + k] = v;
+        [&](int idx, double2 v) {
+          if (idx < Q) emit(idx, make_double2(v.x * inv, v.y * inv));  // outputs dc < Q only
+        });
+  } else {
+    for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) emit(dc, make_double2(0.0, 0.0));
   }
 }
 
@@ -681,6 +680,8 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const double2* fx = FX + lay.at(b, r, 0);
   const double2* fy = FY + lay.at(b, r, 0);
   const long long fs = (long long)lay.np * 32;
+  const double inv = 1.0 / (double)L;
+  double2* out = D0p + (b * nd0 + k) * (long long)Q;
   spec_fft_block<LOGL>(
       sbuf, tw,
       [&](int idx) {
@@ -688,14 +689,9 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
         const double2 x = fx[o], y = fy[o];
         return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
       },
-      [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
-  __syncthreads();
-  const double inv = 1.0 / (double)L;
-  double2* out = D0p + (b * nd0 + k) * (long long)Q;
-  for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) {
-    const double2 v = sbuf[fpad(dc)];
-    out[dc] = make_double2(v.x * inv, v.y * inv);
-  }
+      [&](int idx, double2 v) {
+        if (idx < Q) out[idx] = make_double2(v.x * inv, v.y * inv);
+      });
 }
 
 // CC(0, dc) = sum over the band's core rows of the per-row transforms
@@ -765,17 +761,16 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const int dr = li - (P - 1);
   if (dr == 0) return;  // k_spec_d0sum
   const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
+  const double inv = 1.0 / (double)L;
   spec_fft_block<LOGL>(
       sbuf, tw,
       [&](int idx) { return g[idx]; },  // segment 0 holds the ordered sum (k_spec_gsum)
-      [&](int idx, double2 v) { sbuf[fpad(idx)] = v; });
-  __syncthreads();
-  const double inv = 1.0 / (double)L;
-  for (int dc = (dr < 0 ? 1 : 0) + threadIdx.x; dc < Q; dc += blockDim.x) {
-    const int cid = cls_slot[class_index(dr, dc, P, Q)];
-    const double2 s = sbuf[fpad(dc)];
-    if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(s.x * inv, s.y * inv);
-  }
+      [&](int idx, double2 v) {
+        if (idx < Q && (dr > 0 || idx > 0)) {
+          const int cid = cls_slot[class_index(dr, idx, P, Q)];
+          if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(v.x * inv, v.y * inv);
+        }
+      });
 }
 
 }  // namespace covgpu
