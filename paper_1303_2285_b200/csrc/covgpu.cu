@@ -123,6 +123,7 @@ struct covgpu_plan {
   double2 *d_tw = nullptr, *d_fx = nullptr, *d_fy = nullptr, *d_gp = nullptr, *d_d0p = nullptr;
   SpecLayout spec_lay{};
   bool spec_smem = false;  // k_spec_corr_smem (P <= 64) instead of the L2-fed k_spec_corr
+  int spec_e = 16;         // row lags per k_spec_corr_smem warp (16: up to 8 warps, 8: up to 16 warps)
   int spec_stages = 2;
   // spectral edge sums: column FFTs of length Lr = 2^spec_logLr (CCol), the
   // unmasked strip-row spectra (RC')
@@ -692,30 +693,19 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   if (pl->spec_smem) {
     const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
     const unsigned blocks = (unsigned)(B * pl->spec_lay.nfb * pl->spec_nseg);
-#define SPEC_CORR(NG)                                                                                   \
-  case NG: {                                                                                            \
-    static bool attr = false;                                                                           \
-    if (!attr) {                                                                                        \
-      cudaFuncSetAttribute(k_spec_corr_smem<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); \
-      attr = true;                                                                                      \
-    }                                                                                                   \
-    k_spec_corr_smem<NG><<<blocks, NG * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay,       \
-                                                            pl->spec_nseg, part, nparts, pl->spec_stages, \
-                                                            pl->d_gp);                                  \
-  } break
-    switch (pl->spec_ngrp) {
-      SPEC_CORR(2); SPEC_CORR(3); SPEC_CORR(4); SPEC_CORR(5); SPEC_CORR(6); SPEC_CORR(7);
-      default: {
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(k_spec_corr_smem<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-          attr = true;
-        }
-        k_spec_corr_smem<8><<<blocks, 8 * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, pl->spec_nseg,
-                                                         part, nparts, pl->spec_stages, pl->d_gp);
+    auto launch_corr = [&](auto kern) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
       }
-    }
-#undef SPEC_CORR
+      kern<<<blocks, pl->spec_ngrp * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, pl->spec_nseg, part,
+                                                   nparts, pl->spec_stages, pl->d_gp);
+    };
+    if (pl->spec_e == 8)
+      launch_corr(k_spec_corr_smem<8, 16>);
+    else
+      launch_corr(k_spec_corr_smem<16, 8>);
   } else {
     k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
         pl->d_fx, pl->d_fy, pr, pl->spec_lay, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts,
@@ -1108,7 +1098,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT"}) {
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
     e += ',';
@@ -1314,6 +1304,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->spec_logLr = logLr;
       pl->spec_logL = logL;
       pl->spec_L = 1 << logL;
+      if (const char* se = getenv("COVGPU_SPEC_E")) pl->spec_e = atoi(se) == 8 ? 8 : 16;
       pl->spec_ngrp = (2 * p - 1 + SPEC_E - 1) / SPEC_E;
       pl->spec_nfb = (pl->spec_L + SPEC_CW * 32 - 1) / (SPEC_CW * 32);
       // row segments: ~6 CTAs of 4 warps per SM, >= 4 windows of rows each.
@@ -1329,6 +1320,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->spec_lay.np = (int)n + 2 * pl->spec_lay.padr;
       const size_t stb = spec_corr_stage_bytes(p);
       pl->spec_smem = pl->spec_ngrp <= 8 && 2 * stb + 64 <= SC_SMEM_BUDGET;
+      // warps of the SMEM kernel: negative and non-negative lags in separate groups
+      if (pl->spec_smem) pl->spec_ngrp = (p - 1 + pl->spec_e - 1) / pl->spec_e + (p + pl->spec_e - 1) / pl->spec_e;
       if (const char* nsm = getenv("COVGPU_SPEC_NO_SMEM")) pl->spec_smem = pl->spec_smem && atoi(nsm) == 0;
       if (pl->spec_smem) {
         pl->spec_stages = (int)std::min<size_t>(4, SC_SMEM_BUDGET / (stb + 16));

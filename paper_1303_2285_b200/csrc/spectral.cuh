@@ -526,11 +526,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-template <int NG>
-__global__ void __launch_bounds__(NG * 32, 1)
+// E row lags per warp, NG = blockDim / 32 warps (<= MAXW): E = 16 with 8
+// warps (255 registers) or E = 8 with 16 warps (128 registers)
+template <int E, int MAXW>
+__global__ void __launch_bounds__(MAXW * 32, 1)
     k_spec_corr_smem(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay,
                      int nseg, int part, int nparts, int stages, double2* __restrict__ Gp) {
-  constexpr int E = SPEC_E;
+  const int NG = blockDim.x >> 5;
   extern __shared__ __align__(128) unsigned char scraw[];
   const int P = pr.P, N = pr.N;
   const int nlag = 2 * P - 1, XR = SC_RC + 2 * P - 2;
@@ -570,20 +572,24 @@ __global__ void __launch_bounds__(NG * 32, 1)
     for (int k = 0; k < stages - 1 && k < nk; ++k) issue(k);
   }
   __syncthreads();
-  const int dr0 = -(P - 1) + w * E;
-  const int drl = min(dr0 + E - 1, P - 1);
-  const int glo = spec_lo(dr0, P), ghi = spec_hi(drl, P, N);   // rows where some lag is active
-  const int blo = spec_lo(drl, P), bhi = spec_hi(dr0, P, N);   // rows where every lag is active
-  double ar[E], ai[E], wr[E], wi[E];
+  // warps 0 .. ngn-1 take the negative lags [-(P-1), -1], the others [0, P-1]
+  // (E per warp, never both signs): the core-row condition then becomes two
+  // per-ROW masks — dr >= 0: y rows r2 >= P-1, x rows r1 <= N-P; dr < 0:
+  // y rows r2 <= N-P, x rows r1 >= P-1 — applied once per row as it enters
+  // the registers, with no per-lag predicates
+  const int ngn = (P - 1 + E - 1) / E;
+  const bool neg = w < ngn;
+  const int dr0 = neg ? -(P - 1) + w * E : (w - ngn) * E;
+  const int drmax = neg ? -1 : P - 1;
   // Gauss form: s1 += xr yr, s2 += xi yi, s3 += (xr + xi)(yr - yi), then
   // Re = s1 + s2, Im = s3 - s1 + s2 — 3 DFMAs per complex MAC instead of 4
   // (the operand sums: one DADD per X row entering the window, one per y)
-  double s1[E], s2[E], s3[E], ws[E];
-  (void)ar;
-  (void)ai;
+  double s1[E], s2[E], s3[E], wr[E], wi[E], ws[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) s1[e] = s2[e] = s3[e] = wr[e] = wi[e] = ws[e] = 0.0;
   const int xoff = (P - 1) - dr0;  // stage X row of (r2 = R + j, lag e) = j + xoff - e
+  const int ylo = neg ? 0 : P - 1, yhi = neg ? N - P : N - 1;  // valid second-element rows
+  const int xlo = neg ? P - 1 : 0, xhi = neg ? N - 1 : N - P;  // valid first-element rows
   for (int k = 0; k < nk; ++k) {
     if (threadIdx.x == 0 && k + stages - 1 < nk) issue(k + stages - 1);
     const int s = k % stages;
@@ -591,58 +597,37 @@ __global__ void __launch_bounds__(NG * 32, 1)
     const int R = (ca + k) * SC_RC;
     const double2* Y = reinterpret_cast<const double2*>(scraw + s * stage_bytes) + lane;
     const double2* X = Y + 32 * SC_RC;
-    if (R + SC_RC - 1 >= glo && R <= ghi && dr0 <= P - 1) {
-      // window: slot kk holds X row (xoff - (E-1) + kk) for kk < E-1 (clamped: those rows only feed
-      // lags past P-1 when negative)
+    // window: slot kk holds X row t = R - dr0 - (E-1) + kk (stage row xoff - (E-1) + kk; clamped
+    // stage rows only feed lags past the warp's range)
 #pragma unroll
-      for (int kk = 0; kk < E - 1; ++kk) {
-        const double2 v = X[max(xoff - (E - 1) + kk, 0) * 32];
-        wr[kk] = v.x;
-        wi[kk] = v.y;
-        ws[kk] = v.x + v.y;
-      }
-#pragma unroll 1
-      for (int j0 = 0; j0 < SC_RC; j0 += E) {
-        const int rb = R + j0;
-        if (rb >= blo && rb + E - 1 <= bhi) {
+    for (int kk = 0; kk < E - 1; ++kk) {
+      const int trow = R - dr0 - (E - 1) + kk;
+      double2 v = X[max(xoff - (E - 1) + kk, 0) * 32];
+      if (trow < xlo || trow > xhi) v = make_double2(0.0, 0.0);
+      wr[kk] = v.x;
+      wi[kk] = v.y;
+      ws[kk] = v.x + v.y;
+    }
+#pragma unroll 2
+    for (int j0 = 0; j0 < SC_RC; j0 += E) {
 #pragma unroll
-          for (int tt = 0; tt < E; ++tt) {
-            const double2 xn = X[(j0 + tt + xoff) * 32];
-            const double2 y = Y[(j0 + tt) * 32];
-            const int nw = (tt + E - 1) % E;
-            wr[nw] = xn.x;
-            wi[nw] = xn.y;
-            ws[nw] = xn.x + xn.y;
-            const double yd = y.x - y.y;
+      for (int tt = 0; tt < E; ++tt) {
+        const int r2 = R + j0 + tt, trow = r2 - dr0;
+        double2 xn = X[(j0 + tt + xoff) * 32];
+        double2 y = Y[(j0 + tt) * 32];
+        if (trow < xlo || trow > xhi) xn = make_double2(0.0, 0.0);
+        if (r2 < ylo || r2 > yhi) y = make_double2(0.0, 0.0);
+        const int nw = (tt + E - 1) % E;
+        wr[nw] = xn.x;
+        wi[nw] = xn.y;
+        ws[nw] = xn.x + xn.y;
+        const double yd = y.x - y.y;
 #pragma unroll
-            for (int e = 0; e < E; ++e) s1[e] = fma(wr[(tt + E - 1 - e) % E], y.x, s1[e]);
+        for (int e = 0; e < E; ++e) s1[e] = fma(wr[(tt + E - 1 - e) % E], y.x, s1[e]);
 #pragma unroll
-            for (int e = 0; e < E; ++e) s2[e] = fma(wi[(tt + E - 1 - e) % E], y.y, s2[e]);
+        for (int e = 0; e < E; ++e) s2[e] = fma(wi[(tt + E - 1 - e) % E], y.y, s2[e]);
 #pragma unroll
-            for (int e = 0; e < E; ++e) s3[e] = fma(ws[(tt + E - 1 - e) % E], yd, s3[e]);
-          }
-        } else {
-#pragma unroll
-          for (int tt = 0; tt < E; ++tt) {
-            const int r2 = rb + tt;
-            const double2 xn = X[(j0 + tt + xoff) * 32];
-            const double2 y = Y[(j0 + tt) * 32];
-            const int nw = (tt + E - 1) % E;
-            wr[nw] = xn.x;
-            wi[nw] = xn.y;
-            ws[nw] = xn.x + xn.y;
-            const double yd = y.x - y.y;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const int dr = dr0 + e;
-              const bool on = r2 >= spec_lo(dr, P) && r2 <= spec_hi(dr, P, N);
-              const int sl = (tt + E - 1 - e) % E;
-              s1[e] = fma(wr[sl], on ? y.x : 0.0, s1[e]);
-              s2[e] = fma(wi[sl], on ? y.y : 0.0, s2[e]);
-              s3[e] = fma(ws[sl], on ? yd : 0.0, s3[e]);
-            }
-          }
-        }
+        for (int e = 0; e < E; ++e) s3[e] = fma(ws[(tt + E - 1 - e) % E], yd, s3[e]);
       }
     }
     __syncwarp();
@@ -653,7 +638,7 @@ __global__ void __launch_bounds__(NG * 32, 1)
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int dr = dr0 + e;
-    if (dr <= P - 1)
+    if (dr <= drmax)
       out[(long long)(dr + P - 1) * (lay.nfb * 32)] = make_double2(s1[e] + s2[e], s3[e] - s1[e] + s2[e]);
   }
 }
