@@ -684,11 +684,24 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
               pl->d_fy0);
   mark("spec_fft");
+  // the dr = 0 row transforms and the edge-row pair FFTs need only the row
+  // spectra: side stream after the FFTs (they fill the SMs around the
+  // correlation kernel)
+  const cudaStream_t st_main = st;
+  if (es != st) {
+    cudaEventRecord(pl->ev_d0, st);
+    cudaStreamWaitEvent(es, pl->ev_d0, 0);
+    st = es;
+  }
   if (rz >= ra)
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr, pl->spec_lay,
               pl->d_tw, ra, rz - ra + 1, rz - ra + 1, pl->d_d0p);
   k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
                                                      pl->d_cls_slot, pl->d_ccpart);
+  if (pl->spec_edges && es != st_main)
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+              pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+  st = st_main;
   mark("spec_rowac");
   if (pl->spec_smem) {
     const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
@@ -729,9 +742,9 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       st = st_main;
     }
     mark("spec_ccol");
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-              pl->spec_lay, pl->d_tw,
-              pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+    if (es == st)  // (timing mode: everything in order on one stream)
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
   }
 }
 
