@@ -642,8 +642,9 @@ void spec_attr(K* fn, int logL) {
   do {                                                                                          \
     auto fn_ = KERNEL<LG>();                                                                    \
     spec_attr(fn_, LG);                                                                         \
-    fn_<<<(unsigned)(GRID), spec_threads<LG>(), sizeof(double2) * ((1 << LG) + (1 << LG) / 8), st>>>( \
-        __VA_ARGS__);                                                                           \
+    const long long items_ = (long long)(GRID);                                                 \
+    fn_<<<(unsigned)((items_ + spec_g<LG>() - 1) / spec_g<LG>()), spec_threads<LG>(),           \
+          sizeof(double2) * spec_g<LG>() * spec_sb_elems<LG>(), st>>>(items_, __VA_ARGS__);     \
   } while (0)
 
 template <typename T>
@@ -729,15 +730,15 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     const long long per_seg = (long long)(2 * pr.P - 1) * L, tot = B * per_seg;
     k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, pl->spec_nseg, per_seg, tot);
   }
-  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_d0p, std::max(0, rz - ra + 1),
-            pl->d_tw, pr, pl->spec_nseg, pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
+  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pr, pl->spec_nseg,
+            pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
   if (pl->spec_edges) {
     mark("spec_dft");
     {
       cudaStream_t st_main = st;
       st = es;  // SPEC_LOGL launches on `st`
       SPEC_LOGL(pl->spec_logLr, SpecK<T>::template colfft, B * 2 * 4 * S1, A, pr, pl->d_twr, pl->d_fc);
-      SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * 2 * (long long)S1 * S1, pl->d_fc, pr,
+      SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * (long long)S1 * S1, pl->d_fc, pr,
                 pl->d_twr, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
       st = st_main;
     }

@@ -109,20 +109,39 @@ __host__ __device__ constexpr int spec_tw_off(int logL, int P0) {
 // One radix-R Stockham pass (autosort, no bit reversal): item i of L/R,
 // k = i mod p (p = product of the radices already applied):
 //     u_r = in[i + r L/R] * w_L^(r k L/(pR)),  DFT_R(u),  out[(i - k) R + k + r p] = u_r.
-// blockDim >= L/8, so a thread holds at most 8 values; in place in SMEM with
-// a barrier between the reads and the writes.  The first pass reads its input
-// through `ld(idx)` (global memory, coalesced), the last pass hands the
-// natural-order spectrum to `st(idx, v)`.
+// One transform per group of L/8 threads (tl = thread in the group, sb = the
+// group's SMEM), so a thread holds at most 8 values; in place in SMEM with a
+// CTA barrier between the reads and the writes (every group of the CTA runs
+// the same pass sequence).  The first pass reads its input through `ld(idx)`
+// (global memory, coalesced), the last pass hands the natural-order spectrum
+// to `st(idx, v)`.
+template <int LOGL>
+__host__ __device__ constexpr int spec_nt() {  // threads per transform
+  return (1 << LOGL) / 8;
+}
+template <int LOGL>
+__host__ __device__ constexpr int spec_g() {  // transforms per CTA: >= 256 threads for short lengths
+  return spec_nt<LOGL>() >= 256 ? 1 : 256 / spec_nt<LOGL>();
+}
+template <int LOGL>
+__host__ __device__ constexpr int spec_threads() {
+  return spec_nt<LOGL>() * spec_g<LOGL>();
+}
+template <int LOGL>
+__host__ __device__ constexpr int spec_sb_elems() {  // SMEM complex values per transform (one pad per 8)
+  return (1 << LOGL) + (1 << LOGL) / 8;
+}
+
 template <int LOGL, int R, int P0, class Load, class Store>
-__device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict__ tw, const Load& ld,
+__device__ __forceinline__ void spec_pass(double2* sb, int tl, const double2* __restrict__ tw, const Load& ld,
                                           const Store& st) {
-  constexpr int L = 1 << LOGL, T = L / R, NTHR = L / 8 > 32 ? L / 8 : 32;
+  constexpr int L = 1 << LOGL, T = L / R, NTHR = spec_nt<LOGL>();
   constexpr int IPT = (T + NTHR - 1) / NTHR;
   constexpr bool first = P0 == 1, last = P0 * R == L;
   double2 u[IPT][R];
 #pragma unroll
   for (int it = 0; it < IPT; ++it) {
-    const int i = threadIdx.x + it * NTHR;
+    const int i = tl + it * NTHR;
     if (i < T) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -138,7 +157,7 @@ __device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict
   const double2* __restrict__ twp = tw + spec_tw_off(LOGL, P0);
 #pragma unroll
   for (int it = 0; it < IPT; ++it) {
-    const int i = threadIdx.x + it * NTHR;
+    const int i = tl + it * NTHR;
     if (i < T) {
       const int k = i & (P0 - 1);
       if (k) {
@@ -178,20 +197,33 @@ __device__ __forceinline__ void spec_pass(double2* sb, const double2* __restrict
 // The whole forward FFT of length 2^LOGL: radix-8 passes, then one radix-4 /
 // radix-2 pass.  tw = the pass-major twiddle table (spec_tw_off).
 template <int LOGL, int P0 = 1, class Load, class Store>
-__device__ __forceinline__ void spec_fft_block(double2* sb, const double2* __restrict__ tw, const Load& ld,
+__device__ __forceinline__ void spec_fft_block(double2* sb, int tl, const double2* __restrict__ tw, const Load& ld,
                                                const Store& st) {
   constexpr int done = P0 == 1 ? 0 : __builtin_ctz(P0);
   constexpr int rem = LOGL - done;
   if constexpr (rem > 0) {
     constexpr int lr = rem >= 3 ? 3 : rem;
-    spec_pass<LOGL, (1 << lr), P0>(sb, tw, ld, st);
-    spec_fft_block<LOGL, (P0 << lr)>(sb, tw, ld, st);
+    spec_pass<LOGL, (1 << lr), P0>(sb, tl, tw, ld, st);
+    spec_fft_block<LOGL, (P0 << lr)>(sb, tl, tw, ld, st);
   }
 }
 
+// This thread's transform: item = CTA * G + group (valid < nitems), tl, SMEM
+struct SpecItem {
+  long long item;
+  int tl;
+  bool valid;
+};
 template <int LOGL>
-constexpr int spec_threads() {
-  return (1 << LOGL) / 8 > 32 ? (1 << LOGL) / 8 : 32;
+__device__ __forceinline__ SpecItem spec_item(long long nitems, double2*& sb, double2* sbuf) {
+  SpecItem it;
+  const int grp = threadIdx.x / spec_nt<LOGL>();
+  it.tl = threadIdx.x % spec_nt<LOGL>();
+  it.item = (long long)blockIdx.x * spec_g<LOGL>() + grp;
+  it.valid = it.item < nitems;
+  if (!it.valid) it.item = nitems - 1;  // keep the index math in range; loads / stores are skipped
+  sb = sbuf + grp * spec_sb_elems<LOGL>();
+  return it;
 }
 
 // Row spectra X_r, Y_r live f-block-major: [b][f / 32][PADR + r][f % 32],
@@ -212,11 +244,13 @@ struct SpecLayout {
 // strip [0, P-1) / bottom strip [N-P+1, N).  Zero-padded to L = 2^LOGL.
 template <typename T, int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_fft(const typename CT<T>::c* __restrict__ A, Problem pr, int mode, SpecLayout lay,
+    k_spec_fft(long long nitems, const typename CT<T>::c* __restrict__ A, Problem pr, int mode, SpecLayout lay,
                const double2* __restrict__ tw, double2* __restrict__ FX, double2* __restrict__ FY) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
-  long long t = blockIdx.x;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  long long t = si.item;
   const int N = pr.N, M = pr.M, Q = pr.Q, S = pr.P - 1;
   int r, clo, chi;
   long long orow;
@@ -241,9 +275,13 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   }
   const typename CT<T>::c* row = A + orow * (long long)M;
   const long long fstride = mode == 0 ? (long long)lay.np * 32 : 32;  // next 32-frequency block
+  const bool ok = si.valid;
   spec_fft_block<LOGL>(
-      sbuf, tw, [&](int idx) { return (idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0); },
-      [&](int idx, double2 v) { out[(idx >> 5) * fstride + (idx & 31)] = v; });
+      sb, si.tl, tw,
+      [&](int idx) { return (ok && idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0); },
+      [&](int idx, double2 v) {
+        if (ok) out[(idx >> 5) * fstride + (idx & 31)] = v;
+      });
 }
 
 // Column FFTs of the edge-column strips (left: columns [0, Q-1), right:
@@ -253,12 +291,14 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // FC[((b*2 + side)*4 + v)*(Q-1) + j][0 .. Lr).
 template <typename T, int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_colfft(const typename CT<T>::c* __restrict__ A, Problem pr, const double2* __restrict__ tw,
-                  double2* __restrict__ FC) {
+    k_spec_colfft(long long nitems, const typename CT<T>::c* __restrict__ A, Problem pr,
+                  const double2* __restrict__ tw, double2* __restrict__ FC) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int N = pr.N, M = pr.M, P = pr.P, Q = pr.Q;
-  long long t = blockIdx.x;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  long long t = si.item;
   const int j = (int)(t % (Q - 1));
   t /= Q - 1;
   const int v = (int)(t % 4);
@@ -270,12 +310,15 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const int rhi = (v == 1 || v == 2) ? N - 1 : N - P;
   const typename CT<T>::c* base = A + b * N * (long long)M + col;
   double2* out = FC + (((b * 2 + side) * 4 + v) * (Q - 1) + j) * (long long)L;
+  const bool ok = si.valid;
   spec_fft_block<LOGL>(
-      sbuf, tw,
+      sb, si.tl, tw,
       [&](int idx) {
-        return (idx >= rlo && idx <= rhi) ? widen2(base[(long long)idx * M]) : make_double2(0.0, 0.0);
+        return (ok && idx >= rlo && idx <= rhi) ? widen2(base[(long long)idx * M]) : make_double2(0.0, 0.0);
       },
-      [&](int idx, double2 v2) { out[idx] = v2; });
+      [&](int idx, double2 v2) {
+        if (ok) out[idx] = v2;
+      });
 }
 
 // Edge-column sums CCol from the column spectra: for strip side, sign and
@@ -287,24 +330,32 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // to part q mod nparts (the others write zeros: the bands are summed).
 template <int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_ccol(const double2* __restrict__ FC, Problem pr, const double2* __restrict__ tw,
+    k_spec_ccol(long long nitems, const double2* __restrict__ FC, Problem pr, const double2* __restrict__ tw,
                 const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls, double2* __restrict__ ccol,
                 long long tot_ccol, int part, int nparts) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int P = pr.P, Q = pr.Q, S1 = Q - 1;
-  long long t = blockIdx.x;
-  const int e = (int)(t % S1);
-  t /= S1;
-  const int c1 = (int)(t % S1);
-  t /= S1;
-  const int sign = (int)(t % 2);
-  t /= 2;
-  const int side = (int)(t % 2);
-  const long long b = t / 2;
-  if (e < c1 || (sign == 1 && e == c1)) return;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  // item = (b, side, pair q): sign 0 pairs e >= c1 first, then sign 1 pairs e > c1
+  const long long np0 = (long long)S1 * (S1 + 1) / 2, np1 = (long long)S1 * (S1 - 1) / 2;
+  long long q = si.item % (np0 + np1);
+  const long long bs = si.item / (np0 + np1);
+  const int side = (int)(bs % 2);
+  const long long b = bs / 2;
+  const int sign = q < np0 ? 0 : 1;
+  if (sign) q -= np0;
+  int c1 = 0;
+  for (;;) {
+    const int cnt = S1 - c1 - sign;
+    if (q < cnt) break;
+    q -= cnt;
+    ++c1;
+  }
+  const int e = c1 + sign + (int)q;
   const int dc = e - c1;
-  const bool mine = ((long long)c1 * S1 + e) % nparts == part;
+  const bool mine = si.valid && ((long long)c1 * S1 + e) % nparts == part;
   const double2* fx = FC + (((b * 2 + side) * 4 + 2 * sign) * S1 + c1) * (long long)L;
   const double2* fy = FC + (((b * 2 + side) * 4 + 2 * sign + 1) * S1 + e) * (long long)L;
   const double inv = 1.0 / (double)L;
@@ -317,22 +368,22 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     const long long o = side ? (long long)(cd.qu - 1) + c1 : c1;
     ccol[b * tot_ccol + cd.ccol_off + o] = v;
   };
-  if (mine) {
-    // the last pass hands over the natural-order outputs: only the P row lags
-    // of this sign are kept, stored straight to CCol (no SMEM round trip)
-    spec_fft_block<LOGL>(
-        sbuf, tw,
-        [&](int idx) {
-          const double2 x = fx[idx], y = fy[idx];
-          return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
-        },
-        [&](int idx, double2 v) {
-          const int dr = sign ? idx - L : idx;
-          if ((sign == 0 && idx < P) || (sign == 1 && dr > -P)) emit(dr, make_double2(v.x * inv, v.y * inv));
-        });
-  } else {
-    for (int k = threadIdx.x; k < P; k += blockDim.x) emit(sign ? -(k + 1) : k, make_double2(0.0, 0.0));
-  }
+  // the last pass hands over the natural-order outputs: only the P row lags
+  // of this sign are kept, stored straight to CCol (no SMEM round trip)
+  spec_fft_block<LOGL>(
+      sb, si.tl, tw,
+      [&](int idx) {
+        if (!mine) return make_double2(0.0, 0.0);
+        const double2 x = fx[idx], y = fy[idx];
+        return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
+      },
+      [&](int idx, double2 v) {
+        const int dr = sign ? idx - L : idx;
+        if (mine && ((sign == 0 && idx < P) || (sign == 1 && dr > -P)))
+          emit(dr, make_double2(v.x * inv, v.y * inv));
+      });
+  if (si.valid && !mine)
+    for (int k = si.tl; k < P; k += spec_nt<LOGL>()) emit(sign ? -(k + 1) : k, make_double2(0.0, 0.0));
 }
 
 // Edge-row sums RC' from the row spectra: for strip rows (i1, i2) (first
@@ -343,13 +394,15 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // segment here (nseg = 1).
 template <int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_rc(const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr, SpecLayout lay,
-              const double2* __restrict__ tw, const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls,
-              double2* __restrict__ rc, long long tot_rc, int part, int nparts) {
+    k_spec_rc(long long nitems, const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr,
+              SpecLayout lay, const double2* __restrict__ tw, const int* __restrict__ cls_slot,
+              const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc, int part, int nparts) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int N = pr.N, P = pr.P, Q = pr.Q, S = P - 1;
-  long long t = blockIdx.x;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  long long t = si.item;
   const int i2 = (int)(t % S);
   t /= S;
   const int i1 = (int)(t % S);
@@ -358,7 +411,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const long long b = t / 2;
   const int dr = i2 - i1;
   const int base = strip ? N - S : 0;
-  const bool mine = ((long long)i1 * S + i2) % nparts == part;
+  const bool mine = si.valid && ((long long)i1 * S + i2) % nparts == part;
   const double2* fx = FX + lay.at(b, base + i1, 0);
   const long long fxs = (long long)lay.np * 32;
   const double2* fy = FY0 + (b * 2 * S + strip * S + i2) * (long long)L;
@@ -372,19 +425,18 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     const int k = strip ? (cd.pv - 1) + i : i;
     rc[b * tot_rc + cd.rc_off + k] = v;
   };
-  if (mine) {
-    spec_fft_block<LOGL>(
-        sbuf, tw,
-        [&](int idx) {
-          const double2 x = fx[(idx >> 5) * fxs + (idx & 31)], y = fy[idx];
-          return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
-        },
-        [&](int idx, double2 v) {
-          if (idx < Q) emit(idx, make_double2(v.x * inv, v.y * inv));  // outputs dc < Q only
-        });
-  } else {
-    for (int dc = threadIdx.x; dc < Q; dc += blockDim.x) emit(dc, make_double2(0.0, 0.0));
-  }
+  spec_fft_block<LOGL>(
+      sb, si.tl, tw,
+      [&](int idx) {
+        if (!mine) return make_double2(0.0, 0.0);
+        const double2 x = fx[(idx >> 5) * fxs + (idx & 31)], y = fy[idx];
+        return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
+      },
+      [&](int idx, double2 v) {
+        if (mine && idx < Q) emit(idx, make_double2(v.x * inv, v.y * inv));  // outputs dc < Q only
+      });
+  if (si.valid && !mine)
+    for (int dc = si.tl; dc < Q; dc += spec_nt<LOGL>()) emit(dc, make_double2(0.0, 0.0));
 }
 
 __device__ __forceinline__ int spec_lo(int dr, int P) { return P - 1 + min(dr, 0); }
@@ -654,13 +706,17 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
 // CTA = (b, row r of the band [row_a, row_a + nrows)).
 template <int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_rowac(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay,
-                 const double2* __restrict__ tw, int row_a, int nrows, int nd0, double2* __restrict__ D0p) {
+    k_spec_rowac(long long nitems, const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr,
+                 SpecLayout lay, const double2* __restrict__ tw, int row_a, int nrows, int nd0,
+                 double2* __restrict__ D0p) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int Q = pr.Q;
-  const int k = (int)(blockIdx.x % nrows);
-  const long long b = blockIdx.x / nrows;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  const bool ok = si.valid;
+  const int k = (int)(si.item % nrows);
+  const long long b = si.item / nrows;
   const int r = row_a + k;
   const double2* fx = FX + lay.at(b, r, 0);
   const double2* fy = FY + lay.at(b, r, 0);
@@ -668,14 +724,15 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const double inv = 1.0 / (double)L;
   double2* out = D0p + (b * nd0 + k) * (long long)Q;
   spec_fft_block<LOGL>(
-      sbuf, tw,
+      sb, si.tl, tw,
       [&](int idx) {
+        if (!ok) return make_double2(0.0, 0.0);
         const long long o = (idx >> 5) * fs + (idx & 31);
         const double2 x = fx[o], y = fy[o];
         return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
       },
       [&](int idx, double2 v) {
-        if (idx < Q) out[idx] = make_double2(v.x * inv, v.y * inv);
+        if (ok && idx < Q) out[idx] = make_double2(v.x * inv, v.y * inv);
       });
 }
 
@@ -734,24 +791,25 @@ __global__ void __launch_bounds__(256)
 // npart = 1 for the finalize).
 template <int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_dft(const double2* __restrict__ Gp, const double2* __restrict__ D0p, int nd0,
-               const double2* __restrict__ tw, Problem pr, int nseg, int nclasses,
-               const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+    k_spec_dft(long long nitems, const double2* __restrict__ Gp, const double2* __restrict__ tw, Problem pr,
+               int nseg, int nclasses, const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int P = pr.P, Q = pr.Q;
   const int nlag = 2 * P - 1;
-  const int li = (int)(blockIdx.x % nlag);
-  const long long b = blockIdx.x / nlag;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  const int li = (int)(si.item % nlag);
+  const long long b = si.item / nlag;
   const int dr = li - (P - 1);
-  if (dr == 0) return;  // k_spec_d0sum
+  const bool ok = si.valid && dr != 0;  // dr = 0: k_spec_d0sum
   const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
   const double inv = 1.0 / (double)L;
   spec_fft_block<LOGL>(
-      sbuf, tw,
-      [&](int idx) { return g[idx]; },  // segment 0 holds the ordered sum (k_spec_gsum)
+      sb, si.tl, tw,
+      [&](int idx) { return ok ? g[idx] : make_double2(0.0, 0.0); },  // segment 0: the ordered sum
       [&](int idx, double2 v) {
-        if (idx < Q && (dr > 0 || idx > 0)) {
+        if (ok && idx < Q && (dr > 0 || idx > 0)) {
           const int cid = cls_slot[class_index(dr, idx, P, Q)];
           if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(v.x * inv, v.y * inv);
         }
