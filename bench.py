@@ -527,6 +527,26 @@ def main() -> None:
                        "d2h_bytes_per_step": r_host.numel() * esz,
                        "ms_per_step": float(te.item()) * 1e3,
                        "path": f"covgpu_plan_execute_host, pinned host buffers, {e2e_layout} R, wall clock"}
+    if not args.no_e2e and world == 1 and w.batch < 8:
+        # streaming form (covgpu_plan_execute_host_async): K estimates back to
+        # back, each with its own pinned H2D of A and D2H of the packed R,
+        # call k+1's copy-in and compute under call k's copy-out
+        a_hosts = [torch.from_numpy(host_a).reshape(w.batch, w.n, w.m).pin_memory() for _ in range(2)]
+        r_hosts = [torch.empty(plan.output_elems("packed"), dtype=tdt).pin_memory() for _ in range(2)]
+        for k in range(2):
+            plan.execute_host_async(a_hosts[k], r_hosts[k], "packed")
+        plan.wait()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            plan.execute_host_async(a_hosts[k % 2], r_hosts[k % 2], "packed")
+        plan.wait()
+        tp = (time.perf_counter() - t0) / args.steps
+        esz = r_hosts[0].element_size()
+        line["e2e_pipelined"] = {
+            "value": entries / tp, "unit": UNIT, "ms_per_step": tp * 1e3,
+            "h2d_bytes_per_step": a_hosts[0].numel() * esz, "d2h_bytes_per_step": r_hosts[0].numel() * esz,
+            "path": "covgpu_plan_execute_host_async x K then covgpu_plan_wait: every step copies its A in and "
+                    "its packed R out (pinned), two estimates in flight; wall clock"}
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sample, threads, t_full = cpu_reference(w, args.cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",

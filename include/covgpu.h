@@ -156,6 +156,22 @@ int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m
 int covgpu_plan_execute_host(covgpu_plan_t plan, const void* A_host, void* R_host, int32_t layout,
                              double scale);
 
+/* Streaming form of covgpu_plan_execute_host for a sequence of estimates
+ * (e.g. one per radar dwell / image frame): enqueues the H2D of A, the
+ * estimate and the D2H of R and returns; up to two calls are in flight (the
+ * device buffers are double-buffered), so call k+1's copy-in and compute run
+ * under call k's copy-out.  The host must not write A_host or read R_host
+ * until covgpu_plan_wait returns (later calls may reuse the same buffers:
+ * the copies of calls sharing a device slot are ordered); pinned memory for
+ * full PCIe bandwidth.  Batched
+ * plans (batch >= 8) run synchronously (they pipeline internally).
+ * covgpu_plan_wait blocks until every enqueued call has finished and returns
+ * the first error.  The reference's API is synchronous (SPEC.md:341,
+ * engine.py:108-147); this is an addition for throughput. */
+int covgpu_plan_execute_host_async(covgpu_plan_t plan, const void* A_host, void* R_host, int32_t layout,
+                                   double scale);
+int covgpu_plan_wait(covgpu_plan_t plan);
+
 /* Bench utility: FP64 (dtype COVGPU_C128) or FP32 (COVGPU_C64) FMA-pipe
  * throughput in TFLOP/s, measured for about `seconds` on `device` — the
  * roofline denominator of the covariance kernels. */

@@ -66,6 +66,8 @@ _SIGS = {
         [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _dbl, _vp, ctypes.c_int],
     ),
     "covgpu_plan_execute_host": (ctypes.c_int, [_vp, _vp, _vp, _i32, _dbl]),
+    "covgpu_plan_execute_host_async": (ctypes.c_int, [_vp, _vp, _vp, _i32, _dbl]),
+    "covgpu_plan_wait": (ctypes.c_int, [_vp]),
     "covgpu_probe_fma_peak": (ctypes.c_int, [ctypes.c_int, _i32, _dbl, ctypes.POINTER(_dbl)]),
     "covgpu_probe_dmma_peak": (ctypes.c_int, [ctypes.c_int, _dbl, ctypes.POINTER(_dbl)]),
     "covgpu_bulk_geometry": (ctypes.c_int, [_i64, _i64, _i64, _i32, _i32, _i32, _p32, _p32]),

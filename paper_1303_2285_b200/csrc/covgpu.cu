@@ -205,6 +205,15 @@ struct covgpu_plan {
   void* hR = nullptr;
   size_t hA_bytes = 0, hR_bytes = 0;
   std::mutex host_mu;
+  // streaming host path (covgpu_plan_execute_host_async): two slots of device
+  // buffers, copy-in / compute (host_stream) / copy-out streams
+  cudaStream_t as_in = nullptr, as_out = nullptr;
+  void* asA[2] = {};
+  void* asR[2] = {};
+  size_t asA_bytes = 0, asR_bytes = 0;
+  cudaEvent_t as_ev_in[2] = {}, as_ev_comp[2] = {}, as_ev_out[2] = {};
+  long long as_n = 0;
+  int as_err = 0;
   std::mutex exec_mu;  // executes mutate plan state (tensor-map cache, timing events)
   // pipelined host path for batches: sub-batch plans, streams and buffers
   static constexpr int kPipeSlots = 3;
@@ -299,6 +308,15 @@ void plan_free(covgpu_plan* pl) {
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
   cudaFree(pl->d_ecm_tickets);
+  if (pl->as_in) cudaStreamDestroy(pl->as_in);
+  if (pl->as_out) cudaStreamDestroy(pl->as_out);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(pl->asA[k]);
+    cudaFree(pl->asR[k]);
+    if (pl->as_ev_in[k]) cudaEventDestroy(pl->as_ev_in[k]);
+    if (pl->as_ev_comp[k]) cudaEventDestroy(pl->as_ev_comp[k]);
+    if (pl->as_ev_out[k]) cudaEventDestroy(pl->as_ev_out[k]);
+  }
   cudaFree(pl->d_tw);
   cudaFree(pl->d_fx);
   cudaFree(pl->d_fy);
@@ -1989,6 +2007,90 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
   CUDA_TRY(cudaMemcpyAsync(R_host, pl->hR, r_bytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return COVGPU_OK;
+}
+
+int covgpu_plan_execute_host_async(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
+                                   double scale) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  if (!A_host || !R_host) return fail(COVGPU_EINVAL, "host buffers must be non-NULL");
+  if (layout < COVGPU_DENSE || layout > COVGPU_COMPACT) return fail(COVGPU_EINVAL, "unknown layout");
+  if (pl->batch >= 8) {
+    const int rc = covgpu_plan_execute_host(pl, A_host, R_host, layout, scale);
+    if (rc && !pl->as_err) pl->as_err = rc;
+    return rc;
+  }
+  CUDA_TRY(cudaSetDevice(pl->device));
+  const Problem& pr = pl->pr;
+  const size_t esz = pl->dtype == COVGPU_C128 ? 16 : 8;
+  const size_t a_bytes = (size_t)pl->batch * pr.N * pr.M * esz;
+  long long r_elems;
+  if (layout == COVGPU_DENSE)
+    r_elems = pl->batch * (long long)pr.PQ * pr.PQ;
+  else if (layout == COVGPU_PACKED)
+    r_elems = pl->batch * ((long long)pr.PQ * (pr.PQ + 1) / 2);
+  else
+    r_elems = pl->batch * pl->compact_elems;
+  const size_t r_bytes = (size_t)r_elems * esz;
+  std::lock_guard<std::mutex> lk(pl->host_mu);
+  if (!pl->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->host_stream, cudaStreamNonBlocking));
+  if (!pl->as_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&pl->as_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&pl->as_out, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaEventCreateWithFlags(&pl->as_ev_in[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&pl->as_ev_comp[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&pl->as_ev_out[k], cudaEventDisableTiming));
+    }
+  }
+  if (pl->asA_bytes < a_bytes || pl->asR_bytes < r_bytes) {
+    CUDA_TRY(cudaDeviceSynchronize());  // (re)size only with nothing in flight
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(pl->asA[k]);
+      cudaFree(pl->asR[k]);
+      pl->asA[k] = pl->asR[k] = nullptr;
+    }
+    pl->asA_bytes = pl->asR_bytes = 0;
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaMalloc(&pl->asA[k], a_bytes));
+      CUDA_TRY(cudaMalloc(&pl->asR[k], r_bytes));
+    }
+    pl->asA_bytes = a_bytes;
+    pl->asR_bytes = r_bytes;
+    pl->as_n = 0;
+  }
+  const int sl = (int)(pl->as_n & 1);
+  const bool reuse = pl->as_n >= 2;  // slot used by call k-2
+  // copy-in: A slot free once call k-2's estimate has read it
+  if (reuse) CUDA_TRY(cudaStreamWaitEvent(pl->as_in, pl->as_ev_comp[sl], 0));
+  CUDA_TRY(cudaMemcpyAsync(pl->asA[sl], A_host, a_bytes, cudaMemcpyHostToDevice, pl->as_in));
+  CUDA_TRY(cudaEventRecord(pl->as_ev_in[sl], pl->as_in));
+  // estimate: after its copy-in, and after call k-2's copy-out freed the R slot
+  CUDA_TRY(cudaStreamWaitEvent(pl->host_stream, pl->as_ev_in[sl], 0));
+  if (reuse) CUDA_TRY(cudaStreamWaitEvent(pl->host_stream, pl->as_ev_out[sl], 0));
+  int rc = covgpu_plan_execute(pl, pl->asA[sl], pl->asR[sl], layout, scale, pl->host_stream);
+  if (rc) {
+    if (!pl->as_err) pl->as_err = rc;
+    return rc;
+  }
+  CUDA_TRY(cudaEventRecord(pl->as_ev_comp[sl], pl->host_stream));
+  // copy-out
+  CUDA_TRY(cudaStreamWaitEvent(pl->as_out, pl->as_ev_comp[sl], 0));
+  CUDA_TRY(cudaMemcpyAsync(R_host, pl->asR[sl], r_bytes, cudaMemcpyDeviceToHost, pl->as_out));
+  CUDA_TRY(cudaEventRecord(pl->as_ev_out[sl], pl->as_out));
+  ++pl->as_n;
+  return COVGPU_OK;
+}
+
+int covgpu_plan_wait(covgpu_plan_t pl) {
+  if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  std::lock_guard<std::mutex> lk(pl->host_mu);
+  if (pl->as_out) CUDA_TRY(cudaStreamSynchronize(pl->as_out));
+  if (pl->host_stream) CUDA_TRY(cudaStreamSynchronize(pl->host_stream));
+  if (pl->as_in) CUDA_TRY(cudaStreamSynchronize(pl->as_in));
+  const int e = pl->as_err;
+  pl->as_err = 0;
+  return e;
 }
 
 int covgpu_bulk_geometry(int64_t batch, int64_t n, int64_t m, int32_t p, int32_t q, int32_t dtype,

@@ -66,6 +66,18 @@ class Plan:
         _native.check(rc, "covgpu_plan_execute_host")
         return out_host
 
+    def execute_host_async(self, a_host: torch.Tensor, out_host: torch.Tensor, layout: str = "packed",
+                           scale: float | None = None) -> None:
+        """Enqueue one host-buffer estimate (up to two in flight); the buffers
+        must stay untouched until wait() returns."""
+        rc = self.lib.covgpu_plan_execute_host_async(self.handle, ctypes.c_void_p(a_host.data_ptr()),
+                                                     ctypes.c_void_p(out_host.data_ptr()), LAYOUTS[layout],
+                                                     1.0 / self.k if scale is None else scale)
+        _native.check(rc, "covgpu_plan_execute_host_async")
+
+    def wait(self) -> None:
+        _native.check(self.lib.covgpu_plan_wait(self.handle), "covgpu_plan_wait")
+
     # ---- which sum kernels run (include/covgpu.h: covgpu_plan_path) ----
     PATH_SPECTRAL, PATH_TENSOR, PATH_ROWBAND = 1, 2, 4
 

@@ -695,3 +695,32 @@ def test_spectral_path_vs_oracle(cuda, n, m, p, q, batch, dt, monkeypatch):
         ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), p, q) / k
         err = co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref)
         assert err <= (TOL64 if dt == np.complex128 else TOL32), (b, err)
+
+
+def test_streaming_host_path_matches_sync(cuda):
+    """covgpu_plan_execute_host_async: a sequence of estimates (two in flight,
+    buffers reused) equals the synchronous host call bitwise."""
+    from paper_1303_2285_b200.plan import Plan
+
+    n, m, p, q = 200, 180, 20, 24
+    rng = np.random.default_rng(77)
+    ins = [torch.from_numpy(rng.standard_normal((1, n, m)) + 1j * rng.standard_normal((1, n, m))).pin_memory()
+           for _ in range(3)]
+    plan = Plan(n, m, WindowSpec(p, q), dtype=torch.complex128, device=cuda)
+    ref = []
+    for a in ins:
+        r = torch.empty(plan.output_elems("packed"), dtype=torch.complex128).pin_memory()
+        plan.execute_host(a, r, "packed")
+        ref.append(r.clone())
+    outs = [torch.empty(plan.output_elems("packed"), dtype=torch.complex128).pin_memory() for _ in range(2)]
+    got = []
+    for k, a in enumerate(ins):
+        plan.execute_host_async(a, outs[k % 2], "packed")
+        if k % 2 == 1:
+            plan.wait()
+            got += [outs[0].clone(), outs[1].clone()]
+    plan.wait()
+    got.append(outs[0].clone())
+    plan.close()
+    for r, g in zip(ref, got):
+        assert torch.equal(r, g)
