@@ -34,6 +34,9 @@ namespace covgpu {
 constexpr int SPEC_E = 16;        // row lags per k_spec_corr thread
 constexpr int SPEC_CW = 4;        // warps (32-frequency columns) per k_spec_corr CTA
 constexpr int SPEC_MAX_Q = 512;   // edge-column pairs grow as Q^2
+#ifndef SPEC_CTA_THREADS
+#define SPEC_CTA_THREADS 256        // FFT kernels: transforms per CTA up to this many threads
+#endif
 
 template <typename C2>
 __device__ __forceinline__ double2 widen2(C2 v) {
@@ -121,7 +124,7 @@ __host__ __device__ constexpr int spec_nt() {  // threads per transform
 }
 template <int LOGL>
 __host__ __device__ constexpr int spec_g() {  // transforms per CTA: >= 256 threads for short lengths
-  return spec_nt<LOGL>() >= 256 ? 1 : 256 / spec_nt<LOGL>();
+  return spec_nt<LOGL>() >= SPEC_CTA_THREADS ? 1 : SPEC_CTA_THREADS / spec_nt<LOGL>();
 }
 template <int LOGL>
 __host__ __device__ constexpr int spec_threads() {
