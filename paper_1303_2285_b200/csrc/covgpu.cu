@@ -637,11 +637,15 @@ std::vector<double2> spec_twiddles(int logL) {
 // instantiation: up to (L + L/8) complex values).
 template <typename K>
 void spec_attr(K* fn, int logL) {
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    done = true;
-  }
+  // once per kernel instantiation (keyed on the function, not its type: the
+  // LOGL instantiations of one kernel share a signature)
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const void* f = (const void*)fn;
+  if (std::find(done.begin(), done.end(), f) != done.end()) return;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  done.push_back(f);
   (void)logL;
 }
 #define SPEC_LOGL(lg, KERNEL, GRID, ...)                                                        \
