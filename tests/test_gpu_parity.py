@@ -666,6 +666,7 @@ def test_row_band_sums_and_class_range_finalize(cuda):
     (257, 513, 70, 33, 1, np.complex128),   # P > 64: the L2-fed correlation kernel (9 lag groups)
     (128, 128, 8, 16, 5, np.complex64),     # cfg4 shape, complex64 inputs (FP64 spectral arithmetic)
     (100, 77, 12, 20, 3, np.complex64),
+    (40, 3000, 6, 9, 1, np.complex128),     # L = 4096 after shorter lengths in this process (SMEM attribute)
 ])
 def test_spectral_path_vs_oracle(cuda, n, m, p, q, batch, dt, monkeypatch):
     """The frequency-domain sums (spectral.cuh) forced on small and ragged
