@@ -396,7 +396,16 @@ def main() -> None:
         prof = ROOT / "profiles" / f"ncu_{w.name}_summary.json"
         if prof.exists():
             try:
-                roof["traffic"] = json.loads(prof.read_text()).get(f"{dom}_dram_bytes_per_launch")
+                summ = json.loads(prof.read_text())
+                roof["traffic"] = summ.get(f"{dom}_dram_bytes_per_launch")
+                wf = summ.get(f"{dom}_lsu_wavefronts_per_launch")
+                if wf:
+                    # the walk is bound by the L1 / LSU data pipe (1 wavefront per SM per
+                    # cycle), not DRAM: the same launch against that roof
+                    sm_hz = 148 * 1.965e9
+                    ach = wf / (kernel_ms[dom] * 1e-3)
+                    roof["lsu"] = {"wavefronts_per_launch": wf, "achieved_per_s": ach, "peak_per_s": sm_hz,
+                                   "frac": ach / sm_hz, "source": summ.get(f"{dom}_lsu_note")}
             except (ValueError, OSError):
                 pass
 
