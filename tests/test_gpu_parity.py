@@ -667,6 +667,7 @@ def test_row_band_sums_and_class_range_finalize(cuda):
     (128, 128, 8, 16, 5, np.complex64),     # cfg4 shape, complex64 inputs (FP64 spectral arithmetic)
     (100, 77, 12, 20, 3, np.complex64),
     (40, 3000, 6, 9, 1, np.complex128),     # L = 4096 after shorter lengths in this process (SMEM attribute)
+    (300, 400, 20, 100, 1, np.complex128),  # Q > 64: wide edge strips (99 columns), 9801 column pairs
 ])
 def test_spectral_path_vs_oracle(cuda, n, m, p, q, batch, dt, monkeypatch):
     """The frequency-domain sums (spectral.cuh) forced on small and ragged
