@@ -215,6 +215,17 @@ struct covgpu_plan {
   long long as_n = 0;
   int as_err = 0;
   std::mutex exec_mu;  // executes mutate plan state (tensor-map cache, timing events)
+  // CUDA-graph replay of covgpu_plan_execute: the second call with the same
+  // (A, R, layout, scale) captures the launch sequence (side-stream fork /
+  // join included) on cap_stream; later identical calls launch the graph
+  bool use_graph = true;  // COVGPU_NO_GRAPH=1: off
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_A = nullptr;
+  void* g_R = nullptr;
+  int g_layout = -1;
+  double g_scale = 0.0;
+  int g_hits = 0;
   // pipelined host path for batches: sub-batch plans, streams and buffers
   static constexpr int kPipeSlots = 3;
   covgpu_plan* pipe[kPipeSlots] = {};
@@ -308,6 +319,8 @@ void plan_free(covgpu_plan* pl) {
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
   cudaFree(pl->d_ecm_tickets);
+  if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+  if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   if (pl->as_in) cudaStreamDestroy(pl->as_in);
   if (pl->as_out) cudaStreamDestroy(pl->as_out);
   for (int k = 0; k < 2; ++k) {
@@ -1134,7 +1147,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E"}) {
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
     e += ',';
@@ -1229,6 +1242,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     pl->bulk_variant = v;
     if (const char* nt = getenv("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
     if (const char* nd = getenv("COVGPU_NO_DIRECT")) pl->no_direct = atoi(nd) != 0;
+    if (const char* ng = getenv("COVGPU_NO_GRAPH")) pl->use_graph = atoi(ng) == 0;
     pl->E = kBulkVariants[v].E;
     pl->NW = kBulkVariants[v].NW;
   }
@@ -1612,8 +1626,49 @@ int covgpu_plan_execute(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_
   CUDA_TRY(cudaSetDevice(pl->device));
   cudaStream_t st = (cudaStream_t)stream;
   std::lock_guard<std::mutex> lk(pl->exec_mu);
-  if (pl->dtype == COVGPU_C128) return launch_all<double>(pl, A_dev, R_dev, layout, scale, st);
-  return launch_all<float>(pl, A_dev, R_dev, layout, scale, st);
+  auto run = [&](cudaStream_t s) {
+    return pl->dtype == COVGPU_C128 ? launch_all<double>(pl, A_dev, R_dev, layout, scale, s)
+                                    : launch_all<float>(pl, A_dev, R_dev, layout, scale, s);
+  };
+  if (!pl->use_graph || pl->timing || pl->band_wait || pl->ks_out || !pl->clean) return run(st);
+  const bool same = A_dev == pl->g_A && R_dev == pl->g_R && layout == pl->g_layout && scale == pl->g_scale;
+  if (same && pl->gexec) {
+    CUDA_TRY(cudaGraphLaunch(pl->gexec, st));
+    return COVGPU_OK;
+  }
+  if (!same) {
+    if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+    pl->g_A = A_dev;
+    pl->g_R = R_dev;
+    pl->g_layout = layout;
+    pl->g_scale = scale;
+    pl->g_hits = 0;
+  }
+  if (++pl->g_hits < 2) return run(st);  // first call: plain launches (attributes, tensor maps settle)
+  // second identical call: capture on a private stream (the caller's may be the
+  // legacy default stream, which cannot be captured), then launch on the caller's
+  if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = run(pl->cap_stream);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(pl->cap_stream, &g);
+  if (rc || ce != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    pl->use_graph = false;  // capture not possible here: plain launches from now on
+    return rc ? rc : run(st);
+  }
+  const cudaError_t ie = cudaGraphInstantiate(&pl->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    pl->gexec = nullptr;
+    pl->use_graph = false;
+    return run(st);
+  }
+  CUDA_TRY(cudaGraphLaunch(pl->gexec, st));
+  return COVGPU_OK;
 }
 
 int64_t covgpu_plan_workspace_bytes(covgpu_plan_t pl) { return pl ? pl->ws_bytes : -1; }

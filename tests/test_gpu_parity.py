@@ -726,3 +726,29 @@ def test_streaming_host_path_matches_sync(cuda):
     plan.close()
     for r, g in zip(ref, got):
         assert torch.equal(r, g)
+
+
+@pytest.mark.parametrize("n,m,p,q,force_spectral", [(32, 32, 4, 4, False), (120, 100, 12, 16, True)])
+def test_graph_replay_bitwise(cuda, n, m, p, q, force_spectral, monkeypatch):
+    """Repeated executes on the same buffers are captured into a CUDA graph
+    (from the second call) and replayed; every replay reads the buffer's
+    current contents and equals a graph-free plan bitwise."""
+    from paper_1303_2285_b200.plan import Plan
+
+    if force_spectral:
+        monkeypatch.setenv("COVGPU_SPECTRAL", "1")
+    plan = Plan(n, m, WindowSpec(p, q), dtype=torch.complex128, device=cuda)
+    monkeypatch.setenv("COVGPU_NO_GRAPH", "1")
+    ref_plan = Plan(n, m, WindowSpec(p, q), dtype=torch.complex128, device=cuda)
+    rng = np.random.default_rng(5)
+    a = torch.empty((1, n, m), dtype=torch.complex128, device=cuda)
+    out = plan.alloc_output()
+    ref = ref_plan.alloc_output()
+    for it in range(4):
+        a.copy_(torch.as_tensor(rng.standard_normal((1, n, m)) + 1j * rng.standard_normal((1, n, m))))
+        plan.execute(a, out)
+        ref_plan.execute(a, ref)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), it
+    plan.close()
+    ref_plan.close()
