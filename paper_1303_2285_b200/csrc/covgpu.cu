@@ -185,6 +185,14 @@ struct covgpu_plan {
   long long* d_uc_off = nullptr;  // compact offset per UC index (-1: not in shard)
   long long ntasks = 0;
   int fin_kr = 0;             // k_finalize_v rows per lane (0: wide finalize)
+  // chunked walk for the synchronous host path (covgpu_plan_execute_host):
+  // u-chunk bounds, saved walk state, an event per chunk
+  static constexpr int kMaxFinChunks = 4;
+  int fin_nchunks = 1;
+  int fin_ubound[kMaxFinChunks + 1] = {};
+  double2* d_fin_state = nullptr;
+  cudaEvent_t ev_fin_chunk[kMaxFinChunks] = {};
+  cudaStream_t out_stream = nullptr;
   int sat_chunk = 0;
   long long ws_bytes = 0;
   size_t fin_smem = 0;
@@ -330,6 +338,10 @@ void plan_free(covgpu_plan* pl) {
     if (pl->as_ev_comp[k]) cudaEventDestroy(pl->as_ev_comp[k]);
     if (pl->as_ev_out[k]) cudaEventDestroy(pl->as_ev_out[k]);
   }
+  cudaFree(pl->d_fin_state);
+  if (pl->out_stream) cudaStreamDestroy(pl->out_stream);
+  for (auto& e : pl->ev_fin_chunk)
+    if (e) cudaEventDestroy(e);
   cudaFree(pl->d_tw);
   cudaFree(pl->d_fx);
   cudaFree(pl->d_fy);
@@ -1022,19 +1034,27 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                 \
       (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses,           \
       npart, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
-      pl->nseg, cdst, rstride, scale, direct ? layout : (int)COVGPU_COMPACT)
-    if (direct) {
-      switch (pl->fin_kr) {
-        case 1: FINV(1, true); break;
-        case 2: FINV(2, true); break;
-        default: FINV(4, true);
+      pl->nseg, cdst, rstride, scale, direct ? layout : (int)COVGPU_COMPACT, u0, u1, wst)
+    // u-chunks (host path: rows [P u0, P u1) of R are complete after a chunk;
+    // an event per chunk lets the copy-out start while the walk continues)
+    const int nch = (direct && pl->fin_nchunks > 1 && pl->d_fin_state) ? pl->fin_nchunks : 1;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int u0 = nch > 1 ? pl->fin_ubound[ch] : 0, u1 = nch > 1 ? pl->fin_ubound[ch + 1] : (1 << 30);
+      double2* wst = nch > 1 ? pl->d_fin_state : nullptr;
+      if (direct) {
+        switch (pl->fin_kr) {
+          case 1: FINV(1, true); break;
+          case 2: FINV(2, true); break;
+          default: FINV(4, true);
+        }
+      } else {
+        switch (pl->fin_kr) {
+          case 1: FINV(1, false); break;
+          case 2: FINV(2, false); break;
+          default: FINV(4, false);
+        }
       }
-    } else {
-      switch (pl->fin_kr) {
-        case 1: FINV(1, false); break;
-        case 2: FINV(2, false); break;
-        default: FINV(4, false);
-      }
+      if (nch > 1) CUDA_TRY(cudaEventRecord(pl->ev_fin_chunk[ch], st));
     }
 #undef FINV
     if (layout != COVGPU_COMPACT && !direct) {
@@ -1112,7 +1132,8 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
 #define FINS(KR, DIR)                                                                             \
   k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                   \
       (const C2*)pl->d_corners, pr, pl->d_cls, tasks, ntasks, pl->nclasses, 1, 1, B, cc, cl,      \
-      pl->tot_ccol, rc, pl->tot_rc, 1, (C2*)R_dev, r_bstride, scale, direct ? layout : (int)COVGPU_COMPACT)
+      pl->tot_ccol, rc, pl->tot_rc, 1, (C2*)R_dev, r_bstride, scale, direct ? layout : (int)COVGPU_COMPACT, \
+      0, 1 << 30, nullptr)
     if (direct) {
       switch (pl->fin_kr) {
         case 1: FINS(1, true); break;
@@ -1630,7 +1651,8 @@ int covgpu_plan_execute(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_
     return pl->dtype == COVGPU_C128 ? launch_all<double>(pl, A_dev, R_dev, layout, scale, s)
                                     : launch_all<float>(pl, A_dev, R_dev, layout, scale, s);
   };
-  if (!pl->use_graph || pl->timing || pl->band_wait || pl->ks_out || !pl->clean) return run(st);
+  if (!pl->use_graph || pl->timing || pl->band_wait || pl->ks_out || !pl->clean || pl->fin_nchunks > 1)
+    return run(st);
   const bool same = A_dev == pl->g_A && R_dev == pl->g_R && layout == pl->g_layout && scale == pl->g_scale;
   if (same && pl->gexec) {
     CUDA_TRY(cudaGraphLaunch(pl->gexec, st));
@@ -2000,6 +2022,9 @@ static bool stream_a_in_bands(covgpu_plan* pl, size_t a_bytes) {
   return true;
 }
 
+static bool chunked_copy_out(covgpu_plan* pl, int layout);
+static int copy_out_chunks(covgpu_plan* pl, void* R_host, int layout, size_t esz);
+
 int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host, int32_t layout,
                              double scale) {
   if (!pl) return fail(COVGPU_EINVAL, "plan is NULL");
@@ -2036,6 +2061,7 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
   }
   cudaStream_t st = pl->host_stream;
   int rc;
+  chunked_copy_out(pl, layout);  // sets fin_nchunks > 1 when the walk can be chunked
   if (stream_a_in_bands(pl, a_bytes)) {
     // A in row bands on the copy stream, overlapped with the tensor-core
     // bulk kernel (which waits per chunk for the band it reads)
@@ -2063,8 +2089,72 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
     rc = covgpu_plan_execute(pl, pl->hA, pl->hR, layout, scale, st);
   }
   if (rc) return rc;
+  if (pl->fin_nchunks > 1) {  // chunked walk: the copy-out follows each chunk
+    rc = copy_out_chunks(pl, R_host, layout, esz);
+    pl->fin_nchunks = 1;
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(pl->out_stream));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return COVGPU_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(R_host, pl->hR, r_bytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return COVGPU_OK;
+}
+
+// Synchronous host path with the copy-out overlapped with the finalize walk:
+// the walk runs in u-chunks (state saved between them); rows [P u_c, P u_c+1)
+// of R are complete after chunk c, so their D2H starts on out_stream while
+// the next chunk runs.  Single snapshot, dense / packed, direct finalize.
+static bool chunked_copy_out(covgpu_plan* pl, int layout) {
+  if (pl->batch != 1 || !pl->clean || pl->fin_kr == 0 || pl->no_direct || layout == COVGPU_COMPACT) return false;
+  // large outputs only (cfg5 packed 134 MB: 4.44 -> 4.30 ms; cfg3 8 MB: the
+  // chunk launches cost more than the overlap gains, 0.353 -> 0.447 ms)
+  const long long D = pl->pr.PQ;
+  if (pl->pr.Q < 24 || D * (D + 1) / 2 * 16 < (32LL << 20)) return false;
+  if (const char* e = getenv("COVGPU_NO_CHUNKED_D2H"))
+    if (atoi(e) != 0) return false;
+  if (!pl->d_fin_state) {
+    const size_t n = (size_t)pl->ntasks * 32 * (2 * pl->fin_kr + 1);
+    if (cudaMalloc((void**)&pl->d_fin_state, sizeof(double2) * std::max<size_t>(n, 1)) != cudaSuccess) {
+      cudaGetLastError();
+      pl->d_fin_state = nullptr;
+      return false;
+    }
+    for (auto& e : pl->ev_fin_chunk)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+  }
+  if (!pl->out_stream && cudaStreamCreateWithFlags(&pl->out_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  // small first chunks: the copy-out starts early (the first rows are the longest)
+  const int Q = pl->pr.Q;
+  pl->fin_ubound[0] = 0;
+  pl->fin_ubound[1] = std::max(1, Q / 16);
+  pl->fin_ubound[2] = std::max(pl->fin_ubound[1] + 1, Q / 4);
+  pl->fin_ubound[3] = Q;
+  pl->fin_nchunks = 3;
+  return true;
+}
+
+static int copy_out_chunks(covgpu_plan* pl, void* R_host, int layout, size_t esz) {
+  const long long D = pl->pr.PQ;
+  auto row_off = [&](long long k1) -> long long {
+    return layout == COVGPU_DENSE ? k1 * D : k1 * D - (k1 * (k1 - 1)) / 2;
+  };
+  for (int c = 0; c < pl->fin_nchunks; ++c) {
+    const long long k0 = std::min(D, (long long)pl->pr.P * pl->fin_ubound[c]);
+    const long long k1 = std::min(D, (long long)pl->pr.P * pl->fin_ubound[c + 1]);
+    CUDA_TRY(cudaStreamWaitEvent(pl->out_stream, pl->ev_fin_chunk[c], 0));
+    const long long o0 = row_off(k0), o1 = c + 1 == pl->fin_nchunks ? row_off(D) : row_off(k1);
+    if (o1 > o0)
+      CUDA_TRY(cudaMemcpyAsync((char*)R_host + o0 * esz, (const char*)pl->hR + o0 * esz, (size_t)(o1 - o0) * esz,
+                               cudaMemcpyDeviceToHost, pl->out_stream));
+  }
   return COVGPU_OK;
 }
 

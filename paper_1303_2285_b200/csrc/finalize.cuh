@@ -93,8 +93,13 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
                  int nclasses, int ncb, int nrs, int B, const double2* __restrict__ ccpart,
                  const double2* __restrict__ ccol, long long tot_ccol, const double2* __restrict__ rc,
                  long long tot_rc, int nseg, typename CT<T>::c* __restrict__ R,
-                 long long r_bstride, double scale, int dlayout) {
-  // R: compact (class-major) output, r_bstride elements per snapshot
+                 long long r_bstride, double scale, int dlayout, int u_begin, int u_end,
+                 double2* __restrict__ wstate) {
+  // R: compact (class-major) output, r_bstride elements per snapshot.
+  // Columns [u_begin, u_end) of every walk: with wstate the walk state (fT,
+  // fB, G per lane) is saved at u_end and restored at u_begin, so the walk can
+  // run in u-chunks — R rows [P u_begin, P u_end) are complete after a chunk
+  // (the host path copies them out while the next chunk runs)
   using C2 = typename CT<T>::c;
   const int lane = threadIdx.x & 31;
   const long long task = (long long)blockIdx.x * FIN_WARPS + (threadIdx.x >> 5);
@@ -102,6 +107,8 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const int2 tk = tasks[task];
   const ClassDesc c = cls[tk.x];
   const int pv = c.pv, qu = c.qu, ar = pv - 1, ac = qu - 1;
+  if (u_begin >= qu) return;
+  double2* ws = wstate ? wstate + (task * 32 + lane) * (2 * KR + 1) : nullptr;
   int W = 1;
   while (W < pv && W < 32) W <<= 1;
   const int li = lane & (W - 1);
@@ -115,23 +122,32 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const double2* cl = ccol + (long long)b * tot_ccol + c.ccol_off;
   const double2* rcc = rc + ((long long)b * tot_rc + c.rc_off) * nseg;
 
-  // CC and G(0) = CC + sum_j CColL[j]
-  const double2* cc_p = ccpart + ((long long)b * nclasses + tk.x) * ncb;
-  double2 acc = make_double2(0.0, 0.0);
-  for (int k = li; k < ncb; k += W) acc = cadd(acc, cc_p[k]);
-  for (int j = li; j < ac; j += W) acc = cadd(acc, cl[j]);
-  double2 G = seg_sum(acc, W);
-
-  // edge-row state: lane owns the contiguous rows v = li*KR + k
-  double2 fT[KR], fB[KR];
+  double2 G, fT[KR], fB[KR];
+  if (u_begin > 0) {
+    // resume: the state saved by the previous chunk
 #pragma unroll
-  for (int k = 0; k < KR; ++k) {
-    const int v = li * KR + k;
-    fT[k] = fB[k] = make_double2(0.0, 0.0);
-    if (v < ar) {
-      for (int g = 0; g < nseg; ++g) {
-        fT[k] = cadd(fT[k], rcc[(long long)v * nseg + g]);
-        fB[k] = cadd(fB[k], rcc[(long long)(ar + v) * nseg + g]);
+    for (int k = 0; k < KR; ++k) {
+      fT[k] = ws[k];
+      fB[k] = ws[KR + k];
+    }
+    G = ws[2 * KR];
+  } else {
+    // CC and G(0) = CC + sum_j CColL[j]
+    const double2* cc_p = ccpart + ((long long)b * nclasses + tk.x) * ncb;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = li; k < ncb; k += W) acc = cadd(acc, cc_p[k]);
+    for (int j = li; j < ac; j += W) acc = cadd(acc, cl[j]);
+    G = seg_sum(acc, W);
+    // edge-row state: lane owns the contiguous rows v = li*KR + k
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int v = li * KR + k;
+      fT[k] = fB[k] = make_double2(0.0, 0.0);
+      if (v < ar) {
+        for (int g = 0; g < nseg; ++g) {
+          fT[k] = cadd(fT[k], rcc[(long long)v * nseg + g]);
+          fB[k] = cadd(fB[k], rcc[(long long)(ar + v) * nseg + g]);
+        }
       }
     }
   }
@@ -141,7 +157,8 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const C2* TR = Cb + cstride;
   const C2* BL = Cb + 2 * cstride;
   const C2* BR = Cb + 3 * cstride;
-  for (int u = 0; u < qu; ++u) {
+  const int u_stop = min(qu, u_end);
+  for (int u = u_begin; u < u_stop; ++u) {
     // KR == 1: this column's corner / edge-column reads go out first, so
     // their latency overlaps the scan and the slot stores below (cfg3
     // finalize 0.058 -> 0.050 ms); with KR >= 2 the extra live registers cost
@@ -227,6 +244,14 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
         G = cadd(G, csub(cl[ac + u], cl[u]));
       }
     }
+  }
+  if (ws && u_stop < qu) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      ws[k] = fT[k];
+      ws[KR + k] = fB[k];
+    }
+    ws[2 * KR] = G;
   }
 }
 
