@@ -660,6 +660,19 @@ std::vector<double2> spec_twiddles(int logL) {
 // Spectral kernels are instantiated for FFT lengths 2^6 .. 2^12; SPEC_LOGL
 // dispatches a launch on the runtime log2 length (SMEM attribute set once per
 // instantiation: up to (L + L/8) complex values).
+// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda)
+PFN_cuStreamWaitValue32_v11070 stream_wait_value() {
+  static PFN_cuStreamWaitValue32_v11070 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  }();
+  return fn;
+}
+
 template <typename K>
 void spec_attr(K* fn, int logL) {
   // once per kernel instantiation (keyed on the function, not its type: the
@@ -726,11 +739,25 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   // side stream (es): the edge-column sums depend only on A; main stream:
   // row spectra -> dr = 0 per-row transforms, correlation -> output FFT ->
   // edge rows
-  SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
-            pl->d_fy);
+  if (pl->band_wait && B == 1 && stream_wait_value()) {
+    // host path streaming A in row bands: each band's row FFTs start as soon
+    // as the copy stream has signalled the band (under the rest of the H2D)
+    const int nb = (pr.N + pl->band_rows - 1) / pl->band_rows;
+    for (int k = 0; k < nb; ++k) {
+      const int r0 = k * pl->band_rows, r1 = std::min(pr.N, r0 + pl->band_rows);
+      stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
+                          CU_STREAM_WAIT_VALUE_GEQ);
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
+                pl->d_fx, pl->d_fy, r0, r1 - r0);
+    }
+  } else {
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
+              pl->d_fy, 0, pr.N);
+  }
+  if (pl->band_wait) cudaStreamWaitEvent(st, pl->ev_h2d, 0);  // the rest reads all of A
   if (pl->spec_edges)
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
-              pl->d_fy0);
+              pl->d_fy0, 0, pr.N);
   mark("spec_fft");
   // the dr = 0 row transforms and the edge-row pair FFTs need only the row
   // spectra: side stream after the FFTs (they fill the SMs around the
@@ -946,7 +973,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   // bulk over every column block (which also yields the edge-column sums)
   bool mma = false;
   if (pl->use_spec) {
-    if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
+    // (band_wait: launch_spectral waits per band for the row FFTs, then for all of A)
     launch_spectral<T>(pl, A, st, es, mark);
     launches += 8;  // rowac, fft x2, corr, gsum, dft, colfft, ccol, rc
     mma = true;

@@ -248,7 +248,8 @@ struct SpecLayout {
 template <typename T, int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_fft(long long nitems, const typename CT<T>::c* __restrict__ A, Problem pr, int mode, SpecLayout lay,
-               const double2* __restrict__ tw, double2* __restrict__ FX, double2* __restrict__ FY) {
+               const double2* __restrict__ tw, double2* __restrict__ FX, double2* __restrict__ FY, int row0,
+               int nrows) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   double2* sb;
@@ -258,11 +259,11 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   int r, clo, chi;
   long long orow;
   double2* out;
-  if (mode == 0) {
+  if (mode == 0) {  // rows [row0, row0 + nrows)
     const int which = (int)(t & 1);
     t >>= 1;
-    r = (int)(t % N);
-    const long long b = t / N;
+    r = row0 + (int)(t % nrows);
+    const long long b = t / nrows;
     clo = which ? Q - 1 : 0;
     chi = which ? M - 1 : M - Q;
     orow = b * N + r;
