@@ -657,6 +657,11 @@ std::vector<double2> spec_twiddles(int logL) {
   return t;
 }
 
+// G partial slots reserved for the banded correlation of the host path
+constexpr int kMaxBandSlots = 32;
+// rows per H2D band of the single-snapshot host path: ~16 bands, >= 64 rows
+int host_band_rows(long long n) { return (int)std::max(64LL, (n + 15) / 16); }
+
 // Spectral kernels are instantiated for FFT lengths 2^6 .. 2^12; SPEC_LOGL
 // dispatches a launch on the runtime log2 length (SMEM attribute set once per
 // instantiation: up to (L + L/8) complex values).
@@ -739,16 +744,58 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   // side stream (es): the edge-column sums depend only on A; main stream:
   // row spectra -> dr = 0 per-row transforms, correlation -> output FFT ->
   // edge rows
+  // correlation launch for chunk range `part_` of `nparts_` into G slots [slot0, slot0 + nseg_)
+  auto corr_smem = [&](int nseg_, int part_, int nparts_, int slot0, int nslots) {
+    const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
+    const unsigned blocks = (unsigned)(B * pl->spec_lay.nfb * nseg_);
+    auto kern = pl->spec_e == 8 ? &k_spec_corr_smem<8, 16> : &k_spec_corr_smem<16, 8>;
+    {
+      static std::mutex mu;
+      static std::vector<const void*> done;
+      std::lock_guard<std::mutex> lk(mu);
+      if (std::find(done.begin(), done.end(), (const void*)kern) == done.end()) {
+        cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        done.push_back((const void*)kern);
+      }
+    }
+    kern<<<blocks, pl->spec_ngrp * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, nseg_, part_, nparts_,
+                                                pl->spec_stages, pl->d_gp, slot0, nslots);
+  };
+  int gslots = pl->spec_nseg;  // G partial slots the output FFT sums
+  bool corr_done = false;
   if (pl->band_wait && B == 1 && stream_wait_value()) {
     // host path streaming A in row bands: each band's row FFTs start as soon
-    // as the copy stream has signalled the band (under the rest of the H2D)
-    const int nb = (pr.N + pl->band_rows - 1) / pl->band_rows;
-    for (int k = 0; k < nb; ++k) {
-      const int r0 = k * pl->band_rows, r1 = std::min(pr.N, r0 + pl->band_rows);
-      stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
-                          CU_STREAM_WAIT_VALUE_GEQ);
-      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
-                pl->d_fx, pl->d_fy, r0, r1 - r0);
+    // as the copy stream has signalled the band, and (SMEM correlation) each
+    // band's rows of the correlation as soon as its +P-1 halo is transformed —
+    // under the rest of the H2D
+    const int br = pl->band_rows, nb = (pr.N + br - 1) / br;
+    const int nch = (pr.N + SC_RC - 1) / SC_RC;
+    const bool band_corr = pl->spec_smem && nb <= kMaxBandSlots;
+    int fft_done = 0;  // bands transformed
+    auto fft_upto = [&](int m) {  // row FFTs of bands [fft_done, m]
+      for (; fft_done <= m && fft_done < nb; ++fft_done) {
+        const int k = fft_done, r0 = k * br, r1 = std::min(pr.N, r0 + br);
+        stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
+                  pl->d_fx, pl->d_fy, r0, r1 - r0);
+      }
+    };
+    for (int j = 0; j < nb; ++j) {
+      if (!band_corr) {
+        fft_upto(j);
+        continue;
+      }
+      // part j of nb chunk ranges reads X rows up to its last row + P-1
+      const int cz = (int)((long long)nch * (j + 1) / nb);
+      const int hi = std::min(pr.N - 1, cz * SC_RC - 1 + pr.P - 1);
+      fft_upto(hi / br);
+      corr_smem(1, j, nb, j, nb);
+    }
+    fft_upto(nb - 1);
+    if (band_corr) {
+      gslots = nb;
+      corr_done = true;
     }
   } else {
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
@@ -778,33 +825,20 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
               pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
   st = st_main;
   mark("spec_rowac");
-  if (pl->spec_smem) {
-    const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
-    const unsigned blocks = (unsigned)(B * pl->spec_lay.nfb * pl->spec_nseg);
-    auto launch_corr = [&](auto kern) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-      }
-      kern<<<blocks, pl->spec_ngrp * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, pl->spec_nseg, part,
-                                                   nparts, pl->spec_stages, pl->d_gp);
-    };
-    if (pl->spec_e == 8)
-      launch_corr(k_spec_corr_smem<8, 16>);
-    else
-      launch_corr(k_spec_corr_smem<16, 8>);
+  if (corr_done) {
+  } else if (pl->spec_smem) {
+    corr_smem(pl->spec_nseg, part, nparts, 0, pl->spec_nseg);
   } else {
     k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
         pl->d_fx, pl->d_fy, pr, pl->spec_lay, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts,
         pl->d_gp);
   }
   mark("spec_corr");
-  if (pl->spec_nseg > 1) {  // row-segment partials -> segment 0, in order
+  if (gslots > 1) {  // row-segment partials -> slot 0, in order
     const long long per_seg = (long long)(2 * pr.P - 1) * L, tot = B * per_seg;
-    k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, pl->spec_nseg, per_seg, tot);
+    k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, gslots, per_seg, tot);
   }
-  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pr, pl->spec_nseg,
+  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pr, gslots,
             pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
   if (pl->spec_edges) {
     mark("spec_dft");
@@ -1437,6 +1471,13 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
           }
         }
         pl->spec_nseg = best;
+        // single snapshots the host path streams in row bands: one row segment
+        // per band, so the band-wise correlation under the H2D adds the same
+        // partials in the same order as the device path (bitwise equal)
+        if (batch == 1 && pl->use_mma && n * m * 16 >= (8LL << 20)) {
+          const long long nb = (n + host_band_rows(n) - 1) / host_band_rows(n);
+          if (nb <= kMaxBandSlots) pl->spec_nseg = (int)nb;
+        }
       }
       const long long d0rows = n - 2LL * p + 2;
       pl->spec_nd0 = (int)std::max(1LL, d0rows);  // N = 2P-2: no core rows
@@ -1559,7 +1600,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const size_t fxe = (size_t)batch * pl->spec_lay.nfb * pl->spec_lay.np * 32;
     if ((rc = dalloc(&pl->d_tw, L, &ws)) || (rc = dalloc(&pl->d_fx, fxe, &ws)) ||
         (rc = dalloc(&pl->d_fy, fxe, &ws)) ||
-        (rc = dalloc(&pl->d_gp, (size_t)batch * pl->spec_nseg * (2 * p - 1) * L, &ws)) ||
+        (rc = dalloc(&pl->d_gp, (size_t)batch * std::max(pl->spec_nseg, batch == 1 ? kMaxBandSlots : 1) *
+                                    (2 * p - 1) * L, &ws)) ||
         (rc = dalloc(&pl->d_d0p, (size_t)batch * pl->spec_nd0 * q, &ws))) {
       plan_free(pl.get());
       return rc;
@@ -2044,8 +2086,7 @@ static bool stream_a_in_bands(covgpu_plan* pl, size_t a_bytes) {
     }
     pl->band_base = 0;
   }
-  // ~16 bands, at least 64 rows each
-  pl->band_rows = std::max(64, (pl->pr.N + 15) / 16);
+  pl->band_rows = host_band_rows(pl->pr.N);
   return true;
 }
 

@@ -587,7 +587,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 template <int E, int MAXW>
 __global__ void __launch_bounds__(MAXW * 32, 1)
     k_spec_corr_smem(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay,
-                     int nseg, int part, int nparts, int stages, double2* __restrict__ Gp) {
+                     int nseg, int part, int nparts, int stages, double2* __restrict__ Gp, int slot0, int nslots) {
   const int NG = blockDim.x >> 5;
   extern __shared__ __align__(128) unsigned char scraw[];
   const int P = pr.P, N = pr.N;
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   const int f = fb * 32 + lane;
-  double2* out = Gp + (b * nseg + seg) * (long long)nlag * (lay.nfb * 32) + f;
+  double2* out = Gp + (b * nslots + slot0 + seg) * (long long)nlag * (lay.nfb * 32) + f;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int dr = dr0 + e;
