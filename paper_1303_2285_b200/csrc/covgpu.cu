@@ -149,6 +149,7 @@ struct covgpu_plan {
   int band_rows = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_h2d = nullptr;
+  cudaEvent_t ev_strips = nullptr;  // spectral host path: edge columns + strip rows copied
   bool use_erm = false;
   int erm_dct = 1;
   const void* erm_ptr = nullptr;
@@ -326,6 +327,7 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_rtasks);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
+  if (pl->ev_strips) cudaEventDestroy(pl->ev_strips);
   cudaFree(pl->d_ecm_tickets);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
@@ -665,6 +667,8 @@ int host_band_rows(long long n) { return (int)std::max(64LL, (n + 15) / 16); }
 // Spectral kernels are instantiated for FFT lengths 2^6 .. 2^12; SPEC_LOGL
 // dispatches a launch on the runtime log2 length (SMEM attribute set once per
 // instantiation: up to (L + L/8) complex values).
+#define CUDA_TRY_V(expr) (void)(expr)
+
 // cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda)
 PFN_cuStreamWaitValue32_v11070 stream_wait_value() {
   static PFN_cuStreamWaitValue32_v11070 fn = [] {
@@ -763,22 +767,43 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   };
   int gslots = pl->spec_nseg;  // G partial slots the output FFT sums
   bool corr_done = false;
-  if (pl->band_wait && B == 1 && stream_wait_value()) {
-    // host path streaming A in row bands: each band's row FFTs start as soon
-    // as the copy stream has signalled the band, and (SMEM correlation) each
-    // band's rows of the correlation as soon as its +P-1 halo is transformed —
-    // under the rest of the H2D
-    const int br = pl->band_rows, nb = (pr.N + br - 1) / br;
-    const int nch = (pr.N + SC_RC - 1) / SC_RC;
+  const bool band_mode = pl->band_wait && B == 1 && stream_wait_value();
+  if (band_mode) {
+    // host path streaming A: the copy stream sends the edge columns and the
+    // top / bottom strip rows first (ev_strips), then the remaining rows in
+    // bands (band counter).  Strip-row spectra right after ev_strips (the
+    // side stream's edge sums start from them); each band's row FFTs and
+    // dr = 0 row transforms as soon as the band is signalled; each band's
+    // rows of the correlation once its +P-1 halo is transformed — all under
+    // the rest of the H2D.
+    const int N = pr.N;
+    CUDA_TRY_V(cudaStreamWaitEvent(st, pl->ev_strips, 0));
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * S * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
+              pl->d_fy, 0, S);
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * S * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
+              pl->d_fy, N - S, S);
+    if (pl->spec_edges)
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
+                pl->d_fy0, 0, N);
+    if (es != st) {  // the side stream: edge-row pair FFTs from the strip spectra
+      cudaEventRecord(pl->ev_d0, st);
+      cudaStreamWaitEvent(es, pl->ev_d0, 0);
+    }
+    const int br = pl->band_rows, nb = (N + br - 1) / br;
+    const int nch = (N + SC_RC - 1) / SC_RC;
     const bool band_corr = pl->spec_smem && nb <= kMaxBandSlots;
     int fft_done = 0;  // bands transformed
-    auto fft_upto = [&](int m) {  // row FFTs of bands [fft_done, m]
+    auto fft_upto = [&](int m) {  // rows of bands [fft_done, m] outside the strips
       for (; fft_done <= m && fft_done < nb; ++fft_done) {
-        const int k = fft_done, r0 = k * br, r1 = std::min(pr.N, r0 + br);
+        const int k = fft_done, r0 = std::max(S, k * br), r1 = std::min(N - S, (k + 1) * br);
         stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
                             CU_STREAM_WAIT_VALUE_GEQ);
+        if (r1 <= r0) continue;
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
                   pl->d_fx, pl->d_fy, r0, r1 - r0);
+        // dr = 0 rows: the core rows [P-1, N-P] = the non-strip rows
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (r1 - r0), pl->d_fx, pl->d_fy, pr,
+                  pl->spec_lay, pl->d_tw, r0, r1 - r0, rz - ra + 1, r0 - ra, pl->d_d0p);
       }
     };
     for (int j = 0; j < nb; ++j) {
@@ -788,7 +813,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       }
       // part j of nb chunk ranges reads X rows up to its last row + P-1
       const int cz = (int)((long long)nch * (j + 1) / nb);
-      const int hi = std::min(pr.N - 1, cz * SC_RC - 1 + pr.P - 1);
+      const int hi = std::min(N - 1, cz * SC_RC - 1 + pr.P - 1);
       fft_upto(hi / br);
       corr_smem(1, j, nb, j, nb);
     }
@@ -797,34 +822,44 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       gslots = nb;
       corr_done = true;
     }
+    mark("spec_fft");
+    k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
+                                                       pl->d_cls_slot, pl->d_ccpart);
+    if (pl->spec_edges && es != st) {
+      const cudaStream_t st_main = st;
+      st = es;
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      st = st_main;
+    }
+    mark("spec_rowac");
   } else {
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
               pl->d_fy, 0, pr.N);
+    if (pl->spec_edges)
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
+                pl->d_fy0, 0, pr.N);
+    mark("spec_fft");
+    // the dr = 0 row transforms and the edge-row pair FFTs need only the row
+    // spectra: side stream after the FFTs (they fill the SMs around the
+    // correlation kernel)
+    const cudaStream_t st_main = st;
+    if (es != st) {
+      cudaEventRecord(pl->ev_d0, st);
+      cudaStreamWaitEvent(es, pl->ev_d0, 0);
+      st = es;
+    }
+    if (rz >= ra)
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr,
+                pl->spec_lay, pl->d_tw, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
+    k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
+                                                       pl->d_cls_slot, pl->d_ccpart);
+    if (pl->spec_edges && es != st_main)
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+    st = st_main;
+    mark("spec_rowac");
   }
-  if (pl->band_wait) cudaStreamWaitEvent(st, pl->ev_h2d, 0);  // the rest reads all of A
-  if (pl->spec_edges)
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
-              pl->d_fy0, 0, pr.N);
-  mark("spec_fft");
-  // the dr = 0 row transforms and the edge-row pair FFTs need only the row
-  // spectra: side stream after the FFTs (they fill the SMs around the
-  // correlation kernel)
-  const cudaStream_t st_main = st;
-  if (es != st) {
-    cudaEventRecord(pl->ev_d0, st);
-    cudaStreamWaitEvent(es, pl->ev_d0, 0);
-    st = es;
-  }
-  if (rz >= ra)
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr, pl->spec_lay,
-              pl->d_tw, ra, rz - ra + 1, rz - ra + 1, pl->d_d0p);
-  k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
-                                                     pl->d_cls_slot, pl->d_ccpart);
-  if (pl->spec_edges && es != st_main)
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-              pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
-  st = st_main;
-  mark("spec_rowac");
   if (corr_done) {
   } else if (pl->spec_smem) {
     corr_smem(pl->spec_nseg, part, nparts, 0, pl->spec_nseg);
@@ -1001,7 +1036,10 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(es, pl->ev_fork, 0));
   }
-  if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(es, pl->ev_h2d, 0));
+  // (spectral host path: the side stream's kernels read only the early-copied
+  // edge columns / strip rows and spectra made from them)
+  if (pl->band_wait)
+    CUDA_TRY(cudaStreamWaitEvent(es, pl->use_spec && pl->batch == 1 ? pl->ev_strips : pl->ev_h2d, 0));
   mark("start");
   // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
   // bulk over every column block (which also yields the edge-column sums)
@@ -2137,10 +2175,44 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
     const size_t row_bytes = (size_t)pr.M * esz;
     auto wv = stream_write_value();
     const unsigned base = pl->band_base;
+    const bool strips_first = pl->use_spec && pl->batch == 1;
+    const int S = pr.P - 1, Sc = pr.Q - 1;
+    char* dA = (char*)pl->hA;
+    const char* hA = (const char*)A_host;
+    const size_t mid0 = (size_t)Sc * esz, midw = (size_t)(pr.M - 2 * Sc) * esz;
+    if (strips_first) {
+      // spectral engine: the edge columns (all rows) and the top / bottom strip
+      // rows first — the edge sums need only these — then the other rows' middle
+      // columns in bands
+      if (!pl->ev_strips) CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_strips, cudaEventDisableTiming));
+      if (Sc > 0) {
+        CUDA_TRY(cudaMemcpy2DAsync(dA, row_bytes, hA, row_bytes, (size_t)Sc * esz, pr.N, cudaMemcpyHostToDevice,
+                                   pl->copy_stream));
+        CUDA_TRY(cudaMemcpy2DAsync(dA + (size_t)(pr.M - Sc) * esz, row_bytes, hA + (size_t)(pr.M - Sc) * esz,
+                                   row_bytes, (size_t)Sc * esz, pr.N, cudaMemcpyHostToDevice, pl->copy_stream));
+      }
+      if (S > 0 && midw > 0) {
+        CUDA_TRY(cudaMemcpy2DAsync(dA + mid0, row_bytes, hA + mid0, row_bytes, midw, S, cudaMemcpyHostToDevice,
+                                   pl->copy_stream));
+        CUDA_TRY(cudaMemcpy2DAsync(dA + (size_t)(pr.N - S) * row_bytes + mid0, row_bytes,
+                                   hA + (size_t)(pr.N - S) * row_bytes + mid0, row_bytes, midw, S,
+                                   cudaMemcpyHostToDevice, pl->copy_stream));
+      }
+      CUDA_TRY(cudaEventRecord(pl->ev_strips, pl->copy_stream));
+    }
     for (int k = 0; k < nb; ++k) {
-      const int r0 = k * pl->band_rows, r1 = std::min(pr.N, r0 + pl->band_rows);
-      CUDA_TRY(cudaMemcpyAsync((char*)pl->hA + r0 * row_bytes, (const char*)A_host + r0 * row_bytes,
-                               (r1 - r0) * row_bytes, cudaMemcpyHostToDevice, pl->copy_stream));
+      int r0 = k * pl->band_rows, r1 = std::min(pr.N, r0 + pl->band_rows);
+      if (strips_first) {
+        r0 = std::max(r0, S);
+        r1 = std::min(r1, pr.N - S);
+        if (r1 > r0 && midw > 0)
+          CUDA_TRY(cudaMemcpy2DAsync(dA + (size_t)r0 * row_bytes + mid0, row_bytes,
+                                     hA + (size_t)r0 * row_bytes + mid0, row_bytes, midw, r1 - r0,
+                                     cudaMemcpyHostToDevice, pl->copy_stream));
+      } else {
+        CUDA_TRY(cudaMemcpyAsync(dA + r0 * row_bytes, hA + r0 * row_bytes, (r1 - r0) * row_bytes,
+                                 cudaMemcpyHostToDevice, pl->copy_stream));
+      }
       if (wv(pl->copy_stream, (CUdeviceptr)pl->d_band_flag, base + (unsigned)k + 1u, 0) != CUDA_SUCCESS)
         return fail(COVGPU_ECUDA, "cuStreamWriteValue32");
     }

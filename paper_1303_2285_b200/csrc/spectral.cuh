@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
 template <int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_rowac(long long nitems, const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr,
-                 SpecLayout lay, const double2* __restrict__ tw, int row_a, int nrows, int nd0,
+                 SpecLayout lay, const double2* __restrict__ tw, int row_a, int nrows, int nd0, int kbase,
                  double2* __restrict__ D0p) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const double2* fy = FY + lay.at(b, r, 0);
   const long long fs = (long long)lay.np * 32;
   const double inv = 1.0 / (double)L;
-  double2* out = D0p + (b * nd0 + k) * (long long)Q;
+  double2* out = D0p + (b * nd0 + kbase + k) * (long long)Q;
   spec_fft_block<LOGL>(
       sb, si.tl, tw,
       [&](int idx) {
