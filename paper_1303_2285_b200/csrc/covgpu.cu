@@ -2035,7 +2035,9 @@ static int execute_host_pipelined(covgpu_plan_t pl, const void* A_host, void* R_
   const Problem& pr = pl->pr;
   const size_t esz = pl->dtype == COVGPU_C128 ? 16 : 8;
   const long long B = pl->batch;
-  const long long nch = std::min<long long>(16, B);
+  long long nsub = 32;  // cfg4: 16 -> 3.38 ms, 32 -> 3.03 ms, 64 -> 3.72 ms (bidirectional PCIe floor 2.68 ms)
+  if (const char* e = getenv("COVGPU_PIPE_SUBBATCHES")) nsub = std::max(2, atoi(e));
+  const long long nch = std::min<long long>(nsub, B);
   const long long sub = (B + nch - 1) / nch;
   const long long tail = B - (B - 1) / sub * sub;  // size of the last sub-batch
   long long r_per_b;
