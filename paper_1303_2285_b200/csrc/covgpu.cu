@@ -845,8 +845,28 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     }
     mark("spec_rowac");
   } else {
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
-              pl->d_fy, 0, pr.N);
+    if (nparts > 1 && pl->spec_smem) {
+      // multi-GPU row band: transform only the rows this part reads — its
+      // correlation rows +- P-1, its dr = 0 rows and the two strips (edge-row
+      // pairs); overlapping ranges write the same values
+      const int nch = (pr.N + SC_RC - 1) / SC_RC;
+      const int pieces = nparts * pl->spec_nseg;
+      const int c0 = (int)((long long)nch * part * pl->spec_nseg / pieces);
+      const int c1 = (int)((long long)nch * (part + 1) * pl->spec_nseg / pieces);
+      int ranges[4][2] = {{std::max(0, c0 * SC_RC - (pr.P - 1)), std::min(pr.N, c1 * SC_RC + pr.P - 1)},
+                          {ra, rz + 1},
+                          {0, S},
+                          {pr.N - S, pr.N}};
+      for (auto& rg : ranges) {
+        const int r0 = std::max(0, rg[0]), r1 = std::min(pr.N, rg[1]);
+        if (r1 > r0)
+          SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
+                    pl->d_fx, pl->d_fy, r0, r1 - r0);
+      }
+    } else {
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
+                pl->d_fy, 0, pr.N);
+    }
     if (pl->spec_edges)
       SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
                 pl->d_fy0, 0, pr.N);

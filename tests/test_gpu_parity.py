@@ -637,10 +637,13 @@ def test_row_band_sums_and_class_range_finalize(cuda):
     assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= 1e-15
     full_c = plan.finalize_sums(a, s1, plan.alloc_output("compact"), "compact")
     assert (torch.linalg.norm(full_c - ref_c) / torch.linalg.norm(ref_c)).item() <= 1e-15
-    # three bands summed
+    # three bands summed, each on a fresh plan (as on its own GPU: a band may
+    # read only the row spectra it computed itself)
     tot = plan.alloc_sums()
     for part in range(3):
-        tot += plan.execute_sums(a, plan.alloc_sums(), part, 3)
+        pp = Plan(n, m, win, dtype=torch.complex128, device=cuda)
+        tot += pp.execute_sums(a, pp.alloc_sums(), part, 3)
+        pp.close()
     got3 = plan.finalize_sums(a, tot, plan.alloc_output(), "dense")
     err = (torch.linalg.norm(got3 - ref) / torch.linalg.norm(ref)).item()
     assert err <= 1e-14, err
