@@ -550,19 +550,23 @@ def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, spectr
         assert err_cc <= 1e-13, err_cc
 
 
-def test_host_path_streams_a_in_bands_bitwise(cuda):
-    """Single-snapshot host path on the tensor-core kernels: A is copied in
-    row bands while k_bulk_dmma runs (band counter written by the copy
-    stream); R must equal the device-resident result bit for bit, twice in a
-    row (the band counter carries over between executes)."""
+@pytest.mark.parametrize("n,m,p,q,spectral", [(1024, 1024, 64, 64, True), (1500, 900, 40, 50, True),
+                                              (1024, 1024, 64, 64, False)])
+def test_host_path_streams_a_in_bands_bitwise(cuda, n, m, p, q, spectral, monkeypatch):
+    """Single-snapshot host path: A is copied in row bands (spectral engine:
+    edge columns and strip rows first) while the kernels run (band counter
+    written by the copy stream); R must equal the device-resident result bit
+    for bit, twice in a row (the band counter carries over between executes)
+    and with the finalize walk chunked under the copy-out."""
     from paper_1303_2285_b200.plan import Plan
 
-    n = m = 1024
-    p = q = 64
+    if not spectral:
+        monkeypatch.setenv("COVGPU_NO_SPECTRAL", "1")
     rng = np.random.default_rng(5)
     a = torch.from_numpy(rng.standard_normal((1, n, m)) + 1j * rng.standard_normal((1, n, m))).pin_memory()
     win = WindowSpec(p, q)
     plan = Plan(n, m, win, dtype=torch.complex128, device=cuda)
+    assert plan.spectral == spectral
     dev = plan.alloc_output("packed")
     plan.execute(a.to(cuda), dev, "packed")
     out = torch.empty(plan.output_elems("packed"), dtype=torch.complex128).pin_memory()
