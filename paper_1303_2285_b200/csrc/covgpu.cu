@@ -130,6 +130,9 @@ struct covgpu_plan {
   bool spec_edges = false;
   int spec_logLr = 0;
   double2 *d_twr = nullptr, *d_fc = nullptr, *d_fy0 = nullptr;
+  // full twiddle tables w_L^j / w_Lr^j for the output-pruned transforms
+  double2 *d_twf = nullptr, *d_twrf = nullptr;
+  bool spec_prune_q = false, spec_prune_p = false;  // Q <= 64 (row-spectrum pairs) / P <= 64 (column pairs)
   // edge-row sums on the tensor cores (P <= 65)
   // host path streaming A in row bands (batch 1, tensor-core path): the
   // copy stream bumps *d_band_flag after each band; k_bulk_dmma waits on it,
@@ -361,6 +364,8 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_gp);
   cudaFree(pl->d_d0p);
   cudaFree(pl->d_twr);
+  cudaFree(pl->d_twf);
+  cudaFree(pl->d_twrf);
   cudaFree(pl->d_fc);
   cudaFree(pl->d_fy0);
 }
@@ -741,6 +746,23 @@ struct SpecK {
   static auto rc() { return &k_spec_rc<LG>; }
   template <int LG>
   static auto rowac() { return &k_spec_rowac<LG>; }
+  // output-pruned variants (first 64 outputs; L >= 512, else the full FFT)
+  template <int LG>
+  static auto rcp() {
+    if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_rc<LG, true>; else return &k_spec_rc<LG, false>;
+  }
+  template <int LG>
+  static auto rowacp() {
+    if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_rowac<LG, true>; else return &k_spec_rowac<LG, false>;
+  }
+  template <int LG>
+  static auto dftp() {
+    if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_dft<LG, true>; else return &k_spec_dft<LG, false>;
+  }
+  template <int LG>
+  static auto ccolp() {
+    if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_ccol<LG, true>; else return &k_spec_ccol<LG, false>;
+  }
 };
 
 // spectral core sums (spectral.cuh) for band ks_part of ks_nparts: writes
@@ -813,8 +835,12 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
                   pl->d_fx, pl->d_fy, r0, r1 - r0);
         // dr = 0 rows: the core rows [P-1, N-P] = the non-strip rows
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (r1 - r0), pl->d_fx, pl->d_fy, pr,
-                  pl->spec_lay, pl->d_tw, r0, r1 - r0, rz - ra + 1, r0 - ra, pl->d_d0p);
+        if (pl->spec_prune_q)
+          SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (r1 - r0), pl->d_fx, pl->d_fy, pr,
+                    pl->spec_lay, pl->d_tw, pl->d_twf, r0, r1 - r0, rz - ra + 1, r0 - ra, pl->d_d0p);
+        else
+          SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (r1 - r0), pl->d_fx, pl->d_fy, pr,
+                    pl->spec_lay, pl->d_tw, pl->d_twf, r0, r1 - r0, rz - ra + 1, r0 - ra, pl->d_d0p);
       }
     };
     for (int j = 0; j < nb; ++j) {
@@ -839,8 +865,12 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     if (pl->spec_edges && es != st) {
       const cudaStream_t st_main = st;
       st = es;
-      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      if (pl->spec_prune_q)
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      else
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
       st = st_main;
     }
     mark("spec_rowac");
@@ -881,13 +911,21 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       st = es;
     }
     if (rz >= ra)
-      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr,
-                pl->spec_lay, pl->d_tw, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
+      if (pl->spec_prune_q)
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
+      else
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
     k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
                                                        pl->d_cls_slot, pl->d_ccpart);
     if (pl->spec_edges && es != st_main)
-      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      if (pl->spec_prune_q)
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      else
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
     st = st_main;
     mark("spec_rowac");
   }
@@ -904,22 +942,34 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     const long long per_seg = (long long)(2 * pr.P - 1) * L, tot = B * per_seg;
     k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, gslots, per_seg, tot);
   }
-  SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pr, gslots,
-            pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
+  if (pl->spec_prune_q)
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template dftp, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
+              pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
+  else
+    SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
+              pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
   if (pl->spec_edges) {
     mark("spec_dft");
     {
       cudaStream_t st_main = st;
       st = es;  // SPEC_LOGL launches on `st`
       SPEC_LOGL(pl->spec_logLr, SpecK<T>::template colfft, B * 2 * 4 * S1, A, pr, pl->d_twr, pl->d_fc);
-      SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * (long long)S1 * S1, pl->d_fc, pr,
-                pl->d_twr, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+      if (pl->spec_prune_p)
+        SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccolp, B * 2 * (long long)S1 * S1, pl->d_fc, pr,
+                  pl->d_twr, pl->d_twrf, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+      else
+        SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * (long long)S1 * S1, pl->d_fc, pr,
+                  pl->d_twr, pl->d_twrf, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
       st = st_main;
     }
     mark("spec_ccol");
     if (es == st)  // (timing mode: everything in order on one stream)
-      SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                pl->spec_lay, pl->d_tw, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      if (pl->spec_prune_q)
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+      else
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
   }
 }
 
@@ -1298,7 +1348,8 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH"}) {
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH",
+                        "COVGPU_SPEC_NO_PRUNE"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
     e += ',';
@@ -1667,6 +1718,30 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const size_t L = (size_t)pl->spec_L;
     const std::vector<double2> tw = spec_twiddles(pl->spec_logL);
     const size_t fxe = (size_t)batch * pl->spec_lay.nfb * pl->spec_lay.np * 32;
+    auto full_table = [&](int logn) {
+      std::vector<double2> t((size_t)1 << logn);
+      const long double pi2 = 6.283185307179586476925286766559L;
+      for (size_t j = 0; j < t.size(); ++j) {
+        const long double a = -pi2 * (long double)j / (long double)t.size();
+        t[j] = make_double2((double)cosl(a), (double)sinl(a));
+      }
+      return t;
+    };
+    const std::vector<double2> twf = full_table(pl->spec_logL);
+    const std::vector<double2> twrf = full_table(pl->spec_logLr);
+    pl->spec_prune_q = q <= (1 << SPEC_LOGOUT) && pl->spec_logL >= SPEC_LOGOUT + 3;
+    pl->spec_prune_p = p <= (1 << SPEC_LOGOUT) && pl->spec_logLr >= SPEC_LOGOUT + 3;
+    if (const char* np = getenv("COVGPU_SPEC_NO_PRUNE"))
+      if (atoi(np) != 0) pl->spec_prune_q = pl->spec_prune_p = false;
+    if ((rc = dalloc(&pl->d_twf, twf.size(), &ws)) || (rc = dalloc(&pl->d_twrf, twrf.size(), &ws))) {
+      plan_free(pl.get());
+      return rc;
+    }
+    if (cudaMemcpy(pl->d_twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(pl->d_twrf, twrf.data(), sizeof(double2) * twrf.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      plan_free(pl.get());
+      return fail(COVGPU_ECUDA, "twiddle upload");
+    }
     if ((rc = dalloc(&pl->d_tw, L, &ws)) || (rc = dalloc(&pl->d_fx, fxe, &ws)) ||
         (rc = dalloc(&pl->d_fy, fxe, &ws)) ||
         (rc = dalloc(&pl->d_gp, (size_t)batch * std::max(pl->spec_nseg, batch == 1 ? kMaxBandSlots : 1) *

@@ -211,6 +211,64 @@ __device__ __forceinline__ void spec_fft_block(double2* sb, int tl, const double
   }
 }
 
+// Output-pruned transform for the kernels that keep only the first NOUT = 64
+// outputs (edge sums, dr = 0 rows, output FFT: Q, P <= 64).  With
+// n = m + (L/64) n', the two radix-8 passes leave V_m[k] = sum_n' u[m + (L/64) n']
+// w_64^(n' k) at SMEM position 64 m + k (Stockham layout), and
+//     out[k] = sum_{m < L/64} w_L^(m k) V_m[k],   k < 64,
+// replaces the remaining passes (L = 2048: 2 of 4 SMEM round trips, 30 % of
+// the butterflies).  Thread (k, q) sums a contiguous quarter of the m in order
+// (twiddles from the full table, then a depth <= L/256 recurrence), the
+// quarters are added in a fixed order.  twf[j] = w_L^j (host-made).
+constexpr int SPEC_LOGOUT = 6;
+
+template <int LOGL, int P0, int LOGSTOP, class Load, class Store>
+__device__ __forceinline__ void spec_passes_upto(double2* sb, int tl, const double2* __restrict__ tw,
+                                                 const Load& ld, const Store& st) {
+  constexpr int done = P0 == 1 ? 0 : __builtin_ctz(P0);
+  if constexpr (done < LOGSTOP) {
+    constexpr int lr = (LOGL - done) >= 3 ? 3 : (LOGL - done);
+    static_assert(done + lr <= LOGSTOP, "pruned FFT: the radix-8 passes must land on 2^LOGSTOP");
+    spec_pass<LOGL, (1 << lr), P0>(sb, tl, tw, ld, st);
+    spec_passes_upto<LOGL, (P0 << lr), LOGSTOP>(sb, tl, tw, ld, st);
+  }
+}
+
+template <int LOGL, class Load, class Store>
+__device__ __forceinline__ void spec_fft_pruned(double2* sb, int tl, const double2* __restrict__ tw,
+                                                const double2* __restrict__ twf, const Load& ld, const Store& st) {
+  constexpr int L = 1 << LOGL, NOUT = 1 << SPEC_LOGOUT, M1 = L / NOUT;
+  constexpr int NT = spec_nt<LOGL>(), NQ = NT / NOUT;
+  static_assert(LOGL >= SPEC_LOGOUT + 3 && NQ >= 1, "pruned FFT needs L >= 8 NOUT");
+  spec_passes_upto<LOGL, 1, SPEC_LOGOUT>(sb, tl, tw, ld, [](int, double2) {});
+  const int k = tl % NOUT, q = tl / NOUT;
+  constexpr int MQ = M1 / NQ;
+  double2 acc = make_double2(0.0, 0.0);
+  {
+    const int m0 = q * MQ;
+    double2 w = twf[(m0 * k) & (L - 1)];
+    const double2 step = twf[k];
+#pragma unroll 4
+    for (int m = m0; m < m0 + MQ; ++m) {
+      acc = cadd(acc, cmul(sb[fpad(m * NOUT + k)], w));
+      w = cmul(w, step);
+    }
+  }
+  if constexpr (NQ > 1) {
+    __syncthreads();  // every V read
+    sb[tl] = acc;
+    __syncthreads();
+    if (q == 0) {
+      double2 s = sb[k];
+#pragma unroll
+      for (int qq = 1; qq < NQ; ++qq) s = cadd(s, sb[k + qq * NOUT]);
+      st(k, s);
+    }
+  } else {
+    st(k, acc);
+  }
+}
+
 // This thread's transform: item = CTA * G + group (valid < nitems), tl, SMEM
 struct SpecItem {
   long long item;
@@ -332,9 +390,10 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // versions (index Lr + dr).  CTA = (b, side, sign, c1, e); pairs with e < c1
 // (and e == c1 for sign -) exit; in multi-GPU row-band mode pair q belongs
 // to part q mod nparts (the others write zeros: the bands are summed).
-template <int LOGL>
+template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_ccol(long long nitems, const double2* __restrict__ FC, Problem pr, const double2* __restrict__ tw,
+                const double2* __restrict__ twf,
                 const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls, double2* __restrict__ ccol,
                 long long tot_ccol, int part, int nparts) {
   extern __shared__ double2 sbuf[];
@@ -374,18 +433,38 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   };
   // the last pass hands over the natural-order outputs: only the P row lags
   // of this sign are kept, stored straight to CCol (no SMEM round trip)
-  spec_fft_block<LOGL>(
-      sb, si.tl, tw,
-      [&](int idx) {
-        if (!mine) return make_double2(0.0, 0.0);
-        const double2 x = fx[idx], y = fy[idx];
-        return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
-      },
-      [&](int idx, double2 v) {
-        const int dr = sign ? idx - L : idx;
-        if (mine && ((sign == 0 && idx < P) || (sign == 1 && dr > -P)))
-          emit(dr, make_double2(v.x * inv, v.y * inv));
-      });
+  if constexpr (PRUNE) {
+    // lags dr < 0 sit at the top of the spectrum (L + dr): transform the
+    // conjugate product and conjugate the first outputs instead
+    spec_fft_pruned<LOGL>(
+        sb, si.tl, tw, twf,
+        [&](int idx) {
+          if (!mine) return make_double2(0.0, 0.0);
+          const double2 x = fx[idx], y = fy[idx];
+          const double re = fma(x.x, y.x, x.y * y.y), im = fma(x.y, y.x, -x.x * y.y);  // x conj(y)
+          return make_double2(re, sign ? -im : im);
+        },
+        [&](int idx, double2 v) {
+          if (!mine || idx >= P) return;
+          if (sign == 0)
+            emit(idx, make_double2(v.x * inv, v.y * inv));
+          else if (idx > 0)
+            emit(-idx, make_double2(v.x * inv, -v.y * inv));
+        });
+  } else {
+    spec_fft_block<LOGL>(
+        sb, si.tl, tw,
+        [&](int idx) {
+          if (!mine) return make_double2(0.0, 0.0);
+          const double2 x = fx[idx], y = fy[idx];
+          return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
+        },
+        [&](int idx, double2 v) {
+          const int dr = sign ? idx - L : idx;
+          if (mine && ((sign == 0 && idx < P) || (sign == 1 && dr > -P)))
+            emit(dr, make_double2(v.x * inv, v.y * inv));
+        });
+  }
   if (si.valid && !mine)
     for (int k = si.tl; k < P; k += spec_nt<LOGL>()) emit(sign ? -(k + 1) : k, make_double2(0.0, 0.0));
 }
@@ -396,10 +475,10 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // (X masked to the slot-0 box columns [0, M-Q], Y0 unmasked).  CTA = (b,
 // strip, i1, i2); multi-GPU: pair q belongs to part q mod nparts.  RC' has one
 // segment here (nseg = 1).
-template <int LOGL>
+template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_rc(long long nitems, const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr,
-              SpecLayout lay, const double2* __restrict__ tw, const int* __restrict__ cls_slot,
+              SpecLayout lay, const double2* __restrict__ tw, const double2* __restrict__ twf, const int* __restrict__ cls_slot,
               const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc, int part, int nparts) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
@@ -429,16 +508,18 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     const int k = strip ? (cd.pv - 1) + i : i;
     rc[b * tot_rc + cd.rc_off + k] = v;
   };
-  spec_fft_block<LOGL>(
-      sb, si.tl, tw,
-      [&](int idx) {
-        if (!mine) return make_double2(0.0, 0.0);
-        const double2 x = fx[(idx >> 5) * fxs + (idx & 31)], y = fy[idx];
-        return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
-      },
-      [&](int idx, double2 v) {
-        if (mine && idx < Q) emit(idx, make_double2(v.x * inv, v.y * inv));  // outputs dc < Q only
-      });
+  auto ld = [&](int idx) {
+    if (!mine) return make_double2(0.0, 0.0);
+    const double2 x = fx[(idx >> 5) * fxs + (idx & 31)], y = fy[idx];
+    return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));
+  };
+  auto stf = [&](int idx, double2 v) {
+    if (mine && idx < Q) emit(idx, make_double2(v.x * inv, v.y * inv));  // outputs dc < Q only
+  };
+  if constexpr (PRUNE)
+    spec_fft_pruned<LOGL>(sb, si.tl, tw, twf, ld, stf);
+  else
+    spec_fft_block<LOGL>(sb, si.tl, tw, ld, stf);
   if (si.valid && !mine)
     for (int dc = si.tl; dc < Q; dc += spec_nt<LOGL>()) emit(dc, make_double2(0.0, 0.0));
 }
@@ -708,10 +789,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
 // error at dc > 0 (numpy, cfg5); per row the error is ~eps log L of the row
 // energy and adds incoherently over rows (~1e-15 relative, numpy, cfg5).
 // CTA = (b, row r of the band [row_a, row_a + nrows)).
-template <int LOGL>
+template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_rowac(long long nitems, const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr,
-                 SpecLayout lay, const double2* __restrict__ tw, int row_a, int nrows, int nd0, int kbase,
+                 SpecLayout lay, const double2* __restrict__ tw, const double2* __restrict__ twf, int row_a, int nrows, int nd0, int kbase,
                  double2* __restrict__ D0p) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
@@ -727,17 +808,19 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const long long fs = (long long)lay.np * 32;
   const double inv = 1.0 / (double)L;
   double2* out = D0p + (b * nd0 + kbase + k) * (long long)Q;
-  spec_fft_block<LOGL>(
-      sb, si.tl, tw,
-      [&](int idx) {
-        if (!ok) return make_double2(0.0, 0.0);
-        const long long o = (idx >> 5) * fs + (idx & 31);
-        const double2 x = fx[o], y = fy[o];
-        return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
-      },
-      [&](int idx, double2 v) {
-        if (ok && idx < Q) out[idx] = make_double2(v.x * inv, v.y * inv);
-      });
+  auto ld = [&](int idx) {
+    if (!ok) return make_double2(0.0, 0.0);
+    const long long o = (idx >> 5) * fs + (idx & 31);
+    const double2 x = fx[o], y = fy[o];
+    return make_double2(fma(x.x, y.x, x.y * y.y), fma(x.y, y.x, -x.x * y.y));  // x conj(y)
+  };
+  auto stf = [&](int idx, double2 v) {
+    if (ok && idx < Q) out[idx] = make_double2(v.x * inv, v.y * inv);
+  };
+  if constexpr (PRUNE)
+    spec_fft_pruned<LOGL>(sb, si.tl, tw, twf, ld, stf);
+  else
+    spec_fft_block<LOGL>(sb, si.tl, tw, ld, stf);
 }
 
 // CC(0, dc) = sum over the band's core rows of the per-row transforms
@@ -793,9 +876,10 @@ __global__ void __launch_bounds__(256)
 // dc in [0, Q); for dr = 0 the ordered sum of the space-domain partials.
 // CTA = (snapshot b, row lag dr).  Writes the classes' CC slot (one partial:
 // npart = 1 for the finalize).
-template <int LOGL>
+template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
-    k_spec_dft(long long nitems, const double2* __restrict__ Gp, const double2* __restrict__ tw, Problem pr,
+    k_spec_dft(long long nitems, const double2* __restrict__ Gp, const double2* __restrict__ tw,
+               const double2* __restrict__ twf, Problem pr,
                int nseg, int nclasses, const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
@@ -809,15 +893,17 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const bool ok = si.valid && dr != 0;  // dr = 0: k_spec_d0sum
   const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
   const double inv = 1.0 / (double)L;
-  spec_fft_block<LOGL>(
-      sb, si.tl, tw,
-      [&](int idx) { return ok ? g[idx] : make_double2(0.0, 0.0); },  // segment 0: the ordered sum
-      [&](int idx, double2 v) {
-        if (ok && idx < Q && (dr > 0 || idx > 0)) {
-          const int cid = cls_slot[class_index(dr, idx, P, Q)];
-          if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(v.x * inv, v.y * inv);
-        }
-      });
+  auto ld = [&](int idx) { return ok ? g[idx] : make_double2(0.0, 0.0); };  // segment 0: the ordered sum
+  auto stf = [&](int idx, double2 v) {
+    if (ok && idx < Q && (dr > 0 || idx > 0)) {
+      const int cid = cls_slot[class_index(dr, idx, P, Q)];
+      if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(v.x * inv, v.y * inv);
+    }
+  };
+  if constexpr (PRUNE)
+    spec_fft_pruned<LOGL>(sb, si.tl, tw, twf, ld, stf);
+  else
+    spec_fft_block<LOGL>(sb, si.tl, tw, ld, stf);
 }
 
 }  // namespace covgpu
