@@ -122,6 +122,11 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const double2* cl = ccol + (long long)b * tot_ccol + c.ccol_off;
   const double2* rcc = rc + ((long long)b * tot_rc + c.rc_off) * nseg;
 
+  // row ownership: KR == 1 one row per lane; KR > 1 strided rows v = li + W k
+  // (the lanes' corner loads are then contiguous: 4 L1 wavefronts per warp
+  // load instead of 8 for interleaved pairs; the walk's scan runs once per k)
+  constexpr bool STRIDED = KR > 1;
+  auto rowv = [&](int k) { return STRIDED ? li + W * k : li * KR + k; };
   double2 G, fT[KR], fB[KR];
   if (u_begin > 0) {
     // resume: the state saved by the previous chunk
@@ -138,10 +143,10 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     for (int k = li; k < ncb; k += W) acc = cadd(acc, cc_p[k]);
     for (int j = li; j < ac; j += W) acc = cadd(acc, cl[j]);
     G = seg_sum(acc, W);
-    // edge-row state: lane owns the contiguous rows v = li*KR + k
+    // edge-row state of the lane's rows
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
-      const int v = li * KR + k;
+      const int v = rowv(k);
       fT[k] = fB[k] = make_double2(0.0, 0.0);
       if (v < ar) {
         for (int g = 0; g < nseg; ++g) {
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     auto load_corners = [&]() {
 #pragma unroll
       for (int k = 0; k < 1; ++k) {
-        const int v = li * KR + k;
+        const int v = rowv(k);
         if (v < ar) {
           const long long o1 = (long long)u * Sx + v + c.s1;
           const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
@@ -194,18 +199,32 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     // S(v+1) = S(v) - fullT_v + fullB_v  (drop the leaving edge row, add the
     // entering one) — one exclusive scan of (fB - fT) plus one reduction of fT
     double2 d[KR], tsum = make_double2(0.0, 0.0), run = make_double2(0.0, 0.0);
+    double2 base = make_double2(0.0, 0.0);
+    if constexpr (STRIDED) {
+      // rows li + W k: prefix over v = sum of the earlier k rounds (all lanes)
+      // + this round's exclusive lane prefix
 #pragma unroll
-    for (int k = 0; k < KR; ++k) {
-      d[k] = run;  // in-lane exclusive prefix
-      run = cadd(run, csub(fB[k], fT[k]));
-      tsum = cadd(tsum, fT[k]);
+      for (int k = 0; k < KR; ++k) tsum = cadd(tsum, fT[k]);
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        double2 totk;
+        d[k] = cadd(run, seg_prefix_excl(csub(fB[k], fT[k]), li, W, &totk));
+        run = cadd(run, totk);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        d[k] = run;  // in-lane exclusive prefix
+        run = cadd(run, csub(fB[k], fT[k]));
+        tsum = cadd(tsum, fT[k]);
+      }
+      double2 tot;
+      base = seg_prefix_excl(run, li, W, &tot);
     }
-    double2 tot;
-    const double2 base = seg_prefix_excl(run, li, W, &tot);
     const double2 s0 = cadd(G, seg_sum(tsum, W));
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
-      const int v = li * KR + k;
+      const int v = rowv(k);
       if (active && v < pv) {
         const double2 sv = cadd(s0, cadd(base, d[k]));
         if constexpr (DIRECT) {
@@ -233,7 +252,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
       } else {
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
-          const int v = li * KR + k;
+          const int v = rowv(k);
           if (v < ar) {
             const long long o1 = (long long)u * Sx + v + c.s1;
             const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
