@@ -72,14 +72,28 @@ __device__ inline double2 seg_suffix_incl(double2 v, int li, int W, double2* tot
   total->y = __shfl_sync(0xffffffffu, inc.y, 0, W);
   return inc;
 }
+// inc += the value `off` lanes below, when that lane is in the segment: the
+// shfl's own in-range predicate guards the adds (no selects of a zero)
+__device__ inline void shfl_up_acc(double2& inc, int off, int segc) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 a0, a1, b0, b1;\n\t.reg .f64 t0, t1;\n\t"
+      "mov.b64 {a0, a1}, %0;\n\t"
+      "mov.b64 {b0, b1}, %1;\n\t"
+      "shfl.sync.up.b32 a0|p, a0, %2, %3, -1;\n\t"
+      "shfl.sync.up.b32 a1, a1, %2, %3, -1;\n\t"
+      "shfl.sync.up.b32 b0, b0, %2, %3, -1;\n\t"
+      "shfl.sync.up.b32 b1, b1, %2, %3, -1;\n\t"
+      "mov.b64 t0, {a0, a1};\n\t"
+      "mov.b64 t1, {b0, b1};\n\t"
+      "@p add.f64 %0, %0, t0;\n\t"
+      "@p add.f64 %1, %1, t1;\n\t}"
+      : "+d"(inc.x), "+d"(inc.y)
+      : "r"(off), "r"(segc));
+}
 __device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* total) {
+  (void)li;
   double2 inc = v;
-  for (int off = 1; off < W; off <<= 1) {
-    double2 n;
-    n.x = __shfl_up_sync(0xffffffffu, inc.x, off, W);
-    n.y = __shfl_up_sync(0xffffffffu, inc.y, off, W);
-    if (li >= off) inc = cadd(inc, n);
-  }
+  const int segc = (32 - W) << 8;
+  for (int off = 1; off < W; off <<= 1) shfl_up_acc(inc, off, segc);
   total->x = __shfl_sync(0xffffffffu, inc.x, W - 1, W);
   total->y = __shfl_sync(0xffffffffu, inc.y, W - 1, W);
   return csub(inc, v);
@@ -157,12 +171,41 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     }
   }
   const bool zero_im = (c.d == 0);
-  const long long rb = (long long)b * r_bstride;
-  const C2* TL = Cb;
-  const C2* TR = Cb + cstride;
-  const C2* BL = Cb + 2 * cstride;
-  const C2* BR = Cb + 3 * cstride;
   const int u_stop = min(qu, u_end);
+  // rounds k that hold rows v < pv (the plan's KR covers its largest class)
+  const int kre = STRIDED ? min(KR, (pv + W - 1) / W) : 1;
+  // incremental addressing (the per-slot 64-bit index products were a third
+  // of the kernel's instructions): per row k, the corner pointers of column u
+  // (o1) and u + dc (o2) step by Sx, the output offsets by one window column
+  const long long cs = cstride;
+  const C2* p1[KR];
+  const C2* p2[KR];
+  long long ro[KR], ro2[KR];
+  int rk1[KR];
+  const long long D = pr.PQ;
+  const long long rb = (long long)b * r_bstride;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int v = rowv(k);
+    p1[k] = Cb + (long long)u_begin * Sx + v + c.s1;
+    p2[k] = Cb + (long long)(u_begin + c.dc) * Sx + v + c.s2;
+    const long long k1 = (long long)pr.P * u_begin + c.s1 + v;
+    rk1[k] = (int)k1;
+    if constexpr (DIRECT) {
+      if (dlayout == COVGPU_DENSE) {
+        ro[k] = rb + k1 * (D + 1) + c.d;
+        ro2[k] = rb + k1 * (D + 1) + (long long)c.d * D;
+      } else {
+        ro[k] = rb + packed_off(k1, k1 + c.d, D);
+        ro2[k] = 0;
+      }
+    } else {
+      ro[k] = rb + c.slot_off + (long long)u_begin * pv + v;
+      ro2[k] = 0;
+    }
+  }
+  const long long dstep = (long long)pr.P * (D + 1);
+  const long long pstep0 = (long long)pr.P * D - (long long)pr.P * (pr.P - 1) / 2;
   for (int u = u_begin; u < u_stop; ++u) {
     // KR == 1: this column's corner / edge-column reads go out first, so
     // their latency overlaps the scan and the slot stores below (cfg3
@@ -170,30 +213,25 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     // more occupancy than the overlap gains (cfg5 0.242 -> 0.277 ms), so the
     // reads stay next to their use
     const bool upd = u < ac;
-    C2 q[1][8];
+    C2 q[8];
     double2 clr = make_double2(0.0, 0.0), cll = make_double2(0.0, 0.0);
-    auto load_corners = [&]() {
-#pragma unroll
-      for (int k = 0; k < 1; ++k) {
-        const int v = rowv(k);
-        if (v < ar) {
-          const long long o1 = (long long)u * Sx + v + c.s1;
-          const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
-          q[k][0] = TR[o1];
-          q[k][1] = TR[o2];
-          q[k][2] = TL[o1];
-          q[k][3] = TL[o2];
-          q[k][4] = BR[o1];
-          q[k][5] = BR[o2];
-          q[k][6] = BL[o1];
-          q[k][7] = BL[o2];
-        }
-      }
-      clr = cl[ac + u];
-      cll = cl[u];
-    };
     if constexpr (KR == 1) {
-      if (upd) load_corners();
+      if (upd) {
+        if (li < ar) {
+          const C2* a1 = p1[0];
+          const C2* a2 = p2[0];
+          q[0] = a1[cs];
+          q[1] = a2[cs];
+          q[2] = a1[0];
+          q[3] = a2[0];
+          q[4] = a1[3 * cs];
+          q[5] = a2[3 * cs];
+          q[6] = a1[2 * cs];
+          q[7] = a2[2 * cs];
+        }
+        clr = cl[ac + u];
+        cll = cl[u];
+      }
     }
     // the diagonal-segment walk along v:  S(0) = G + sum_i fullT_i,
     // S(v+1) = S(v) - fullT_v + fullB_v  (drop the leaving edge row, add the
@@ -207,9 +245,12 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
       for (int k = 0; k < KR; ++k) tsum = cadd(tsum, fT[k]);
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
-        double2 totk;
-        d[k] = cadd(run, seg_prefix_excl(csub(fB[k], fT[k]), li, W, &totk));
-        run = cadd(run, totk);
+        d[k] = run;
+        if (k < kre) {
+          double2 totk;
+          d[k] = cadd(run, seg_prefix_excl(csub(fB[k], fT[k]), li, W, &totk));
+          run = cadd(run, totk);
+        }
       }
     } else {
 #pragma unroll
@@ -225,43 +266,65 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
       const int v = rowv(k);
-      if (active && v < pv) {
+      if (k < kre && active && v < pv) {
         const double2 sv = cadd(s0, cadd(base, d[k]));
+        C2 val;
+        val.x = (T)(sv.x * scale);
+        val.y = (T)(zero_im ? 0.0 : sv.y * scale);
+        // DIRECT: dense / packed R straight from the walk (the scattered
+        // diagonal stores merge in L2 well enough to beat a separate expand);
+        // otherwise the compact slot (u-major, then v) for k_expand
+        R[ro[k]] = val;
         if constexpr (DIRECT) {
-          // dense / packed R straight from the walk (the scattered diagonal
-          // stores merge in L2 well enough to beat a separate expand)
-          write_slot<T>(R, dlayout, rb, c, pr, v, u, sv.x * scale, zero_im ? 0.0 : sv.y * scale);
-        } else {
-          // compact slot (u-major, then v): lanes write consecutive addresses;
-          // k_expand turns it into the dense / packed layout with coalesced stores
-          C2 val;
-          val.x = (T)(sv.x * scale);
-          val.y = (T)(zero_im ? 0.0 : sv.y * scale);
-          R[rb + c.slot_off + (long long)u * pv + v] = val;
+          if (dlayout == COVGPU_DENSE && !zero_im) {
+            C2 cv;
+            cv.x = val.x;
+            cv.y = -val.y;  // lower triangle = exact conjugate of the upper
+            R[ro2[k]] = cv;
+          }
         }
       }
     }
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      if constexpr (DIRECT) {
+        if (dlayout == COVGPU_DENSE) {
+          ro[k] += dstep;
+          ro2[k] += dstep;
+        } else {
+          ro[k] += pstep0 - (long long)pr.P * rk1[k];
+          rk1[k] += pr.P;
+        }
+      } else {
+        ro[k] += pv;
+      }
+    }
     if (upd) {
-      // corner products of column u (left) and bw+u (right), each formed once
+      // corner products of column u (left) and u + dc (right), each formed once
       if constexpr (KR == 1) {
         if (li < ar) {
-          fT[0] = cadd(fT[0], csub(cmulconj<T>(q[0][0], q[0][1]), cmulconj<T>(q[0][2], q[0][3])));
-          fB[0] = cadd(fB[0], csub(cmulconj<T>(q[0][4], q[0][5]), cmulconj<T>(q[0][6], q[0][7])));
+          fT[0] = cadd(fT[0], csub(cmulconj<T>(q[0], q[1]), cmulconj<T>(q[2], q[3])));
+          fB[0] = cadd(fB[0], csub(cmulconj<T>(q[4], q[5]), cmulconj<T>(q[6], q[7])));
         }
         G = cadd(G, csub(clr, cll));
       } else {
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
           const int v = rowv(k);
-          if (v < ar) {
-            const long long o1 = (long long)u * Sx + v + c.s1;
-            const long long o2 = (long long)(u + c.dc) * Sx + v + c.s2;
-            fT[k] = cadd(fT[k], csub(cmulconj<T>(TR[o1], TR[o2]), cmulconj<T>(TL[o1], TL[o2])));
-            fB[k] = cadd(fB[k], csub(cmulconj<T>(BR[o1], BR[o2]), cmulconj<T>(BL[o1], BL[o2])));
+          if (k < kre && v < ar) {
+            const C2* a1 = p1[k];
+            const C2* a2 = p2[k];
+            fT[k] = cadd(fT[k], csub(cmulconj<T>(a1[cs], a2[cs]), cmulconj<T>(a1[0], a2[0])));
+            fB[k] = cadd(fB[k], csub(cmulconj<T>(a1[3 * cs], a2[3 * cs]), cmulconj<T>(a1[2 * cs], a2[2 * cs])));
           }
         }
         G = cadd(G, csub(cl[ac + u], cl[u]));
       }
+    }
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      p1[k] += Sx;
+      p2[k] += Sx;
     }
   }
   if (ws && u_stop < qu) {
