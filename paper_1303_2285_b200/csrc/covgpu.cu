@@ -1060,6 +1060,17 @@ void launch_edge(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st) {
       A, pl->pr, pl->S, pl->ndg, pl->nseg, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, total);
 }
 
+// k_finalize_v row mapping: contiguous rows per lane (corners stored with the
+// row permutation of kr = fin_kr) except for dense R written straight from
+// the walk (strided rows, plain corner layout) — finalize.cuh
+static inline bool fin_contig(const covgpu_plan* pl, int layout, bool direct) {
+  (void)pl;
+  return !(direct && layout == COVGPU_DENSE);
+}
+static inline int fin_corner_kr(const covgpu_plan* pl, int layout, bool direct) {
+  return fin_contig(pl, layout, direct) ? std::max(pl->fin_kr, 1) : 1;
+}
+
 template <typename T>
 int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, double scale,
                cudaStream_t st) {
@@ -1189,9 +1200,10 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     return COVGPU_OK;
   }
   if (pl->fin_kr > 0) {
-    const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
+    const int ckr = fin_corner_kr(pl, layout, layout != COVGPU_COMPACT && !pl->no_direct);
+    const long long nc = 4LL * corner_rows(pr.P, ckr) * (pr.Q - 1) * B;
     if (nc > 0) {
-      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, (C2*)pl->d_corners);
+      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, ckr, (C2*)pl->d_corners);
       ++launches;
     }
   }
@@ -1210,11 +1222,18 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     const bool direct = layout != COVGPU_COMPACT && !pl->no_direct;
     C2* cdst = (layout == COVGPU_COMPACT || direct) ? R : (C2*)pl->d_slots;
     const long long rstride = direct ? r_bstride : pl->compact_elems;
-#define FINV(KR, DIR)                                                                           \
-  k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                 \
+#define FINV(KR, DIR)                                                                        \
+  do {                                                                                       \
+    if (contig)                                                                              \
+      k_finalize_v<T, KR, DIR, true><<<blocks, FIN_WARPS * 32, 0, st>>>(FINV_ARGS);                \
+    else                                                                                     \
+      k_finalize_v<T, KR, DIR, false><<<blocks, FIN_WARPS * 32, 0, st>>>(FINV_ARGS);               \
+  } while (0)
+#define FINV_ARGS                                                                               \
       (const C2*)pl->d_corners, pr, pl->d_cls, pl->d_tasks, pl->ntasks, pl->nclasses,           \
       npart, pl->nrs, B, pl->d_ccpart, pl->d_ccol, pl->tot_ccol, pl->d_rc, pl->tot_rc, \
-      pl->nseg, cdst, rstride, scale, direct ? layout : (int)COVGPU_COMPACT, u0, u1, wst)
+      pl->nseg, cdst, rstride, scale, direct ? layout : (int)COVGPU_COMPACT, u0, u1, wst
+    const bool contig = fin_contig(pl, layout, direct);
     // u-chunks (host path: rows [P u0, P u1) of R are complete after a chunk;
     // an event per chunk lets the copy-out start while the walk continues)
     const int nch = (direct && pl->fin_nchunks > 1 && pl->d_fin_state) ? pl->fin_nchunks : 1;
@@ -1237,6 +1256,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       if (nch > 1) CUDA_TRY(cudaEventRecord(pl->ev_fin_chunk[ch], st));
     }
 #undef FINV
+#undef FINV_ARGS
     if (layout != COVGPU_COMPACT && !direct) {
       ++launches;
       mark("finalize");
@@ -1301,19 +1321,27 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
   else
     r_bstride = pl->compact_elems;
   const C2* A = (const C2*)A_dev;
-  const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
-  if (nc > 0) k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, (C2*)pl->d_corners);
+  const int ckr = fin_corner_kr(pl, layout, layout != COVGPU_COMPACT);
+  const long long nc = 4LL * corner_rows(pr.P, ckr) * (pr.Q - 1) * B;
+  if (nc > 0) k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, ckr, (C2*)pl->d_corners);
   if (ntasks > 0) {
     const double2* cc = sums;
     const double2* cl = sums + (long long)B * pl->nclasses;
     const double2* rc = cl + (long long)B * pl->tot_ccol;
     const unsigned blocks = (unsigned)((ntasks + FIN_WARPS - 1) / FIN_WARPS);
     const bool direct = layout != COVGPU_COMPACT;
-#define FINS(KR, DIR)                                                                             \
-  k_finalize_v<T, KR, DIR><<<blocks, FIN_WARPS * 32, 0, st>>>(                                   \
+#define FINS(KR, DIR)                                                                        \
+  do {                                                                                       \
+    if (contig)                                                                              \
+      k_finalize_v<T, KR, DIR, true><<<blocks, FIN_WARPS * 32, 0, st>>>(FINS_ARGS);                \
+    else                                                                                     \
+      k_finalize_v<T, KR, DIR, false><<<blocks, FIN_WARPS * 32, 0, st>>>(FINS_ARGS);               \
+  } while (0)
+#define FINS_ARGS                                                                                 \
       (const C2*)pl->d_corners, pr, pl->d_cls, tasks, ntasks, pl->nclasses, 1, 1, B, cc, cl,      \
       pl->tot_ccol, rc, pl->tot_rc, 1, (C2*)R_dev, r_bstride, scale, direct ? layout : (int)COVGPU_COMPACT, \
-      0, 1 << 30, nullptr)
+      0, 1 << 30, nullptr
+    const bool contig = fin_contig(pl, layout, direct);
     if (direct) {
       switch (pl->fin_kr) {
         case 1: FINS(1, true); break;
@@ -1328,6 +1356,7 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
       }
     }
 #undef FINS
+#undef FINS_ARGS
   }
   CUDA_TRY(cudaGetLastError());
   return COVGPU_OK;
@@ -1800,7 +1829,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->ntasks = (long long)tasks.size();
       pl->h_tasks = tasks;
       const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
-      const size_t cbytes = (size_t)batch * 4 * (size_t)std::max(p - 1, 0) * (size_t)std::max(q - 1, 0) * esz;
+      const size_t cbytes = (size_t)batch * 4 * (size_t)corner_rows(p, std::max(pl->fin_kr, 1)) * (size_t)std::max(q - 1, 0) * esz;
       std::vector<long long> uc_off(nuc, -1);
       for (const auto& cd : pl->h_cls) uc_off[cd.uc] = cd.slot_off;
       cudaError_t e1 = cudaMalloc(&pl->d_corners, std::max<size_t>(cbytes, 16));

@@ -34,20 +34,40 @@ namespace covgpu {
 constexpr int FIN_WARPS = 4;
 constexpr int FINV_MAX_P = 128;
 
-// Transposed corner blocks of A: C[b][k][j][i], k = TL, TR, BL, BR, each
+// Transposed corner blocks of A: C[b][k][j][ph], k = TL, TR, BL, BR, each
 // (P-1) rows x (Q-1) columns of A (the only elements corner products read).
+// Rows are stored permuted for k_finalize_v's rows-per-lane walk: row i sits
+// at ph = (i % kr) * Wp + i / kr (Wp = ceil((P-1)/kr), column stride kr*Wp),
+// so the lanes' reads of rows li*kr + k + s (fixed k, any shift s) are
+// consecutive addresses while each lane still owns contiguous rows.
+__host__ __device__ inline int corner_rows(int P, int kr) {
+  const int S = P > 1 ? P - 1 : 0;
+  return kr * ((S + kr - 1) / kr);
+}
+__host__ __device__ inline int corner_phys(int i, int P, int kr) {
+  const int wp = corner_rows(P, kr) / kr;
+  return (i % kr) * wp + i / kr;
+}
 template <typename T>
-__global__ void k_corners(const typename CT<T>::c* __restrict__ A, Problem pr, int B,
+__global__ void k_corners(const typename CT<T>::c* __restrict__ A, Problem pr, int B, int kr,
                           typename CT<T>::c* __restrict__ C) {
-  const int S = pr.P - 1, Wc = pr.Q - 1;
-  const long long per = 4LL * S * Wc;
+  using C2 = typename CT<T>::c;
+  const int S = pr.P - 1, Sp = corner_rows(pr.P, kr), Wc = pr.Q - 1, wp = Sp / kr;
+  const long long per = 4LL * Sp * Wc;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= per * B) return;
   const int b = (int)(tid / per);
   long long r = tid % per;
-  const int k = (int)(r / ((long long)S * Wc));
-  r %= (long long)S * Wc;
-  const int j = (int)(r / S), i = (int)(r % S);
+  const int k = (int)(r / ((long long)Sp * Wc));
+  r %= (long long)Sp * Wc;
+  const int j = (int)(r / Sp), ph = (int)(r % Sp);
+  const int i = (ph % wp) * kr + ph / wp;
+  if (i >= S) {
+    C2 z;
+    z.x = z.y = (T)0;
+    C[tid] = z;
+    return;
+  }
   const int row = (k < 2 ? 0 : pr.N - S) + i;
   const int col = ((k & 1) ? pr.M - Wc : 0) + j;
   C[tid] = A[((long long)b * pr.N + row) * pr.M + col];
@@ -100,7 +120,7 @@ __device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* tot
 }
 
 // task = (class, snapshot group); W = min(32, pow2ceil(pv)) lanes per snapshot
-template <typename T, int KR, bool DIRECT>
+template <typename T, int KR, bool DIRECT, bool CONTIG>
 __global__ void __launch_bounds__(FIN_WARPS * 32)
     k_finalize_v(const typename CT<T>::c* __restrict__ corners, Problem pr,
                  const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
@@ -129,18 +149,23 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   const int b_raw = tk.y * (32 / W) + lane / W;
   const bool active = b_raw < B;
   const int b = active ? b_raw : B - 1;
-  const int Sx = pr.P - 1, Wc = pr.Q - 1;
+  constexpr int CKR = CONTIG ? KR : 1;  // corner row permutation (k_corners kr)
+  const int Sx = corner_rows(pr.P, CKR), Wc = pr.Q - 1;
   const long long cstride = (long long)Sx * Wc;
   const C2* Cb = corners + (long long)b * 4 * cstride;
   (void)nrs;  // bulk row segments are off (nrs == 1): ccol holds whole-column sums
   const double2* cl = ccol + (long long)b * tot_ccol + c.ccol_off;
   const double2* rcc = rc + ((long long)b * tot_rc + c.rc_off) * nseg;
 
-  // row ownership: KR == 1 one row per lane; KR > 1 strided rows v = li + W k
-  // (the lanes' corner loads are then contiguous: 4 L1 wavefronts per warp
-  // load instead of 8 for interleaved pairs; the walk's scan runs once per k)
-  constexpr bool STRIDED = KR > 1;
-  auto rowv = [&](int k) { return STRIDED ? li + W * k : li * KR + k; };
+  // row ownership, kre = ceil(pv / W) <= KR rounds (classes with pv <= 32
+  // run one).  CONTIG: lane li owns the contiguous rows v = li*kre + k (one
+  // in-lane prefix + one segmented scan per column; the permuted corner
+  // layout keeps each round's corner reads consecutive).  Otherwise rows are
+  // strided, v = li + W k (one scan per round) — kept for dense R, whose
+  // mirrored stores run markedly slower from the contiguous mapping (cfg5
+  // 0.245 vs 0.214 ms, while compact / packed gain: 0.185 -> 0.163 ms)
+  const int kre = min(KR, (pv + W - 1) / W);
+  auto rowv = [&](int k) { return CONTIG ? li * kre + k : li + W * k; };
   double2 G, fT[KR], fB[KR];
   if (u_begin > 0) {
     // resume: the state saved by the previous chunk
@@ -172,8 +197,6 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
   }
   const bool zero_im = (c.d == 0);
   const int u_stop = min(qu, u_end);
-  // rounds k that hold rows v < pv (the plan's KR covers its largest class)
-  const int kre = STRIDED ? min(KR, (pv + W - 1) / W) : 1;
   // incremental addressing (the per-slot 64-bit index products were a third
   // of the kernel's instructions): per row k, the corner pointers of column u
   // (o1) and u + dc (o2) step by Sx, the output offsets by one window column
@@ -187,8 +210,8 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
 #pragma unroll
   for (int k = 0; k < KR; ++k) {
     const int v = rowv(k);
-    p1[k] = Cb + (long long)u_begin * Sx + v + c.s1;
-    p2[k] = Cb + (long long)(u_begin + c.dc) * Sx + v + c.s2;
+    p1[k] = Cb + (long long)u_begin * Sx + corner_phys(min(v, Sx - 1) + c.s1, pr.P, CKR);
+    p2[k] = Cb + (long long)(u_begin + c.dc) * Sx + corner_phys(min(v, Sx - 1) + c.s2, pr.P, CKR);
     const long long k1 = (long long)pr.P * u_begin + c.s1 + v;
     rk1[k] = (int)k1;
     if constexpr (DIRECT) {
@@ -238,8 +261,19 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
     // entering one) — one exclusive scan of (fB - fT) plus one reduction of fT
     double2 d[KR], tsum = make_double2(0.0, 0.0), run = make_double2(0.0, 0.0);
     double2 base = make_double2(0.0, 0.0);
-    if constexpr (STRIDED) {
-      // rows li + W k: prefix over v = sum of the earlier k rounds (all lanes)
+    if constexpr (CONTIG) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        d[k] = run;  // in-lane exclusive prefix
+        if (k < kre) {
+          run = cadd(run, csub(fB[k], fT[k]));
+          tsum = cadd(tsum, fT[k]);
+        }
+      }
+      double2 tot;
+      base = seg_prefix_excl(run, li, W, &tot);
+    } else {
+      // rows li + W k: prefix over v = the earlier rounds' totals (all lanes)
       // + this round's exclusive lane prefix
 #pragma unroll
       for (int k = 0; k < KR; ++k) tsum = cadd(tsum, fT[k]);
@@ -252,15 +286,6 @@ __global__ void __launch_bounds__(FIN_WARPS * 32)
           run = cadd(run, totk);
         }
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        d[k] = run;  // in-lane exclusive prefix
-        run = cadd(run, csub(fB[k], fT[k]));
-        tsum = cadd(tsum, fT[k]);
-      }
-      double2 tot;
-      base = seg_prefix_excl(run, li, W, &tot);
     }
     const double2 s0 = cadd(G, seg_sum(tsum, W));
 #pragma unroll
