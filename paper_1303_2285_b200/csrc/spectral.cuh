@@ -27,6 +27,8 @@
 // Every sum runs in a fixed order: results are bitwise reproducible.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace covgpu {
@@ -735,38 +737,55 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
     const double2* Y = reinterpret_cast<const double2*>(scraw + s * stage_bytes) + lane;
     const double2* X = Y + 32 * SC_RC;
     // window: slot kk holds X row t = R - dr0 - (E-1) + kk (stage row xoff - (E-1) + kk; clamped
-    // stage rows only feed lags past the warp's range)
+    // stage rows only feed lags past the warp's range).  Filled at the
+    // segment's first chunk only: SC_RC is a multiple of E, so at a chunk
+    // boundary the slots already hold exactly these rows (entered, masked,
+    // during the previous chunk)
+    static_assert(SC_RC % E == 0, "chunk rows must be a multiple of the lag window");
+    if (k == 0) {
 #pragma unroll
-    for (int kk = 0; kk < E - 1; ++kk) {
-      const int trow = R - dr0 - (E - 1) + kk;
-      double2 v = X[max(xoff - (E - 1) + kk, 0) * 32];
-      if (trow < xlo || trow > xhi) v = make_double2(0.0, 0.0);
-      wr[kk] = v.x;
-      wi[kk] = v.y;
-      ws[kk] = v.x + v.y;
-    }
-#pragma unroll 2
-    for (int j0 = 0; j0 < SC_RC; j0 += E) {
-#pragma unroll
-      for (int tt = 0; tt < E; ++tt) {
-        const int r2 = R + j0 + tt, trow = r2 - dr0;
-        double2 xn = X[(j0 + tt + xoff) * 32];
-        double2 y = Y[(j0 + tt) * 32];
-        if (trow < xlo || trow > xhi) xn = make_double2(0.0, 0.0);
-        if (r2 < ylo || r2 > yhi) y = make_double2(0.0, 0.0);
-        const int nw = (tt + E - 1) % E;
-        wr[nw] = xn.x;
-        wi[nw] = xn.y;
-        ws[nw] = xn.x + xn.y;
-        const double yd = y.x - y.y;
-#pragma unroll
-        for (int e = 0; e < E; ++e) s1[e] = fma(wr[(tt + E - 1 - e) % E], y.x, s1[e]);
-#pragma unroll
-        for (int e = 0; e < E; ++e) s2[e] = fma(wi[(tt + E - 1 - e) % E], y.y, s2[e]);
-#pragma unroll
-        for (int e = 0; e < E; ++e) s3[e] = fma(ws[(tt + E - 1 - e) % E], yd, s3[e]);
+      for (int kk = 0; kk < E - 1; ++kk) {
+        const int trow = R - dr0 - (E - 1) + kk;
+        double2 v = X[max(xoff - (E - 1) + kk, 0) * 32];
+        if (trow < xlo || trow > xhi) v = make_double2(0.0, 0.0);
+        wr[kk] = v.x;
+        wi[kk] = v.y;
+        ws[kk] = v.x + v.y;
       }
     }
+    // the row masks only bite in the first / last chunks: interior chunks
+    // (every entering X row and every Y row valid) run without them
+    const bool interior = R - dr0 >= xlo && R + SC_RC - 1 - dr0 <= xhi && R >= ylo && R + SC_RC - 1 <= yhi;
+    auto walk = [&](auto masked) {
+#pragma unroll 2
+      for (int j0 = 0; j0 < SC_RC; j0 += E) {
+#pragma unroll
+        for (int tt = 0; tt < E; ++tt) {
+          const int r2 = R + j0 + tt, trow = r2 - dr0;
+          double2 xn = X[(j0 + tt + xoff) * 32];
+          double2 y = Y[(j0 + tt) * 32];
+          if constexpr (decltype(masked)::value) {
+            if (trow < xlo || trow > xhi) xn = make_double2(0.0, 0.0);
+            if (r2 < ylo || r2 > yhi) y = make_double2(0.0, 0.0);
+          }
+          const int nw = (tt + E - 1) % E;
+          wr[nw] = xn.x;
+          wi[nw] = xn.y;
+          ws[nw] = xn.x + xn.y;
+          const double yd = y.x - y.y;
+#pragma unroll
+          for (int e = 0; e < E; ++e) s1[e] = fma(wr[(tt + E - 1 - e) % E], y.x, s1[e]);
+#pragma unroll
+          for (int e = 0; e < E; ++e) s2[e] = fma(wi[(tt + E - 1 - e) % E], y.y, s2[e]);
+#pragma unroll
+          for (int e = 0; e < E; ++e) s3[e] = fma(ws[(tt + E - 1 - e) % E], yd, s3[e]);
+        }
+      }
+    };
+    if (interior)
+      walk(std::false_type{});
+    else
+      walk(std::true_type{});
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
