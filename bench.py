@@ -20,6 +20,8 @@ measured on this GPU right before the run, memory-bound kernels against
 MEASURED_PEAKS.json's HBM figure, each with its algorithmic flops or bytes),
 `roofline` (the dominant kernel's entry), `tensor_core_path` /
 `cuda_core_path` (the same workload on the other two sum engines),
+`packed_output` (the same step writing the packed upper triangle, the
+reference's own output layout, instead of dense Hermitian R),
 `cpu_baseline` (the oracle's multithreaded
 C port of the reference's class kernel on this host's cores, bounded sample,
 extrapolated by product count), `e2e` (same metric through the C ABI with
@@ -434,7 +436,8 @@ def main() -> None:
     # events — reported, not the headline: the FP64 tensor-core core sums
     # (COVGPU_NO_SPECTRAL) and the north_star's CUDA-core recurrence kernels
     # (COVGPU_NO_MMA: also the path of shapes outside the spectral gates)
-    def side_path(env):
+    def side_path(env, lay=None):
+        lay = lay or layout
         for k, v in env.items():
             os.environ[k] = v
         try:
@@ -442,27 +445,34 @@ def main() -> None:
         finally:
             for k in env:
                 del os.environ[k]
-        cout = cplan.alloc_output(layout)
+        cout = cplan.alloc_output(lay)
         for _ in range(2):
-            cplan.execute(a, cout, layout)
+            cplan.execute(a, cout, lay)
         torch.cuda.synchronize(dev)
         tot, nst = 0.0, 5
         for _ in range(nst):
             flush.fill_(1)
             torch.cuda.synchronize(dev)
             e0.record()
-            cplan.execute(a, cout, layout)
+            cplan.execute(a, cout, lay)
             e1.record()
             torch.cuda.synchronize(dev)
             tot += e0.elapsed_time(e1)
         cplan.set_timing(True)
         flush.fill_(1)
         torch.cuda.synchronize(dev)
-        cplan.execute(a, cout, layout)
+        cplan.execute(a, cout, lay)
         ck = dict(zip(cplan.kernel_names(), cplan.kernel_times()))
         cplan.close()
         return tot / nst, ck
 
+    if world == 1 and not rowband and layout == "dense":
+        # the reference's own output format is the packed upper triangle
+        # (core.py:60-72): the same estimate written packed, for comparison
+        pms, pk = side_path({}, "packed")
+        line["packed_output"] = {"ms_per_step": pms, "value": entries / (pms * 1e-3), "kernel_ms": pk,
+                                 "note": "same step, R written as the packed upper triangle (the "
+                                         "reference's output layout) instead of dense Hermitian R"}
     if world == 1 and not args.no_cuda_core and not rowband and "spec_corr" in kernel_ms:
         tms, tk = side_path({"COVGPU_NO_SPECTRAL": "1"})
         tach = 6.0 * core_p * w.batch / (tk["bulk_dmma"] * 1e-3) / 1e12 if tk.get("bulk_dmma") else None
