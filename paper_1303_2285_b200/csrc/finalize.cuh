@@ -33,6 +33,12 @@ namespace covgpu {
 
 constexpr int FIN_WARPS = 4;
 constexpr int FINV_MAX_P = 128;
+// complex64 walks with one row per lane (cfg4: short walks, latency-bound on
+// the per-class sum reads): 6 CTAs per SM (80 registers) 0.269 -> 0.245 ms;
+// 8 CTAs spill
+#ifndef FIN_MINB_F1
+#define FIN_MINB_F1 6
+#endif
 
 // Transposed corner blocks of A: C[b][k][j][ph], k = TL, TR, BL, BR, each
 // (P-1) rows x (Q-1) columns of A (the only elements corner products read).
@@ -121,7 +127,7 @@ __device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* tot
 
 // task = (class, snapshot group); W = min(32, pow2ceil(pv)) lanes per snapshot
 template <typename T, int KR, bool DIRECT, bool CONTIG>
-__global__ void __launch_bounds__(FIN_WARPS * 32)
+__global__ void __launch_bounds__(FIN_WARPS * 32, (KR == 1 && sizeof(T) == 4) ? FIN_MINB_F1 : 1)
     k_finalize_v(const typename CT<T>::c* __restrict__ corners, Problem pr,
                  const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
                  int nclasses, int ncb, int nrs, int B, const double2* __restrict__ ccpart,
