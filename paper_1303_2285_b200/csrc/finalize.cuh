@@ -34,11 +34,17 @@ namespace covgpu {
 constexpr int FIN_WARPS = 4;
 constexpr int FINV_MAX_P = 128;
 // complex64 walks with one row per lane (cfg4: short walks, latency-bound on
-// the per-class sum reads): 6 CTAs per SM (80 registers) 0.269 -> 0.245 ms;
-// 8 CTAs spill
+// the per-class sum reads): 6 CTAs per SM (80 registers) 0.249-0.253 ->
+// 0.245-0.249 ms (within noise); 8 CTAs spill
 #ifndef FIN_MINB_F1
 #define FIN_MINB_F1 6
 #endif
+// CTAs per SM asked of ptxas (an explicit 1 would let it spend up to 255
+// registers): the occupancy each instantiation reached without a hint
+// (double KR = 2: 96 registers, 5 CTAs), except complex64 KR = 1 (above)
+constexpr int fin_min_blocks(size_t tsize, int kr) {
+  return (kr == 1 && tsize == 4) ? FIN_MINB_F1 : kr == 2 ? 5 : 4;
+}
 
 // Transposed corner blocks of A: C[b][k][j][ph], k = TL, TR, BL, BR, each
 // (P-1) rows x (Q-1) columns of A (the only elements corner products read).
@@ -127,7 +133,7 @@ __device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* tot
 
 // task = (class, snapshot group); W = min(32, pow2ceil(pv)) lanes per snapshot
 template <typename T, int KR, bool DIRECT, bool CONTIG>
-__global__ void __launch_bounds__(FIN_WARPS * 32, (KR == 1 && sizeof(T) == 4) ? FIN_MINB_F1 : 1)
+__global__ void __launch_bounds__(FIN_WARPS * 32, fin_min_blocks(sizeof(T), KR))
     k_finalize_v(const typename CT<T>::c* __restrict__ corners, Problem pr,
                  const ClassDesc* __restrict__ cls, const int2* __restrict__ tasks, long long ntasks,
                  int nclasses, int ncb, int nrs, int B, const double2* __restrict__ ccpart,
