@@ -131,6 +131,17 @@ __device__ inline double2 seg_prefix_excl(double2 v, int li, int W, double2* tot
   return csub(inc, v);
 }
 
+// packed R (the host path's layout) is written once and not re-read on the
+// device: evict-first stores (st.global.cs) — cfg5 packed finalize 0.171 ->
+// 0.167-0.168 ms over two alternating runs; dense R keeps plain stores (its
+// mirrored halves of a sector arrive from different walks and merge in L2:
+// 0.210-0.214 plain vs 0.214-0.220 ms evict-first)
+template <typename C2>
+__device__ __forceinline__ void fin_store(C2* p, C2 v, bool stream) {
+  if (stream) __stcs(p, v);
+  else *p = v;
+}
+
 // task = (class, snapshot group); W = min(32, pow2ceil(pv)) lanes per snapshot
 template <typename T, int KR, bool DIRECT, bool CONTIG>
 __global__ void __launch_bounds__(FIN_WARPS * 32, fin_min_blocks(sizeof(T), KR))
@@ -311,13 +322,13 @@ __global__ void __launch_bounds__(FIN_WARPS * 32, fin_min_blocks(sizeof(T), KR))
         // DIRECT: dense / packed R straight from the walk (the scattered
         // diagonal stores merge in L2 well enough to beat a separate expand);
         // otherwise the compact slot (u-major, then v) for k_expand
-        R[ro[k]] = val;
+        fin_store(R + ro[k], val, DIRECT && dlayout != COVGPU_DENSE);
         if constexpr (DIRECT) {
           if (dlayout == COVGPU_DENSE && !zero_im) {
             C2 cv;
             cv.x = val.x;
             cv.y = -val.y;  // lower triangle = exact conjugate of the upper
-            R[ro2[k]] = cv;
+            fin_store(R + ro2[k], cv, false);
           }
         }
       }
