@@ -165,7 +165,7 @@ __global__ void __launch_bounds__((EDGE_WARPS + 1) * 32, 1)
   t /= ndg;
   const int strip = (int)(t % 2);
   const int b = (int)(t / 2);
-  const int N = pr.N, M = pr.M, P = pr.P, Q = pr.Q;
+  const int M = pr.M, P = pr.P, Q = pr.Q;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int base = strip ? pr.bh : 0;
   const int dc0 = g * D;
