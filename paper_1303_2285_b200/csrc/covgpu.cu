@@ -50,6 +50,7 @@
 #include "mma.cuh"
 #include "probe.cuh"
 #include "spectral.cuh"
+#include "tile.cuh"
 
 using namespace covgpu;
 
@@ -189,6 +190,15 @@ struct covgpu_plan {
   long long* d_uc_off = nullptr;  // compact offset per UC index (-1: not in shard)
   long long ntasks = 0;
   int fin_kr = 0;             // k_finalize_v rows per lane (0: wide finalize)
+  // tile finalize (tile.cuh): units (snapshot, dc, 32-diagonal band), longest walks first
+  bool use_tile = false;
+  int ft_nwarp = 1;
+  int4* d_units = nullptr;
+  long long n_units = 0;
+  std::vector<int4> h_units;
+  int4* d_runits = nullptr;   // class-range finalize: units holding a class of the range
+  long long n_runits = 0;
+  double2* d_ck = nullptr;    // walk state at the cut steps u = 16 j (k_fin_ckpt)
   // chunked walk for the synchronous host path (covgpu_plan_execute_host):
   // u-chunk bounds, saved walk state, an event per chunk
   static constexpr int kMaxFinChunks = 4;
@@ -335,6 +345,9 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_sat);
   cudaFree(pl->d_corners);
   cudaFree(pl->d_tasks);
+  cudaFree(pl->d_units);
+  cudaFree(pl->d_runits);
+  cudaFree(pl->d_ck);
   cudaFree(pl->d_uc_off);
   cudaFree(pl->d_ecm_part);
   cudaFree(pl->d_band_flag);
@@ -476,6 +489,31 @@ cudaError_t bulk_attrs() {
   return e;
 }
 
+std::string g_attr_fail;  // the kernel whose attribute could not be set (error text)
+
+template <typename T, int NW>
+cudaError_t fin_tile_attr() {
+  const int smem = (int)(ft_unit_smem(NW, sizeof(typename CT<T>::c)) * FtCfg<NW>::UPC);
+  g_attr_fail = "k_fin_tile<" + std::to_string(sizeof(T)) + "," + std::to_string(NW) + "> smem " + std::to_string(smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_PACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (r != cudaSuccess) e = r;
+  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (r != cudaSuccess) e = r;
+  if (e == cudaSuccess) g_attr_fail.clear();
+  return e;
+}
+template <typename T>
+cudaError_t fin_tile_attrs() {
+  cudaError_t e = cudaSuccess, r;
+  if ((r = fin_tile_attr<T, 1>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 2>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 4>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 8>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 16>()) != cudaSuccess) return r;
+  return e;
+}
+
 cudaError_t set_attrs() {
   static cudaError_t once = [] {
     cudaError_t e = bulk_attrs<double>();
@@ -515,6 +553,11 @@ cudaError_t set_attrs() {
       e = r;
     if ((r = cudaFuncSetAttribute(k_finalize<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024)) != cudaSuccess)
+      e = r;
+    if ((r = fin_tile_attrs<double>()) != cudaSuccess) e = r;
+    if ((r = fin_tile_attrs<float>()) != cudaSuccess) e = r;
+    if ((r = cudaFuncSetAttribute(k_fin_ckpt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ftk_smem(FINV_MAX_P))) != cudaSuccess)
       e = r;
     return e;
   }();
@@ -1071,6 +1114,87 @@ static inline int fin_corner_kr(const covgpu_plan* pl, int layout, bool direct) 
   return fin_contig(pl, layout, direct) ? std::max(pl->fin_kr, 1) : 1;
 }
 
+// Tile-finalize units (tile.cuh): (snapshot, dc, band of 32 circular
+// diagonals, steps [u_lo, u_hi)) holding at least one class of plan slots
+// [lo, hi).  Walks are cut at u = 16 j (the state there comes from
+// k_fin_ckpt); pieces are ordered longest first, the bands of one
+// (snapshot, dc, piece) adjacent (their row segments share sectors).
+std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi) {
+  const int P = pl->pr.P, Q = pl->pr.Q;
+  std::vector<char> has((size_t)(2 * P - 1) * Q, 0);
+  for (int sl = lo; sl < hi; ++sl) {
+    const ClassDesc& c = pl->h_cls[sl];
+    has[(size_t)(c.dr + P - 1) * Q + c.dc] = 1;
+  }
+  struct Piece {
+    int4 u;
+    int len;
+  };
+  std::vector<Piece> pieces;
+  for (int dc = 0; dc < Q; ++dc) {
+    const int qu = Q - dc;
+    for (int u0 = 0; u0 < qu; u0 += FT_CK) {
+      const int u1 = std::min(qu, u0 + FT_CK);
+      for (long long b = 0; b < pl->batch; ++b)
+        for (int d0 = 0; d0 < P; d0 += 32) {
+          bool any = false;  // circular diagonal c holds classes (c, dc) and (c - P, dc)
+          for (int c = d0; c < std::min(P, d0 + 32); ++c)
+            any = any || has[(size_t)(c + P - 1) * Q + dc] || (dc > 0 && c > 0 && has[(size_t)(c - 1) * Q + dc]);
+          if (any) pieces.push_back({make_int4((int)b, dc, d0, u0 | (u1 << 16)), u1 - u0});
+        }
+    }
+  }
+  std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.len > y.len; });
+  std::vector<int4> units;
+  units.reserve(pieces.size());
+  for (const Piece& pc : pieces) units.push_back(pc.u);
+  return units;
+}
+
+// the walk state at the cut steps (needs the corner blocks and RC')
+void launch_fin_ckpt(covgpu_plan* pl, const double2* rc, int nseg, int slot_lo, int slot_hi, cudaStream_t st) {
+  if (!pl->d_ck) return;
+  const long long per = (long long)pl->pr.P * pl->pr.P;
+  const long long n = (per + FTK_THREADS - 1) / FTK_THREADS * pl->pr.Q * pl->batch;
+  k_fin_ckpt<<<(unsigned)n, FTK_THREADS, ftk_smem(pl->pr.P), st>>>(
+      (const double2*)pl->d_corners, pl->pr, pl->d_cls, pl->d_cls_slot, (int)pl->batch, rc, pl->tot_rc, nseg,
+      pl->d_ck, slot_lo, slot_hi);
+}
+
+template <typename T>
+void launch_fin_tile(covgpu_plan* pl, const int4* units, long long nunits, const double2* ccpart, int npart,
+                     const double2* ccol, const double2* rc, int nseg, typename CT<T>::c* R, long long rstride,
+                     double scale, int layout, int u0, int u1, double2* wst, int slot_lo, int slot_hi,
+                     cudaStream_t st) {
+  using C2 = typename CT<T>::c;
+  if (nunits <= 0) return;
+#define FT_LAUNCH(NW, LAY)                                                                                  \
+  do {                                                                                                      \
+    constexpr int upc = FtCfg<NW>::UPC;                                                                     \
+    const unsigned grid = (unsigned)((nunits + upc - 1) / upc);                                             \
+    const size_t smem = ft_unit_smem(NW, sizeof(C2)) * upc;                                                 \
+    k_fin_tile<T, NW, LAY><<<grid, FtCfg<NW>::THREADS, smem, st>>>(                                         \
+        (const double2*)pl->d_corners, pl->pr, pl->d_cls, pl->d_cls_slot, units, (int)nunits, pl->nclasses, \
+        npart, ccpart, ccol, pl->tot_ccol, rc, pl->tot_rc, nseg, pl->d_ck, R, rstride, scale, u0, u1, wst,  \
+        slot_lo, slot_hi);                                                                                  \
+  } while (0)
+#define FT_LAY(NW)                                                           \
+  do {                                                                       \
+    if (layout == COVGPU_DENSE) FT_LAUNCH(NW, COVGPU_DENSE);                 \
+    else if (layout == COVGPU_PACKED) FT_LAUNCH(NW, COVGPU_PACKED);          \
+    else FT_LAUNCH(NW, COVGPU_COMPACT);                                      \
+  } while (0)
+  switch (pl->ft_nwarp) {
+    case 1: FT_LAY(1); break;
+    case 2: FT_LAY(2); break;
+    case 4: FT_LAY(4); break;
+    case 8: FT_LAY(8); break;
+    default: FT_LAY(16);
+  }
+#undef FT_LAY
+#undef FT_LAUNCH
+}
+
 template <typename T>
 int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, double scale,
                cudaStream_t st) {
@@ -1110,7 +1234,8 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     return COVGPU_OK;
   }
 
-  CUDA_TRY(set_attrs());
+  if (set_attrs() != cudaSuccess)
+    return fail(COVGPU_ECUDA, std::string("kernel attributes: ") + cudaGetErrorString(set_attrs()) + " " + g_attr_fail);
   pl->nev = 0;
   auto mark = [&](const char* name) {
     if (pl->timing && pl->nev < covgpu_plan::kMaxEv) {
@@ -1200,18 +1325,37 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     return COVGPU_OK;
   }
   if (pl->fin_kr > 0) {
-    const int ckr = fin_corner_kr(pl, layout, layout != COVGPU_COMPACT && !pl->no_direct);
+    const int ckr = pl->use_tile ? 1 : fin_corner_kr(pl, layout, layout != COVGPU_COMPACT && !pl->no_direct);
     const long long nc = 4LL * corner_rows(pr.P, ckr) * (pr.Q - 1) * B;
     if (nc > 0) {
-      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, ckr, (C2*)pl->d_corners);
+      if (pl->use_tile)
+        k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, (double2*)pl->d_corners);
+      else
+        k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, ckr, (C2*)pl->d_corners);
       ++launches;
     }
+    if (pl->use_tile && pl->d_ck) {  // (P = 1: no corner rows, the cut states are the RC'-free zeros)
+      launch_fin_ckpt(pl, pl->d_rc, pl->nseg, 0, INT_MAX, es);
+      ++launches;
+    }
+    if (!fork) mark("fin_ckpt");  // (timing: corners + cut states on the main stream)
   }
   if (fork) {
     CUDA_TRY(cudaEventRecord(pl->ev_join, es));
     CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
   }
-  if (pl->fin_kr > 0) {
+  if (pl->use_tile) {
+    // tile finalize straight into the requested layout; u-chunks for the
+    // host path (rows [P u0, P u1) of R are complete after a chunk, an event
+    // per chunk lets the copy-out start while the walk continues)
+    const int nch = (layout != COVGPU_COMPACT && pl->fin_nchunks > 1 && pl->d_fin_state) ? pl->fin_nchunks : 1;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int u0 = nch > 1 ? pl->fin_ubound[ch] : 0, u1 = nch > 1 ? pl->fin_ubound[ch + 1] : (1 << 30);
+      launch_fin_tile<T>(pl, pl->d_units, pl->n_units, pl->d_ccpart, npart, pl->d_ccol, pl->d_rc, pl->nseg, R,
+                         r_bstride, scale, layout, u0, u1, nch > 1 ? pl->d_fin_state : nullptr, 0, INT_MAX, st);
+      if (nch > 1) CUDA_TRY(cudaEventRecord(pl->ev_fin_chunk[ch], st));
+    }
+  } else if (pl->fin_kr > 0) {
     const unsigned blocks = (unsigned)((pl->ntasks + FIN_WARPS - 1) / FIN_WARPS);
     // finalize into the compact layout (R itself, or the plan's scratch),
     // then expand to dense / packed with coalesced stores
@@ -1296,7 +1440,7 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
     return fail(COVGPU_EINVAL, "a class range finalizes into the compact layout");
   const int2* tasks = pl->d_tasks;
   long long ntasks = pl->ntasks;
-  if (!full) {
+  if (!full && !pl->use_tile) {
     if (pl->rtask_lo != c_lo || pl->rtask_hi != c_hi) {
       std::vector<int2> sub;
       for (const int2& t : pl->h_tasks)
@@ -1321,9 +1465,41 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
   else
     r_bstride = pl->compact_elems;
   const C2* A = (const C2*)A_dev;
-  const int ckr = fin_corner_kr(pl, layout, layout != COVGPU_COMPACT);
+  const int ckr = pl->use_tile ? 1 : fin_corner_kr(pl, layout, layout != COVGPU_COMPACT);
   const long long nc = 4LL * corner_rows(pr.P, ckr) * (pr.Q - 1) * B;
-  if (nc > 0) k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, ckr, (C2*)pl->d_corners);
+  if (nc > 0) {
+    if (pl->use_tile)
+      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, (double2*)pl->d_corners);
+    else
+      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, ckr, (C2*)pl->d_corners);
+  }
+  if (pl->use_tile) {
+    const double2* cc = sums;
+    const double2* cl = sums + (long long)B * pl->nclasses;
+    const double2* rc = cl + (long long)B * pl->tot_ccol;
+    launch_fin_ckpt(pl, rc, 1, c_lo, c_hi, st);
+    const int4* units = pl->d_units;
+    long long nunits = pl->n_units;
+    if (!full) {
+      if (pl->rtask_lo != c_lo || pl->rtask_hi != c_hi) {
+        const std::vector<int4> sub = fin_tile_units(pl, c_lo, c_hi);
+        cudaFree(pl->d_runits);
+        pl->d_runits = nullptr;
+        CUDA_TRY(cudaMalloc((void**)&pl->d_runits, sizeof(int4) * std::max<size_t>(sub.size(), 1)));
+        if (!sub.empty())
+          CUDA_TRY(cudaMemcpy(pl->d_runits, sub.data(), sizeof(int4) * sub.size(), cudaMemcpyHostToDevice));
+        pl->n_runits = (long long)sub.size();
+        pl->rtask_lo = c_lo;
+        pl->rtask_hi = c_hi;
+      }
+      units = pl->d_runits;
+      nunits = pl->n_runits;
+    }
+    launch_fin_tile<T>(pl, units, nunits, cc, 1, cl, rc, 1, (C2*)R_dev, r_bstride, scale, layout, 0, 1 << 30,
+                       nullptr, c_lo, c_hi, st);
+    CUDA_TRY(cudaGetLastError());
+    return COVGPU_OK;
+  }
   if (ntasks > 0) {
     const double2* cc = sums;
     const double2* cl = sums + (long long)B * pl->nclasses;
@@ -1812,6 +1988,17 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     pl->fin_smem = sizeof(double2) * (size_t)FIN_WARPS * 4 * (size_t)q;
     if (p <= FINV_MAX_P) {
       pl->fin_kr = p <= 32 ? 1 : p <= 64 ? 2 : 4;
+      pl->use_tile = getenv("COVGPU_FIN_WALK") == nullptr || atoi(getenv("COVGPU_FIN_WALK")) == 0;
+      pl->ft_nwarp = ft_nwarp(p);
+      pl->h_units = fin_tile_units(pl.get(), 0, pl->nclasses);
+      pl->n_units = (long long)pl->h_units.size();
+      if (pl->use_tile && ft_nck(q) > 0) {
+        const size_t ckn = (size_t)batch * q * ft_nck(q) * 2 * (size_t)p * p;
+        if ((rc = dalloc(&pl->d_ck, ckn, &ws))) {
+          plan_free(pl.get());
+          return rc;
+        }
+      }
       // tasks: (class, snapshot group of 32/W snapshots), W = min(32, pow2ceil(pv))
       std::vector<int2> tasks;
       for (int ci = 0; ci < pl->nclasses; ++ci) {
@@ -1828,7 +2015,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       });
       pl->ntasks = (long long)tasks.size();
       pl->h_tasks = tasks;
-      const size_t esz = dtype == COVGPU_C128 ? 16 : 8;
+      const size_t esz = (dtype == COVGPU_C128 || pl->use_tile) ? 16 : 8;  // tile walk: corners widened to double
       const size_t cbytes = (size_t)batch * 4 * (size_t)corner_rows(p, std::max(pl->fin_kr, 1)) * (size_t)std::max(q - 1, 0) * esz;
       std::vector<long long> uc_off(nuc, -1);
       for (const auto& cd : pl->h_cls) uc_off[cd.uc] = cd.slot_off;
@@ -1836,6 +2023,9 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       if (e1 == cudaSuccess) e1 = cudaMalloc((void**)&pl->d_uc_off, sizeof(long long) * nuc);
       if (e1 == cudaSuccess)
         e1 = cudaMemcpy(pl->d_uc_off, uc_off.data(), sizeof(long long) * nuc, cudaMemcpyHostToDevice);
+      if (e1 == cudaSuccess) e1 = cudaMalloc((void**)&pl->d_units, sizeof(int4) * std::max<size_t>(pl->h_units.size(), 1));
+      if (e1 == cudaSuccess && !pl->h_units.empty())
+        e1 = cudaMemcpy(pl->d_units, pl->h_units.data(), sizeof(int4) * pl->h_units.size(), cudaMemcpyHostToDevice);
       if (e1 == cudaSuccess) e1 = cudaMalloc((void**)&pl->d_tasks, sizeof(int2) * std::max<size_t>(tasks.size(), 1));
       if (e1 == cudaSuccess && !tasks.empty())
         e1 = cudaMemcpy(pl->d_tasks, tasks.data(), sizeof(int2) * tasks.size(), cudaMemcpyHostToDevice);
@@ -2415,7 +2605,8 @@ static bool chunked_copy_out(covgpu_plan* pl, int layout) {
   if (const char* e = getenv("COVGPU_NO_CHUNKED_D2H"))
     if (atoi(e) != 0) return false;
   if (!pl->d_fin_state) {
-    const size_t n = (size_t)pl->ntasks * 32 * (2 * pl->fin_kr + 1);
+    const size_t n = pl->use_tile ? (size_t)pl->n_units * 32 * pl->ft_nwarp * FT_STATE
+                                  : (size_t)pl->ntasks * 32 * (2 * pl->fin_kr + 1);
     if (cudaMalloc((void**)&pl->d_fin_state, sizeof(double2) * std::max<size_t>(n, 1)) != cudaSuccess) {
       cudaGetLastError();
       pl->d_fin_state = nullptr;

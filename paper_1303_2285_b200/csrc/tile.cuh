@@ -1,0 +1,533 @@
+// K3 — tile finalize (k_fin_tile): the diagonal-segment walk written as
+// coalesced row segments of R's P x P blocks.
+//
+// Block (u, u+dc) of R (rows P u + r1, columns P (u+dc) + r2, r1, r2 in
+// [0, P)) holds, on its diagonal dr = r2 - r1, slot u of class (dr, dc):
+// entry (r1, r1+dr) is slot (v = r1 - s1, u) (_numba_kernels.py:100-106).
+// With the class's top / bottom edge-row state indexed by the pair of A rows
+// it multiplies — F_T[r1][r2] = fullT_i(u), F_B[r1][r2] = fullB_i(u) with
+// i = min(r1, r2) — the walk along the diagonal reads
+//   O(r1)   = G(u) + sum_{k >= r1} F_T[k][k+dr] + sum_{k < r1} F_B[k][k+dr]
+//   O(r1+1) = O(r1) - F_T[r1][r1+dr] + F_B[r1][r1+dr]
+// (drop the leaving edge row, add the entering one), and the step u -> u+1
+// of every class of one column offset dc is ONE rank-2 update of the state
+// by four strip columns of A (the corner products, each formed once):
+//   F_T += TR[u] (x) conj(TR[u+dc]) - TL[u] (x) conj(TL[u+dc])    (top strip)
+//   F_B += BR[u] (x) conj(BR[u+dc]) - BL[u] (x) conj(BL[u+dc])    (bottom strip)
+//   G   += CColR[u] - CColL[u].
+//
+// Circular diagonals: diagonal dr = c (rows [0, P-c)) and dr = c-P (rows
+// [P-c, P)) have complementary rows, so lane c of a warp walks the block's
+// entries (r1, (r1 + c) mod P) for all rows — two classes, one segment each,
+// and no idle slot (dc > 0).  Unit = (snapshot, dc, band of 32 circular
+// diagonals, steps [u_lo, u_hi)); warp w owns rows 8w .. 8w+7 and carries
+// F_T / F_B of its 8 entries in registers.  Per step u: the row-group totals
+// of both segments meet in SMEM (one unit barrier per step) to give each
+// warp its carries; a warp's store of row r1 covers 32 consecutive columns
+// (mod P) of R's row P u + r1; dense R's mirrored block (u+dc, u) is written
+// one step later from a double-buffered SMEM stage, again as row segments;
+// the strip columns of the next step are prefetched with cp.async.
+//
+// Walks are cut at u = 16 j: k_fin_ckpt computes the state at those steps
+// (off the critical path: it reads only the corner blocks of A), so every
+// unit walks <= 16 steps and the launch fills the SMs.  The cut grid is a
+// fixed function of u, and every value depends only on its class's sums and
+// the fixed 8-row grouping: class subsets (shards), layouts, batches and
+// u-chunked launches give the same bits; packed R equals dense R's upper
+// triangle bitwise.
+#pragma once
+
+#include "common.cuh"
+
+namespace covgpu {
+
+#ifndef FT_CTA_WARPS
+#define FT_CTA_WARPS 8
+#endif
+constexpr int FT_RPT = 8;  // rows per thread
+constexpr int FT_CK = 16;  // checkpoint spacing (steps)
+
+template <int NWARP>
+struct FtCfg {
+  static constexpr int UPC = NWARP >= FT_CTA_WARPS ? 1 : FT_CTA_WARPS / NWARP;  // units per CTA
+  static constexpr int THREADS = 32 * NWARP * UPC;
+};
+
+// walk state saved between u-chunked launches: F_T[8], F_B[8], G1, G2
+constexpr int FT_STATE = 2 * FT_RPT + 2;
+
+inline int ft_nwarp(int P) {
+  int w = 1;
+  while (w * FT_RPT < P) w <<= 1;
+  return w;
+}
+__host__ __device__ inline int ft_nck(int Q) { return (Q - 1) / FT_CK; }  // checkpoints per (snapshot, dc)
+
+// SMEM per unit: strip vectors [2 bufs][8][PP] double2 (entries [P-1, PP)
+// stay zero: out-of-strip rows read them, the update needs no guards),
+// row-group totals [2 bufs][T1, B1, T2, B2][nwarp][32] double2, edge-column
+// sums of the step [2 bufs][class 1, 2][L, R][32] double2, stage
+// [2 bufs][PP][32] (output precision)
+__host__ __device__ inline size_t ft_vec_bytes(int nwarp) { return (size_t)2 * 8 * nwarp * FT_RPT * 16; }
+__host__ __device__ inline size_t ft_tot_bytes(int nwarp) { return (size_t)2 * 4 * nwarp * 32 * 16; }
+__host__ __device__ inline size_t ft_gcol_bytes() { return (size_t)2 * 4 * 32 * 16; }
+// (P > 64: one stage buffer, the mirror follows its step after a second barrier)
+__host__ __device__ inline int ft_stage_bufs(int nwarp) { return nwarp <= 8 ? 2 : 1; }
+__host__ __device__ inline size_t ft_unit_smem(int nwarp, size_t esz) {
+  return ft_vec_bytes(nwarp) + ft_tot_bytes(nwarp) + ft_gcol_bytes() +
+         (size_t)ft_stage_bufs(nwarp) * nwarp * FT_RPT * 32 * esz;
+}
+
+__device__ __forceinline__ void ft_unit_sync(int id, int nthreads) {
+  if (nthreads == 32)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// f += a (x) conj(b) - c (x) conj(d), accumulated with FMAs in double
+__device__ __forceinline__ void ft_rank2(double2& f, double2 a, double2 b, double2 c, double2 d) {
+  f.x = fma(a.x, b.x, f.x);
+  f.x = fma(a.y, b.y, f.x);
+  f.x = fma(-c.x, d.x, f.x);
+  f.x = fma(-c.y, d.y, f.x);
+  f.y = fma(a.y, b.x, f.y);
+  f.y = fma(-a.x, b.y, f.y);
+  f.y = fma(-c.y, d.x, f.y);
+  f.y = fma(c.x, d.y, f.y);
+}
+
+// Corner blocks widened to double for the tile walk: C[b][blk][col][row],
+// blk = TL, TR, BL, BR, each (P-1) rows x (Q-1) columns of A.
+template <typename T>
+__global__ void k_corners_d(const typename CT<T>::c* __restrict__ A, Problem pr, int B,
+                            double2* __restrict__ C) {
+  const int S = pr.P - 1, Wc = pr.Q - 1;
+  const long long per = 4LL * S * Wc;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= per * B) return;
+  const int b = (int)(tid / per);
+  long long r = tid % per;
+  const int k = (int)(r / ((long long)S * Wc));
+  r %= (long long)S * Wc;
+  const int j = (int)(r / S), i = (int)(r % S);
+  const int row = (k < 2 ? 0 : pr.N - S) + i;
+  const int col = ((k & 1) ? pr.M - Wc : 0) + j;
+  const auto v = A[((long long)b * pr.N + row) * pr.M + col];
+  C[tid] = make_double2((double)v.x, (double)v.y);
+}
+
+// The two classes on circular diagonal c of column offset dc: (c, dc) on
+// rows [0, P-c) and (c-P, dc) on rows [P-c, P) (dc > 0, c > 0 only)
+struct FtLane {
+  int slot1, slot2;  // plan slots (-1: absent)
+  long long rc1, rc2, cl1, cl2, so1, so2;
+};
+__device__ inline FtLane ft_lane(int c, int dc, int P, int Q, const ClassDesc* __restrict__ cls,
+                                 const int* __restrict__ cls_slot, int lo, int hi) {
+  FtLane L{-1, -1, 0, 0, 0, 0, 0, 0};
+  if (c < P) {
+    int s = cls_slot[class_index(c, dc, P, Q)];
+    if (s >= lo && s < hi) {
+      L.slot1 = s;
+      L.rc1 = cls[s].rc_off;
+      L.cl1 = cls[s].ccol_off;
+      L.so1 = cls[s].slot_off;
+    }
+    if (dc > 0 && c > 0) {
+      s = cls_slot[class_index(c - P, dc, P, Q)];
+      if (s >= lo && s < hi) {
+        L.slot2 = s;
+        L.rc2 = cls[s].rc_off;
+        L.cl2 = cls[s].ccol_off;
+        L.so2 = cls[s].slot_off;
+      }
+    }
+  }
+  return L;
+}
+
+// F(0) of entry (r1, (r1 + c) mod P): full_i(0) = RC'_i (top), RC'_{ar+i}
+// (bottom) of the entry's class, i = v = the entry's slot row
+__device__ inline void ft_init_entry(int r1, int c, int P, const FtLane& L, const double2* __restrict__ rcb,
+                                     int nseg, double2& fT, double2& fB) {
+  fT = fB = make_double2(0.0, 0.0);
+  const int bnd = P - c;
+  const bool seg1 = r1 < bnd;
+  const int v = seg1 ? r1 : r1 - bnd, ar = seg1 ? P - c - 1 : c - 1;
+  if (r1 >= P || (seg1 ? L.slot1 : L.slot2) < 0 || v >= ar) return;
+  const double2* rcp = rcb + (seg1 ? L.rc1 : L.rc2) * nseg;
+  for (int g = 0; g < nseg; ++g) {
+    fT = cadd(fT, rcp[(long long)v * nseg + g]);
+    fB = cadd(fB, rcp[(long long)(ar + v) * nseg + g]);
+  }
+}
+
+// Walk state at the cut steps u = 16 j (j = 1 .. ft_nck(Q), u < Q - dc) for
+// every (snapshot, dc, row, circular diagonal), computed with the walk's own
+// update arithmetic (same operands, same order: the bits a continuous walk
+// would carry); layout ck[b][dc][j-1][T, B][row][c].  CTA = 256 consecutive
+// entries (r1, c) of one (snapshot, dc); the strip columns of FT_CK steps at
+// a time are staged in SMEM (rows the CTA needs for the first operand, all
+// rows for the second).
+constexpr int FTK_THREADS = 256;
+__host__ __device__ inline int ftk_rows(int P) {  // first-operand rows per CTA
+  return FTK_THREADS / P + 2 < P ? FTK_THREADS / P + 2 : P;
+}
+__host__ __device__ inline size_t ftk_smem(int P) {
+  return (size_t)FT_CK * 4 * (ftk_rows(P) + P) * sizeof(double2);
+}
+__global__ void __launch_bounds__(FTK_THREADS) k_fin_ckpt(const double2* __restrict__ corners, Problem pr,
+                                                          const ClassDesc* __restrict__ cls,
+                                                          const int* __restrict__ cls_slot, int B,
+                                                          const double2* __restrict__ rc, long long tot_rc,
+                                                          int nseg, double2* __restrict__ ck, int slot_lo,
+                                                          int slot_hi) {
+  extern __shared__ __align__(16) double2 ftk[];
+  const int P = pr.P, Q = pr.Q, S = P - 1, Wc = Q - 1, nck = ft_nck(Q);
+  const long long per = (long long)P * P;
+  const int cpd = (int)((per + FTK_THREADS - 1) / FTK_THREADS);  // CTAs per (snapshot, dc)
+  const int dc = (int)(blockIdx.x / cpd % Q), b = (int)(blockIdx.x / cpd / Q);
+  const int qu = Q - dc;
+  if (qu <= FT_CK) return;                      // no cut inside this walk (CTA-uniform)
+  const int last = ((qu - 1) / FT_CK) * FT_CK;  // last cut step (< qu)
+  const int e = (int)(blockIdx.x % cpd) * FTK_THREADS + threadIdx.x;
+  const bool on = e < per;
+  const int c = on ? e % P : 0, r1 = on ? e / P : 0;
+  const int rlo = (int)(blockIdx.x % cpd) * FTK_THREADS / P, NR = ftk_rows(P);
+  double2 fT = make_double2(0.0, 0.0), fB = fT;
+  if (on) {
+    const FtLane L = ft_lane(c, dc, P, Q, cls, cls_slot, slot_lo, slot_hi);
+    ft_init_entry(r1, c, P, L, rc + (long long)b * tot_rc * nseg, nseg, fT, fB);
+  }
+  const int r2 = (r1 + c) % P;
+  const bool live = on && r1 < S && r2 < S;  // other entries read zero strip rows: no change
+  const double2* cb = corners + (long long)b * 4 * S * Wc;
+  // staged chunk: A-operand rows [t][blk][NR] (blk = TL, TR, BL, BR at column
+  // t), B-operand rows [t][blk][P] (column t + dc)
+  double2* sa = ftk;
+  double2* sq = ftk + FT_CK * 4 * NR;
+  double2* out = ck + (((long long)b * Q + dc) * nck) * 2 * per + e;
+  for (int t0 = 0; t0 < last; t0 += FT_CK) {
+    __syncthreads();
+    for (int x = threadIdx.x; x < FT_CK * 4 * (NR + P); x += FTK_THREADS) {
+      const bool isa = x < FT_CK * 4 * NR;
+      const int y = isa ? x : x - FT_CK * 4 * NR, len = isa ? NR : P;
+      const int t = y / (4 * len), blk = y / len % 4, i = y % len;
+      const int row = isa ? rlo + i : i, col = t0 + t + (isa ? 0 : dc);
+      // rows outside the strip (and columns past the last cut) read as zero
+      const bool ok = row < S && col < Wc;
+      cp_async_elem<16>((isa ? sa : sq) + y, cb + (ok ? ((long long)blk * Wc + col) * S + row : 0), ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (live) {
+      const int ia = r1 - rlo;
+#pragma unroll 4
+      for (int t = 0; t < FT_CK; ++t) {
+        const double2* a = sa + t * 4 * NR + ia;
+        const double2* q = sq + t * 4 * P + r2;
+        ft_rank2(fT, a[NR], q[P], a[0], q[0]);
+        ft_rank2(fB, a[3 * NR], q[3 * P], a[2 * NR], q[2 * P]);
+      }
+    }
+    if (on) {
+      double2* o = out + (long long)(t0 / FT_CK) * 2 * per;
+      o[0] = fT;
+      o[per] = fB;
+    }
+  }
+}
+
+template <typename T, int NWARP, int LAYOUT>
+__global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
+    k_fin_tile(const double2* __restrict__ corners, Problem pr, const ClassDesc* __restrict__ cls,
+               const int* __restrict__ cls_slot, const int4* __restrict__ units, int nunits, int nclasses,
+               int npart, const double2* __restrict__ ccpart, const double2* __restrict__ ccol,
+               long long tot_ccol, const double2* __restrict__ rc, long long tot_rc, int nseg,
+               const double2* __restrict__ ck, typename CT<T>::c* __restrict__ R, long long r_bstride,
+               double scale, int u_begin, int u_end, double2* __restrict__ wstate, int slot_lo, int slot_hi) {
+  using C2 = typename CT<T>::c;
+  constexpr int UPC = FtCfg<NWARP>::UPC, UT = 32 * NWARP, PP = NWARP * FT_RPT;
+  constexpr bool DENSE = LAYOUT == COVGPU_DENSE, PACKED = LAYOUT == COVGPU_PACKED;
+  constexpr bool STAGE2 = NWARP <= 8;  // double-buffered stage: the mirror runs one step later
+  extern __shared__ __align__(16) unsigned char ft_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int us = warp / NWARP, w = warp - us * NWARP, ut = (int)threadIdx.x - us * UT;
+  const int unit = blockIdx.x * UPC + us;
+  if (unit >= nunits) return;  // unit-uniform: the barriers below involve only this unit
+  const int4 un = units[unit];
+  const int b = un.x, dc = un.y, d0 = un.z, u_lo = un.w & 0xffff, u_hi = un.w >> 16;
+  const int P = pr.P, Q = pr.Q, ac = Q - dc - 1, S = P - 1, Wc = Q - 1;
+  // emitted steps of this launch; a unit resumed by a later u-chunk restores
+  // the state the previous chunk saved, a fresh one starts from F(u_lo)
+  const int e0 = max(u_lo, u_begin), e1 = min(u_hi, u_end);
+  if (e0 >= e1) return;
+  const bool resume = e0 > u_lo;
+  unsigned char* sb = ft_smem + (size_t)us * ft_unit_smem(NWARP, sizeof(C2));
+  double2* const vec = (double2*)sb;
+  double2* const tot0 = (double2*)(sb + ft_vec_bytes(NWARP));
+  double2* const gcol0 = (double2*)(sb + ft_vec_bytes(NWARP) + ft_tot_bytes(NWARP));
+  C2* const stage0 = (C2*)(sb + ft_vec_bytes(NWARP) + ft_tot_bytes(NWARP) + ft_gcol_bytes());
+  const int bar = 1 + us;
+
+  const int c = d0 + lane;  // this lane's circular diagonal
+  const FtLane L = ft_lane(c, dc, P, Q, cls, cls_slot, slot_lo, slot_hi);
+  const int bnd = P - c;  // first row of segment 2
+  const int r0 = w * FT_RPT;
+  const int pv1 = P - c, pv2 = c;
+  // per-row masks: output entry, mirrored entry; the mirror writer lane l
+  // handles source lane m = 31 - l (its columns ascend with l)
+  unsigned omask = 0;
+  int boff[FT_RPT];  // strip index of the row's second A row (P-1: a zero entry)
+#pragma unroll
+  for (int k = 0; k < FT_RPT; ++k) {
+    const int r1 = r0 + k, r2 = (r1 + c) % P;
+    if (r1 < P && ((r1 < bnd) ? L.slot1 : L.slot2) >= 0) omask |= 1u << k;
+    boff[k] = r2 < S ? r2 : S;
+  }
+  const int m = 31 - lane, cm = d0 + m;
+  const bool m1 = __shfl_sync(0xffffffffu, L.slot1, m) >= 0 && (dc > 0 || cm > 0);
+  const bool m2 = __shfl_sync(0xffffffffu, L.slot2, m) >= 0;
+  unsigned mmask = 0;
+  int mcol[FT_RPT];  // mirror row r2 = r0 + k: source row (r2 - cm) mod P
+#pragma unroll
+  for (int k = 0; k < FT_RPT; ++k) {
+    const int r2 = r0 + k;
+    const int src = cm < P ? ((r2 - cm) % P + P) % P : 0;
+    mcol[k] = src;
+    if (cm < P && r2 < P && (src < P - cm ? m1 : m2)) mmask |= 1u << k;
+  }
+  const bool wout = __any_sync(0xffffffffu, omask != 0);
+  const bool wmir = DENSE && __any_sync(0xffffffffu, mmask != 0);
+  const double2* clb = ccol + (long long)b * tot_ccol;
+  double* const wsp = wstate ? (double*)(wstate + ((long long)unit * UT + ut) * FT_STATE) : nullptr;
+
+  double2 fT[FT_RPT], fB[FT_RPT], G1 = make_double2(0.0, 0.0), G2 = G1;
+  if (resume) {
+#pragma unroll
+    for (int k = 0; k < FT_RPT; ++k) {
+      fT[k] = make_double2(wsp[4 * k], wsp[4 * k + 1]);
+      fB[k] = make_double2(wsp[4 * k + 2], wsp[4 * k + 3]);
+    }
+    G1 = make_double2(wsp[4 * FT_RPT], wsp[4 * FT_RPT + 1]);
+    G2 = make_double2(wsp[4 * FT_RPT + 2], wsp[4 * FT_RPT + 3]);
+  } else {
+    if (u_lo == 0) {
+      const double2* rcb = rc + (long long)b * tot_rc * nseg;
+#pragma unroll
+      for (int k = 0; k < FT_RPT; ++k) ft_init_entry(r0 + k, c, P, L, rcb, nseg, fT[k], fB[k]);
+    } else {
+      const long long per = (long long)P * P;
+      const double2* ckp = ck + (((long long)b * Q + dc) * ft_nck(Q) + (u_lo / FT_CK - 1)) * 2 * per + c;
+#pragma unroll
+      for (int k = 0; k < FT_RPT; ++k) {
+        const int r1 = r0 + k;
+        fT[k] = fB[k] = make_double2(0.0, 0.0);
+        if (r1 < P && c < P) {
+          fT[k] = ckp[(long long)r1 * P];
+          fB[k] = ckp[per + (long long)r1 * P];
+        }
+      }
+    }
+    // G(u_lo) = CC + sum_{j < u_lo} CColR[j] + sum_{u_lo <= j < ac} CColL[j]
+    // per class (the walk's G(0) plus its first u_lo updates): warp w adds
+    // columns j = w (mod NWARP), the partials meet in SMEM (fixed order)
+    double2 g1 = make_double2(0.0, 0.0), g2 = g1;
+    if (w == 0) {
+      for (int k = 0; k < npart; ++k) {
+        if (L.slot1 >= 0) g1 = cadd(g1, ccpart[((long long)b * nclasses + L.slot1) * npart + k]);
+        if (L.slot2 >= 0) g2 = cadd(g2, ccpart[((long long)b * nclasses + L.slot2) * npart + k]);
+      }
+    }
+#pragma unroll 4
+    for (int j = w; j < ac; j += NWARP) {
+      const int o = j < u_lo ? ac + j : j;
+      if (L.slot1 >= 0) g1 = cadd(g1, clb[L.cl1 + o]);
+      if (L.slot2 >= 0) g2 = cadd(g2, clb[L.cl2 + o]);
+    }
+    tot0[w * 32 + lane] = g1;
+    tot0[(NWARP + w) * 32 + lane] = g2;
+    ft_unit_sync(bar, UT);
+    for (int x = 0; x < NWARP; ++x) {
+      G1 = cadd(G1, tot0[x * 32 + lane]);
+      G2 = cadd(G2, tot0[(NWARP + x) * 32 + lane]);
+    }
+  }
+  ft_unit_sync(bar, UT);  // tot0 is reused by the steps
+  for (int e = ut; e < 2 * 4 * 32; e += UT) gcol0[e] = make_double2(0.0, 0.0);  // absent classes stay 0
+  for (int e = ut; e < 2 * 8 * PP; e += UT) vec[e] = make_double2(0.0, 0.0);   // the zero padding
+  ft_unit_sync(bar, UT);
+
+  // strip columns of step u (only while u < ac): 0 TL[u], 1 TR[u],
+  // 2 TL[u+dc], 3 TR[u+dc], 4 BL[u], 5 BR[u], 6 BL[u+dc], 7 BR[u+dc]; this
+  // thread copies elements ut and ut + UT (8 (P-1) < 2 UT), and the step's
+  // CColL / CColR of both classes of its lane (gcol [class][L, R][lane])
+  const double2* cb = corners + (long long)b * 4 * S * Wc;
+  const double2* psrc[2];
+  int pdst[2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int e = ut + x * UT;
+    const int v = e / S, i = e - v * S;
+    pdst[x] = e < 8 * S ? v * PP + i : -1;
+    const int blk = ((v >> 2) << 1) | (v & 1);
+    psrc[x] = cb + ((long long)blk * Wc + ((v & 2) ? dc : 0)) * S + i;
+  }
+  const double2* gsrc[4];
+  int gdst[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int e = lane + 32 * x;  // e = (class * 2 + side) * 32 + lane; warp x of the unit copies it
+    const int cl = x >> 1, side = x & 1;
+    const bool ok = w == x % NWARP && (cl == 0 ? L.slot1 : L.slot2) >= 0;
+    gdst[x] = ok ? e : -1;
+    gsrc[x] = clb + (cl == 0 ? L.cl1 : L.cl2) + (side ? ac : 0);
+  }
+  auto prefetch = [&](int uu, int buf) {
+    if (uu < ac && uu < e1) {
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+        if (pdst[x] >= 0) cp_async_elem<16>(vec + buf * 8 * PP + pdst[x], psrc[x] + (long long)uu * S, true);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        if (gdst[x] >= 0) cp_async_elem<16>(gcol0 + buf * 128 + gdst[x], gsrc[x] + uu, true);
+    }
+    cp_async_commit();
+  };
+  int u = e0;
+  prefetch(u, u & 1);
+
+  const long long D = pr.PQ;
+  C2* const Rb = R + (long long)b * r_bstride;
+  const bool zero_im = dc == 0 && c == 0;  // class (0,0): R's real main diagonal (rows < bnd = P)
+  // mirror of step um: block (um+dc, um), row P(um+dc) + r2, column P um + src
+  // (the source row), conjugated (the lower triangle = exact conjugate)
+  auto mirror = [&](int um, int buf) {
+    const C2* stg = stage0 + (STAGE2 ? buf : 0) * PP * 32 + m;
+    C2* row = Rb + ((long long)P * (um + dc) + r0) * D + (long long)P * um;
+#pragma unroll
+    for (int k = 0; k < FT_RPT; ++k) {
+      C2 val = stg[mcol[k] * 32];
+      val.y = -val.y;
+      if ((mmask >> k) & 1u) row[mcol[k]] = val;
+      row += D;
+    }
+  };
+  bool prev = false;  // the previous step emitted (its mirror is pending)
+  for (; u < e1; ++u) {
+    const int buf = u & 1;
+    double2* const tot = tot0 + buf * 4 * NWARP * 32;
+    {
+      double2 t1 = make_double2(0.0, 0.0), b1 = t1, t2 = t1, b2 = t1;
+#pragma unroll
+      for (int k = 0; k < FT_RPT; ++k) {
+        if (r0 + k < bnd) {
+          t1 = cadd(t1, fT[k]);
+          b1 = cadd(b1, fB[k]);
+        } else {
+          t2 = cadd(t2, fT[k]);
+          b2 = cadd(b2, fB[k]);
+        }
+      }
+      tot[w * 32 + lane] = t1;
+      tot[(NWARP + w) * 32 + lane] = b1;
+      tot[(2 * NWARP + w) * 32 + lane] = t2;
+      tot[(3 * NWARP + w) * 32 + lane] = b2;
+    }
+    cp_async_wait<0>();  // this step's strip columns and edge-column sums
+    ft_unit_sync(bar, UT);
+    prefetch(u + 1, buf ^ 1);
+    if (STAGE2 && DENSE && prev && wmir) mirror(u - 1, buf ^ 1);
+    if (wout) {
+      // O at the warp's first row of each segment: G + top rows from there
+      // down + bottom rows above it (x < w: bottoms, x >= w: tops)
+      double2 o1 = G1, o2 = G2;
+#pragma unroll
+      for (int x = 0; x < NWARP; ++x) {
+        o1 = cadd(o1, tot[((x < w ? NWARP : 0) + x) * 32 + lane]);
+        o2 = cadd(o2, tot[((x < w ? 3 * NWARP : 2 * NWARP) + x) * 32 + lane]);
+      }
+      C2* const stg = stage0 + (STAGE2 ? buf : 0) * PP * 32 + r0 * 32 + lane;
+      const long long k1 = (long long)P * u + r0;
+      const int col0 = (r0 + c) % P;  // column of row r0 in the block
+      C2* dst;
+      if constexpr (DENSE)
+        dst = Rb + k1 * D + (long long)P * (u + dc) + col0;
+      else if constexpr (PACKED)
+        dst = Rb + packed_off(k1, (long long)P * (u + dc) + col0, D);
+      else
+        dst = Rb + (r0 < bnd ? L.so1 + (long long)u * pv1 + r0 : L.so2 + (long long)u * pv2 + (r0 - bnd));
+      double2 o = r0 < bnd ? o1 : o2;
+#pragma unroll
+      for (int k = 0; k < FT_RPT; ++k) {
+        const int r1 = r0 + k;
+        if (k > 0 && r1 == bnd) {
+          o = o2;  // segment 2 starts: the second class's walk
+          if constexpr (!DENSE && !PACKED) dst = Rb + L.so2 + (long long)u * pv2;
+        }
+        C2 val;
+        val.x = (T)(o.x * scale);
+        val.y = zero_im ? (T)0 : (T)(o.y * scale);
+        if ((omask >> k) & 1u) {
+          if constexpr (PACKED)
+            __stcs(dst, val);
+          else
+            *dst = val;
+        }
+        if constexpr (DENSE) stg[k * 32] = val;
+        if (k + 1 < FT_RPT) {
+          o = cadd(o, csub(fB[k], fT[k]));
+          // next row; the column wraps from P-1 to 0 after row bnd-1
+          const int wrapP = (r1 + 1 == bnd) ? P : 0;
+          if constexpr (DENSE)
+            dst += D + 1 - wrapP;
+          else if constexpr (PACKED)
+            dst += D - (k1 + k) - wrapP;
+          else
+            dst += 1;
+        }
+      }
+    }
+    prev = true;
+    if constexpr (!STAGE2 && DENSE) {
+      ft_unit_sync(bar, UT);
+      if (wmir) mirror(u, 0);
+      prev = false;
+    }
+    if (u < ac) {
+      // every row (no guards): entries outside the strip read zeros
+      const double2* va = vec + buf * 8 * PP + r0;
+      const double2* vq = vec + buf * 8 * PP;
+#pragma unroll
+      for (int k = 0; k < FT_RPT; ++k) {
+        ft_rank2(fT[k], va[1 * PP + k], vq[3 * PP + boff[k]], va[0 * PP + k], vq[2 * PP + boff[k]]);
+        ft_rank2(fB[k], va[5 * PP + k], vq[7 * PP + boff[k]], va[4 * PP + k], vq[6 * PP + boff[k]]);
+      }
+      const double2* gc = gcol0 + buf * 128 + lane;
+      G1 = cadd(G1, csub(gc[32], gc[0]));  // + CColR[u] - CColL[u]
+      G2 = cadd(G2, csub(gc[96], gc[64]));
+    }
+  }
+  cp_async_wait<0>();
+  if (STAGE2 && DENSE && prev) {
+    ft_unit_sync(bar, UT);
+    if (wmir) mirror(e1 - 1, (e1 - 1) & 1);
+  }
+  if (wsp && e1 < u_hi) {
+#pragma unroll
+    for (int k = 0; k < FT_RPT; ++k) {
+      wsp[4 * k] = fT[k].x;
+      wsp[4 * k + 1] = fT[k].y;
+      wsp[4 * k + 2] = fB[k].x;
+      wsp[4 * k + 3] = fB[k].y;
+    }
+    wsp[4 * FT_RPT] = G1.x;
+    wsp[4 * FT_RPT + 1] = G1.y;
+    wsp[4 * FT_RPT + 2] = G2.x;
+    wsp[4 * FT_RPT + 3] = G2.y;
+  }
+}
+
+}  // namespace covgpu
