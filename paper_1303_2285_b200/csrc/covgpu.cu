@@ -198,7 +198,11 @@ struct covgpu_plan {
   std::vector<int4> h_units;
   int4* d_runits = nullptr;   // class-range finalize: units holding a class of the range
   long long n_runits = 0;
-  double2* d_ck = nullptr;    // walk state at the cut steps u = 16 j (k_fin_ckpt)
+  double2* d_ck = nullptr;    // per-chunk state updates delta_j (the tile kernel's DELTA mode)
+  int4* d_dunits = nullptr;   // DELTA-mode units (all classes) and for the class range
+  long long n_dunits = 0;
+  int4* d_rdunits = nullptr;
+  long long n_rdunits = 0;
   // chunked walk for the synchronous host path (covgpu_plan_execute_host):
   // u-chunk bounds, saved walk state, an event per chunk
   static constexpr int kMaxFinChunks = 4;
@@ -348,6 +352,8 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_units);
   cudaFree(pl->d_runits);
   cudaFree(pl->d_ck);
+  cudaFree(pl->d_dunits);
+  cudaFree(pl->d_rdunits);
   cudaFree(pl->d_uc_off);
   cudaFree(pl->d_ecm_part);
   cudaFree(pl->d_band_flag);
@@ -495,10 +501,12 @@ template <typename T, int NW>
 cudaError_t fin_tile_attr() {
   const int smem = (int)(ft_unit_smem(NW, sizeof(typename CT<T>::c)) * FtCfg<NW>::UPC);
   g_attr_fail = "k_fin_tile<" + std::to_string(sizeof(T)) + "," + std::to_string(NW) + "> smem " + std::to_string(smem);
-  cudaError_t e = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaError_t r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_PACKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_PACKED, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (r != cudaSuccess) e = r;
-  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_COMPACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_COMPACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (r != cudaSuccess) e = r;
+  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (r != cudaSuccess) e = r;
   if (e == cudaSuccess) g_attr_fail.clear();
   return e;
@@ -556,9 +564,7 @@ cudaError_t set_attrs() {
       e = r;
     if ((r = fin_tile_attrs<double>()) != cudaSuccess) e = r;
     if ((r = fin_tile_attrs<float>()) != cudaSuccess) e = r;
-    if ((r = cudaFuncSetAttribute(k_fin_ckpt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ftk_smem(FINV_MAX_P))) != cudaSuccess)
-      e = r;
+
     return e;
   }();
   return once;
@@ -1119,7 +1125,8 @@ static inline int fin_corner_kr(const covgpu_plan* pl, int layout, bool direct) 
 // [lo, hi).  Walks are cut at u = 16 j (the state there comes from
 // k_fin_ckpt); pieces are ordered longest first, the bands of one
 // (snapshot, dc, piece) adjacent (their row segments share sectors).
-std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi) {
+// delta: the chunk units [16 (j-1), 16 j) of every cut step 16 j < Q - dc
+std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi, bool delta = false) {
   const int P = pl->pr.P, Q = pl->pr.Q;
   std::vector<char> has((size_t)(2 * P - 1) * Q, 0);
   for (int sl = lo; sl < hi; ++sl) {
@@ -1135,6 +1142,7 @@ std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi) {
     const int qu = Q - dc;
     for (int u0 = 0; u0 < qu; u0 += FT_CK) {
       const int u1 = std::min(qu, u0 + FT_CK);
+      if (delta && u1 >= qu) break;  // no cut after this chunk
       for (long long b = 0; b < pl->batch; ++b)
         for (int d0 = 0; d0 < P; d0 += 32) {
           bool any = false;  // circular diagonal c holds classes (c, dc) and (c - P, dc)
@@ -1151,38 +1159,29 @@ std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi) {
   return units;
 }
 
-// the walk state at the cut steps (needs the corner blocks and RC')
-void launch_fin_ckpt(covgpu_plan* pl, const double2* rc, int nseg, int slot_lo, int slot_hi, cudaStream_t st) {
-  if (!pl->d_ck) return;
-  const long long per = (long long)pl->pr.P * pl->pr.P;
-  const long long n = (per + FTK_THREADS - 1) / FTK_THREADS * pl->pr.Q * pl->batch;
-  k_fin_ckpt<<<(unsigned)n, FTK_THREADS, ftk_smem(pl->pr.P), st>>>(
-      (const double2*)pl->d_corners, pl->pr, pl->d_cls, pl->d_cls_slot, (int)pl->batch, rc, pl->tot_rc, nseg,
-      pl->d_ck, slot_lo, slot_hi);
-}
-
 template <typename T>
 void launch_fin_tile(covgpu_plan* pl, const int4* units, long long nunits, const double2* ccpart, int npart,
                      const double2* ccol, const double2* rc, int nseg, typename CT<T>::c* R, long long rstride,
                      double scale, int layout, int u0, int u1, double2* wst, int slot_lo, int slot_hi,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool delta = false) {
   using C2 = typename CT<T>::c;
   if (nunits <= 0) return;
-#define FT_LAUNCH(NW, LAY)                                                                                  \
+#define FT_LAUNCH(NW, LAY, DEL)                                                                             \
   do {                                                                                                      \
     constexpr int upc = FtCfg<NW>::UPC;                                                                     \
     const unsigned grid = (unsigned)((nunits + upc - 1) / upc);                                             \
     const size_t smem = ft_unit_smem(NW, sizeof(C2)) * upc;                                                 \
-    k_fin_tile<T, NW, LAY><<<grid, FtCfg<NW>::THREADS, smem, st>>>(                                         \
+    k_fin_tile<T, NW, LAY, DEL><<<grid, FtCfg<NW>::THREADS, smem, st>>>(                                    \
         (const double2*)pl->d_corners, pl->pr, pl->d_cls, pl->d_cls_slot, units, (int)nunits, pl->nclasses, \
         npart, ccpart, ccol, pl->tot_ccol, rc, pl->tot_rc, nseg, pl->d_ck, R, rstride, scale, u0, u1, wst,  \
         slot_lo, slot_hi);                                                                                  \
   } while (0)
 #define FT_LAY(NW)                                                           \
   do {                                                                       \
-    if (layout == COVGPU_DENSE) FT_LAUNCH(NW, COVGPU_DENSE);                 \
-    else if (layout == COVGPU_PACKED) FT_LAUNCH(NW, COVGPU_PACKED);          \
-    else FT_LAUNCH(NW, COVGPU_COMPACT);                                      \
+    if (delta) FT_LAUNCH(NW, COVGPU_DENSE, true);                            \
+    else if (layout == COVGPU_DENSE) FT_LAUNCH(NW, COVGPU_DENSE, false);     \
+    else if (layout == COVGPU_PACKED) FT_LAUNCH(NW, COVGPU_PACKED, false);   \
+    else FT_LAUNCH(NW, COVGPU_COMPACT, false);                               \
   } while (0)
   switch (pl->ft_nwarp) {
     case 1: FT_LAY(1); break;
@@ -1258,6 +1257,21 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->band_wait)
     CUDA_TRY(cudaStreamWaitEvent(es, pl->use_spec && pl->batch == 1 ? pl->ev_strips : pl->ev_h2d, 0));
   mark("start");
+  if (pl->use_tile) {
+    // the tile walk's corner blocks and per-chunk state updates need only the
+    // corners of A: first on the side stream, under the sums
+    const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
+    if (nc > 0) {
+      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, (double2*)pl->d_corners);
+      ++launches;
+    }
+    if (pl->n_dunits > 0) {
+      launch_fin_tile<T>(pl, pl->d_dunits, pl->n_dunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0,
+                         COVGPU_DENSE, 0, 1 << 30, nullptr, 0, INT_MAX, es, true);
+      ++launches;
+    }
+    if (!fork) mark("fin_delta");
+  }
   // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
   // bulk over every column block (which also yields the edge-column sums)
   bool mma = false;
@@ -1324,21 +1338,13 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     pl->launches = launches;
     return COVGPU_OK;
   }
-  if (pl->fin_kr > 0) {
-    const int ckr = pl->use_tile ? 1 : fin_corner_kr(pl, layout, layout != COVGPU_COMPACT && !pl->no_direct);
+  if (pl->fin_kr > 0 && !pl->use_tile) {
+    const int ckr = fin_corner_kr(pl, layout, layout != COVGPU_COMPACT && !pl->no_direct);
     const long long nc = 4LL * corner_rows(pr.P, ckr) * (pr.Q - 1) * B;
     if (nc > 0) {
-      if (pl->use_tile)
-        k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, (double2*)pl->d_corners);
-      else
-        k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, ckr, (C2*)pl->d_corners);
+      k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, ckr, (C2*)pl->d_corners);
       ++launches;
     }
-    if (pl->use_tile && pl->d_ck) {  // (P = 1: no corner rows, the cut states are the RC'-free zeros)
-      launch_fin_ckpt(pl, pl->d_rc, pl->nseg, 0, INT_MAX, es);
-      ++launches;
-    }
-    if (!fork) mark("fin_ckpt");  // (timing: corners + cut states on the main stream)
   }
   if (fork) {
     CUDA_TRY(cudaEventRecord(pl->ev_join, es));
@@ -1477,24 +1483,36 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
     const double2* cc = sums;
     const double2* cl = sums + (long long)B * pl->nclasses;
     const double2* rc = cl + (long long)B * pl->tot_ccol;
-    launch_fin_ckpt(pl, rc, 1, c_lo, c_hi, st);
+    const int4* dunits = pl->d_dunits;
+    long long ndunits = pl->n_dunits;
     const int4* units = pl->d_units;
     long long nunits = pl->n_units;
     if (!full) {
       if (pl->rtask_lo != c_lo || pl->rtask_hi != c_hi) {
         const std::vector<int4> sub = fin_tile_units(pl, c_lo, c_hi);
+        const std::vector<int4> dsub = fin_tile_units(pl, c_lo, c_hi, true);
         cudaFree(pl->d_runits);
-        pl->d_runits = nullptr;
+        cudaFree(pl->d_rdunits);
+        pl->d_runits = pl->d_rdunits = nullptr;
         CUDA_TRY(cudaMalloc((void**)&pl->d_runits, sizeof(int4) * std::max<size_t>(sub.size(), 1)));
+        CUDA_TRY(cudaMalloc((void**)&pl->d_rdunits, sizeof(int4) * std::max<size_t>(dsub.size(), 1)));
         if (!sub.empty())
           CUDA_TRY(cudaMemcpy(pl->d_runits, sub.data(), sizeof(int4) * sub.size(), cudaMemcpyHostToDevice));
+        if (!dsub.empty())
+          CUDA_TRY(cudaMemcpy(pl->d_rdunits, dsub.data(), sizeof(int4) * dsub.size(), cudaMemcpyHostToDevice));
         pl->n_runits = (long long)sub.size();
+        pl->n_rdunits = (long long)dsub.size();
         pl->rtask_lo = c_lo;
         pl->rtask_hi = c_hi;
       }
       units = pl->d_runits;
       nunits = pl->n_runits;
+      dunits = pl->d_rdunits;
+      ndunits = pl->n_rdunits;
     }
+    if (ndunits > 0)
+      launch_fin_tile<T>(pl, dunits, ndunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0, COVGPU_DENSE, 0,
+                         1 << 30, nullptr, 0, INT_MAX, st, true);
     launch_fin_tile<T>(pl, units, nunits, cc, 1, cl, rc, 1, (C2*)R_dev, r_bstride, scale, layout, 0, 1 << 30,
                        nullptr, c_lo, c_hi, st);
     CUDA_TRY(cudaGetLastError());
@@ -1994,9 +2012,15 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->n_units = (long long)pl->h_units.size();
       if (pl->use_tile && ft_nck(q) > 0) {
         const size_t ckn = (size_t)batch * q * ft_nck(q) * 2 * (size_t)p * p;
-        if ((rc = dalloc(&pl->d_ck, ckn, &ws))) {
+        const std::vector<int4> du = fin_tile_units(pl.get(), 0, pl->nclasses, true);
+        pl->n_dunits = (long long)du.size();
+        if ((rc = dalloc(&pl->d_ck, ckn, &ws)) || (rc = dalloc(&pl->d_dunits, std::max<size_t>(du.size(), 1), &ws))) {
           plan_free(pl.get());
           return rc;
+        }
+        if (!du.empty() && cudaMemcpy(pl->d_dunits, du.data(), sizeof(int4) * du.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+          plan_free(pl.get());
+          return fail(COVGPU_ECUDA, "delta units upload");
         }
       }
       // tasks: (class, snapshot group of 32/W snapshots), W = min(32, pow2ceil(pv))

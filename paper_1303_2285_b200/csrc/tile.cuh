@@ -28,9 +28,11 @@
 // one step later from a double-buffered SMEM stage, again as row segments;
 // the strip columns of the next step are prefetched with cp.async.
 //
-// Walks are cut at u = 16 j: k_fin_ckpt computes the state at those steps
-// (off the critical path: it reads only the corner blocks of A), so every
-// unit walks <= 16 steps and the launch fills the SMs.  The cut grid is a
+// Walks are cut at u = 16 j: the same kernel in DELTA mode adds up each
+// 16-step chunk's updates (from zero; it reads only the corner blocks of A,
+// so it runs first, off the critical path), and a unit starting at u_lo = 16 j
+// takes F(u_lo) = F(0) + delta_1 + ... + delta_j.  Every unit walks <= 16
+// steps and the launch fills the SMs.  The cut grid is a
 // fixed function of u, and every value depends only on its class's sums and
 // the fixed 8-row grouping: class subsets (shards), layouts, batches and
 // u-chunked launches give the same bits; packed R equals dense R's upper
@@ -44,7 +46,10 @@ namespace covgpu {
 #ifndef FT_CTA_WARPS
 #define FT_CTA_WARPS 8
 #endif
-constexpr int FT_RPT = 8;  // rows per thread
+#ifndef FT_RPT_DEF
+#define FT_RPT_DEF 8
+#endif
+constexpr int FT_RPT = FT_RPT_DEF;  // rows per thread
 constexpr int FT_CK = 16;  // checkpoint spacing (steps)
 
 template <int NWARP>
@@ -63,12 +68,14 @@ inline int ft_nwarp(int P) {
 }
 __host__ __device__ inline int ft_nck(int Q) { return (Q - 1) / FT_CK; }  // checkpoints per (snapshot, dc)
 
-// SMEM per unit: strip vectors [2 bufs][8][PP] double2 (entries [P-1, PP)
-// stay zero: out-of-strip rows read them, the update needs no guards),
+// SMEM per unit: strip vectors [2 bufs][12 PP] double2 — first operands
+// TL, TR, BL, BR at column u ([PP] each), second operands at column u + dc
+// ([2 PP] each, the strip twice: index (r1 + c) mod P needs no wrap) —
+// with entries outside the strip zero (the update needs no guards),
 // row-group totals [2 bufs][T1, B1, T2, B2][nwarp][32] double2, edge-column
 // sums of the step [2 bufs][class 1, 2][L, R][32] double2, stage
 // [2 bufs][PP][32] (output precision)
-__host__ __device__ inline size_t ft_vec_bytes(int nwarp) { return (size_t)2 * 8 * nwarp * FT_RPT * 16; }
+__host__ __device__ inline size_t ft_vec_bytes(int nwarp) { return (size_t)2 * 12 * nwarp * FT_RPT * 16; }
 __host__ __device__ inline size_t ft_tot_bytes(int nwarp) { return (size_t)2 * 4 * nwarp * 32 * 16; }
 __host__ __device__ inline size_t ft_gcol_bytes() { return (size_t)2 * 4 * 32 * 16; }
 // (P > 64: one stage buffer, the mirror follows its step after a second barrier)
@@ -163,90 +170,18 @@ __device__ inline void ft_init_entry(int r1, int c, int P, const FtLane& L, cons
   }
 }
 
-// Walk state at the cut steps u = 16 j (j = 1 .. ft_nck(Q), u < Q - dc) for
-// every (snapshot, dc, row, circular diagonal), computed with the walk's own
-// update arithmetic (same operands, same order: the bits a continuous walk
-// would carry); layout ck[b][dc][j-1][T, B][row][c].  CTA = 256 consecutive
-// entries (r1, c) of one (snapshot, dc); the strip columns of FT_CK steps at
-// a time are staged in SMEM (rows the CTA needs for the first operand, all
-// rows for the second).
-constexpr int FTK_THREADS = 256;
-__host__ __device__ inline int ftk_rows(int P) {  // first-operand rows per CTA
-  return FTK_THREADS / P + 2 < P ? FTK_THREADS / P + 2 : P;
-}
-__host__ __device__ inline size_t ftk_smem(int P) {
-  return (size_t)FT_CK * 4 * (ftk_rows(P) + P) * sizeof(double2);
-}
-__global__ void __launch_bounds__(FTK_THREADS) k_fin_ckpt(const double2* __restrict__ corners, Problem pr,
-                                                          const ClassDesc* __restrict__ cls,
-                                                          const int* __restrict__ cls_slot, int B,
-                                                          const double2* __restrict__ rc, long long tot_rc,
-                                                          int nseg, double2* __restrict__ ck, int slot_lo,
-                                                          int slot_hi) {
-  extern __shared__ __align__(16) double2 ftk[];
-  const int P = pr.P, Q = pr.Q, S = P - 1, Wc = Q - 1, nck = ft_nck(Q);
-  const long long per = (long long)P * P;
-  const int cpd = (int)((per + FTK_THREADS - 1) / FTK_THREADS);  // CTAs per (snapshot, dc)
-  const int dc = (int)(blockIdx.x / cpd % Q), b = (int)(blockIdx.x / cpd / Q);
-  const int qu = Q - dc;
-  if (qu <= FT_CK) return;                      // no cut inside this walk (CTA-uniform)
-  const int last = ((qu - 1) / FT_CK) * FT_CK;  // last cut step (< qu)
-  const int e = (int)(blockIdx.x % cpd) * FTK_THREADS + threadIdx.x;
-  const bool on = e < per;
-  const int c = on ? e % P : 0, r1 = on ? e / P : 0;
-  const int rlo = (int)(blockIdx.x % cpd) * FTK_THREADS / P, NR = ftk_rows(P);
-  double2 fT = make_double2(0.0, 0.0), fB = fT;
-  if (on) {
-    const FtLane L = ft_lane(c, dc, P, Q, cls, cls_slot, slot_lo, slot_hi);
-    ft_init_entry(r1, c, P, L, rc + (long long)b * tot_rc * nseg, nseg, fT, fB);
-  }
-  const int r2 = (r1 + c) % P;
-  const bool live = on && r1 < S && r2 < S;  // other entries read zero strip rows: no change
-  const double2* cb = corners + (long long)b * 4 * S * Wc;
-  // staged chunk: A-operand rows [t][blk][NR] (blk = TL, TR, BL, BR at column
-  // t), B-operand rows [t][blk][P] (column t + dc)
-  double2* sa = ftk;
-  double2* sq = ftk + FT_CK * 4 * NR;
-  double2* out = ck + (((long long)b * Q + dc) * nck) * 2 * per + e;
-  for (int t0 = 0; t0 < last; t0 += FT_CK) {
-    __syncthreads();
-    for (int x = threadIdx.x; x < FT_CK * 4 * (NR + P); x += FTK_THREADS) {
-      const bool isa = x < FT_CK * 4 * NR;
-      const int y = isa ? x : x - FT_CK * 4 * NR, len = isa ? NR : P;
-      const int t = y / (4 * len), blk = y / len % 4, i = y % len;
-      const int row = isa ? rlo + i : i, col = t0 + t + (isa ? 0 : dc);
-      // rows outside the strip (and columns past the last cut) read as zero
-      const bool ok = row < S && col < Wc;
-      cp_async_elem<16>((isa ? sa : sq) + y, cb + (ok ? ((long long)blk * Wc + col) * S + row : 0), ok);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    if (live) {
-      const int ia = r1 - rlo;
-#pragma unroll 4
-      for (int t = 0; t < FT_CK; ++t) {
-        const double2* a = sa + t * 4 * NR + ia;
-        const double2* q = sq + t * 4 * P + r2;
-        ft_rank2(fT, a[NR], q[P], a[0], q[0]);
-        ft_rank2(fB, a[3 * NR], q[3 * P], a[2 * NR], q[2 * P]);
-      }
-    }
-    if (on) {
-      double2* o = out + (long long)(t0 / FT_CK) * 2 * per;
-      o[0] = fT;
-      o[per] = fB;
-    }
-  }
-}
-
-template <typename T, int NWARP, int LAYOUT>
-__global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
+#ifndef FT_MINB
+#define FT_MINB 1
+#endif
+// DELTA: unit = (snapshot, dc, band, chunk [16 (j-1), 16 j)); the chunk's
+// state updates from zero go to ck[b][dc][j-1][T, B][row][c] (no output)
+template <typename T, int NWARP, int LAYOUT, bool DELTA>
+__global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB)
     k_fin_tile(const double2* __restrict__ corners, Problem pr, const ClassDesc* __restrict__ cls,
                const int* __restrict__ cls_slot, const int4* __restrict__ units, int nunits, int nclasses,
                int npart, const double2* __restrict__ ccpart, const double2* __restrict__ ccol,
                long long tot_ccol, const double2* __restrict__ rc, long long tot_rc, int nseg,
-               const double2* __restrict__ ck, typename CT<T>::c* __restrict__ R, long long r_bstride,
+               double2* __restrict__ ck, typename CT<T>::c* __restrict__ R, long long r_bstride,
                double scale, int u_begin, int u_end, double2* __restrict__ wstate, int slot_lo, int slot_hi) {
   using C2 = typename CT<T>::c;
   constexpr int UPC = FtCfg<NWARP>::UPC, UT = 32 * NWARP, PP = NWARP * FT_RPT;
@@ -280,23 +215,20 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
   // per-row masks: output entry, mirrored entry; the mirror writer lane l
   // handles source lane m = 31 - l (its columns ascend with l)
   unsigned omask = 0;
-  int boff[FT_RPT];  // strip index of the row's second A row (P-1: a zero entry)
 #pragma unroll
   for (int k = 0; k < FT_RPT; ++k) {
-    const int r1 = r0 + k, r2 = (r1 + c) % P;
+    const int r1 = r0 + k;
     if (r1 < P && ((r1 < bnd) ? L.slot1 : L.slot2) >= 0) omask |= 1u << k;
-    boff[k] = r2 < S ? r2 : S;
   }
+  const int r2_0 = (r0 + c) % P;  // second A row of row r0 (rows r0 + k: r2_0 + k in the doubled strip)
   const int m = 31 - lane, cm = d0 + m;
   const bool m1 = __shfl_sync(0xffffffffu, L.slot1, m) >= 0 && (dc > 0 || cm > 0);
   const bool m2 = __shfl_sync(0xffffffffu, L.slot2, m) >= 0;
   unsigned mmask = 0;
-  int mcol[FT_RPT];  // mirror row r2 = r0 + k: source row (r2 - cm) mod P
+  const int msrc0 = cm < P ? ((r0 - cm) % P + P) % P : 0;  // mirror row r0 + k: source row (msrc0 + k) mod P
 #pragma unroll
   for (int k = 0; k < FT_RPT; ++k) {
-    const int r2 = r0 + k;
-    const int src = cm < P ? ((r2 - cm) % P + P) % P : 0;
-    mcol[k] = src;
+    const int r2 = r0 + k, src = (msrc0 + k) % P;
     if (cm < P && r2 < P && (src < P - cm ? m1 : m2)) mmask |= 1u << k;
   }
   const bool wout = __any_sync(0xffffffffu, omask != 0);
@@ -305,7 +237,12 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
   double* const wsp = wstate ? (double*)(wstate + ((long long)unit * UT + ut) * FT_STATE) : nullptr;
 
   double2 fT[FT_RPT], fB[FT_RPT], G1 = make_double2(0.0, 0.0), G2 = G1;
-  if (resume) {
+  const long long per = (long long)P * P;
+  const double2* ckb = ck + ((long long)b * Q + dc) * ft_nck(Q) * 2 * per + c;
+  if (DELTA) {
+#pragma unroll
+    for (int k = 0; k < FT_RPT; ++k) fT[k] = fB[k] = make_double2(0.0, 0.0);
+  } else if (resume) {
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) {
       fT[k] = make_double2(wsp[4 * k], wsp[4 * k + 1]);
@@ -314,20 +251,17 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
     G1 = make_double2(wsp[4 * FT_RPT], wsp[4 * FT_RPT + 1]);
     G2 = make_double2(wsp[4 * FT_RPT + 2], wsp[4 * FT_RPT + 3]);
   } else {
-    if (u_lo == 0) {
-      const double2* rcb = rc + (long long)b * tot_rc * nseg;
+    // F(u_lo) = F(0) + delta_1 + ... + delta_{u_lo / 16} (fixed order)
+    const double2* rcb = rc + (long long)b * tot_rc * nseg;
 #pragma unroll
-      for (int k = 0; k < FT_RPT; ++k) ft_init_entry(r0 + k, c, P, L, rcb, nseg, fT[k], fB[k]);
-    } else {
-      const long long per = (long long)P * P;
-      const double2* ckp = ck + (((long long)b * Q + dc) * ft_nck(Q) + (u_lo / FT_CK - 1)) * 2 * per + c;
+    for (int k = 0; k < FT_RPT; ++k) ft_init_entry(r0 + k, c, P, L, rcb, nseg, fT[k], fB[k]);
+    for (int j = 0; j < u_lo / FT_CK; ++j) {
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
         const int r1 = r0 + k;
-        fT[k] = fB[k] = make_double2(0.0, 0.0);
         if (r1 < P && c < P) {
-          fT[k] = ckp[(long long)r1 * P];
-          fB[k] = ckp[per + (long long)r1 * P];
+          fT[k] = cadd(fT[k], ckb[(long long)j * 2 * per + (long long)r1 * P]);
+          fB[k] = cadd(fB[k], ckb[(long long)j * 2 * per + per + (long long)r1 * P]);
         }
       }
     }
@@ -357,42 +291,49 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
   }
   ft_unit_sync(bar, UT);  // tot0 is reused by the steps
   for (int e = ut; e < 2 * 4 * 32; e += UT) gcol0[e] = make_double2(0.0, 0.0);  // absent classes stay 0
-  for (int e = ut; e < 2 * 8 * PP; e += UT) vec[e] = make_double2(0.0, 0.0);   // the zero padding
+  for (int e = ut; e < 2 * 12 * PP; e += UT) vec[e] = make_double2(0.0, 0.0);  // the zero padding
   ft_unit_sync(bar, UT);
 
-  // strip columns of step u (only while u < ac): 0 TL[u], 1 TR[u],
-  // 2 TL[u+dc], 3 TR[u+dc], 4 BL[u], 5 BR[u], 6 BL[u+dc], 7 BR[u+dc]; this
-  // thread copies elements ut and ut + UT (8 (P-1) < 2 UT), and the step's
-  // CColL / CColR of both classes of its lane (gcol [class][L, R][lane])
+  // strip columns of step u (only while u < ac): first operands TL, TR, BL,
+  // BR at column u (element e < 4 S), second operands at column u + dc, each
+  // copied twice (e >= 4 S); this thread copies elements ut, ut + UT, ut + 2 UT
+  // (12 (P-1) < 3 UT), and warp x % NWARP the step's CColL / CColR of class
+  // x / 2 of its lane (gcol [class][L, R][lane])
   const double2* cb = corners + (long long)b * 4 * S * Wc;
-  const double2* psrc[2];
-  int pdst[2];
+  const double2* psrc[3];
+  int pdst[3];
 #pragma unroll
-  for (int x = 0; x < 2; ++x) {
+  for (int x = 0; x < 3; ++x) {
     const int e = ut + x * UT;
-    const int v = e / S, i = e - v * S;
-    pdst[x] = e < 8 * S ? v * PP + i : -1;
-    const int blk = ((v >> 2) << 1) | (v & 1);
-    psrc[x] = cb + ((long long)blk * Wc + ((v & 2) ? dc : 0)) * S + i;
-  }
-  const double2* gsrc[4];
-  int gdst[4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int e = lane + 32 * x;  // e = (class * 2 + side) * 32 + lane; warp x of the unit copies it
-    const int cl = x >> 1, side = x & 1;
-    const bool ok = w == x % NWARP && (cl == 0 ? L.slot1 : L.slot2) >= 0;
-    gdst[x] = ok ? e : -1;
-    gsrc[x] = clb + (cl == 0 ? L.cl1 : L.cl2) + (side ? ac : 0);
+    int dst = -1, blk = 0, i = 0, col = 0;
+    if (e < 4 * S) {
+      blk = e / S;
+      i = e - blk * S;
+      dst = blk * PP + i;
+    } else if (e < 12 * S) {
+      const int e2 = e - 4 * S;
+      blk = e2 / (2 * S);
+      const int rem = e2 - blk * 2 * S, copy = rem / S;
+      i = rem - copy * S;
+      dst = 4 * PP + blk * 2 * PP + copy * P + i;
+      col = dc;
+    }
+    pdst[x] = dst;
+    psrc[x] = cb + ((long long)blk * Wc + col) * S + i;
   }
   auto prefetch = [&](int uu, int buf) {
     if (uu < ac && uu < e1) {
 #pragma unroll
-      for (int x = 0; x < 2; ++x)
-        if (pdst[x] >= 0) cp_async_elem<16>(vec + buf * 8 * PP + pdst[x], psrc[x] + (long long)uu * S, true);
+      for (int x = 0; x < 3; ++x)
+        if (pdst[x] >= 0) cp_async_elem<16>(vec + buf * 12 * PP + pdst[x], psrc[x] + (long long)uu * S, true);
+      if (!DELTA) {
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-        if (gdst[x] >= 0) cp_async_elem<16>(gcol0 + buf * 128 + gdst[x], gsrc[x] + uu, true);
+        for (int x = 0; x < 4; ++x) {
+          const long long co = x < 2 ? L.cl1 : L.cl2;
+          if (w == x % NWARP && (x < 2 ? L.slot1 : L.slot2) >= 0)
+            cp_async_elem<16>(gcol0 + buf * 128 + x * 32 + lane, clb + co + ((x & 1) ? ac : 0) + uu, true);
+        }
+      }
     }
     cp_async_commit();
   };
@@ -409,9 +350,11 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
     C2* row = Rb + ((long long)P * (um + dc) + r0) * D + (long long)P * um;
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) {
-      C2 val = stg[mcol[k] * 32];
+      int src = msrc0 + k;
+      if (src >= P) src -= P;
+      C2 val = stg[src * 32];
       val.y = -val.y;
-      if ((mmask >> k) & 1u) row[mcol[k]] = val;
+      if ((mmask >> k) & 1u) row[src] = val;
       row += D;
     }
   };
@@ -419,7 +362,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
   for (; u < e1; ++u) {
     const int buf = u & 1;
     double2* const tot = tot0 + buf * 4 * NWARP * 32;
-    {
+    if constexpr (!DELTA) {
       double2 t1 = make_double2(0.0, 0.0), b1 = t1, t2 = t1, b2 = t1;
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
@@ -439,8 +382,8 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
     cp_async_wait<0>();  // this step's strip columns and edge-column sums
     ft_unit_sync(bar, UT);
     prefetch(u + 1, buf ^ 1);
-    if (STAGE2 && DENSE && prev && wmir) mirror(u - 1, buf ^ 1);
-    if (wout) {
+    if (!DELTA && STAGE2 && DENSE && prev && wmir) mirror(u - 1, buf ^ 1);
+    if (!DELTA && wout) {
       // O at the warp's first row of each segment: G + top rows from there
       // down + bottom rows above it (x < w: bottoms, x >= w: tops)
       double2 o1 = G1, o2 = G2;
@@ -490,20 +433,20 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
         }
       }
     }
-    prev = true;
-    if constexpr (!STAGE2 && DENSE) {
+    prev = !DELTA;
+    if constexpr (!DELTA && !STAGE2 && DENSE) {
       ft_unit_sync(bar, UT);
       if (wmir) mirror(u, 0);
       prev = false;
     }
     if (u < ac) {
       // every row (no guards): entries outside the strip read zeros
-      const double2* va = vec + buf * 8 * PP + r0;
-      const double2* vq = vec + buf * 8 * PP;
+      const double2* va = vec + buf * 12 * PP + r0;
+      const double2* vq = vec + buf * 12 * PP + 4 * PP + r2_0;
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
-        ft_rank2(fT[k], va[1 * PP + k], vq[3 * PP + boff[k]], va[0 * PP + k], vq[2 * PP + boff[k]]);
-        ft_rank2(fB[k], va[5 * PP + k], vq[7 * PP + boff[k]], va[4 * PP + k], vq[6 * PP + boff[k]]);
+        ft_rank2(fT[k], va[PP + k], vq[2 * PP + k], va[k], vq[k]);
+        ft_rank2(fB[k], va[3 * PP + k], vq[6 * PP + k], va[2 * PP + k], vq[4 * PP + k]);
       }
       const double2* gc = gcol0 + buf * 128 + lane;
       G1 = cadd(G1, csub(gc[32], gc[0]));  // + CColR[u] - CColL[u]
@@ -511,6 +454,18 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, 1)
     }
   }
   cp_async_wait<0>();
+  if constexpr (DELTA) {
+    double2* o = (double2*)ckb + (long long)(u_lo / FT_CK) * 2 * per;
+#pragma unroll
+    for (int k = 0; k < FT_RPT; ++k) {
+      const int r1 = r0 + k;
+      if (r1 < P && c < P) {
+        o[(long long)r1 * P] = fT[k];
+        o[per + (long long)r1 * P] = fB[k];
+      }
+    }
+    return;
+  }
   if (STAGE2 && DENSE && prev) {
     ft_unit_sync(bar, UT);
     if (wmir) mirror(e1 - 1, (e1 - 1) & 1);
