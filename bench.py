@@ -70,40 +70,117 @@ def products(w):
     return um_count(n, m, p, q), bulk, edge, corner, core
 
 
-def cpu_reference(w, budget_s: float, seed: int = 0):
+def cpu_reference(w, budget_s: float):
     """Time the oracle's C port of the reference's class kernel (SAT per
-    class, thread pool over classes) on a stratified class sample; return
-    (entries/s extrapolated by product count, sample description, threads)."""
+    class, pthread pool over classes like engine.py:158-190) on this host's
+    cores.  One snapshot: the FULL workload (every class), no extrapolation.
+    A batch: whole snapshots (every class) until >= 64 snapshots and
+    `budget_s` are reached, scaled by the snapshot count.
+    Returns (R entries/s, sample description, threads, seconds for the
+    workload)."""
     from oracle import covoracle_c
-    from paper_1303_2285_b200.combinations import pair_count, unique_combinations
-    from paper_1303_2285_b200.core import WindowSpec
     from paper_1303_2285_b200.workloads import make_input
 
     a = make_input(w)
-    a0 = (a if w.batch == 1 else a[0]).astype(np.complex128)
-    combos = unique_combinations(WindowSpec(w.p, w.q))
-    mu = np.array([pair_count(c, w.n, w.m) for c in combos], dtype=np.float64)
     threads = covoracle_c.max_threads()
-    # calibrate on a small stratified sample, then size the timed sample
-    ncls = len(combos)
-    probe = np.linspace(0, ncls - 1, min(ncls, max(threads, 16))).round().astype(np.int32)
-    t0 = time.perf_counter()
-    covoracle_c.estimate_packed(a0, w.p, w.q, probe, threads)
-    t_probe = max(time.perf_counter() - t0, 1e-6)
-    per_prod = t_probe / mu[probe].sum()
-    want = int(ncls * min(1.0, budget_s / max(per_prod * mu.sum(), 1e-9)))
-    want = max(min(ncls, want), min(ncls, threads))
-    ids = np.unique(np.linspace(0, ncls - 1, want).round().astype(np.int32))
-    t0 = time.perf_counter()
-    covoracle_c.estimate_packed(a0, w.p, w.q, ids, threads)
-    t = time.perf_counter() - t0
-    t_full = t * mu.sum() / mu[ids].sum() * w.batch
     entries = float(w.pq) ** 2 * w.batch
-    frac = mu[ids].sum() / mu.sum()
-    sample = (f"{len(ids)} of {ncls} offset classes (stratified, {frac:.1%} of the products) of "
-              f"{'1 snapshot of ' if w.batch > 1 else ''}{w.name} in {t:.2f} s on {threads} threads, "
-              f"extrapolated by product count to the full workload ({t_full:.1f} s)")
+    if w.batch == 1:
+        t0 = time.perf_counter()
+        covoracle_c.estimate_packed(a.astype(np.complex128), w.p, w.q, None, threads)
+        t = time.perf_counter() - t0
+        return entries / t, (f"full workload ({w.name}: all offset classes, {w.pq}x{w.pq} R) in {t:.2f} s "
+                             f"on {threads} threads, no extrapolation"), threads, t
+    done, t0 = 0, time.perf_counter()
+    while done < w.batch and (done < 64 or time.perf_counter() - t0 < budget_s):
+        covoracle_c.estimate_packed(a[done].astype(np.complex128), w.p, w.q, None, threads)
+        done += 1
+    t = time.perf_counter() - t0
+    t_full = t * w.batch / done
+    sample = (f"{done} of {w.batch} snapshots of {w.name} (every offset class) in {t:.2f} s on {threads} "
+              f"threads" + ("" if done == w.batch else f", scaled by snapshot count ({t_full:.2f} s for all)"))
     return entries / t_full, sample, threads, t_full
+
+
+def stock_reference(w, budget_s: float):
+    """The UNMODIFIED reference package (covcomb, installed into baseline/_ref
+    from /root/reference/pkg) through its own code path on this host:
+    cfg1-cfg3 the fastest stock call measured in SURVEY.md §6 (numba
+    seq-opt / estimate_parallel on all cores), the whole workload; cfg4
+    estimate_batch on all cores over a snapshot subset; cfg5 the stock numpy
+    class kernel (engine._run_class, what measure_combination_times times,
+    engine.py:258-288) over a stratified class sample, scaled by each class's
+    product count (the full run is ~40 min single-threaded).  None when the
+    package is not installed."""
+    ref_root = ROOT / "baseline" / "_ref"
+    if not (ref_root / "covcomb").exists():
+        return None
+    if str(ref_root) not in sys.path:
+        sys.path.insert(0, str(ref_root))
+    try:
+        import covcomb
+        from covcomb import combinations as cc_comb
+        from covcomb import engine as cc_engine
+    except Exception as exc:  # noqa: BLE001 — report, never fail the bench
+        return {"unavailable": f"covcomb import failed: {exc}"}
+    from paper_1303_2285_b200.workloads import make_input
+
+    ncores = len(os.sched_getaffinity(0))
+    a = make_input(w)
+    win = covcomb.WindowSpec(w.p, w.q)
+    entries = float(w.pq) ** 2 * w.batch
+
+    def best(fn, reps=2):
+        fn()  # warm (numba JIT / caches)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    try:
+        if w.name == "cfg1":
+            t = best(lambda: covcomb.estimate_combinations(a, win, "seq-opt", backend="numba"), reps=5)
+            call, cores, sample = "estimate_combinations(mode='seq-opt', backend='numba')", 1, "full workload"
+        elif w.batch == 1 and w.name != "cfg5":
+            a2 = a.astype(np.complex128)
+            t = best(lambda: covcomb.estimate_parallel(a2, win, threads=ncores, backend="numba"),
+                     reps=1 if w.name == "cfg3" else 2)
+            call, cores, sample = f"estimate_parallel(threads={ncores}, backend='numba')", ncores, "full workload"
+        elif w.batch > 1:
+            nb = 64
+            sub = [x.astype(np.complex128) for x in a[:nb]]
+            t_sub = best(lambda: covcomb.estimate_batch(sub, win, threads=ncores, backend="numba"), reps=1)
+            t = t_sub * w.batch / nb
+            call, cores = f"estimate_batch(threads={ncores}, backend='numba')", ncores
+            sample = f"{nb} of {w.batch} snapshots in {t_sub:.2f} s, scaled by snapshot count"
+        else:
+            from covcomb import backend as cc_backend
+            from covcomb import core as cc_core
+
+            mat = cc_core.as_input_matrix(a)
+            name = cc_backend.resolve_backend("numpy")
+            kern = cc_engine._load_kernels(name)
+            combos = cc_comb.unique_combinations(win)
+            mu = np.array([cc_comb.pair_count(c, w.n, w.m) for c in combos], dtype=np.float64)
+            out = covcomb.CovarianceMatrix(win.stack_size).packed
+            scratch = np.empty(cc_engine._max_scratch(combos, win), dtype=np.complex128)
+            pane = np.empty(mat.n * mat.m, dtype=np.complex128)
+            cc_engine._run_class(kern, name, mat.array, combos[0], win, out, scratch, pane)  # warm
+            ids = np.linspace(0, len(combos) - 1, max(8, int(budget_s / 0.3))).round().astype(int)
+            ids = np.unique(ids)
+            t0 = time.perf_counter()
+            for i in ids:
+                cc_engine._run_class(kern, name, mat.array, combos[i], win, out, scratch, pane)
+            t_s = time.perf_counter() - t0
+            t = t_s * mu.sum() / mu[ids].sum()
+            call, cores = "engine._run_class per class, backend='numpy' (the fastest stock path at cfg5)", 1
+            sample = (f"{len(ids)} of {len(combos)} offset classes (stratified) in {t_s:.1f} s, scaled by "
+                      f"product count to all classes ({t:.0f} s)")
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"stock covcomb run failed: {exc}"}
+    return {"value": entries / t, "unit": UNIT, "cores": cores, "kind": "reference", "call": call,
+            "sample": sample, "seconds_for_workload": t}
 
 
 class ClockSampler:
@@ -163,7 +240,19 @@ class ClockSampler:
         }
 
 
+def bench_config(w, layout: str, world: int = 1, rowband: bool = False, sums_mib: float = 0.0) -> dict:
+    """The `config` object both arms print (same keys, same values)."""
+    return {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
+            "input": w.dtype, "output": layout, "l2": "flushed between steps (256 MiB write)",
+            "parallelism": (f"row-band x{world}: per-band sums, one all-reduce of [CC|CCol|RC'] "
+                            f"({sums_mib:.1f} MiB), class-range finalize")
+            if rowband else (f"class-shard x{world}" if world > 1 else "single GPU")}
+
+
 def run_reference(args, rank: int) -> None:
+    """Reference arm: the reference's algorithm (the oracle's C port of its
+    SAT class kernel) on all host cores, the FULL workload every step (no
+    extrapolation), plus one timing of the unmodified covcomb package."""
     from paper_1303_2285_b200.workloads import workload
 
     if rank != 0:
@@ -171,23 +260,28 @@ def run_reference(args, rank: int) -> None:
     w = workload(args.config)
     for _ in range(args.warmup):
         cpu_reference(w, args.ref_budget)
-    vals, samples, threads = [], None, 1
+    vals, samples, threads, ts = [], None, 1, []
     for _ in range(args.steps):
-        v, samples, threads, _t = cpu_reference(w, args.ref_budget)
+        v, samples, threads, t = cpu_reference(w, args.ref_budget)
         vals.append(v)
+        ts.append(t)
     value = statistics.median(vals)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(w.pq) ** 2 * w.batch / value * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": f"synthetic ({w.name}: seeded, BASELINE.json config)",
-        "config": {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
-                   "input": w.dtype, "path": "oracle C port of the reference class kernel"},
+        "dtype": "f64", "data": f"synthetic ({w.name}: seeded CN(0,1)/sinusoid inputs of BASELINE.json)",
+        "config": bench_config(w, args.layout, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": samples},
+                         "sample": samples,
+                         "path": "oracle C port of the reference class kernel (packed upper triangle)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "timed_seconds": sum(ts),
     }
+    if not args.no_stock:
+        line["stock_reference"] = stock_reference(w, args.ref_budget * 3)
     print(json.dumps(line), flush=True)
 
 
@@ -201,7 +295,9 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of CPU-baseline sample")
-    ap.add_argument("--ref-budget", type=float, default=4.0, help="seconds per reference-arm step")
+    ap.add_argument("--ref-budget", type=float, default=4.0,
+                    help="seconds of snapshots per reference-arm step (batched configs; >= 64 snapshots)")
+    ap.add_argument("--no-stock", action="store_true", help="skip the unmodified-covcomb timing")
     ap.add_argument("--layout", default="dense", choices=["dense", "packed", "compact"])
     ap.add_argument("--rowband", action="store_true",
                     help="use the multi-GPU row-band mode also at N=1 (testing)")
@@ -391,7 +487,7 @@ def main() -> None:
         dom = max(per_kernel, key=lambda k: kernel_ms[k])
         roof = dict(per_kernel[dom])
         roof["kernel"] = {"spec_corr": "k_spec_corr_smem", "spec_fft": "k_spec_fft",
-                          "bulk_dmma": "k_bulk_dmma3", "bulk": "k_bulk_tma", "finalize": "k_finalize_v",
+                          "bulk_dmma": "k_bulk_dmma3", "bulk": "k_bulk_tma", "finalize": "k_fin_tile",
                           "expand": "k_expand"}.get(dom, dom)
         roof["share_of_step"] = kernel_ms[dom] / max(sum(kernel_ms.values()), 1e-12)
         roof["traffic"] = None
@@ -416,11 +512,7 @@ def main() -> None:
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64" if w.dtype == "c128" else "f32",
         "data": f"synthetic ({w.name}: seeded CN(0,1)/sinusoid inputs of BASELINE.json)",
-        "config": {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
-                   "input": w.dtype, "output": layout, "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": (f"row-band x{world}: per-band sums, one all-reduce of [CC|CCol|RC'] "
-                                   f"({sums.numel() * 16 / 2**20:.1f} MiB), class-range finalize")
-                   if rowband else (f"class-shard x{world}" if world > 1 else "single GPU")},
+        "config": bench_config(w, layout, world, rowband, sums.numel() * 16 / 2**20 if rowband else 0.0),
         "effective_gflops": flops / (ms * 1e-3) / 1e9,
         "effective_gflops_note": "8 x UM (the paper's unique products) / step time; the spectral path "
                                  "does fewer flops than that, so this is not a hardware rate",
@@ -570,6 +662,8 @@ def main() -> None:
         v, sample, threads, t_full = cpu_reference(w, args.cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": sample}
+        if not args.no_stock:
+            line["cpu_baseline_stock"] = stock_reference(w, args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()

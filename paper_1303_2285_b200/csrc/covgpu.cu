@@ -241,6 +241,11 @@ struct covgpu_plan {
   long long as_n = 0;
   int as_err = 0;
   std::mutex exec_mu;  // executes mutate plan state (tensor-map cache, timing events)
+  // the workspace is shared by every execute of the plan: an execute on a
+  // stream other than the previous one's waits for it (event ev_done)
+  cudaEvent_t ev_done = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
   // CUDA-graph replay of covgpu_plan_execute: the second call with the same
   // (A, R, layout, scale) captures the launch sequence (side-stream fork /
   // join included) on cap_stream; later identical calls launch the graph
@@ -363,6 +368,7 @@ void plan_free(covgpu_plan* pl) {
   if (pl->ev_strips) cudaEventDestroy(pl->ev_strips);
   cudaFree(pl->d_ecm_tickets);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+  if (pl->ev_done) cudaEventDestroy(pl->ev_done);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   if (pl->as_in) cudaStreamDestroy(pl->as_in);
   if (pl->as_out) cudaStreamDestroy(pl->as_out);
@@ -1580,10 +1586,37 @@ std::string path_env() {
   return e;
 }
 
+// Plans cached per shape for the one-shot calls, held by shared ownership:
+// evicting an entry never frees a plan another thread is still executing
+// (the last holder's release destroys it).
 std::mutex g_cache_mu;
-std::map<PlanKey, covgpu_plan*> g_cache;
+std::map<PlanKey, std::shared_ptr<covgpu_plan>> g_cache;
 
 }  // namespace
+
+extern "C" {
+static int plan_execute_locked(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_t layout, double scale,
+                               cudaStream_t st);
+}
+
+// Order this execute after the plan's previous one when it runs on another
+// stream (the workspace is per plan), and record its completion.
+static int plan_stream_enter(covgpu_plan* pl, cudaStream_t st) {
+  if (!pl->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_done, cudaEventDisableTiming));
+  if (pl->has_last && pl->last_stream != st) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_done, 0));
+  return COVGPU_OK;
+}
+static int plan_stream_leave(covgpu_plan* pl, cudaStream_t st, int rc) {
+  const cudaError_t e = cudaEventRecord(pl->ev_done, st);
+  if (e == cudaSuccess) {
+    pl->last_stream = st;
+    pl->has_last = true;
+  } else {
+    cudaGetLastError();
+    if (!rc) rc = fail(COVGPU_ECUDA, std::string("completion event: ") + cudaGetErrorString(e));
+  }
+  return rc;
+}
 
 extern "C" {
 
@@ -2103,6 +2136,13 @@ int covgpu_plan_execute(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_
   CUDA_TRY(cudaSetDevice(pl->device));
   cudaStream_t st = (cudaStream_t)stream;
   std::lock_guard<std::mutex> lk(pl->exec_mu);
+  if (int rc0 = plan_stream_enter(pl, st)) return rc0;
+  const int rc = plan_execute_locked(pl, A_dev, R_dev, layout, scale, st);
+  return plan_stream_leave(pl, st, rc);
+}
+
+static int plan_execute_locked(covgpu_plan_t pl, const void* A_dev, void* R_dev, int32_t layout, double scale,
+                               cudaStream_t st) {
   auto run = [&](cudaStream_t s) {
     return pl->dtype == COVGPU_C128 ? launch_all<double>(pl, A_dev, R_dev, layout, scale, s)
                                     : launch_all<float>(pl, A_dev, R_dev, layout, scale, s);
@@ -2204,6 +2244,7 @@ int covgpu_plan_execute_sums(covgpu_plan_t pl, const void* A_dev, void* sums_dev
   CUDA_TRY(cudaSetDevice(pl->device));
   std::lock_guard<std::mutex> lk(pl->exec_mu);
   if ((uintptr_t)A_dev % 16 != 0) return fail(COVGPU_EINVAL, "A must be 16-byte aligned");
+  if (int rc0 = plan_stream_enter(pl, (cudaStream_t)stream)) return rc0;
   pl->ks_part = part;
   pl->ks_nparts = nparts;
   pl->ks_out = (double2*)sums_dev;
@@ -2215,7 +2256,7 @@ int covgpu_plan_execute_sums(covgpu_plan_t pl, const void* A_dev, void* sums_dev
   pl->ks_part = 0;
   pl->ks_nparts = 1;
   pl->ks_out = nullptr;
-  return rc;
+  return plan_stream_leave(pl, (cudaStream_t)stream, rc);
 }
 
 int covgpu_plan_finalize_sums(covgpu_plan_t pl, const void* A_dev, const void* sums_dev, void* R_dev,
@@ -2229,11 +2270,14 @@ int covgpu_plan_finalize_sums(covgpu_plan_t pl, const void* A_dev, const void* s
   CUDA_TRY(cudaSetDevice(pl->device));
   std::lock_guard<std::mutex> lk(pl->exec_mu);
   CUDA_TRY(set_attrs());
-  if (pl->dtype == COVGPU_C128)
-    return finalize_from_sums<double>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale, class_lo,
-                                      class_hi, (cudaStream_t)stream);
-  return finalize_from_sums<float>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale, class_lo,
-                                   class_hi, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (int rc0 = plan_stream_enter(pl, st)) return rc0;
+  const int rc = pl->dtype == COVGPU_C128
+                     ? finalize_from_sums<double>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale,
+                                                  class_lo, class_hi, st)
+                     : finalize_from_sums<float>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale,
+                                                 class_lo, class_hi, st);
+  return plan_stream_leave(pl, st, rc);
 }
 
 int64_t covgpu_plan_class_slot_offset(covgpu_plan_t pl, int32_t class_index) {
@@ -2262,7 +2306,7 @@ int covgpu_plan_destroy(covgpu_plan_t pl) {
   return COVGPU_OK;
 }
 
-static int cached_plan(covgpu_plan_t* out, int device, int64_t batch, int64_t n, int64_t m,
+static int cached_plan(std::shared_ptr<covgpu_plan>* out, int device, int64_t batch, int64_t n, int64_t m,
                        int32_t p, int32_t q, int32_t dtype, const int32_t* ids, int32_t nids) {
   PlanKey key{device, dtype, batch, n, m, p, q, {}, path_env()};
   if (ids) key.ids.assign(ids, ids + nids);
@@ -2272,14 +2316,13 @@ static int cached_plan(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     *out = it->second;
     return COVGPU_OK;
   }
-  if (g_cache.size() >= 32) {  // evict one entry (cudaFree waits for its in-flight work)
-    auto victim = g_cache.begin();
-    covgpu_plan_destroy(victim->second);
-    g_cache.erase(victim);
-  }
-  int rc = covgpu_plan_create(out, device, batch, n, m, p, q, dtype, ids, nids);
+  if (g_cache.size() >= 32) g_cache.erase(g_cache.begin());  // (freed when its last user is done)
+  covgpu_plan_t raw = nullptr;
+  int rc = covgpu_plan_create(&raw, device, batch, n, m, p, q, dtype, ids, nids);
   if (rc) return rc;
-  g_cache[key] = *out;
+  std::shared_ptr<covgpu_plan> sp(raw, [](covgpu_plan* x) { covgpu_plan_destroy(x); });
+  g_cache[key] = sp;
+  *out = std::move(sp);
   return COVGPU_OK;
 }
 
@@ -2288,10 +2331,10 @@ int covgpu_estimate(const void* A_dev, int64_t batch, int64_t n, int64_t m, int3
                     double scale, void* R_dev, void* stream) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
-  covgpu_plan_t pl = nullptr;
+  std::shared_ptr<covgpu_plan> pl;
   int rc = cached_plan(&pl, dev, batch, n, m, p, q, dtype, class_ids, n_classes);
   if (rc) return rc;
-  return covgpu_plan_execute(pl, A_dev, R_dev, layout, scale, stream);
+  return covgpu_plan_execute(pl.get(), A_dev, R_dev, layout, scale, stream);
 }
 
 int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m, int32_t p,
@@ -2300,10 +2343,10 @@ int covgpu_estimate_host(const void* A_host, int64_t batch, int64_t n, int64_t m
   int rc = validate(batch, n, m, p, q, dtype);
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(device));
-  covgpu_plan_t pl = nullptr;
+  std::shared_ptr<covgpu_plan> pl;
   rc = cached_plan(&pl, device, batch, n, m, p, q, dtype, nullptr, 0);
   if (rc) return rc;
-  return covgpu_plan_execute_host(pl, A_host, R_host, layout, scale);
+  return covgpu_plan_execute_host(pl.get(), A_host, R_host, layout, scale);
 }
 
 namespace {
@@ -2541,6 +2584,10 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
   }
   cudaStream_t st = pl->host_stream;
   int rc;
+  struct ChunkReset {  // the chunked walk is this call's only: reset on every exit path
+    covgpu_plan* p;
+    ~ChunkReset() { p->fin_nchunks = 1; }
+  } chunk_reset{pl};
   chunked_copy_out(pl, layout);  // sets fin_nchunks > 1 when the walk can be chunked
   if (stream_a_in_bands(pl, a_bytes)) {
     // A in row bands on the copy stream, overlapped with the tensor-core
@@ -2629,6 +2676,13 @@ static bool chunked_copy_out(covgpu_plan* pl, int layout) {
   if (const char* e = getenv("COVGPU_NO_CHUNKED_D2H"))
     if (atoi(e) != 0) return false;
   if (!pl->d_fin_state) {
+    // events first: the state buffer marks a completed setup
+    for (auto& e : pl->ev_fin_chunk)
+      if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        e = nullptr;
+        return false;
+      }
     const size_t n = pl->use_tile ? (size_t)pl->n_units * 32 * pl->ft_nwarp * FT_STATE
                                   : (size_t)pl->ntasks * 32 * (2 * pl->fin_kr + 1);
     if (cudaMalloc((void**)&pl->d_fin_state, sizeof(double2) * std::max<size_t>(n, 1)) != cudaSuccess) {
@@ -2636,11 +2690,6 @@ static bool chunked_copy_out(covgpu_plan* pl, int layout) {
       pl->d_fin_state = nullptr;
       return false;
     }
-    for (auto& e : pl->ev_fin_chunk)
-      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-      }
   }
   if (!pl->out_stream && cudaStreamCreateWithFlags(&pl->out_stream, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
@@ -2773,7 +2822,7 @@ int covgpu_scatter_compact(const void* compact_dev, int64_t batch, int64_t n, in
   if (rc) return rc;
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
-  covgpu_plan_t pl = nullptr;
+  std::shared_ptr<covgpu_plan> pl;
   rc = cached_plan(&pl, dev, batch, n, m, p, q, dtype, class_ids, n_classes);
   if (rc) return rc;
   if (pl->nclasses == 0 || pl->compact_elems == 0) return COVGPU_OK;

@@ -32,6 +32,7 @@ class Plan:
                                          window.p, window.q, _DT[dtype], self._ids, self._nids)
         _native.check(rc, "covgpu_plan_create")
         self.handle = handle
+        self._inflight = []  # host buffers of enqueued execute_host_async calls (kept alive)
 
     @property
     def k(self) -> int:
@@ -45,10 +46,32 @@ class Plan:
         fn = torch.zeros if zero else torch.empty
         return fn(self.output_elems(layout), dtype=self.dtype, device=self.device)
 
-    def execute(self, a: torch.Tensor, out: torch.Tensor, layout: str = "dense",
-                scale: float | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    # ---- argument checks (the C ABI takes raw pointers and trusts sizes) ----
+    def _check_input(self, a: torch.Tensor, on_device: bool) -> None:
         if a.dtype != self.dtype or not a.is_contiguous() or a.numel() != self.batch * self.n * self.m:
             raise ValueError("input does not match the plan (shape, dtype, contiguity)")
+        self._check_place(a, on_device, "input")
+
+    def _check_output(self, out: torch.Tensor, layout: str, on_device: bool) -> None:
+        if layout not in LAYOUTS:
+            raise ValueError(f"unknown layout {layout!r}")
+        want = self.output_elems(layout)
+        if out.dtype != self.dtype or not out.is_contiguous() or out.numel() != want:
+            raise ValueError(f"output must be a contiguous {self.dtype} tensor of {want} elements "
+                             f"({layout} layout), got {out.dtype} with {out.numel()}")
+        self._check_place(out, on_device, "output")
+
+    def _check_place(self, t: torch.Tensor, on_device: bool, what: str) -> None:
+        if on_device:
+            if not t.is_cuda or t.device != self.device:
+                raise ValueError(f"{what} must be on {self.device}, got {t.device}")
+        elif t.is_cuda:
+            raise ValueError(f"{what} must be a host tensor for the host-buffer path")
+
+    def execute(self, a: torch.Tensor, out: torch.Tensor, layout: str = "dense",
+                scale: float | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        self._check_input(a, True)
+        self._check_output(out, layout, True)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = self.lib.covgpu_plan_execute(self.handle, ctypes.c_void_p(a.data_ptr()),
                                           ctypes.c_void_p(out.data_ptr()), LAYOUTS[layout],
@@ -60,6 +83,8 @@ class Plan:
     def execute_host(self, a_host: torch.Tensor, out_host: torch.Tensor, layout: str = "packed",
                      scale: float | None = None) -> torch.Tensor:
         """End to end on host buffers (pin them for full PCIe bandwidth)."""
+        self._check_input(a_host, False)
+        self._check_output(out_host, layout, False)
         rc = self.lib.covgpu_plan_execute_host(self.handle, ctypes.c_void_p(a_host.data_ptr()),
                                                ctypes.c_void_p(out_host.data_ptr()), LAYOUTS[layout],
                                                1.0 / self.k if scale is None else scale)
@@ -69,14 +94,19 @@ class Plan:
     def execute_host_async(self, a_host: torch.Tensor, out_host: torch.Tensor, layout: str = "packed",
                            scale: float | None = None) -> None:
         """Enqueue one host-buffer estimate (up to two in flight); the buffers
-        must stay untouched until wait() returns."""
+        must stay untouched until wait() returns (the plan keeps them alive)."""
+        self._check_input(a_host, False)
+        self._check_output(out_host, layout, False)
+        self._inflight.append((a_host, out_host))
         rc = self.lib.covgpu_plan_execute_host_async(self.handle, ctypes.c_void_p(a_host.data_ptr()),
                                                      ctypes.c_void_p(out_host.data_ptr()), LAYOUTS[layout],
                                                      1.0 / self.k if scale is None else scale)
         _native.check(rc, "covgpu_plan_execute_host_async")
 
     def wait(self) -> None:
-        _native.check(self.lib.covgpu_plan_wait(self.handle), "covgpu_plan_wait")
+        rc = self.lib.covgpu_plan_wait(self.handle)
+        self._inflight.clear()
+        _native.check(rc, "covgpu_plan_wait")
 
     # ---- which sum kernels run (include/covgpu.h: covgpu_plan_path) ----
     PATH_SPECTRAL, PATH_TENSOR, PATH_ROWBAND = 1, 2, 4
@@ -107,8 +137,10 @@ class Plan:
     def execute_sums(self, a: torch.Tensor, sums: torch.Tensor, part: int = 0, nparts: int = 1,
                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """Part `part` of `nparts` row bands of every sum, reduced into `sums`."""
+        self._check_input(a, True)
         if sums.dtype != torch.complex128 or sums.numel() != self.sums_elems() or not sums.is_contiguous():
             raise ValueError("sums buffer does not match the plan")
+        self._check_place(sums, True, "sums")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = self.lib.covgpu_plan_execute_sums(self.handle, ctypes.c_void_p(a.data_ptr()),
                                                ctypes.c_void_p(sums.data_ptr()), part, nparts,
@@ -121,6 +153,20 @@ class Plan:
                       scale: float | None = None, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """R (or the compact slots of classes [class_lo, class_hi)) from reduced sums."""
         hi = self.num_classes if class_hi is None else class_hi
+        self._check_input(a, True)
+        if sums.dtype != torch.complex128 or sums.numel() != self.sums_elems() or not sums.is_contiguous():
+            raise ValueError("sums buffer does not match the plan")
+        self._check_place(sums, True, "sums")
+        if not 0 <= class_lo <= hi <= self.num_classes:
+            raise ValueError("class range outside the plan")
+        if layout == "compact" and (class_lo, hi) != (0, self.num_classes):
+            want = self.class_slot_offset(hi) - self.class_slot_offset(class_lo)
+            if out.dtype != self.dtype or not out.is_contiguous() or out.numel() < self.class_slot_offset(hi):
+                raise ValueError(f"compact output must hold the plan's slots up to class {hi} "
+                                 f"({self.class_slot_offset(hi)} elements; the range has {want})")
+            self._check_place(out, True, "output")
+        else:
+            self._check_output(out, layout, True)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = self.lib.covgpu_plan_finalize_sums(
             self.handle, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(sums.data_ptr()),

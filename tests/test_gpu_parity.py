@@ -792,3 +792,41 @@ def test_wide_window_layouts_vs_oracle(cuda, spectral, n, m, p, q, monkeypatch):
     assert compact.numel() == packed.numel()
     assert abs(complex(compact.sum()) - complex(packed.sum())) <= 1e-12 * float(packed.abs().sum())
     assert_hermitian(dense.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg2-c64", "cfg3", "cfg5"])
+def test_full_size_every_entry_against_c_oracle(cuda, name):
+    """Every entry of R at the BASELINE size against the pinned C restatement
+    of the reference's class kernel (oracle/covoracle.c, itself pinned to the
+    reference's golden vectors by test_oracle.py): relF <= 1e-12 (c128) /
+    1e-5 (c64, oracle on the exactly up-cast input), and the worst single
+    entry relative to R's largest modulus."""
+    from oracle import covoracle_c
+
+    w = workload(name)
+    a = make_input(w)
+    got = estimate_tensor(a, WindowSpec(w.p, w.q)).cpu().numpy()
+    assert_hermitian(got)
+    ref = covoracle_c.estimate_packed(a.astype(np.complex128), w.p, w.q) / w.k
+    mine = packed_of(got.astype(np.complex128))
+    err = co.rel_frobenius(mine, ref)
+    worst = float(np.max(np.abs(mine - ref)) / np.max(np.abs(ref)))
+    print(f"{name} every entry vs C oracle: relF {err:.3e}, max entry error / max |R| {worst:.3e}")
+    assert err <= (TOL64 if w.dtype == "c128" else TOL32)
+
+
+def test_cfg4_every_snapshot_against_c_oracle(cuda):
+    """All 1024 cfg4 snapshots, every entry, against the pinned C oracle."""
+    from oracle import covoracle_c
+
+    w = workload("cfg4")
+    stack = make_input(w)
+    got = estimate_batch_tensor(stack, WindowSpec(w.p, w.q)).cpu().numpy()
+    worst = 0.0
+    for b in range(w.batch):
+        assert_hermitian(got[b])
+        ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), w.p, w.q) / w.k
+        err = co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref)
+        worst = max(worst, err)
+    print(f"cfg4 worst relF over all {w.batch} snapshots vs C oracle {worst:.3e}")
+    assert worst <= TOL32
