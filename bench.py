@@ -340,15 +340,32 @@ def main() -> None:
         plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, class_ids=ids, device=dev)
     layout = args.layout if world == 1 and not rowband else "compact"
     if rowband:
-        from paper_1303_2285_b200.distributed import class_ranges
+        # fixed row parts (distributed.ROWBAND_PARTS) whatever the GPU count:
+        # this rank's run of parts, one all-to-all of the slices each rank's
+        # finalize range needs, the parts added in part order (R bitwise the
+        # same at any N); A is split by row bands: every rank holds (resident)
+        # only the rows / strips its parts read
+        from paper_1303_2285_b200 import distributed as dd
 
-        sums = plan.alloc_sums()
+        nparts = dd.ROWBAND_PARTS
+        p_lo, p_hi = dd.part_ranges(nparts, world)[rank]
+        part_sums = [plan.alloc_sums() for _ in range(p_lo, p_hi)]
+        sums = part_sums[0]
         offsets = [plan.class_slot_offset(i) for i in range(plan.num_classes + 1)]
-        c_lo, c_hi = class_ranges(offsets, world)[rank]
-    host_a = make_input(w) if rank == 0 else None
-    a = torch.empty((w.batch, w.n, w.m), dtype=tdt, device=dev)
-    if rank == 0:
+        ranges = dd.class_ranges(offsets, world)
+        c_lo, c_hi = ranges[rank]
+        slices = [plan.sums_range(lo, hi) for lo, hi in ranges]
+        width = [sum(e - b for b, e in sl) for sl in slices]
+        recv_sizes = [(hi - lo) * width[rank] for lo, hi in dd.part_ranges(nparts, world)]
+        regions = dd.rowband_regions(plan, (p_lo, p_hi), nparts)
+    host_a = make_input(w) if (rank == 0 or rowband) else None
+    a = torch.zeros((w.batch, w.n, w.m), dtype=tdt, device=dev)
+    if rank == 0 and not rowband:
         a.copy_(torch.from_numpy(host_a).reshape(a.shape))
+    if rowband:
+        ha = torch.from_numpy(host_a).reshape(w.n, w.m)
+        for r0, r1, c0, c1 in regions:
+            a[0, r0:r1, c0:c1] = ha[r0:r1, c0:c1].to(dev)
     out = plan.alloc_output(layout)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
@@ -360,14 +377,15 @@ def main() -> None:
     a_real = torch.view_as_real(a)  # collectives on the real view (no complex dtypes in NCCL)
 
     def step():
-        if world > 1:
-            dist.broadcast(a_real, src=0)
         if rowband:
-            plan.execute_sums(a, sums, rank, world)
-            if world > 1:
-                dist.all_reduce(torch.view_as_real(sums))
-            plan.finalize_sums(a, sums, out, "compact", c_lo, c_hi)
+            for j, part in enumerate(range(p_lo, p_hi)):
+                plan.execute_sums(a, part_sums[j], part, nparts)
+            got = dd._all_to_all(dd._rowband_send(part_sums, slices), recv_sizes, part_sums[0])
+            red = dd._rowband_reduce(got, width[rank], slices[rank], part_sums[0])
+            plan.finalize_sums(a, red, out, "compact", c_lo, c_hi)
         else:
+            if world > 1:
+                dist.broadcast(a_real, src=0)
             plan.execute(a, out, layout)
 
     for _ in range(max(args.warmup, 0)):
@@ -398,14 +416,28 @@ def main() -> None:
     # (kernels serialised on one stream for this, so intervals are per kernel)
     plan.set_timing(True)
     kern = []
+    fin_ms = []
     for _ in range(max(3, min(args.steps, 10))):
         flush.fill_(1)
         torch.cuda.synchronize(dev)
         if rowband:
-            plan.execute_sums(a, sums, rank, world)
+            kk = None
+            for j, part in enumerate(range(p_lo, p_hi)):
+                plan.execute_sums(a, part_sums[j], part, nparts)
+                t_j = plan.kernel_times()
+                kk = t_j if kk is None else [x + y for x, y in zip(kk, t_j)]
+            kern.append(kk)
+            got = dd._all_to_all(dd._rowband_send(part_sums, slices), recv_sizes, part_sums[0])
+            red = dd._rowband_reduce(got, width[rank], slices[rank], part_sums[0])
+            torch.cuda.synchronize(dev)
+            e0.record()
+            plan.finalize_sums(a, red, out, "compact", c_lo, c_hi)  # delta + tile walk of the range
+            e1.record()
+            torch.cuda.synchronize(dev)
+            fin_ms.append(e0.elapsed_time(e1))
         else:
             plan.execute(a, out, layout)
-        kern.append(plan.kernel_times())
+            kern.append(plan.kernel_times())
     knames = plan.kernel_names()
     plan.set_timing(False)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -422,6 +454,8 @@ def main() -> None:
     if kt is not None and kt.size:
         for name, col in zip(knames, kt.mean(axis=0)):
             kernel_ms[name] = float(col)
+    if fin_ms:
+        kernel_ms["finalize"] = float(np.mean(fin_ms))
     shard_frac = 1.0 if ids is None else shard_cost(w.n, w.m, win, ids) / um
     if rowband:
         shard_frac = 1.0 / world
@@ -512,14 +546,14 @@ def main() -> None:
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64" if w.dtype == "c128" else "f32",
         "data": f"synthetic ({w.name}: seeded CN(0,1)/sinusoid inputs of BASELINE.json)",
-        "config": bench_config(w, layout, world, rowband, sums.numel() * 16 / 2**20 if rowband else 0.0),
+        "config": bench_config(w, layout, world, rowband, sum(recv_sizes) * 16 / 2**20 if rowband else 0.0),
         "effective_gflops": flops / (ms * 1e-3) / 1e9,
         "effective_gflops_note": "8 x UM (the paper's unique products) / step time; the spectral path "
                                  "does fewer flops than that, so this is not a hardware rate",
         "kernel_ms": kernel_ms,
         "kernel_roofline": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac")}
                             for k, v in per_kernel.items()},
-        "gpu_launches": (plan.launches + (2 if rowband else 0)) * args.steps,
+        "gpu_launches": (plan.launches * ((p_hi - p_lo) if rowband else 1) + (3 if rowband else 0)) * args.steps,
         "roofline": roof,
         "clocks": clocks.summary(),
     }
@@ -588,16 +622,18 @@ def main() -> None:
 
     # end to end through the C ABI with pinned host buffers
     if not args.no_e2e and rowband:
-        # end to end for row bands: rank 0's pinned host A -> device, broadcast,
-        # band sums, all-reduce, class-range finalize, D2H of the rank's range
-        a_host = torch.from_numpy(host_a if rank == 0 else make_input(w)).reshape(
-            w.batch, w.n, w.m).pin_memory()
+        # end to end for row bands: every rank copies (pinned H2D, its own
+        # PCIe link) only the regions of A its parts read, runs its parts,
+        # the all-to-all, the range finalize, and copies its compact range
+        # of R back (D2H) — the host input is visible to every rank
+        a_host = torch.from_numpy(host_a).reshape(w.n, w.m).pin_memory()
         lo_off, hi_off = offsets[c_lo], offsets[c_hi]
         r_host = torch.empty(hi_off - lo_off, dtype=tdt).pin_memory()
+        h2d = sum((r1 - r0) * (c1 - c0) for r0, r1, c0, c1 in regions) * a_host.element_size()
 
         def e2e_step():
-            if rank == 0:
-                a.copy_(a_host, non_blocking=True)
+            for r0, r1, c0, c1 in regions:
+                a[0, r0:r1, c0:c1].copy_(a_host[r0:r1, c0:c1], non_blocking=True)
             step()
             r_host.copy_(out[lo_off:hi_off], non_blocking=True)
             torch.cuda.synchronize(dev)
@@ -613,11 +649,12 @@ def main() -> None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         esz = r_host.element_size()
         line["e2e"] = {"value": entries / float(te.item()), "unit": UNIT,
-                       "h2d_bytes_per_step": a_host.numel() * esz if rank == 0 else 0,
+                       "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": r_host.numel() * esz,
                        "ms_per_step": float(te.item()) * 1e3,
-                       "path": "row bands: pinned H2D of A on rank 0, broadcast, execute_sums, all-reduce, "
-                               "finalize_sums (class range), D2H of the rank's compact range; wall clock"}
+                       "path": "row bands: pinned H2D of the rank's regions of A (band rows + strips), "
+                               "execute_sums of its parts, all-to-all, finalize_sums (class range), D2H of "
+                               "the rank's compact range; wall clock, max over ranks"}
     elif not args.no_e2e:
         e2e_layout = "packed" if world == 1 else "compact"
         a_host = torch.from_numpy(host_a if rank == 0 else make_input(w)).reshape(

@@ -117,12 +117,14 @@ int32_t covgpu_plan_kernel_times(covgpu_plan_t plan, float* ms, int32_t max_n);
 int32_t covgpu_plan_kernel_names(covgpu_plan_t plan, char* buf, int32_t len);
 
 /* Multi-GPU row bands (the core / edge sums are sums over rows and columns
- * of A, so they split over the K dimension with one exchange: an all-reduce
- * of the per-band sums; replaces the reference's per-class work split,
- * engine.py:158-190, with a split that keeps every GPU on the tensor-core
- * path).  sums_elems: complex128 values of the reduced-sums buffer
- * [CC | CCol | RC'].  execute_sums: part `part` of `nparts` of every sum
- * (rank = part); the caller all-reduces the buffers (sum).  finalize_sums:
+ * of A, so they split over the K dimension with one exchange of the per-band
+ * sums; replaces the reference's per-class work split, engine.py:158-190,
+ * with a split that keeps every GPU on the spectral / tensor-core sums).
+ * sums_elems: complex128 values of the sums buffer [CC | CCol | RC'].
+ * execute_sums: part `part` of `nparts` of every sum (the driver runs a
+ * FIXED number of parts, independent of the GPU count, and adds the parts of
+ * a class range in part order, so R is bitwise the same on any number of
+ * GPUs; distributed.py).  finalize_sums:
  * corners + diagonal-segment walk from the reduced sums for plan classes
  * [class_lo, class_hi) (a sub-range writes its slots of the COMPACT layout;
  * the full range may write DENSE / PACKED).  class_slot_offset: compact
@@ -136,6 +138,19 @@ int covgpu_plan_finalize_sums(covgpu_plan_t plan, const void* A_dev, const void*
                               int32_t layout, double scale, int32_t class_lo, int32_t class_hi,
                               void* stream);
 int64_t covgpu_plan_class_slot_offset(covgpu_plan_t plan, int32_t class_index);
+
+/* Where the sums of plan classes [class_lo, class_hi) of snapshot 0 sit in
+ * the sums buffer: out[0..5] = [cc_begin, cc_end, ccol_begin, ccol_end,
+ * rc_begin, rc_end) — the slices a GPU finalizing that range needs (the
+ * row-band exchange sends only those).  Returns 0 or an error code. */
+int covgpu_plan_sums_range(covgpu_plan_t plan, int32_t class_lo, int32_t class_hi, int64_t* out);
+
+/* Rows of A that part `part` of `nparts` of execute_sums reads besides the
+ * top / bottom P-1 strip rows and the first / last Q-1 columns of every row:
+ * [*row_begin, *row_end).  A GPU holding only those regions of A (the rest
+ * unset) computes the same part bit for bit: the row-band input split. */
+int covgpu_plan_band_rows(covgpu_plan_t plan, int32_t part, int32_t nparts, int32_t* row_begin,
+                          int32_t* row_end);
 
 int covgpu_plan_destroy(covgpu_plan_t plan);
 

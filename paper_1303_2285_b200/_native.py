@@ -56,6 +56,8 @@ _SIGS = {
     "covgpu_plan_execute_sums": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, _vp]),
     "covgpu_plan_finalize_sums": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _dbl, _i32, _i32, _vp]),
     "covgpu_plan_class_slot_offset": (_i64, [_vp, _i32]),
+    "covgpu_plan_sums_range": (ctypes.c_int, [_vp, _i32, _i32, ctypes.POINTER(_i64)]),
+    "covgpu_plan_band_rows": (ctypes.c_int, [_vp, _i32, _i32, _p32, _p32]),
     "covgpu_plan_destroy": (ctypes.c_int, [_vp]),
     "covgpu_estimate": (
         ctypes.c_int,

@@ -853,6 +853,17 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     kern<<<blocks, pl->spec_ngrp * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, nseg_, part_, nparts_,
                                                 pl->spec_stages, pl->d_gp, slot0, nslots);
   };
+  if (nparts > 1) {
+    // only this part's edge pairs are computed: the others' CCol / RC' stay zero
+    if (pl->spec_edges) {
+      CUDA_TRY_V(cudaMemsetAsync(pl->d_ccol, 0, sizeof(double2) * (size_t)(B * pl->tot_ccol), es));
+      CUDA_TRY_V(cudaMemsetAsync(pl->d_rc, 0, sizeof(double2) * (size_t)(B * pl->tot_rc), es));
+      if (es != st) {
+        cudaEventRecord(pl->ev_d0, es);
+        cudaStreamWaitEvent(st, pl->ev_d0, 0);
+      }
+    }
+  }
   int gslots = pl->spec_nseg;  // G partial slots the output FFT sums
   bool corr_done = false;
   const bool band_mode = pl->band_wait && B == 1 && stream_wait_value();
@@ -921,11 +932,13 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       const cudaStream_t st_main = st;
       st = es;
       if (pl->spec_prune_q)
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
+                  B * 2 * (long long)S * S);
       else
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
+                  B * 2 * (long long)S * S);
       st = st_main;
     }
     mark("spec_rowac");
@@ -976,11 +989,13 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
                                                        pl->d_cls_slot, pl->d_ccpart);
     if (pl->spec_edges && es != st_main)
       if (pl->spec_prune_q)
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
+                  B * 2 * (long long)S * S);
       else
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
+                  B * 2 * (long long)S * S);
     st = st_main;
     mark("spec_rowac");
   }
@@ -1010,21 +1025,25 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       st = es;  // SPEC_LOGL launches on `st`
       SPEC_LOGL(pl->spec_logLr, SpecK<T>::template colfft, B * 2 * 4 * S1, A, pr, pl->d_twr, pl->d_fc);
       if (pl->spec_prune_p)
-        SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccolp, B * 2 * (long long)S1 * S1, pl->d_fc, pr,
-                  pl->d_twr, pl->d_twrf, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+        SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccolp, (B * 2 * (long long)S1 * S1 + nparts - 1) / nparts, pl->d_fc, pr,
+                  pl->d_twr, pl->d_twrf, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts,
+                  B * 2 * (long long)S1 * S1);
       else
-        SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, B * 2 * (long long)S1 * S1, pl->d_fc, pr,
-                  pl->d_twr, pl->d_twrf, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts);
+        SPEC_LOGL(pl->spec_logLr, SpecK<T>::template ccol, (B * 2 * (long long)S1 * S1 + nparts - 1) / nparts, pl->d_fc, pr,
+                  pl->d_twr, pl->d_twrf, pl->d_cls_slot, pl->d_cls, pl->d_ccol, pl->tot_ccol, part, nparts,
+                  B * 2 * (long long)S1 * S1);
       st = st_main;
     }
     mark("spec_ccol");
     if (es == st)  // (timing mode: everything in order on one stream)
       if (pl->spec_prune_q)
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
+                  B * 2 * (long long)S * S);
       else
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, B * 2 * (long long)S * S, pl->d_fx, pl->d_fy0, pr,
-                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts);
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
+                  pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
+                  B * 2 * (long long)S * S);
   }
 }
 
@@ -1263,7 +1282,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->band_wait)
     CUDA_TRY(cudaStreamWaitEvent(es, pl->use_spec && pl->batch == 1 ? pl->ev_strips : pl->ev_h2d, 0));
   mark("start");
-  if (pl->use_tile) {
+  if (pl->use_tile && !pl->ks_out) {
     // the tile walk's corner blocks and per-chunk state updates need only the
     // corners of A: first on the side stream, under the sums
     const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
@@ -2278,6 +2297,48 @@ int covgpu_plan_finalize_sums(covgpu_plan_t pl, const void* A_dev, const void* s
                      : finalize_from_sums<float>(pl, A_dev, (const double2*)sums_dev, R_dev, layout, scale,
                                                  class_lo, class_hi, st);
   return plan_stream_leave(pl, st, rc);
+}
+
+int covgpu_plan_sums_range(covgpu_plan_t pl, int32_t class_lo, int32_t class_hi, int64_t* out) {
+  if (!pl || !out) return fail(COVGPU_EINVAL, "plan or output is NULL");
+  if (class_lo < 0 || class_hi > pl->nclasses || class_lo > class_hi)
+    return fail(COVGPU_EINVAL, "class range outside the plan");
+  const long long B = pl->batch;
+  auto ccol = [&](int c) { return c < pl->nclasses ? pl->h_cls[c].ccol_off : pl->tot_ccol; };
+  auto rcof = [&](int c) { return c < pl->nclasses ? pl->h_cls[c].rc_off : pl->tot_rc; };
+  const long long base_cl = B * pl->nclasses, base_rc = base_cl + B * pl->tot_ccol;
+  out[0] = class_lo;
+  out[1] = class_hi;
+  out[2] = base_cl + ccol(class_lo);
+  out[3] = base_cl + ccol(class_hi);
+  out[4] = base_rc + rcof(class_lo);
+  out[5] = base_rc + rcof(class_hi);
+  return COVGPU_OK;
+}
+
+int covgpu_plan_band_rows(covgpu_plan_t pl, int32_t part, int32_t nparts, int32_t* row_begin, int32_t* row_end) {
+  if (!pl || !row_begin || !row_end) return fail(COVGPU_EINVAL, "plan or output is NULL");
+  if (nparts < 1 || part < 0 || part >= nparts) return fail(COVGPU_EINVAL, "part must be in [0, nparts)");
+  const Problem& pr = pl->pr;
+  *row_begin = 0;
+  *row_end = pr.N;
+  if (!pl->use_spec || !pl->spec_smem || nparts == 1) return COVGPU_OK;  // (the whole of A)
+  // launch_spectral's row-band ranges: correlation chunks +- P-1, dr = 0 rows
+  const int rows_lo = pr.P - 1, nrows = pr.N - 2 * pr.P + 2;
+  const int ra = rows_lo + (int)((long long)nrows * part / nparts);
+  const int rz = rows_lo + (int)((long long)nrows * (part + 1) / nparts) - 1;
+  const int nch = (pr.N + SC_RC - 1) / SC_RC;
+  const int pieces = nparts * pl->spec_nseg;
+  const int c0 = (int)((long long)nch * part * pl->spec_nseg / pieces);
+  const int c1 = (int)((long long)nch * (part + 1) * pl->spec_nseg / pieces);
+  int lo = std::max(0, c0 * SC_RC - (pr.P - 1)), hi = std::min(pr.N, c1 * SC_RC + pr.P - 1);
+  if (rz >= ra) {
+    lo = std::min(lo, ra);
+    hi = std::max(hi, rz + 1);
+  }
+  *row_begin = lo;
+  *row_end = hi;
+  return COVGPU_OK;
 }
 
 int64_t covgpu_plan_class_slot_offset(covgpu_plan_t pl, int32_t class_index) {

@@ -390,23 +390,27 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 //     CCol(dr, dc)[c1] = (1/Lr) sum_f Xc1[f] conj(Ye[f]) w^(f dr),
 // dr in [0, P) from the + versions (index dr), dr in (-P, 0) from the -
 // versions (index Lr + dr).  CTA = (b, side, sign, c1, e); pairs with e < c1
-// (and e == c1 for sign -) exit; in multi-GPU row-band mode pair q belongs
-// to part q mod nparts (the others write zeros: the bands are summed).
+// (and e == c1 for sign -) exit; in multi-GPU row-band mode item g belongs
+// to part g mod nparts, and only the part's items are launched (the caller
+// zeroes CCol first: the parts are summed).
 template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_ccol(long long nitems, const double2* __restrict__ FC, Problem pr, const double2* __restrict__ tw,
                 const double2* __restrict__ twf,
                 const int* __restrict__ cls_slot, const ClassDesc* __restrict__ cls, double2* __restrict__ ccol,
-                long long tot_ccol, int part, int nparts) {
+                long long tot_ccol, int part, int nparts, long long total) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int P = pr.P, Q = pr.Q, S1 = Q - 1;
   double2* sb;
   const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  long long g = si.item * nparts + part;  // this part's items: g = part (mod nparts)
+  const bool own = si.valid && g < total;
+  if (!own) g = total - 1;                 // (index math in range; loads / stores skipped)
   // item = (b, side, pair q): sign 0 pairs e >= c1 first, then sign 1 pairs e > c1
   const long long np0 = (long long)S1 * (S1 + 1) / 2, np1 = (long long)S1 * (S1 - 1) / 2;
-  long long q = si.item % (np0 + np1);
-  const long long bs = si.item / (np0 + np1);
+  long long q = g % (np0 + np1);
+  const long long bs = g / (np0 + np1);
   const int side = (int)(bs % 2);
   const long long b = bs / 2;
   const int sign = q < np0 ? 0 : 1;
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   }
   const int e = c1 + sign + (int)q;
   const int dc = e - c1;
-  const bool mine = si.valid && ((long long)c1 * S1 + e) % nparts == part;
+  const bool mine = own;
   const double2* fx = FC + (((b * 2 + side) * 4 + 2 * sign) * S1 + c1) * (long long)L;
   const double2* fy = FC + (((b * 2 + side) * 4 + 2 * sign + 1) * S1 + e) * (long long)L;
   const double inv = 1.0 / (double)L;
@@ -467,27 +471,30 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
             emit(dr, make_double2(v.x * inv, v.y * inv));
         });
   }
-  if (si.valid && !mine)
-    for (int k = si.tl; k < P; k += spec_nt<LOGL>()) emit(sign ? -(k + 1) : k, make_double2(0.0, 0.0));
 }
 
 // Edge-row sums RC' from the row spectra: for strip rows (i1, i2) (first
 // element row base + i1, second base + i2, dr = i2 - i1),
 //     RC'(dr, dc) of pane row min(i1, i2) = (1/L) sum_f X_{base+i1}[f] conj(Y0_{i2}[f]) w^(f dc)
 // (X masked to the slot-0 box columns [0, M-Q], Y0 unmasked).  CTA = (b,
-// strip, i1, i2); multi-GPU: pair q belongs to part q mod nparts.  RC' has one
+// strip, i1, i2); multi-GPU: item g belongs to part g mod nparts, only the
+// part's items are launched (the caller zeroes RC' first).  RC' has one
 // segment here (nseg = 1).
 template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_rc(long long nitems, const double2* __restrict__ FX, const double2* __restrict__ FY0, Problem pr,
               SpecLayout lay, const double2* __restrict__ tw, const double2* __restrict__ twf, const int* __restrict__ cls_slot,
-              const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc, int part, int nparts) {
+              const ClassDesc* __restrict__ cls, double2* __restrict__ rc, long long tot_rc, int part, int nparts,
+              long long total) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int N = pr.N, P = pr.P, Q = pr.Q, S = P - 1;
   double2* sb;
   const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
-  long long t = si.item;
+  long long g = si.item * nparts + part;
+  const bool own = si.valid && g < total;
+  if (!own) g = total - 1;
+  long long t = g;
   const int i2 = (int)(t % S);
   t /= S;
   const int i1 = (int)(t % S);
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   const long long b = t / 2;
   const int dr = i2 - i1;
   const int base = strip ? N - S : 0;
-  const bool mine = si.valid && ((long long)i1 * S + i2) % nparts == part;
+  const bool mine = own;
   const double2* fx = FX + lay.at(b, base + i1, 0);
   const long long fxs = (long long)lay.np * 32;
   const double2* fy = FY0 + (b * 2 * S + strip * S + i2) * (long long)L;
@@ -522,8 +529,6 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     spec_fft_pruned<LOGL>(sb, si.tl, tw, twf, ld, stf);
   else
     spec_fft_block<LOGL>(sb, si.tl, tw, ld, stf);
-  if (si.valid && !mine)
-    for (int dc = si.tl; dc < Q; dc += spec_nt<LOGL>()) emit(dc, make_double2(0.0, 0.0));
 }
 
 __device__ __forceinline__ int spec_lo(int dr, int P) { return P - 1 + min(dr, 0); }

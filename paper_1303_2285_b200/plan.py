@@ -181,6 +181,22 @@ class Plan:
             return len(set(self.class_ids))
         return int(self.lib.covgpu_num_classes(self.window.p, self.window.q))
 
+    def sums_range(self, class_lo: int, class_hi: int) -> list[tuple[int, int]]:
+        """The sums-buffer slices ([CC, CCol, RC'] parts) of plan classes
+        [class_lo, class_hi): what a GPU finalizing that range needs."""
+        out = (ctypes.c_int64 * 6)()
+        _native.check(self.lib.covgpu_plan_sums_range(self.handle, class_lo, class_hi, out),
+                      "covgpu_plan_sums_range")
+        return [(int(out[0]), int(out[1])), (int(out[2]), int(out[3])), (int(out[4]), int(out[5]))]
+
+    def band_rows(self, part: int, nparts: int) -> tuple[int, int]:
+        """Rows of A that execute_sums(part, nparts) reads besides the strips
+        (top / bottom P-1 rows) and the first / last Q-1 columns."""
+        r0, r1 = ctypes.c_int32(), ctypes.c_int32()
+        _native.check(self.lib.covgpu_plan_band_rows(self.handle, part, nparts, ctypes.byref(r0),
+                                                     ctypes.byref(r1)), "covgpu_plan_band_rows")
+        return int(r0.value), int(r1.value)
+
     def class_slot_offset(self, i: int) -> int:
         """Compact offset of plan class i (i == num_classes: total slots)."""
         return int(self.lib.covgpu_plan_class_slot_offset(self.handle, i))

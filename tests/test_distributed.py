@@ -19,6 +19,8 @@ from paper_1303_2285_b200.distributed import (
     ShardOps,
     class_ranges,
     estimate_batch_sharded,
+    part_ranges,
+    simulate_rowband,
     estimate_rowband,
     estimate_sharded,
     shard_bounds,
@@ -56,17 +58,20 @@ def oracle_ops() -> ShardOps:
 
 
 def oracle_band_ops() -> BandOps:
-    """Row-band ops on the CPU oracle.  A band's partial 'sums' here are the
+    """Row-band ops on the CPU oracle.  A part's 'sums' here are the
     unnormalised slot sums over a band of window-placement rows (linear in
-    the products, so the all-reduce of the bands is the full slot sums) in
-    compact (UC-major) order; finalizing a class range scales its slots by
-    1/K — the same orchestration as the CUDA ops, with oracle-defined sums."""
+    the products, so adding the parts gives the full slot sums) in compact
+    (UC-major) order; finalizing a class range scales its slots by 1/K — the
+    same orchestration as the CUDA ops, with oracle-defined sums."""
 
-    def slot_offsets(window, n, m):
+    def offsets_for(window):
         offs = [0]
         for dr, dc in co.unique_combinations(window.p, window.q):
             offs.append(offs[-1] + (window.p - abs(dr)) * (window.q - dc))
         return offs
+
+    def slot_offsets(a, window):
+        return offsets_for(window)
 
     def compute_sums(a, window, part, nparts):
         arr = a.numpy()
@@ -82,17 +87,21 @@ def oracle_band_ops() -> BandOps:
                 parts.append(np.zeros((window.p - abs(dr)) * (window.q - dc), dtype=np.complex128))
         return torch.from_numpy(np.concatenate(parts))
 
+    def sums_slices(a, window, lo, hi):
+        offs = offsets_for(window)
+        return [(offs[lo], offs[hi])]
+
     def finalize_range(a, window, sums, lo, hi):
         n, m = a.shape
         k = (n - window.p + 1) * (m - window.q + 1)
-        offs = slot_offsets(window, n, m)
+        offs = offsets_for(window)
         return sums[offs[lo]:offs[hi]] / k
 
     def expand_dense(compact, window, n, m, dtype, device):
         nuc = len(co.unique_combinations(window.p, window.q))
         return oracle_ops().scatter_dense([compact], [list(range(nuc))], window, n, m, dtype, device)
 
-    return BandOps(slot_offsets, compute_sums, finalize_range, expand_dense)
+    return BandOps(slot_offsets, compute_sums, sums_slices, finalize_range, expand_dense)
 
 
 def _free_port():
@@ -136,6 +145,14 @@ def _worker(rank, world, port, results):
         out["band_comp"] = comp_b.numpy()
         if rank == 0:
             out["band_err"] = co.rel_frobenius(dense_b.numpy(), co.covariance(a.numpy(), p, q))
+            out["band_dense"] = dense_b.numpy()
+        # a mismatching input on rank 0 is refused on every rank before the broadcast
+        try:
+            estimate_rowband(a.to(torch.complex64) if rank == 0 else None, (n, m), WindowSpec(p, q),
+                             ops=oracle_band_ops(), device=torch.device("cpu"))
+            out["mismatch"] = "accepted"
+        except ValueError:
+            out["mismatch"] = "refused"
         results[rank] = out
     finally:
         dist.destroy_process_group()
@@ -158,6 +175,13 @@ def test_two_rank_sharded_estimate():
     nuc = len(co.unique_combinations(5, 4))
     assert r0["band_range"][0] == 0 and r0["band_range"][1] == r1["band_range"][0]
     assert r1["band_range"][1] == nuc
+    # N-invariance: the same bits as the one-process run (fixed parts, fixed order)
+    rng = np.random.default_rng(7)
+    a = torch.from_numpy(rng.standard_normal((20, 18)) + 1j * rng.standard_normal((20, 18)))
+    dense1, _, _ = estimate_rowband(a, (20, 18), WindowSpec(5, 4), gather=True, ops=oracle_band_ops(),
+                                    device=torch.device("cpu"))
+    assert np.array_equal(dense1.numpy(), r0["band_dense"])
+    assert r0["mismatch"] == "refused" and r1["mismatch"] == "refused"
 
 
 def test_shard_bounds_cover_batch():
@@ -180,3 +204,24 @@ def test_class_ranges_balance_slots():
         assert all(rng[i][1] == rng[i + 1][0] for i in range(world - 1))
         loads = [offs[h] - offs[l] for l, h in rng]
         assert max(loads) - min(loads) <= 2 * 64 * 64  # within one class of even
+
+
+def test_simulated_ranks_match_one_rank_bitwise():
+    """simulate_rowband (the W-rank computation in one process) gives the
+    same bits for W = 1, 2, 4, 8 (the row parts are fixed, their sums added
+    in part order), and the result is the covariance."""
+    rng = np.random.default_rng(11)
+    a = torch.from_numpy(rng.standard_normal((23, 19)) + 1j * rng.standard_normal((23, 19)))
+    win = WindowSpec(5, 4)
+    ref = simulate_rowband([a], win, ops=oracle_band_ops())
+    assert co.rel_frobenius(ref.numpy(), co.covariance(a.numpy(), 5, 4)) <= 1e-13
+    for world in (2, 4, 8):
+        got = simulate_rowband([a] * world, win, ops=oracle_band_ops())
+        assert torch.equal(got, ref), world
+
+
+def test_part_ranges_cover_parts():
+    for world in (1, 2, 3, 4, 8):
+        spans = part_ranges(8, world)
+        assert spans[0][0] == 0 and spans[-1][1] == 8
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))

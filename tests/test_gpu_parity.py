@@ -830,3 +830,45 @@ def test_cfg4_every_snapshot_against_c_oracle(cuda):
         worst = max(worst, err)
     print(f"cfg4 worst relF over all {w.batch} snapshots vs C oracle {worst:.3e}")
     assert worst <= TOL32
+
+
+@pytest.mark.parametrize("name", ["rowband-mid", "cfg5"])
+def test_row_bands_bitwise_across_gpu_counts(cuda, name):
+    """The multi-GPU row-band mode run as W ranks in one process (the
+    all-to-all becomes list routing): W = 1, 2, 4, 8 give the same bits
+    (fixed row parts, added in part order), the result matches the C oracle,
+    and a rank whose A holds only rowband_regions of its parts (NaN
+    elsewhere) produces the same bits — the row-band input split."""
+    from oracle import covoracle_c
+    from paper_1303_2285_b200.distributed import (ROWBAND_PARTS, part_ranges, rowband_regions,
+                                                  simulate_rowband)
+    from paper_1303_2285_b200.plan import Plan
+
+    if name == "cfg5":
+        w = workload("cfg5")
+        a_np, n, m, p, q = make_input(w), w.n, w.m, w.p, w.q
+    else:
+        n, m, p, q = 400, 420, 50, 56
+        rng = np.random.default_rng(77)
+        a_np = rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))
+    a = torch.as_tensor(a_np, device=cuda)
+    win = WindowSpec(p, q)
+    ref = simulate_rowband([a], win)
+    assert_hermitian(ref.cpu().numpy())
+    k = (n - p + 1) * (m - q + 1)
+    oracle = covoracle_c.estimate_packed(a_np, p, q) / k
+    err = co.rel_frobenius(packed_of(ref.cpu().numpy()), oracle)
+    print(f"{name} row bands vs C oracle relF {err:.3e}")
+    assert err <= TOL64
+    plan = Plan(n, m, win, dtype=torch.complex128, device=cuda)
+    for world in (2, 4, 8):
+        bufs = []
+        for r in range(world):
+            # rank r's own buffer: only the regions its parts read, NaN elsewhere
+            b = torch.full((n, m), complex("nan+nanj"), dtype=torch.complex128, device=cuda)
+            for r0, r1, c0, c1 in rowband_regions(plan, part_ranges(ROWBAND_PARTS, world)[r]):
+                b[r0:r1, c0:c1] = a[r0:r1, c0:c1]
+            bufs.append(b)
+        got = simulate_rowband(bufs, win)
+        assert torch.equal(got, ref), world
+    plan.close()
