@@ -503,16 +503,21 @@ cudaError_t bulk_attrs() {
 
 std::string g_attr_fail;  // the kernel whose attribute could not be set (error text)
 
-template <typename T, int NW>
+template <typename T, int NW, int LANES>
 cudaError_t fin_tile_attr() {
-  const int smem = (int)(ft_unit_smem(NW, sizeof(typename CT<T>::c)) * FtCfg<NW>::UPC);
+  // the largest window of this instantiation (P = 8 NW) needs the most SMEM
+  const int smem = (int)(ft_unit_smem(8 * NW, NW, 32 / LANES, sizeof(typename CT<T>::c)) * FtCfg<NW>::UPC);
   g_attr_fail = "k_fin_tile<" + std::to_string(sizeof(T)) + "," + std::to_string(NW) + "> smem " + std::to_string(smem);
-  cudaError_t e = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaError_t r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_PACKED, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE, false, LANES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_PACKED, false, LANES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (r != cudaSuccess) e = r;
-  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_COMPACT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_COMPACT, false, LANES>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (r != cudaSuccess) e = r;
-  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  r = cudaFuncSetAttribute(k_fin_tile<T, NW, COVGPU_DENSE, true, LANES>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (r != cudaSuccess) e = r;
   if (e == cudaSuccess) g_attr_fail.clear();
   return e;
@@ -520,11 +525,11 @@ cudaError_t fin_tile_attr() {
 template <typename T>
 cudaError_t fin_tile_attrs() {
   cudaError_t e = cudaSuccess, r;
-  if ((r = fin_tile_attr<T, 1>()) != cudaSuccess) return r;
-  if ((r = fin_tile_attr<T, 2>()) != cudaSuccess) return r;
-  if ((r = fin_tile_attr<T, 4>()) != cudaSuccess) return r;
-  if ((r = fin_tile_attr<T, 8>()) != cudaSuccess) return r;
-  if ((r = fin_tile_attr<T, 16>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 1, 8>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 2, 16>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 4, 32>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 8, 32>()) != cudaSuccess) return r;
+  if ((r = fin_tile_attr<T, 16, 32>()) != cudaSuccess) return r;
   return e;
 }
 
@@ -1163,15 +1168,16 @@ std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi, bool del
     int len;
   };
   std::vector<Piece> pieces;
+  const int lanes = ft_lanes(P), subs = 32 / lanes;  // snapshots per warp
   for (int dc = 0; dc < Q; ++dc) {
     const int qu = Q - dc;
     for (int u0 = 0; u0 < qu; u0 += FT_CK) {
       const int u1 = std::min(qu, u0 + FT_CK);
       if (delta && u1 >= qu) break;  // no cut after this chunk
-      for (long long b = 0; b < pl->batch; ++b)
-        for (int d0 = 0; d0 < P; d0 += 32) {
+      for (long long b = 0; b < pl->batch; b += subs)
+        for (int d0 = 0; d0 < P; d0 += lanes) {
           bool any = false;  // circular diagonal c holds classes (c, dc) and (c - P, dc)
-          for (int c = d0; c < std::min(P, d0 + 32); ++c)
+          for (int c = d0; c < std::min(P, d0 + lanes); ++c)
             any = any || has[(size_t)(c + P - 1) * Q + dc] || (dc > 0 && c > 0 && has[(size_t)(c - 1) * Q + dc]);
           if (any) pieces.push_back({make_int4((int)b, dc, d0, u0 | (u1 << 16)), u1 - u0});
         }
@@ -1191,29 +1197,29 @@ void launch_fin_tile(covgpu_plan* pl, const int4* units, long long nunits, const
                      cudaStream_t st, bool delta = false) {
   using C2 = typename CT<T>::c;
   if (nunits <= 0) return;
-#define FT_LAUNCH(NW, LAY, DEL)                                                                             \
+#define FT_LAUNCH(NW, LN, LAY, DEL)                                                                         \
   do {                                                                                                      \
     constexpr int upc = FtCfg<NW>::UPC;                                                                     \
     const unsigned grid = (unsigned)((nunits + upc - 1) / upc);                                             \
-    const size_t smem = ft_unit_smem(NW, sizeof(C2)) * upc;                                                 \
-    k_fin_tile<T, NW, LAY, DEL><<<grid, FtCfg<NW>::THREADS, smem, st>>>(                                    \
-        (const double2*)pl->d_corners, pl->pr, pl->d_cls, pl->d_cls_slot, units, (int)nunits, pl->nclasses, \
-        npart, ccpart, ccol, pl->tot_ccol, rc, pl->tot_rc, nseg, pl->d_ck, R, rstride, scale, u0, u1, wst,  \
-        slot_lo, slot_hi);                                                                                  \
+    const size_t smem = ft_unit_smem(pl->pr.P, NW, 32 / LN, sizeof(C2)) * upc;                              \
+    k_fin_tile<T, NW, LAY, DEL, LN><<<grid, FtCfg<NW>::THREADS, smem, st>>>(                                \
+        (const double2*)pl->d_corners, pl->pr, (int)pl->batch, pl->d_cls, pl->d_cls_slot, units,            \
+        (int)nunits, pl->nclasses, npart, ccpart, ccol, pl->tot_ccol, rc, pl->tot_rc, nseg, pl->d_ck, R,    \
+        rstride, scale, u0, u1, wst, slot_lo, slot_hi);                                                     \
   } while (0)
-#define FT_LAY(NW)                                                           \
+#define FT_LAY(NW, LN)                                                       \
   do {                                                                       \
-    if (delta) FT_LAUNCH(NW, COVGPU_DENSE, true);                            \
-    else if (layout == COVGPU_DENSE) FT_LAUNCH(NW, COVGPU_DENSE, false);     \
-    else if (layout == COVGPU_PACKED) FT_LAUNCH(NW, COVGPU_PACKED, false);   \
-    else FT_LAUNCH(NW, COVGPU_COMPACT, false);                               \
+    if (delta) FT_LAUNCH(NW, LN, COVGPU_DENSE, true);                        \
+    else if (layout == COVGPU_DENSE) FT_LAUNCH(NW, LN, COVGPU_DENSE, false); \
+    else if (layout == COVGPU_PACKED) FT_LAUNCH(NW, LN, COVGPU_PACKED, false); \
+    else FT_LAUNCH(NW, LN, COVGPU_COMPACT, false);                           \
   } while (0)
   switch (pl->ft_nwarp) {
-    case 1: FT_LAY(1); break;
-    case 2: FT_LAY(2); break;
-    case 4: FT_LAY(4); break;
-    case 8: FT_LAY(8); break;
-    default: FT_LAY(16);
+    case 1: FT_LAY(1, 8); break;
+    case 2: FT_LAY(2, 16); break;
+    case 4: FT_LAY(4, 32); break;
+    case 8: FT_LAY(8, 32); break;
+    default: FT_LAY(16, 32);
   }
 #undef FT_LAY
 #undef FT_LAUNCH
@@ -1285,9 +1291,10 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->use_tile && !pl->ks_out) {
     // the tile walk's corner blocks and per-chunk state updates need only the
     // corners of A: first on the side stream, under the sums
-    const long long nc = 4LL * (pr.P - 1) * (pr.Q - 1) * B;
+    const int PP = 8 * pl->ft_nwarp;
+    const long long nc = (long long)(pr.Q - 1) * ft_colw(pr.P, PP) * B;
     if (nc > 0) {
-      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, (double2*)pl->d_corners);
+      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, PP, (double2*)pl->d_corners);
       ++launches;
     }
     if (pl->n_dunits > 0) {
@@ -1498,10 +1505,12 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
   const C2* A = (const C2*)A_dev;
   const int ckr = pl->use_tile ? 1 : fin_corner_kr(pl, layout, layout != COVGPU_COMPACT);
   const long long nc = 4LL * corner_rows(pr.P, ckr) * (pr.Q - 1) * B;
-  if (nc > 0) {
-    if (pl->use_tile)
-      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, (double2*)pl->d_corners);
-    else
+  if (pl->use_tile) {
+    const int PP = 8 * pl->ft_nwarp;
+    const long long ncd = (long long)(pr.Q - 1) * ft_colw(pr.P, PP) * B;
+    if (ncd > 0)
+      k_corners_d<T><<<(unsigned)((ncd + 255) / 256), 256, 0, st>>>(A, pr, B, PP, (double2*)pl->d_corners);
+  } else if (nc > 0) {
       k_corners<T><<<(unsigned)((nc + 255) / 256), 256, 0, st>>>(A, pr, B, ckr, (C2*)pl->d_corners);
   }
   if (pl->use_tile) {
@@ -2092,7 +2101,9 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->ntasks = (long long)tasks.size();
       pl->h_tasks = tasks;
       const size_t esz = (dtype == COVGPU_C128 || pl->use_tile) ? 16 : 8;  // tile walk: corners widened to double
-      const size_t cbytes = (size_t)batch * 4 * (size_t)corner_rows(p, std::max(pl->fin_kr, 1)) * (size_t)std::max(q - 1, 0) * esz;
+      const size_t cbytes = pl->use_tile
+          ? (size_t)batch * (size_t)std::max(q - 1, 0) * ft_colw(p, 8 * pl->ft_nwarp) * 16
+          : (size_t)batch * 4 * (size_t)corner_rows(p, std::max(pl->fin_kr, 1)) * (size_t)std::max(q - 1, 0) * esz;
       std::vector<long long> uc_off(nuc, -1);
       for (const auto& cd : pl->h_cls) uc_off[cd.uc] = cd.slot_off;
       cudaError_t e1 = cudaMalloc(&pl->d_corners, std::max<size_t>(cbytes, 16));

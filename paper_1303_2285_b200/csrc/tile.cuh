@@ -46,10 +46,7 @@ namespace covgpu {
 #ifndef FT_CTA_WARPS
 #define FT_CTA_WARPS 8
 #endif
-#ifndef FT_RPT_DEF
-#define FT_RPT_DEF 8
-#endif
-constexpr int FT_RPT = FT_RPT_DEF;  // rows per thread
+constexpr int FT_RPT = 8;  // rows per thread
 constexpr int FT_CK = 16;  // checkpoint spacing (steps)
 
 template <int NWARP>
@@ -66,22 +63,32 @@ inline int ft_nwarp(int P) {
   while (w * FT_RPT < P) w <<= 1;
   return w;
 }
+// lanes per snapshot: small windows pack 32 / lanes snapshots into a warp
+inline int ft_lanes(int P) { return P > 16 ? 32 : P > 8 ? 16 : 8; }
 __host__ __device__ inline int ft_nck(int Q) { return (Q - 1) / FT_CK; }  // checkpoints per (snapshot, dc)
 
-// SMEM per unit: strip vectors [2 bufs][12 PP] double2 — first operands
-// TL, TR, BL, BR at column u ([PP] each), second operands at column u + dc
-// ([2 PP] each, the strip twice: index (r1 + c) mod P needs no wrap) —
-// with entries outside the strip zero (the update needs no guards),
-// row-group totals [2 bufs][T1, B1, T2, B2][nwarp][32] double2, edge-column
-// sums of the step [2 bufs][class 1, 2][L, R][32] double2, stage
-// [2 bufs][PP][32] (output precision)
-__host__ __device__ inline size_t ft_vec_bytes(int nwarp) { return (size_t)2 * 12 * nwarp * FT_RPT * 16; }
+// Corner blocks per (snapshot, column j of the (Q-1)-column strips), widened
+// to double, in the layout one step's SMEM copy takes as is: first operands
+// TL, TR, BL, BR ([PP] each: rows [0, P-1) of A's top / bottom strip, zero
+// beyond), then second operands TL, TR, BL, BR ([2P] each: the P-1 strip rows
+// and a zero, twice — index (r1 + c) mod P then needs no wrap).
+__host__ __device__ inline int ft_colw(int P, int PP) { return 4 * PP + 8 * P; }
+
+// SMEM per unit: strip vectors [2 bufs][subs][colw + 8] double2 (8 zeros of
+// slack: rows past P read in range), row-group totals [2 bufs][T1, B1, T2,
+// B2][nwarp][32] double2, edge-column sums of the step [2 bufs][class 1,
+// 2][L, R][32] double2, stage [bufs][PP][32] (output precision)
+__host__ __device__ inline size_t ft_vec_elems(int P, int PP) { return (size_t)ft_colw(P, PP) + 8; }
 __host__ __device__ inline size_t ft_tot_bytes(int nwarp) { return (size_t)2 * 4 * nwarp * 32 * 16; }
 __host__ __device__ inline size_t ft_gcol_bytes() { return (size_t)2 * 4 * 32 * 16; }
-// (P > 64: one stage buffer, the mirror follows its step after a second barrier)
-__host__ __device__ inline int ft_stage_bufs(int nwarp) { return nwarp <= 8 ? 2 : 1; }
-__host__ __device__ inline size_t ft_unit_smem(int nwarp, size_t esz) {
-  return ft_vec_bytes(nwarp) + ft_tot_bytes(nwarp) + ft_gcol_bytes() +
+// (P > 64, or a one-warp unit: one stage buffer, the mirror follows its step
+// after a second barrier — for one warp a __syncwarp)
+__host__ __device__ inline int ft_stage_bufs(int nwarp) { return nwarp >= 2 && nwarp <= 8 ? 2 : 1; }
+__host__ __device__ inline size_t ft_vec_bytes(int P, int nwarp, int subs) {
+  return (size_t)2 * subs * ft_vec_elems(P, nwarp * FT_RPT) * 16;
+}
+__host__ __device__ inline size_t ft_unit_smem(int P, int nwarp, int subs, size_t esz) {
+  return ft_vec_bytes(P, nwarp, subs) + ft_tot_bytes(nwarp) + ft_gcol_bytes() +
          (size_t)ft_stage_bufs(nwarp) * nwarp * FT_RPT * 32 * esz;
 }
 
@@ -104,24 +111,32 @@ __device__ __forceinline__ void ft_rank2(double2& f, double2 a, double2 b, doubl
   f.y = fma(c.x, d.y, f.y);
 }
 
-// Corner blocks widened to double for the tile walk: C[b][blk][col][row],
-// blk = TL, TR, BL, BR, each (P-1) rows x (Q-1) columns of A.
+// k_corners_d: the corner layout above, thread per element
 template <typename T>
-__global__ void k_corners_d(const typename CT<T>::c* __restrict__ A, Problem pr, int B,
+__global__ void k_corners_d(const typename CT<T>::c* __restrict__ A, Problem pr, int B, int PP,
                             double2* __restrict__ C) {
-  const int S = pr.P - 1, Wc = pr.Q - 1;
-  const long long per = 4LL * S * Wc;
+  const int P = pr.P, S = P - 1, Wc = pr.Q - 1, cw = ft_colw(P, PP);
+  const long long per = (long long)Wc * cw;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= per * B) return;
   const int b = (int)(tid / per);
-  long long r = tid % per;
-  const int k = (int)(r / ((long long)S * Wc));
-  r %= (long long)S * Wc;
-  const int j = (int)(r / S), i = (int)(r % S);
-  const int row = (k < 2 ? 0 : pr.N - S) + i;
-  const int col = ((k & 1) ? pr.M - Wc : 0) + j;
-  const auto v = A[((long long)b * pr.N + row) * pr.M + col];
-  C[tid] = make_double2((double)v.x, (double)v.y);
+  const int j = (int)(tid % per / cw), x = (int)(tid % cw);
+  int blk, i;
+  if (x < 4 * PP) {
+    blk = x / PP;
+    i = x % PP;
+  } else {
+    blk = (x - 4 * PP) / (2 * P);
+    i = (x - 4 * PP) % (2 * P) % P;
+  }
+  double2 v = make_double2(0.0, 0.0);
+  if (i < S) {
+    const int row = (blk < 2 ? 0 : pr.N - S) + i;
+    const int col = ((blk & 1) ? pr.M - Wc : 0) + j;
+    const auto a = A[((long long)b * pr.N + row) * pr.M + col];
+    v = make_double2((double)a.x, (double)a.y);
+  }
+  C[tid] = v;
 }
 
 // The two classes on circular diagonal c of column offset dc: (c, dc) on
@@ -173,47 +188,50 @@ __device__ inline void ft_init_entry(int r1, int c, int P, const FtLane& L, cons
 #ifndef FT_MINB
 #define FT_MINB 1
 #endif
-// DELTA: unit = (snapshot, dc, band, chunk [16 (j-1), 16 j)); the chunk's
-// state updates from zero go to ck[b][dc][j-1][T, B][row][c] (no output)
-template <typename T, int NWARP, int LAYOUT, bool DELTA>
+// DELTA: unit = (snapshots, dc, band, chunk [16 (j-1), 16 j)); the chunk's
+// state updates from zero go to ck[b][dc][j-1][T, B][row][c] (no output).
+// LANES < 32: a warp holds 32 / LANES snapshots (lane = (snapshot, c)).
+template <typename T, int NWARP, int LAYOUT, bool DELTA, int LANES>
 __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB)
-    k_fin_tile(const double2* __restrict__ corners, Problem pr, const ClassDesc* __restrict__ cls,
+    k_fin_tile(const double2* __restrict__ corners, Problem pr, int B, const ClassDesc* __restrict__ cls,
                const int* __restrict__ cls_slot, const int4* __restrict__ units, int nunits, int nclasses,
                int npart, const double2* __restrict__ ccpart, const double2* __restrict__ ccol,
                long long tot_ccol, const double2* __restrict__ rc, long long tot_rc, int nseg,
                double2* __restrict__ ck, typename CT<T>::c* __restrict__ R, long long r_bstride,
                double scale, int u_begin, int u_end, double2* __restrict__ wstate, int slot_lo, int slot_hi) {
   using C2 = typename CT<T>::c;
-  constexpr int UPC = FtCfg<NWARP>::UPC, UT = 32 * NWARP, PP = NWARP * FT_RPT;
+  constexpr int UPC = FtCfg<NWARP>::UPC, UT = 32 * NWARP, PP = NWARP * FT_RPT, SUBS = 32 / LANES;
   constexpr bool DENSE = LAYOUT == COVGPU_DENSE, PACKED = LAYOUT == COVGPU_PACKED;
-  constexpr bool STAGE2 = NWARP <= 8;  // double-buffered stage: the mirror runs one step later
+  constexpr bool STAGE2 = NWARP >= 2 && NWARP <= 8;  // double-buffered stage: the mirror runs one step later
   extern __shared__ __align__(16) unsigned char ft_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int us = warp / NWARP, w = warp - us * NWARP, ut = (int)threadIdx.x - us * UT;
   const int unit = blockIdx.x * UPC + us;
   if (unit >= nunits) return;  // unit-uniform: the barriers below involve only this unit
   const int4 un = units[unit];
-  const int b = un.x, dc = un.y, d0 = un.z, u_lo = un.w & 0xffff, u_hi = un.w >> 16;
-  const int P = pr.P, Q = pr.Q, ac = Q - dc - 1, S = P - 1, Wc = Q - 1;
+  const int b0 = un.x, dc = un.y, d0 = un.z, u_lo = un.w & 0xffff, u_hi = un.w >> 16;
+  const int P = pr.P, Q = pr.Q, ac = Q - dc - 1, Wc = Q - 1;
   // emitted steps of this launch; a unit resumed by a later u-chunk restores
   // the state the previous chunk saved, a fresh one starts from F(u_lo)
   const int e0 = max(u_lo, u_begin), e1 = min(u_hi, u_end);
   if (e0 >= e1) return;
   const bool resume = e0 > u_lo;
-  unsigned char* sb = ft_smem + (size_t)us * ft_unit_smem(NWARP, sizeof(C2));
+  const int cw = ft_colw(P, PP), vstride = (int)ft_vec_elems(P, PP);
+  unsigned char* sb = ft_smem + (size_t)us * ft_unit_smem(P, NWARP, SUBS, sizeof(C2));
   double2* const vec = (double2*)sb;
-  double2* const tot0 = (double2*)(sb + ft_vec_bytes(NWARP));
-  double2* const gcol0 = (double2*)(sb + ft_vec_bytes(NWARP) + ft_tot_bytes(NWARP));
-  C2* const stage0 = (C2*)(sb + ft_vec_bytes(NWARP) + ft_tot_bytes(NWARP) + ft_gcol_bytes());
+  double2* const tot0 = (double2*)(sb + ft_vec_bytes(P, NWARP, SUBS));
+  double2* const gcol0 = (double2*)(sb + ft_vec_bytes(P, NWARP, SUBS) + ft_tot_bytes(NWARP));
+  C2* const stage0 = (C2*)(sb + ft_vec_bytes(P, NWARP, SUBS) + ft_tot_bytes(NWARP) + ft_gcol_bytes());
   const int bar = 1 + us;
 
-  const int c = d0 + lane;  // this lane's circular diagonal
-  const FtLane L = ft_lane(c, dc, P, Q, cls, cls_slot, slot_lo, slot_hi);
+  const int cl = lane & (LANES - 1), sub = lane / LANES;
+  const int b = b0 + sub;  // this lane's snapshot
+  const int c = d0 + cl;   // this lane's circular diagonal
+  const FtLane L = b < B ? ft_lane(c, dc, P, Q, cls, cls_slot, slot_lo, slot_hi) : FtLane{-1, -1, 0, 0, 0, 0, 0, 0};
   const int bnd = P - c;  // first row of segment 2
   const int r0 = w * FT_RPT;
   const int pv1 = P - c, pv2 = c;
-  // per-row masks: output entry, mirrored entry; the mirror writer lane l
-  // handles source lane m = 31 - l (its columns ascend with l)
+  const int bs = b < B ? b : B - 1;  // (index math of idle lanes in range)
   unsigned omask = 0;
 #pragma unroll
   for (int k = 0; k < FT_RPT; ++k) {
@@ -221,7 +239,8 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     if (r1 < P && ((r1 < bnd) ? L.slot1 : L.slot2) >= 0) omask |= 1u << k;
   }
   const int r2_0 = (r0 + c) % P;  // second A row of row r0 (rows r0 + k: r2_0 + k in the doubled strip)
-  const int m = 31 - lane, cm = d0 + m;
+  // mirror writer: lane l handles the lane m of its snapshot with c(m) = d0 + LANES-1 - cl
+  const int m = sub * LANES + (LANES - 1 - cl), cm = d0 + LANES - 1 - cl;
   const bool m1 = __shfl_sync(0xffffffffu, L.slot1, m) >= 0 && (dc > 0 || cm > 0);
   const bool m2 = __shfl_sync(0xffffffffu, L.slot2, m) >= 0;
   unsigned mmask = 0;
@@ -233,12 +252,12 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
   }
   const bool wout = __any_sync(0xffffffffu, omask != 0);
   const bool wmir = DENSE && __any_sync(0xffffffffu, mmask != 0);
-  const double2* clb = ccol + (long long)b * tot_ccol;
+  const double2* clb = ccol + (long long)bs * tot_ccol;
   double* const wsp = wstate ? (double*)(wstate + ((long long)unit * UT + ut) * FT_STATE) : nullptr;
 
   double2 fT[FT_RPT], fB[FT_RPT], G1 = make_double2(0.0, 0.0), G2 = G1;
   const long long per = (long long)P * P;
-  const double2* ckb = ck + ((long long)b * Q + dc) * ft_nck(Q) * 2 * per + c;
+  const double2* ckb = ck + ((long long)bs * Q + dc) * ft_nck(Q) * 2 * per + c;
   if (DELTA) {
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) fT[k] = fB[k] = make_double2(0.0, 0.0);
@@ -252,7 +271,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     G2 = make_double2(wsp[4 * FT_RPT + 2], wsp[4 * FT_RPT + 3]);
   } else {
     // F(u_lo) = F(0) + delta_1 + ... + delta_{u_lo / 16} (fixed order)
-    const double2* rcb = rc + (long long)b * tot_rc * nseg;
+    const double2* rcb = rc + (long long)bs * tot_rc * nseg;
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) ft_init_entry(r0 + k, c, P, L, rcb, nseg, fT[k], fB[k]);
     for (int j = 0; j < u_lo / FT_CK; ++j) {
@@ -271,8 +290,8 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     double2 g1 = make_double2(0.0, 0.0), g2 = g1;
     if (w == 0) {
       for (int k = 0; k < npart; ++k) {
-        if (L.slot1 >= 0) g1 = cadd(g1, ccpart[((long long)b * nclasses + L.slot1) * npart + k]);
-        if (L.slot2 >= 0) g2 = cadd(g2, ccpart[((long long)b * nclasses + L.slot2) * npart + k]);
+        if (L.slot1 >= 0) g1 = cadd(g1, ccpart[((long long)bs * nclasses + L.slot1) * npart + k]);
+        if (L.slot2 >= 0) g2 = cadd(g2, ccpart[((long long)bs * nclasses + L.slot2) * npart + k]);
       }
     }
 #pragma unroll 4
@@ -290,42 +309,25 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     }
   }
   ft_unit_sync(bar, UT);  // tot0 is reused by the steps
-  for (int e = ut; e < 2 * 4 * 32; e += UT) gcol0[e] = make_double2(0.0, 0.0);  // absent classes stay 0
-  for (int e = ut; e < 2 * 12 * PP; e += UT) vec[e] = make_double2(0.0, 0.0);  // the zero padding
+  for (int e = ut; e < 2 * 4 * 32; e += UT) gcol0[e] = make_double2(0.0, 0.0);            // absent classes stay 0
+  for (int e = ut; e < 2 * SUBS * vstride; e += UT) vec[e] = make_double2(0.0, 0.0);  // slack zeros
   ft_unit_sync(bar, UT);
 
-  // strip columns of step u (only while u < ac): first operands TL, TR, BL,
-  // BR at column u (element e < 4 S), second operands at column u + dc, each
-  // copied twice (e >= 4 S); this thread copies elements ut, ut + UT, ut + 2 UT
-  // (12 (P-1) < 3 UT), and warp x % NWARP the step's CColL / CColR of class
-  // x / 2 of its lane (gcol [class][L, R][lane])
-  const double2* cb = corners + (long long)b * 4 * S * Wc;
-  const double2* psrc[3];
-  int pdst[3];
-#pragma unroll
-  for (int x = 0; x < 3; ++x) {
-    const int e = ut + x * UT;
-    int dst = -1, blk = 0, i = 0, col = 0;
-    if (e < 4 * S) {
-      blk = e / S;
-      i = e - blk * S;
-      dst = blk * PP + i;
-    } else if (e < 12 * S) {
-      const int e2 = e - 4 * S;
-      blk = e2 / (2 * S);
-      const int rem = e2 - blk * 2 * S, copy = rem / S;
-      i = rem - copy * S;
-      dst = 4 * PP + blk * 2 * PP + copy * P + i;
-      col = dc;
-    }
-    pdst[x] = dst;
-    psrc[x] = cb + ((long long)blk * Wc + col) * S + i;
-  }
+  // one step's strip columns: the column-u and column-(u+dc) runs of the
+  // corner layout (ft_colw), one contiguous copy per snapshot; copied by the
+  // snapshot's own lanes (id = w * LANES + cl), plus each lane's CColL /
+  // CColR of its two classes (gcol [class][L, R][lane], warp x % NWARP)
+  const double2* cb = corners + (long long)bs * Wc * cw;
+  const int cid = w * LANES + cl;
   auto prefetch = [&](int uu, int buf) {
     if (uu < ac && uu < e1) {
-#pragma unroll
-      for (int x = 0; x < 3; ++x)
-        if (pdst[x] >= 0) cp_async_elem<16>(vec + buf * 12 * PP + pdst[x], psrc[x] + (long long)uu * S, true);
+      double2* dst = vec + (buf * SUBS + sub) * vstride;
+      if (b < B) {
+        const double2* srcA = cb + (long long)uu * cw;
+        const double2* srcB = cb + (long long)(uu + dc) * cw;
+        for (int j = cid; j < cw; j += NWARP * LANES)
+          cp_async_elem<16>(dst + j, (j < 4 * PP ? srcA : srcB) + j, true);
+      }
       if (!DELTA) {
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
@@ -341,8 +343,10 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
   prefetch(u, u & 1);
 
   const long long D = pr.PQ;
-  C2* const Rb = R + (long long)b * r_bstride;
+  C2* const Rb = R + (long long)bs * r_bstride;
   const bool zero_im = dc == 0 && c == 0;  // class (0,0): R's real main diagonal (rows < bnd = P)
+  const long long ostep = (long long)P * (D + 1);  // block (u, u+dc) -> (u+1, u+1+dc)
+  const int P2 = 2 * P;
   // mirror of step um: block (um+dc, um), row P(um+dc) + r2, column P um + src
   // (the source row), conjugated (the lower triangle = exact conjugate)
   auto mirror = [&](int um, int buf) {
@@ -440,13 +444,13 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
       prev = false;
     }
     if (u < ac) {
-      // every row (no guards): entries outside the strip read zeros
-      const double2* va = vec + buf * 12 * PP + r0;
-      const double2* vq = vec + buf * 12 * PP + 4 * PP + r2_0;
+      // every row (no guards): rows and entries outside the strip read zeros
+      const double2* va = vec + (buf * SUBS + sub) * vstride + r0;
+      const double2* vq = vec + (buf * SUBS + sub) * vstride + 4 * PP + r2_0;
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
-        ft_rank2(fT[k], va[PP + k], vq[2 * PP + k], va[k], vq[k]);
-        ft_rank2(fB[k], va[3 * PP + k], vq[6 * PP + k], va[2 * PP + k], vq[4 * PP + k]);
+        ft_rank2(fT[k], va[PP + k], vq[P2 + k], va[k], vq[k]);
+        ft_rank2(fB[k], va[3 * PP + k], vq[3 * P2 + k], va[2 * PP + k], vq[2 * P2 + k]);
       }
       const double2* gc = gcol0 + buf * 128 + lane;
       G1 = cadd(G1, csub(gc[32], gc[0]));  // + CColR[u] - CColL[u]
@@ -455,13 +459,15 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
   }
   cp_async_wait<0>();
   if constexpr (DELTA) {
-    double2* o = (double2*)ckb + (long long)(u_lo / FT_CK) * 2 * per;
+    if (b < B) {
+      double2* o = (double2*)ckb + (long long)(u_lo / FT_CK) * 2 * per;
 #pragma unroll
-    for (int k = 0; k < FT_RPT; ++k) {
-      const int r1 = r0 + k;
-      if (r1 < P && c < P) {
-        o[(long long)r1 * P] = fT[k];
-        o[per + (long long)r1 * P] = fB[k];
+      for (int k = 0; k < FT_RPT; ++k) {
+        const int r1 = r0 + k;
+        if (r1 < P && c < P) {
+          o[(long long)r1 * P] = fT[k];
+          o[per + (long long)r1 * P] = fB[k];
+        }
       }
     }
     return;
