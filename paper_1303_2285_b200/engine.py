@@ -256,21 +256,42 @@ def measure_unit_times(a, window: WindowSpec, repeats: int = 3, device=None):
     return out
 
 
-def measure_combination_times(a, window: WindowSpec, backend: str | None = None, repeats: int = 3):
+def measure_combination_times(a, window: WindowSpec, backend: str | None = None, repeats: int = 3,
+                              classes=None):
     """Per-class GPU cost in UC order, the reference's trace contract
-    (``engine.py:258-288``): each bulk unit's measured time is apportioned to
-    its classes by product count mu.  Feeds ``write_cost_trace`` and the
+    (``engine.py:258-288``: best-of-repeats wall time of each class kernel):
+    every class is run ALONE as a one-class plan — its sums, edge sums and
+    diagonal-segment walk, nothing apportioned — and timed with CUDA events
+    around the plan's launches.  `classes` restricts the measurement to some
+    UC indices (the others get None).  Feeds ``write_cost_trace`` and the
     reference's scheduling simulator (``schedsim.ingest_measured_costs``)."""
+    from .plan import Plan
+
     resolve_backend(backend)
+    if repeats < 1:
+        raise ValueError(f"repeats must be >= 1, got {repeats}")
     t = _to_device_matrix(a, None, None, ndim=2)
     n, m = t.shape
+    window.validate_for(n, m)
     combos = _comb.unique_combinations(window)
-    cost = [0.0] * len(combos)
-    for ids, secs in measure_unit_times(t, window, repeats):
-        mus = [_comb.pair_count(combos[i], n, m) for i in ids]
-        tot = sum(mus)
-        for i, mu in zip(ids, mus):
-            cost[i] = secs * mu / tot
+    todo = range(len(combos)) if classes is None else sorted(set(int(i) for i in classes))
+    cost = [None] * len(combos)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a3 = t.unsqueeze(0)
+    for i in todo:
+        plan = Plan(n, m, window, dtype=t.dtype, class_ids=[i], device=t.device)
+        dst = plan.alloc_output("compact")
+        plan.execute(a3, dst, "compact")  # warm (attributes, graph capture on the next call)
+        plan.execute(a3, dst, "compact")
+        best = float("inf")
+        for _ in range(repeats):
+            e0.record()
+            plan.execute(a3, dst, "compact")
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        plan.close()
+        cost[i] = best
     return [(combos[i], cost[i]) for i in range(len(combos))]
 
 

@@ -2,6 +2,7 @@
 counters, validation, bench bookkeeping, and the C oracle port."""
 
 import ctypes
+import sys
 import re
 from pathlib import Path
 
@@ -174,3 +175,44 @@ def test_c_oracle_matches_numpy_oracle():
         dr, dc = co.unique_combinations(7, 9)[i]
         off = co.class_packed_offsets(dr, dc, 7, 9)
         assert co.rel_frobenius(part[off], full[off]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_measured_gpu_cost_trace_replays_in_reference_simulator(name):
+    """The per-class GPU cost trace measured on a B200 (tools/cost_trace.py:
+    every class alone as a one-class plan, nothing apportioned) loads through
+    the reference's own schedsim.ingest_measured_costs and replays in its
+    list-scheduling simulator (schedsim.py:92-137, :174-207); its rank
+    correlation with the reference's cost model mu is the committed summary."""
+    import csv
+    import json
+    import shutil
+
+    ref = Path("/root/reference/pkg/src/covcomb")
+    if not ref.exists():
+        pytest.skip("reference package not present (GPU box)")
+    dst = Path("/tmp/covcomb_trace_src")
+    if not dst.exists():
+        shutil.copytree(ref.parent, dst)
+    if str(dst) not in sys.path:
+        sys.path.insert(0, str(dst))
+    from covcomb import WindowSpec as RefWindow
+    from covcomb import schedsim
+
+    from paper_1303_2285_b200.workloads import workload
+
+    w = workload(name)
+    path = ROOT / "profiles" / f"r02_cost_trace_{name}.csv"
+    tasks = schedsim.ingest_measured_costs(path, RefWindow(w.p, w.q))
+    assert len(tasks) == len(unique_combinations(WindowSpec(w.p, w.q)))
+    assert all(t.cost > 0 for t in tasks)
+    with open(path) as fh:
+        rows = list(csv.reader(fh))[1:]
+    assert [(int(r[1]), int(r[2])) for r in rows] == [(c.dr, c.dc) for c in unique_combinations(WindowSpec(w.p, w.q))]
+    lpt = schedsim.simulate(tasks, 148, "longest")
+    fifo = schedsim.simulate(tasks, 148, "fifo")
+    assert lpt.makespan <= fifo.makespan
+    summary = json.loads((ROOT / "profiles" / f"r02_cost_trace_{name}.json").read_text())
+    print(f"{name}: {len(tasks)} measured classes, spearman(cost, mu) = {summary['spearman_cost_vs_mu']:.3f}, "
+          f"LPT speedup on 148 units {float(lpt.speedup):.1f}")
+    assert summary["spearman_cost_vs_mu"] > 0.5
