@@ -50,6 +50,7 @@
 #include "mma.cuh"
 #include "probe.cuh"
 #include "spectral.cuh"
+#include "edgeblk.cuh"
 #include "tile.cuh"
 
 using namespace covgpu;
@@ -134,6 +135,11 @@ struct covgpu_plan {
   // full twiddle tables w_L^j / w_Lr^j for the output-pruned transforms
   double2 *d_twf = nullptr, *d_twrf = nullptr;
   bool spec_prune_q = false, spec_prune_p = false;  // Q <= 64 (row-spectrum pairs) / P <= 64 (column pairs)
+  // edge sums by blocked short-lag correlation (edgeblk.cuh; the default):
+  // block spectra of the strip columns / strip rows, twiddles of the block length
+  bool spec_blk = false;
+  EbGeom ebc{}, ebr{};
+  double2 *d_ebc = nullptr, *d_ebr = nullptr, *d_twbc = nullptr, *d_twbr = nullptr;
   // edge-row sums on the tensor cores (P <= 65)
   // host path streaming A in row bands (batch 1, tensor-core path): the
   // copy stream bumps *d_band_flag after each band; k_bulk_dmma waits on it,
@@ -393,6 +399,10 @@ void plan_free(covgpu_plan* pl) {
   cudaFree(pl->d_twrf);
   cudaFree(pl->d_fc);
   cudaFree(pl->d_fy0);
+  cudaFree(pl->d_ebc);
+  cudaFree(pl->d_ebr);
+  cudaFree(pl->d_twbc);
+  cudaFree(pl->d_twbr);
 }
 
 int pick_lags(int span) {
@@ -767,7 +777,7 @@ void spec_attr(K* fn, int logL) {
   std::lock_guard<std::mutex> lk(mu);
   const void* f = (const void*)fn;
   if (std::find(done.begin(), done.end(), f) != done.end()) return;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 144 * 1024);
   done.push_back(f);
   (void)logL;
 }
@@ -824,6 +834,43 @@ struct SpecK {
     if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_ccol<LG, true>; else return &k_spec_ccol<LG, false>;
   }
 };
+
+// edge sums by blocked short-lag correlation (edgeblk.cuh): block spectra of
+// one strip family (cols: the edge columns -> CCol; else the edge rows -> RC'),
+// then the line-pair tiles of this part
+template <typename T>
+void launch_edges_blocked(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t st, bool cols, int part,
+                          int nparts) {
+  const Problem& pr = pl->pr;
+  const long long B = pl->batch;
+  const EbGeom& g = cols ? pl->ebc : pl->ebr;
+  if (g.nlines <= 0) return;
+  double2* SP = cols ? pl->d_ebc : pl->d_ebr;
+  const double2* tw = cols ? pl->d_twbc : pl->d_twbr;
+  double2* dst = cols ? pl->d_ccol : pl->d_rc;
+  const long long tot = cols ? pl->tot_ccol : pl->tot_rc;
+  const long long nspec = B * 4 * g.nlines * g.nblk;
+#define EB_LAUNCH(LG)                                                                                       \
+  do {                                                                                                      \
+    auto fs = &k_eb_spec<T, LG>;                                                                            \
+    auto fp = &k_eb_pairs<LG>;                                                                              \
+    spec_attr(fs, LG);                                                                                      \
+    spec_attr(fp, LG);                                                                                      \
+    fs<<<(unsigned)((nspec + spec_g<LG>() - 1) / spec_g<LG>()), spec_threads<LG>(),                         \
+         sizeof(double2) * spec_g<LG>() * spec_sb_elems<LG>(), st>>>(nspec, A, pr, g, cols ? 1 : 0, tw, SP); \
+    const long long nti = (g.nlines + EbTile<LG>::TI - 1) / EbTile<LG>::TI,                                 \
+                    ntj = (g.nlines + EbTile<LG>::TJ - 1) / EbTile<LG>::TJ, ntiles = B * 2 * nti * ntj;     \
+    fp<<<(unsigned)((ntiles + nparts - 1) / nparts), 1 << LG, eb_pairs_smem<LG>(), st>>>(                   \
+        SP, pr, g, cols ? 1 : 0, tw, pl->d_cls_slot, pl->d_cls, dst, tot, part, nparts, ntiles);            \
+  } while (0)
+  switch (g.logLb) {
+    case 6: EB_LAUNCH(6); break;
+    case 7: EB_LAUNCH(7); break;
+    case 8: EB_LAUNCH(8); break;
+    default: EB_LAUNCH(9);
+  }
+#undef EB_LAUNCH
+}
 
 // spectral core sums (spectral.cuh) for band ks_part of ks_nparts: writes
 // the one CC partial per class (npart = 1); with spec_edges also the
@@ -886,7 +933,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
               pl->d_fy, 0, S);
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * S * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
               pl->d_fy, N - S, S);
-    if (pl->spec_edges)
+    if (pl->spec_edges && !pl->spec_blk)
       SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
                 pl->d_fy0, 0, N);
     if (es != st) {  // the side stream: edge-row pair FFTs from the strip spectra
@@ -933,7 +980,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     mark("spec_fft");
     k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
                                                        pl->d_cls_slot, pl->d_ccpart);
-    if (pl->spec_edges && es != st) {
+    if (pl->spec_edges && !pl->spec_blk && es != st) {
       const cudaStream_t st_main = st;
       st = es;
       if (pl->spec_prune_q)
@@ -970,7 +1017,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
                 pl->d_fy, 0, pr.N);
     }
-    if (pl->spec_edges)
+    if (pl->spec_edges && !pl->spec_blk)
       SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
                 pl->d_fy0, 0, pr.N);
     mark("spec_fft");
@@ -992,7 +1039,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
                   pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
     k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
                                                        pl->d_cls_slot, pl->d_ccpart);
-    if (pl->spec_edges && es != st_main)
+    if (pl->spec_edges && !pl->spec_blk && es != st_main)
       if (pl->spec_prune_q)
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
                   pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
@@ -1023,7 +1070,14 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   else
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
               pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
-  if (pl->spec_edges) {
+  if (pl->spec_edges && pl->spec_blk) {
+    // blocked short-lag correlation (edgeblk.cuh) on the side stream: reads
+    // only A's strips.  Timing names: spec_ccol = column strips, spec_rc = row strips
+    mark("spec_dft");
+    launch_edges_blocked<T>(pl, A, es, true, part, nparts);
+    mark("spec_ccol");
+    launch_edges_blocked<T>(pl, A, es, false, part, nparts);
+  } else if (pl->spec_edges) {
     mark("spec_dft");
     {
       cudaStream_t st_main = st;
@@ -1606,7 +1660,7 @@ std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
                         "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH",
-                        "COVGPU_SPEC_NO_PRUNE"}) {
+                        "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
     e += ',';
@@ -1839,6 +1893,14 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->spec_edges = true;
       pl->spec_logLr = logLr;
       pl->spec_logL = logL;
+      // edge sums: blocked short-lag correlation (COVGPU_EDGE_PAIRFFT=1, a test
+      // hook, keeps one full-length FFT per line pair)
+      pl->spec_blk = p <= 128 && q <= 128;
+      if (const char* pf = getenv("COVGPU_EDGE_PAIRFFT")) pl->spec_blk = pl->spec_blk && atoi(pf) == 0;
+      if (pl->spec_blk) {
+        pl->ebc = eb_geom((int)p, (int)q - 1, (int)n, (int)(n - p), (int)p - 1);  // strip columns, row lags
+        pl->ebr = eb_geom((int)q, (int)p - 1, (int)m, (int)(m - q), 0);            // strip rows, column lags
+      }
       pl->spec_L = 1 << logL;
       if (const char* se = getenv("COVGPU_SPEC_E")) pl->spec_e = atoi(se) == 8 ? 8 : 16;
       pl->spec_ngrp = (2 * p - 1 + SPEC_E - 1) / SPEC_E;
@@ -2040,7 +2102,20 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       plan_free(pl.get());
       return fail(COVGPU_ECUDA, "twiddle upload");
     }
-    if (pl->spec_edges) {
+    if (pl->spec_edges && pl->spec_blk) {
+      const std::vector<double2> twc = spec_twiddles(pl->ebc.logLb), twr2 = spec_twiddles(pl->ebr.logLb);
+      if ((rc = dalloc(&pl->d_twbc, twc.size(), &ws)) || (rc = dalloc(&pl->d_twbr, twr2.size(), &ws)) ||
+          (rc = dalloc(&pl->d_ebc, std::max<size_t>(1, (size_t)batch * eb_spec_elems(pl->ebc)), &ws)) ||
+          (rc = dalloc(&pl->d_ebr, std::max<size_t>(1, (size_t)batch * eb_spec_elems(pl->ebr)), &ws))) {
+        plan_free(pl.get());
+        return rc;
+      }
+      if (cudaMemcpy(pl->d_twbc, twc.data(), sizeof(double2) * twc.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(pl->d_twbr, twr2.data(), sizeof(double2) * twr2.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        plan_free(pl.get());
+        return fail(COVGPU_ECUDA, "twiddle upload");
+      }
+    } else if (pl->spec_edges) {
       const size_t Lr = (size_t)1 << pl->spec_logLr;
       const std::vector<double2> twr = spec_twiddles(pl->spec_logLr);
       if ((rc = dalloc(&pl->d_twr, Lr, &ws)) ||
