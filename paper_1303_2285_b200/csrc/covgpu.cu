@@ -204,7 +204,8 @@ struct covgpu_plan {
   std::vector<int4> h_units;
   int4* d_runits = nullptr;   // class-range finalize: units holding a class of the range
   long long n_runits = 0;
-  double2* d_ck = nullptr;    // per-chunk state updates delta_j (the tile kernel's DELTA mode)
+  double2* d_ck = nullptr;    // per-chunk state updates delta_j (the tile kernel's DELTA mode), summed in chunk order
+  int ft_ck = FT_CK;          // checkpoint spacing of the tile walk (ft_ckstep)
   int4* d_dunits = nullptr;   // DELTA-mode units (all classes) and for the class range
   long long n_dunits = 0;
   int4* d_rdunits = nullptr;
@@ -1225,8 +1226,8 @@ std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi, bool del
   const int lanes = ft_lanes(P), subs = 32 / lanes;  // snapshots per warp
   for (int dc = 0; dc < Q; ++dc) {
     const int qu = Q - dc;
-    for (int u0 = 0; u0 < qu; u0 += FT_CK) {
-      const int u1 = std::min(qu, u0 + FT_CK);
+    for (int u0 = 0; u0 < qu; u0 += pl->ft_ck) {
+      const int u1 = std::min(qu, u0 + pl->ft_ck);
       if (delta && u1 >= qu) break;  // no cut after this chunk
       for (long long b = 0; b < pl->batch; b += subs)
         for (int d0 = 0; d0 < P; d0 += lanes) {
@@ -1259,7 +1260,7 @@ void launch_fin_tile(covgpu_plan* pl, const int4* units, long long nunits, const
     k_fin_tile<T, NW, LAY, DEL, LN><<<grid, FtCfg<NW>::THREADS, smem, st>>>(                                \
         (const double2*)pl->d_corners, pl->pr, (int)pl->batch, pl->d_cls, pl->d_cls_slot, units,            \
         (int)nunits, pl->nclasses, npart, ccpart, ccol, pl->tot_ccol, rc, pl->tot_rc, nseg, pl->d_ck, R,    \
-        rstride, scale, u0, u1, wst, slot_lo, slot_hi);                                                     \
+        rstride, scale, u0, u1, wst, slot_lo, slot_hi, pl->ft_ck);                                          \
   } while (0)
 #define FT_LAY(NW, LN)                                                       \
   do {                                                                       \
@@ -1277,6 +1278,13 @@ void launch_fin_tile(covgpu_plan* pl, const int4* units, long long nunits, const
   }
 #undef FT_LAY
 #undef FT_LAUNCH
+}
+
+// chunk updates -> running sums over the chunks (tile.cuh k_ck_scan)
+void launch_ck_scan(covgpu_plan* pl, cudaStream_t st) {
+  const long long n = pl->batch * pl->pr.Q * 2LL * pl->pr.P * pl->pr.P;
+  if (ft_nck(pl->pr.Q, pl->ft_ck) > 1)  // one chunk: nothing to add
+    k_ck_scan<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pl->d_ck, (int)pl->batch, pl->pr.P, pl->pr.Q, pl->ft_ck);
 }
 
 template <typename T>
@@ -1354,7 +1362,8 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     if (pl->n_dunits > 0) {
       launch_fin_tile<T>(pl, pl->d_dunits, pl->n_dunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0,
                          COVGPU_DENSE, 0, 1 << 30, nullptr, 0, INT_MAX, es, true);
-      ++launches;
+      launch_ck_scan(pl, es);
+      launches += 2;
     }
     if (!fork) mark("fin_delta");
   }
@@ -1598,9 +1607,11 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
       dunits = pl->d_rdunits;
       ndunits = pl->n_rdunits;
     }
-    if (ndunits > 0)
+    if (ndunits > 0) {
       launch_fin_tile<T>(pl, dunits, ndunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0, COVGPU_DENSE, 0,
                          1 << 30, nullptr, 0, INT_MAX, st, true);
+      launch_ck_scan(pl, st);
+    }
     launch_fin_tile<T>(pl, units, nunits, cc, 1, cl, rc, 1, (C2*)R_dev, r_bstride, scale, layout, 0, 1 << 30,
                        nullptr, c_lo, c_hi, st);
     CUDA_TRY(cudaGetLastError());
@@ -2144,10 +2155,15 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->fin_kr = p <= 32 ? 1 : p <= 64 ? 2 : 4;
       pl->use_tile = getenv("COVGPU_FIN_WALK") == nullptr || atoi(getenv("COVGPU_FIN_WALK")) == 0;
       pl->ft_nwarp = ft_nwarp(p);
+      pl->ft_ck = ft_ckstep(p, q);
+      if (const char* ce = getenv("COVGPU_FT_CK")) {  // (test hook)
+        const int v = atoi(ce);
+        if (v == 4 || v == 8 || v == 16) pl->ft_ck = v;
+      }
       pl->h_units = fin_tile_units(pl.get(), 0, pl->nclasses);
       pl->n_units = (long long)pl->h_units.size();
-      if (pl->use_tile && ft_nck(q) > 0) {
-        const size_t ckn = (size_t)batch * q * ft_nck(q) * 2 * (size_t)p * p;
+      if (pl->use_tile && ft_nck(q, pl->ft_ck) > 0) {
+        const size_t ckn = (size_t)batch * q * ft_nck(q, pl->ft_ck) * 2 * (size_t)p * p;
         const std::vector<int4> du = fin_tile_units(pl.get(), 0, pl->nclasses, true);
         pl->n_dunits = (long long)du.size();
         if ((rc = dalloc(&pl->d_ck, ckn, &ws)) || (rc = dalloc(&pl->d_dunits, std::max<size_t>(du.size(), 1), &ws))) {

@@ -39,6 +39,8 @@
 // triangle bitwise.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace covgpu {
@@ -47,7 +49,7 @@ namespace covgpu {
 #define FT_CTA_WARPS 8
 #endif
 constexpr int FT_RPT = 8;  // rows per thread
-constexpr int FT_CK = 16;  // checkpoint spacing (steps)
+constexpr int FT_CK = 16;  // largest checkpoint spacing (steps); a plan picks 4, 8 or 16 (ft_ckstep)
 
 template <int NWARP>
 struct FtCfg {
@@ -65,7 +67,17 @@ inline int ft_nwarp(int P) {
 }
 // lanes per snapshot: small windows pack 32 / lanes snapshots into a warp
 inline int ft_lanes(int P) { return P > 16 ? 32 : P > 8 ? 16 : 8; }
-__host__ __device__ inline int ft_nck(int Q) { return (Q - 1) / FT_CK; }  // checkpoints per (snapshot, dc)
+__host__ __device__ inline int ft_nck(int Q, int ck) { return (Q - 1) / ck; }  // checkpoints per (snapshot, dc)
+// Checkpoint spacing of a plan: a function of the window only (never of the
+// batch or the class subset, so a snapshot's bits do not depend on them).
+// Large windows have enough (dc, band, chunk) units to fill the SMs with
+// 16-step walks; small ones are latency-bound chains, so they are cut finer.
+inline int ft_ckstep(int P, int Q) {
+  // (P <= 8: several snapshots share a warp and a step is cheap — the
+  // checkpoint traffic of a batch costs more than the longer chains)
+  const int bands = (P + 31) / 32;
+  return Q * bands >= 128 || P <= 8 ? 16 : Q * bands >= 48 ? 8 : 4;
+}
 
 // Corner blocks per (snapshot, column j of the (Q-1)-column strips), widened
 // to double, in the layout one step's SMEM copy takes as is: first operands
@@ -83,7 +95,10 @@ __host__ __device__ inline size_t ft_tot_bytes(int nwarp) { return (size_t)2 * 4
 __host__ __device__ inline size_t ft_gcol_bytes() { return (size_t)2 * 4 * 32 * 16; }
 // (P > 64, or a one-warp unit: one stage buffer, the mirror follows its step
 // after a second barrier — for one warp a __syncwarp)
-__host__ __device__ inline int ft_stage_bufs(int nwarp) { return nwarp >= 2 && nwarp <= 8 ? 2 : 1; }
+#ifndef FT_STAGE2_MAXW
+#define FT_STAGE2_MAXW 4
+#endif
+__host__ __device__ inline int ft_stage_bufs(int nwarp) { return nwarp >= 2 && nwarp <= FT_STAGE2_MAXW ? 2 : 1; }
 __host__ __device__ inline size_t ft_vec_bytes(int P, int nwarp, int subs) {
   return (size_t)2 * subs * ft_vec_elems(P, nwarp * FT_RPT) * 16;
 }
@@ -97,6 +112,31 @@ __device__ __forceinline__ void ft_unit_sync(int id, int nthreads) {
     __syncwarp();
   else
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One complex store under a predicate (no branch: the walk's stores sit in
+// straight-line code); CS: evict-first (packed R is written once, never re-read)
+template <bool CS>
+__device__ __forceinline__ void ft_store(double2* p, double2 v, unsigned on) {
+  if constexpr (CS)
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.cs.v2.f64 [%1], {%2, %3}; }" ::"r"(on), "l"(p),
+                 "d"(v.x), "d"(v.y)
+                 : "memory");
+  else
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.v2.f64 [%1], {%2, %3}; }" ::"r"(on), "l"(p),
+                 "d"(v.x), "d"(v.y)
+                 : "memory");
+}
+template <bool CS>
+__device__ __forceinline__ void ft_store(float2* p, float2 v, unsigned on) {
+  if constexpr (CS)
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.cs.v2.f32 [%1], {%2, %3}; }" ::"r"(on), "l"(p),
+                 "f"(v.x), "f"(v.y)
+                 : "memory");
+  else
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.v2.f32 [%1], {%2, %3}; }" ::"r"(on), "l"(p),
+                 "f"(v.x), "f"(v.y)
+                 : "memory");
 }
 
 // f += a (x) conj(b) - c (x) conj(d), accumulated with FMAs in double
@@ -186,23 +226,24 @@ __device__ inline void ft_init_entry(int r1, int c, int P, const FtLane& L, cons
 }
 
 #ifndef FT_MINB
-#define FT_MINB 1
+#define FT_MINB 2
 #endif
 // DELTA: unit = (snapshots, dc, band, chunk [16 (j-1), 16 j)); the chunk's
 // state updates from zero go to ck[b][dc][j-1][T, B][row][c] (no output).
 // LANES < 32: a warp holds 32 / LANES snapshots (lane = (snapshot, c)).
 template <typename T, int NWARP, int LAYOUT, bool DELTA, int LANES>
-__global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB)
+__global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 1)
     k_fin_tile(const double2* __restrict__ corners, Problem pr, int B, const ClassDesc* __restrict__ cls,
                const int* __restrict__ cls_slot, const int4* __restrict__ units, int nunits, int nclasses,
                int npart, const double2* __restrict__ ccpart, const double2* __restrict__ ccol,
                long long tot_ccol, const double2* __restrict__ rc, long long tot_rc, int nseg,
                double2* __restrict__ ck, typename CT<T>::c* __restrict__ R, long long r_bstride,
-               double scale, int u_begin, int u_end, double2* __restrict__ wstate, int slot_lo, int slot_hi) {
+               double scale, int u_begin, int u_end, double2* __restrict__ wstate, int slot_lo, int slot_hi,
+               int ckstep) {
   using C2 = typename CT<T>::c;
   constexpr int UPC = FtCfg<NWARP>::UPC, UT = 32 * NWARP, PP = NWARP * FT_RPT, SUBS = 32 / LANES;
   constexpr bool DENSE = LAYOUT == COVGPU_DENSE, PACKED = LAYOUT == COVGPU_PACKED;
-  constexpr bool STAGE2 = NWARP >= 2 && NWARP <= 8;  // double-buffered stage: the mirror runs one step later
+  constexpr bool STAGE2 = NWARP >= 2 && NWARP <= FT_STAGE2_MAXW;  // double-buffered stage: the mirror runs one step later
   extern __shared__ __align__(16) unsigned char ft_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int us = warp / NWARP, w = warp - us * NWARP, ut = (int)threadIdx.x - us * UT;
@@ -257,7 +298,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
 
   double2 fT[FT_RPT], fB[FT_RPT], G1 = make_double2(0.0, 0.0), G2 = G1;
   const long long per = (long long)P * P;
-  const double2* ckb = ck + ((long long)bs * Q + dc) * ft_nck(Q) * 2 * per + c;
+  const double2* ckb = ck + ((long long)bs * Q + dc) * ft_nck(Q, ckstep) * 2 * per + c;
   if (DELTA) {
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) fT[k] = fB[k] = make_double2(0.0, 0.0);
@@ -270,17 +311,19 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     G1 = make_double2(wsp[4 * FT_RPT], wsp[4 * FT_RPT + 1]);
     G2 = make_double2(wsp[4 * FT_RPT + 2], wsp[4 * FT_RPT + 3]);
   } else {
-    // F(u_lo) = F(0) + delta_1 + ... + delta_{u_lo / 16} (fixed order)
+    // F(u_lo) = F(0) + (delta_1 + ... + delta_j), j = u_lo / ckstep: the
+    // chunk updates are already summed in chunk order (k_ck_scan)
     const double2* rcb = rc + (long long)bs * tot_rc * nseg;
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) ft_init_entry(r0 + k, c, P, L, rcb, nseg, fT[k], fB[k]);
-    for (int j = 0; j < u_lo / FT_CK; ++j) {
+    if (u_lo > 0) {
+      const double2* cj = ckb + (long long)(u_lo / ckstep - 1) * 2 * per;
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
         const int r1 = r0 + k;
         if (r1 < P && c < P) {
-          fT[k] = cadd(fT[k], ckb[(long long)j * 2 * per + (long long)r1 * P]);
-          fB[k] = cadd(fB[k], ckb[(long long)j * 2 * per + per + (long long)r1 * P]);
+          fT[k] = cadd(fT[k], cj[(long long)r1 * P]);
+          fB[k] = cadd(fB[k], cj[per + (long long)r1 * P]);
         }
       }
     }
@@ -347,19 +390,80 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
   const bool zero_im = dc == 0 && c == 0;  // class (0,0): R's real main diagonal (rows < bnd = P)
   const long long ostep = (long long)P * (D + 1);  // block (u, u+dc) -> (u+1, u+1+dc)
   const int P2 = 2 * P;
-  // mirror of step um: block (um+dc, um), row P(um+dc) + r2, column P um + src
-  // (the source row), conjugated (the lower triangle = exact conjugate)
-  auto mirror = [&](int um, int buf) {
+  // rows k >= kb of this thread belong to segment 2 (the second class; the
+  // block column wraps from P-1 to 0 there).  wstr: some lane of the warp
+  // holds rows of both segments (a function of the geometry only)
+  const int kb = bnd - r0;
+  const bool wstr = __any_sync(0xffffffffu, kb > 0 && kb < FT_RPT);
+  const int col0 = (r0 + c) % P;  // block column of row r0
+  const int kbw = kb > 0 ? kb : FT_RPT;  // rows k >= kbw wrap to column col0 + k - P (kb <= 0: col0 is already wrapped)
+  const int mwrap = P - msrc0;           // mirror rows k >= mwrap read source row msrc0 + k - P
+  // warp-uniform row pointers, stepped by ostep per step: the emitted row
+  // P u + r0 of block (u, u+dc) and the mirrored row P (u+dc) + r0 of block (u+dc, u)
+  C2* rowp = Rb + ((long long)P * e0 + r0) * D + (long long)P * (e0 + dc);
+  C2* mrowp = Rb + ((long long)P * (e0 + dc) + r0) * D + (long long)P * e0;
+  // mirror of the step whose rows start at mrow: lower-block row r0 + k takes
+  // the conjugate of source row (msrc0 + k) mod P of diagonal cm (the lower
+  // triangle = exact conjugate of the upper)
+  auto mirror = [&](C2* mrow, int buf) {
     const C2* stg = stage0 + (STAGE2 ? buf : 0) * PP * 32 + m;
-    C2* row = Rb + ((long long)P * (um + dc) + r0) * D + (long long)P * um;
 #pragma unroll
     for (int k = 0; k < FT_RPT; ++k) {
-      int src = msrc0 + k;
-      if (src >= P) src -= P;
+      const int src = msrc0 + k - (k >= mwrap ? P : 0);
       C2 val = stg[src * 32];
       val.y = -val.y;
-      if ((mmask >> k) & 1u) row[src] = val;
-      row += D;
+      ft_store<false>(mrow + src, val, (mmask >> k) & 1u);
+      mrow += D;
+    }
+  };
+  // the walk over the thread's rows from O at its first row.  STR: the segment
+  // switch is compiled in (warps without straddling lanes skip it); ZI: the
+  // dc = 0 units hold class (0,0), whose imaginary part is written as exactly 0
+  auto emit = [&](auto str, auto zi, double2 o1, double2 o2, int buf) {
+    constexpr bool STR = decltype(str)::value, ZI = decltype(zi)::value;
+    C2* const stg = stage0 + (STAGE2 ? buf : 0) * PP * 32 + r0 * 32 + lane;
+    const long long k1 = (long long)P * u + r0;
+    C2* rk;  // dense / packed: warp-uniform pointer of the row (the lane adds its column); compact: the lane's slot
+    if constexpr (DENSE)
+      rk = rowp;
+    else if constexpr (PACKED)
+      rk = Rb + (k1 * D - (k1 * (k1 - 1)) / 2 - k1 + (long long)P * (u + dc));
+    else
+      rk = Rb + (kb > 0 ? L.so1 + (long long)u * pv1 + r0 : L.so2 + (long long)u * pv2 + (r0 - bnd));
+    double2 o = kb > 0 ? o1 : o2;
+#pragma unroll
+    for (int k = 0; k < FT_RPT; ++k) {
+      int colk = col0 + k;
+      if constexpr (STR) {
+        if (k > 0 && k == kb) {
+          o = o2;  // segment 2 starts: the second class's walk
+          if constexpr (!DENSE && !PACKED) rk = Rb + L.so2 + (long long)u * pv2;
+        }
+        if (k > 0 && k >= kbw) colk -= P;
+      }
+      C2 val;
+      val.x = (T)(o.x * scale);
+      val.y = (T)(o.y * scale);
+      if constexpr (ZI) {
+        if (zero_im) val.y = (T)0;
+      }
+      const unsigned on = (omask >> k) & 1u;
+      if constexpr (PACKED)
+        ft_store<true>(rk + colk, val, on);
+      else if constexpr (DENSE)
+        ft_store<false>(rk + colk, val, on);
+      else
+        ft_store<false>(rk, val, on);
+      if constexpr (DENSE) stg[k * 32] = val;
+      if (k + 1 < FT_RPT) {
+        o = cadd(o, csub(fB[k], fT[k]));
+        if constexpr (DENSE)
+          rk += D;
+        else if constexpr (PACKED)
+          rk += D - 1 - (k1 + k);
+        else
+          rk += 1;
+      }
     }
   };
   bool prev = false;  // the previous step emitted (its mirror is pending)
@@ -367,26 +471,41 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     const int buf = u & 1;
     double2* const tot = tot0 + buf * 4 * NWARP * 32;
     if constexpr (!DELTA) {
+      // row-group totals of the two segments (t: top states, b: bottom states)
       double2 t1 = make_double2(0.0, 0.0), b1 = t1, t2 = t1, b2 = t1;
+      if (wstr) {
 #pragma unroll
-      for (int k = 0; k < FT_RPT; ++k) {
-        if (r0 + k < bnd) {
+        for (int k = 0; k < FT_RPT; ++k) {
+          if (k < kb) {
+            t1 = cadd(t1, fT[k]);
+            b1 = cadd(b1, fB[k]);
+          } else {
+            t2 = cadd(t2, fT[k]);
+            b2 = cadd(b2, fB[k]);
+          }
+        }
+        tot[w * 32 + lane] = t1;
+        tot[(NWARP + w) * 32 + lane] = b1;
+        tot[(2 * NWARP + w) * 32 + lane] = t2;
+        tot[(3 * NWARP + w) * 32 + lane] = b2;
+      } else {
+        // one segment per lane: sum all rows, store under the lane's segment
+#pragma unroll
+        for (int k = 0; k < FT_RPT; ++k) {
           t1 = cadd(t1, fT[k]);
           b1 = cadd(b1, fB[k]);
-        } else {
-          t2 = cadd(t2, fT[k]);
-          b2 = cadd(b2, fB[k]);
         }
+        const int sg = kb > 0 ? 0 : 2 * NWARP;
+        tot[(sg + w) * 32 + lane] = t1;
+        tot[(sg + NWARP + w) * 32 + lane] = b1;
+        tot[(2 * NWARP - sg + w) * 32 + lane] = t2;  // (zeros: the lane has no rows of the other segment)
+        tot[(3 * NWARP - sg + w) * 32 + lane] = b2;
       }
-      tot[w * 32 + lane] = t1;
-      tot[(NWARP + w) * 32 + lane] = b1;
-      tot[(2 * NWARP + w) * 32 + lane] = t2;
-      tot[(3 * NWARP + w) * 32 + lane] = b2;
     }
     cp_async_wait<0>();  // this step's strip columns and edge-column sums
     ft_unit_sync(bar, UT);
     prefetch(u + 1, buf ^ 1);
-    if (!DELTA && STAGE2 && DENSE && prev && wmir) mirror(u - 1, buf ^ 1);
+    if (!DELTA && STAGE2 && DENSE && prev && wmir) mirror(mrowp - ostep, buf ^ 1);
     if (!DELTA && wout) {
       // O at the warp's first row of each segment: G + top rows from there
       // down + bottom rows above it (x < w: bottoms, x >= w: tops)
@@ -396,53 +515,26 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
         o1 = cadd(o1, tot[((x < w ? NWARP : 0) + x) * 32 + lane]);
         o2 = cadd(o2, tot[((x < w ? 3 * NWARP : 2 * NWARP) + x) * 32 + lane]);
       }
-      C2* const stg = stage0 + (STAGE2 ? buf : 0) * PP * 32 + r0 * 32 + lane;
-      const long long k1 = (long long)P * u + r0;
-      const int col0 = (r0 + c) % P;  // column of row r0 in the block
-      C2* dst;
-      if constexpr (DENSE)
-        dst = Rb + k1 * D + (long long)P * (u + dc) + col0;
-      else if constexpr (PACKED)
-        dst = Rb + packed_off(k1, (long long)P * (u + dc) + col0, D);
-      else
-        dst = Rb + (r0 < bnd ? L.so1 + (long long)u * pv1 + r0 : L.so2 + (long long)u * pv2 + (r0 - bnd));
-      double2 o = r0 < bnd ? o1 : o2;
-#pragma unroll
-      for (int k = 0; k < FT_RPT; ++k) {
-        const int r1 = r0 + k;
-        if (k > 0 && r1 == bnd) {
-          o = o2;  // segment 2 starts: the second class's walk
-          if constexpr (!DENSE && !PACKED) dst = Rb + L.so2 + (long long)u * pv2;
-        }
-        C2 val;
-        val.x = (T)(o.x * scale);
-        val.y = zero_im ? (T)0 : (T)(o.y * scale);
-        if ((omask >> k) & 1u) {
-          if constexpr (PACKED)
-            __stcs(dst, val);
-          else
-            *dst = val;
-        }
-        if constexpr (DENSE) stg[k * 32] = val;
-        if (k + 1 < FT_RPT) {
-          o = cadd(o, csub(fB[k], fT[k]));
-          // next row; the column wraps from P-1 to 0 after row bnd-1
-          const int wrapP = (r1 + 1 == bnd) ? P : 0;
-          if constexpr (DENSE)
-            dst += D + 1 - wrapP;
-          else if constexpr (PACKED)
-            dst += D - (k1 + k) - wrapP;
-          else
-            dst += 1;
-        }
+      if (dc == 0) {
+        if (wstr)
+          emit(std::true_type{}, std::true_type{}, o1, o2, buf);
+        else
+          emit(std::false_type{}, std::true_type{}, o1, o2, buf);
+      } else {
+        if (wstr)
+          emit(std::true_type{}, std::false_type{}, o1, o2, buf);
+        else
+          emit(std::false_type{}, std::false_type{}, o1, o2, buf);
       }
     }
     prev = !DELTA;
     if constexpr (!DELTA && !STAGE2 && DENSE) {
       ft_unit_sync(bar, UT);
-      if (wmir) mirror(u, 0);
+      if (wmir) mirror(mrowp, 0);
       prev = false;
     }
+    rowp += ostep;
+    mrowp += ostep;
     if (u < ac) {
       // every row (no guards): rows and entries outside the strip read zeros
       const double2* va = vec + (buf * SUBS + sub) * vstride + r0;
@@ -460,7 +552,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
   cp_async_wait<0>();
   if constexpr (DELTA) {
     if (b < B) {
-      double2* o = (double2*)ckb + (long long)(u_lo / FT_CK) * 2 * per;
+      double2* o = (double2*)ckb + (long long)(u_lo / ckstep) * 2 * per;
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
         const int r1 = r0 + k;
@@ -474,7 +566,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
   }
   if (STAGE2 && DENSE && prev) {
     ft_unit_sync(bar, UT);
-    if (wmir) mirror(e1 - 1, (e1 - 1) & 1);
+    if (wmir) mirror(mrowp - ostep, (e1 - 1) & 1);
   }
   if (wsp && e1 < u_hi) {
 #pragma unroll
@@ -488,6 +580,24 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP > 8 ? 1 : FT_MINB
     wsp[4 * FT_RPT + 1] = G1.y;
     wsp[4 * FT_RPT + 2] = G2.x;
     wsp[4 * FT_RPT + 3] = G2.y;
+  }
+}
+
+// The per-chunk state updates of one (snapshot, dc) summed in chunk order,
+// in place: ck[j] <- delta_1 + ... + delta_{j+1}.  Thread per element of the
+// [T, B][row][c] block; chunk j of column offset dc exists while
+// (j + 1) ckstep < Q - dc.
+__global__ void k_ck_scan(double2* __restrict__ ck, int B, int P, int Q, int ckstep) {
+  const long long per2 = 2LL * P * P;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)B * Q * per2) return;
+  const int dc = (int)(tid / per2 % Q);
+  const int n = (Q - dc - 1) / ckstep;  // chunks with a cut after them
+  double2* e = ck + (tid / per2) * ft_nck(Q, ckstep) * per2 + tid % per2;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j = 0; j < n; ++j) {
+    acc = cadd(acc, e[(long long)j * per2]);
+    e[(long long)j * per2] = acc;
   }
 }
 
