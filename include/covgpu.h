@@ -95,12 +95,15 @@ int32_t covgpu_plan_launches(covgpu_plan_t plan);
 /* Which sum kernels the plan runs (bit flags): COVGPU_PATH_SPECTRAL — the
  * core / edge sums in the frequency domain (row and column FFTs, per-frequency
  * row-lag correlation); COVGPU_PATH_TENSOR — the core sums as Toeplitz GEMMs
- * on the FP64 tensor cores; neither — the CUDA-core recurrence kernels;
+ * on the FP64 tensor cores; COVGPU_PATH_SNAPSHOT — the sums of each small
+ * complex64 snapshot inside one CTA in FP32 (batched per-snapshot kernel);
+ * none of the three — the CUDA-core recurrence kernels;
  * COVGPU_PATH_ROWBAND — covgpu_plan_execute_sums is available.  Replaces the
  * reference's backend query (backend.resolve_backend, backend.py:45-57). */
 #define COVGPU_PATH_SPECTRAL 1
 #define COVGPU_PATH_TENSOR 2
 #define COVGPU_PATH_ROWBAND 4
+#define COVGPU_PATH_SNAPSHOT 8
 int32_t covgpu_plan_path(covgpu_plan_t plan);
 
 /* Record CUDA events around every kernel of subsequent executes (on the

@@ -52,6 +52,7 @@
 #include "spectral.cuh"
 #include "edgeblk.cuh"
 #include "tile.cuh"
+#include "snap.cuh"
 
 using namespace covgpu;
 
@@ -119,6 +120,7 @@ struct covgpu_plan {
   CUtensorMap ecm_tm{};
   // spectral core sums (spectral.cuh): row FFTs of length L = 2^spec_logL,
   // per-frequency row-lag correlation, output DFT; dr = 0 in the space domain
+  bool use_snap = false;  // per-snapshot FP32 spectral sums (snap.cuh k_snap_spec)
   bool use_spec = false;
   int spec_logL = 0, spec_L = 0, spec_nseg = 1, spec_nfb = 1, spec_ngrp = 1;
   int spec_nd0 = 0;  // dr = 0 per-row partials (core rows)
@@ -1391,13 +1393,24 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     }
   }
   if (!mma && pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: tensor-core kernel unavailable");
-  if (!mma) {
+  bool snap = false;
+  if constexpr (sizeof(T) == 4) {
+    if (!mma && pl->use_snap) {
+      if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));
+      static cudaError_t attr = cudaFuncSetAttribute(k_snap_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+      if (attr != cudaSuccess) return fail(COVGPU_ECUDA, "k_snap_spec shared-memory attribute");
+      k_snap_spec<<<(unsigned)B, K2_THREADS, k2_smem_bytes(pr.N, pr.Q), st>>>(
+          (const float2*)A, pr, B, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
+      snap = true;
+    }
+  }
+  if (!mma && !snap) {
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
     launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
   }
-  const int npart = pl->use_spec ? 1 : mma ? pl->mma_g : pl->ncb * pl->nrs;
+  const int npart = pl->use_spec || snap ? 1 : mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
-  mark(pl->use_spec ? (pl->spec_edges ? "spec_rc" : "spec_dft") : mma ? "bulk_dmma" : "bulk");
+  mark(pl->use_spec ? (pl->spec_edges ? "spec_rc" : "spec_dft") : mma ? "bulk_dmma" : snap ? "snap_spec" : "bulk");
   if (mma && !pl->spec_edges) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
     if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es))) {
       if (pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: edge-column kernel unavailable");
@@ -1670,7 +1683,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK",
                         "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
@@ -1960,6 +1973,12 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->spec_nd0 = (int)std::max(1LL, d0rows);  // N = 2P-2: no core rows
     }
   }
+  // small complex64 snapshots: the sums of a whole snapshot inside one CTA
+  // (snap.cuh).  A function of the shape only (never of the batch), so a
+  // snapshot alone and in a batch run the same arithmetic
+  pl->use_snap = !pl->use_spec && dtype == COVGPU_C64 && pl->clean && class_ids == nullptr && m <= K2_L && p >= 2 &&
+                 p <= K2_E && q >= 2 && q <= K2_MAXQ && k2_smem_bytes((int)n, (int)q) <= 110 * 1024;
+  if (const char* ns = getenv("COVGPU_NO_SNAP")) pl->use_snap = pl->use_snap && atoi(ns) == 0;  // (test hook)
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
   pl->edge_tma = pl->S >= 16 && pl->use_tma;
@@ -2344,6 +2363,7 @@ int32_t covgpu_plan_path(covgpu_plan_t pl) {
   int32_t f = 0;
   if (pl->use_spec) f |= COVGPU_PATH_SPECTRAL;
   else if (pl->use_mma) f |= COVGPU_PATH_TENSOR;
+  else if (pl->use_snap) f |= COVGPU_PATH_SNAPSHOT;
   if (rowband_ok(pl)) f |= COVGPU_PATH_ROWBAND;
   return f;
 }
