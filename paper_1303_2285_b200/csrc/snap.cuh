@@ -28,6 +28,8 @@
 // ~1e-6); every sum has a fixed order, nothing depends on the batch size.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace covgpu {
@@ -155,46 +157,77 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
   for (int e = 0; e < K2_E; ++e) ar[e] = ai[e] = 0.f;
   const int grp = t >> 4, tl = t & 15;
   const int nchunks = (N + K2_CH - 1) / K2_CH;
+  // the X rows of a thread's 8 lags sit in a rotating register window (slot =
+  // row mod 8): half 1 (dr = e) holds rows r2-7 .. r2, half 0 (dr = -(e+1))
+  // rows r2+1 .. r2+8; one row enters per second-element row r2.  The core-row
+  // condition is two per-ROW masks, applied as a row enters the registers:
+  // dr >= 0: y rows r2 >= P-1, x rows r1 <= N-P; dr < 0: y rows r2 <= N-P,
+  // x rows r1 >= P-1
+  float wr[K2_E], wi[K2_E];
+#pragma unroll
+  for (int e = 0; e < K2_E; ++e) wr[e] = wi[e] = 0.f;
+  const float2* const xb = xr + k2_pad(f);
+  // this group's transform of chunk j: the row's 8 inputs per thread, masked
+  // (x: first-element columns c <= M-Q; y: second-element columns c >= Q-1)
+  const bool isy = grp >= 8;
+  auto load_row = [&](int j, float2* u) {
+    const int row = j * K2_CH + (grp & 7);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int c = tl + 16 * r;
+      const bool on = j < nchunks && row < N && c < M && (isy ? c >= Q - 1 : c <= M - Q);
+      u[r] = on ? Ab[(long long)row * M + c] : make_float2(0.f, 0.f);
+    }
+  };
+  auto corr = [&](auto hs, int jc) {
+    constexpr int H = decltype(hs)::value;
+    const float2* yb = yr + (jc & 1) * K2_CH * K2_RS + k2_pad(f);
+#pragma unroll
+    for (int tt = 0; tt < K2_CH; ++tt) {
+      const int r2 = jc * K2_CH + tt;
+      const int rin = H ? r2 : r2 + K2_E;  // the row entering the window (slot tt either way)
+      float2 x = xb[(rin & (K2_XR - 1)) * K2_RS];
+      float2 y = yb[tt * K2_RS];
+      if (H ? rin > N - P : (rin < P - 1 || rin >= N)) x = make_float2(0.f, 0.f);
+      if (H ? (r2 < P - 1 || r2 >= N) : r2 > N - P) y = make_float2(0.f, 0.f);
+      wr[tt] = x.x;
+      wi[tt] = x.y;
+      const float ny = -y.y;
+#pragma unroll
+      for (int e = 0; e < K2_E; ++e) {
+        const int s = H ? (tt - e + K2_E) % K2_E : (tt + 1 + e) % K2_E;  // row r2 - e / r2 + 1 + e
+        ar[e] = fmaf(wr[s], y.x, ar[e]);
+        ai[e] = fmaf(wi[s], y.x, ai[e]);
+        ar[e] = fmaf(wi[s], y.y, ar[e]);
+        ai[e] = fmaf(wr[s], ny, ai[e]);
+      }
+    }
+  };
+  float2 u[8];
+  load_row(0, u);
   for (int j = 0; j <= nchunks; ++j) {
     if (j < nchunks) {
       const int row = j * K2_CH + (grp & 7);
-      const bool isy = grp >= 8;
-      float2 u[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int c = tl + 16 * r;
-        // x: first-element columns c <= M-Q; y: second-element columns c >= Q-1
-        const bool on = row < N && c < M && (isy ? c >= Q - 1 : c <= M - Q);
-        u[r] = on ? Ab[(long long)row * M + c] : make_float2(0.f, 0.f);
-      }
       float2* dst = isy ? yr + ((j & 1) * K2_CH + (grp & 7)) * K2_RS : xr + (row & (K2_XR - 1)) * K2_RS;
       k2_fft128(u, dst, tl, tw64, tw128);
     }
+    load_row(j + 1, u);  // the next chunk's row: its latency hides under the correlation
     __syncthreads();
-    if (j >= 1) {
-      const int jc = j - 1;
-      const float2* yb = yr + (jc & 1) * K2_CH * K2_RS + k2_pad(f);
-      const float2* xb = xr + k2_pad(f);
-#pragma unroll 2
-      for (int k = 0; k < K2_CH; ++k) {
-        const int r2 = jc * K2_CH + k;
-        // core rows: dr >= 0: r2 >= P-1, r1 <= N-P; dr < 0: r2 <= N-P, r1 >= P-1
-        const bool yok = half ? (r2 >= P - 1 && r2 < N) : (r2 <= N - P);
-        float2 y = yb[k * K2_RS];
-        if (!yok) y = make_float2(0.f, 0.f);
+    if (j == 1 && !half) {
+      // half 0's window before r2 = 0: rows 1 .. 7 (row 8 enters at r2 = 0)
 #pragma unroll
-        for (int e = 0; e < K2_E; ++e) {
-          const int r1 = half ? r2 - e : r2 + 1 + e;
-          const bool xok = half ? (r1 >= 0 && r1 <= N - P) : (r1 >= P - 1 && r1 < N);
-          float2 x = xb[(r1 & (K2_XR - 1)) * K2_RS];
-          if (!xok) x = make_float2(0.f, 0.f);
-          // acc += x conj(y)
-          ar[e] = fmaf(x.x, y.x, ar[e]);
-          ar[e] = fmaf(x.y, y.y, ar[e]);
-          ai[e] = fmaf(x.y, y.x, ai[e]);
-          ai[e] = fmaf(-x.x, y.y, ai[e]);
-        }
+      for (int x = 1; x < K2_E; ++x) {
+        float2 v = xb[x * K2_RS];
+        if (x < P - 1 || x >= N) v = make_float2(0.f, 0.f);
+        wr[x] = v.x;
+        wi[x] = v.y;
       }
+    }
+    if (j >= 1) {
+      if (half)
+        corr(std::integral_constant<int, 1>{}, j - 1);
+      else
+        corr(std::integral_constant<int, 0>{}, j - 1);
     }
     __syncthreads();
   }
