@@ -44,6 +44,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# the side runs on the other sum engines (tensor_core_path / cuda_core_path)
+# select them through the library's test hooks; the measured default plan is
+# created with no switch set
+os.environ.setdefault("COVGPU_TEST_HOOKS", "1")
 
 METRIC = "R entries/s and effective GFLOP/s vs FP64/FP32 roofline at 1/2/4/8 B200"
 UNIT = "R entries/s"
@@ -512,6 +516,16 @@ def main() -> None:
             per_kernel[name]["bound"] = "fp64-tensor"
         elif name == "bulk":
             per_kernel[name] = fp_roof(name, 8.0 * bulk_p * B * sf, "8 flops x core-row products")
+        elif name == "snap_spec":
+            # K2 (snap.cuh): per snapshot the 15-lag correlation over L = 128
+            # frequencies, the edge-column pair correlations (pairs of strip
+            # columns x 2P-1 lags x core rows) and 2N + 2P-1 FFTs of length 128
+            corr = sum((n - 2 * p + 2 + abs(dr)) for dr in range(-(p - 1), p)) * 128
+            pairs = sum((n - 2 * p + 2 + abs(dr)) for dr in range(-(p - 1), p)) * (q - 1) * q
+            ffts = (2 * n + 2 * p - 1) * 5 * 128 * 7
+            per_kernel[name] = fp_roof(name, (8.0 * (corr + pairs) + ffts) * B * sf,
+                                       "8 flops x (row-lag correlation MACs over 128 frequencies + edge-column "
+                                       "pair MACs) + 5 L log2 L per FFT (2N + 2P-1 transforms), per snapshot")
         elif name in ("finalize", "expand"):
             nbytes = float(w.pq) ** 2 * esz_in * B * sf if layout == "dense" else None
             if nbytes:
@@ -521,7 +535,7 @@ def main() -> None:
         dom = max(per_kernel, key=lambda k: kernel_ms[k])
         roof = dict(per_kernel[dom])
         roof["kernel"] = {"spec_corr": "k_spec_corr_smem", "spec_fft": "k_spec_fft",
-                          "bulk_dmma": "k_bulk_dmma3", "bulk": "k_bulk_tma", "finalize": "k_fin_tile",
+                          "bulk_dmma": "k_bulk_dmma3", "bulk": "k_bulk_tma", "snap_spec": "k_snap_spec", "finalize": "k_fin_tile",
                           "expand": "k_expand"}.get(dom, dom)
         roof["share_of_step"] = kernel_ms[dom] / max(sum(kernel_ms.values()), 1e-12)
         roof["traffic"] = None
@@ -619,6 +633,15 @@ def main() -> None:
             "note": "COVGPU_NO_MMA=1 COVGPU_NO_SPECTRAL=1: core sums on the FP64 FMA pipe (k_bulk_tma), "
                     "8 flops per core-row product",
         }
+
+    if world == 1 and not rowband and "snap_spec" in kernel_ms:
+        cms, ck = side_path({"COVGPU_NO_SNAP": "1"})
+        cach = 8.0 * bulk_p * w.batch / (ck["bulk"] * 1e-3) / 1e12 if ck.get("bulk") else None
+        line["cuda_core_path"] = {
+            "ms_per_step": cms, "value": entries / (cms * 1e-3), "kernel_ms": ck,
+            "bulk_achieved_tflops": cach, "bulk_frac_of_fma_probe": cach / peak if cach else None,
+            "note": "COVGPU_NO_SNAP=1: the direct FP32 CUDA-core sums (k_bulk_tma, 8 flops per core-row "
+                    "product) instead of the per-snapshot spectral kernel"}
 
     # end to end through the C ABI with pinned host buffers
     if not args.no_e2e and rowband:

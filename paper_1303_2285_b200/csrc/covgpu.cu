@@ -60,6 +60,17 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// The COVGPU_* environment switches (engine forcing, kernel variants) are
+// test hooks: honoured only when COVGPU_TEST_HOOKS=1 is set (tests/conftest.py,
+// bench.py's side runs, tools/); the product path reads no switch.
+const char* hook_env(const char* name) {
+  static const bool on = [] {
+    const char* v = getenv("COVGPU_TEST_HOOKS");
+    return v && atoi(v) != 0;
+  }();
+  return on ? getenv(name) : nullptr;
+}
+
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -446,7 +457,7 @@ int pick_bulk_variant(long long n, long long m, int p, int q, long long batch, i
     v = (span > 8 && waves(16, 4, 2) >= 6.0) ? 6 : 7;
   else
     v = waves(8, 8, 2) >= 6.0 ? 1 : 7;
-  if (const char* env = getenv("COVGPU_BULK_VARIANT")) {
+  if (const char* env = hook_env("COVGPU_BULK_VARIANT")) {
     const int ev = atoi(env);
     if (ev >= 0 && ev < kNumBulkVariants) v = ev;
   }
@@ -1804,9 +1815,9 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   {
     const int v = pick_bulk_variant(n, m, p, q, batch, dtype);
     pl->bulk_variant = v;
-    if (const char* nt = getenv("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
-    if (const char* nd = getenv("COVGPU_NO_DIRECT")) pl->no_direct = atoi(nd) != 0;
-    if (const char* ng = getenv("COVGPU_NO_GRAPH")) pl->use_graph = atoi(ng) == 0;
+    if (const char* nt = hook_env("COVGPU_NO_TMA")) pl->use_tma = atoi(nt) == 0;
+    if (const char* nd = hook_env("COVGPU_NO_DIRECT")) pl->no_direct = atoi(nd) != 0;
+    if (const char* ng = hook_env("COVGPU_NO_GRAPH")) pl->use_graph = atoi(ng) == 0;
     pl->E = kBulkVariants[v].E;
     pl->NW = kBulkVariants[v].NW;
   }
@@ -1836,7 +1847,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const int ncb_r = pl->ncb - (int)((m - q + 1) / 32);
     bool ok = dtype == COVGPU_C128 && pl->clean && class_ids == nullptr && p >= 16 && q >= 24 &&
               p <= FINV_MAX_P && q >= 2 && ncb_l + ncb_r <= pl->ncb && pl->use_tma;
-    if (const char* nm = getenv("COVGPU_NO_MMA")) ok = ok && atoi(nm) == 0;
+    if (const char* nm = hook_env("COVGPU_NO_MMA")) ok = ok && atoi(nm) == 0;
     if (ok) {
       pl->use_mma = true;
       pl->mma_dc = q <= 32 ? 32 : 64;
@@ -1845,7 +1856,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       // operand sums (PREP); 5: kind 1 + PREP with 8-row chunks), 0: 4-DMMA k_bulk_dmma
       // (cfg5 bulk: kind 0 7.06 ms, 1 5.74, 2 5.90, 4 5.75, 5 5.65)
       pl->mma_kind = q <= 32 ? 3 : 5;
-      if (const char* mk = getenv("COVGPU_MMA_KIND")) {
+      if (const char* mk = hook_env("COVGPU_MMA_KIND")) {
         const int k = atoi(mk);
         if (k >= 0 && k <= 5) pl->mma_kind = k;
       }
@@ -1871,7 +1882,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       // 4 warps balanced: cfg5 edge columns 0.647 -> 0.337 ms, but cfg3
       // (Q=32) 0.037 -> 0.074 ms)
       bool ecm = q >= 50 && q <= 65;
-      if (const char* ne = getenv("COVGPU_NO_MMA_EDGE")) ecm = ecm && atoi(ne) == 0;
+      if (const char* ne = hook_env("COVGPU_NO_MMA_EDGE")) ecm = ecm && atoi(ne) == 0;
       if (ecm) {
         // items (snapshot, strip, dr) x G row splits: pick G in [1, 16] for
         // the best fill of 2 CTAs/SM waves (>= 2 chunks of 16 rows per CTA)
@@ -1909,9 +1920,9 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     // (class shards: every shard would repeat the FFTs and the correlation of
     // all lags — the multi-GPU split for this path is row bands)
     bool want = direct_work >= kSpecMinWork && class_ids == nullptr;
-    if (const char* fs = getenv("COVGPU_SPECTRAL")) want = want || atoi(fs) != 0;
+    if (const char* fs = hook_env("COVGPU_SPECTRAL")) want = want || atoi(fs) != 0;
     spec = spec && want;
-    if (const char* ns = getenv("COVGPU_NO_SPECTRAL")) spec = spec && atoi(ns) == 0;
+    if (const char* ns = hook_env("COVGPU_NO_SPECTRAL")) spec = spec && atoi(ns) == 0;
     if (spec) {
       pl->use_spec = true;
       pl->spec_edges = true;
@@ -1920,13 +1931,13 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       // edge sums: blocked short-lag correlation (COVGPU_EDGE_PAIRFFT=1, a test
       // hook, keeps one full-length FFT per line pair)
       pl->spec_blk = p <= 128 && q <= 128;
-      if (const char* pf = getenv("COVGPU_EDGE_PAIRFFT")) pl->spec_blk = pl->spec_blk && atoi(pf) == 0;
+      if (const char* pf = hook_env("COVGPU_EDGE_PAIRFFT")) pl->spec_blk = pl->spec_blk && atoi(pf) == 0;
       if (pl->spec_blk) {
         pl->ebc = eb_geom((int)p, (int)q - 1, (int)n, (int)(n - p), (int)p - 1);  // strip columns, row lags
         pl->ebr = eb_geom((int)q, (int)p - 1, (int)m, (int)(m - q), 0);            // strip rows, column lags
       }
       pl->spec_L = 1 << logL;
-      if (const char* se = getenv("COVGPU_SPEC_E")) pl->spec_e = atoi(se) == 8 ? 8 : 16;
+      if (const char* se = hook_env("COVGPU_SPEC_E")) pl->spec_e = atoi(se) == 8 ? 8 : 16;
       pl->spec_ngrp = (2 * p - 1 + SPEC_E - 1) / SPEC_E;
       pl->spec_nfb = (pl->spec_L + SPEC_CW * 32 - 1) / (SPEC_CW * 32);
       // row segments: ~6 CTAs of 4 warps per SM, >= 4 windows of rows each.
@@ -1944,7 +1955,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->spec_smem = pl->spec_ngrp <= 8 && 2 * stb + 64 <= SC_SMEM_BUDGET;
       // warps of the SMEM kernel: negative and non-negative lags in separate groups
       if (pl->spec_smem) pl->spec_ngrp = (p - 1 + pl->spec_e - 1) / pl->spec_e + (p + pl->spec_e - 1) / pl->spec_e;
-      if (const char* nsm = getenv("COVGPU_SPEC_NO_SMEM")) pl->spec_smem = pl->spec_smem && atoi(nsm) == 0;
+      if (const char* nsm = hook_env("COVGPU_SPEC_NO_SMEM")) pl->spec_smem = pl->spec_smem && atoi(nsm) == 0;
       if (pl->spec_smem) {
         pl->spec_stages = (int)std::min<size_t>(4, SC_SMEM_BUDGET / (stb + 16));
         // row segments: whole waves of 1-CTA/SM blocks, >= 4 chunks per segment
@@ -1978,7 +1989,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   // snapshot alone and in a batch run the same arithmetic
   pl->use_snap = !pl->use_spec && dtype == COVGPU_C64 && pl->clean && class_ids == nullptr && m <= K2_L && p >= 2 &&
                  p <= K2_E && q >= 2 && q <= K2_MAXQ && k2_smem_bytes((int)n, (int)q) <= 110 * 1024;
-  if (const char* ns = getenv("COVGPU_NO_SNAP")) pl->use_snap = pl->use_snap && atoi(ns) == 0;  // (test hook)
+  if (const char* ns = hook_env("COVGPU_NO_SNAP")) pl->use_snap = pl->use_snap && atoi(ns) == 0;  // (test hook)
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
   pl->edge_tma = pl->S >= 16 && pl->use_tma;
@@ -2004,7 +2015,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
 
   if (pl->use_mma && p >= 48 && p <= 65) {  // the 64-row strip tile: P-1 in [47, 64]
     bool erm = true;
-    if (const char* ne = getenv("COVGPU_NO_MMA_EDGE")) erm = atoi(ne) == 0;
+    if (const char* ne = hook_env("COVGPU_NO_MMA_EDGE")) erm = atoi(ne) == 0;
     if (erm) {
       // CTA = (snapshot, strip, r2, lag tile, column segment), 1 CTA/SM: the
       // segment count with the best wave fill (>= 2 column chunks each;
@@ -2107,7 +2118,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const std::vector<double2> twrf = full_table(pl->spec_logLr);
     pl->spec_prune_q = q <= (1 << SPEC_LOGOUT) && pl->spec_logL >= SPEC_LOGOUT + 3;
     pl->spec_prune_p = p <= (1 << SPEC_LOGOUT) && pl->spec_logLr >= SPEC_LOGOUT + 3;
-    if (const char* np = getenv("COVGPU_SPEC_NO_PRUNE"))
+    if (const char* np = hook_env("COVGPU_SPEC_NO_PRUNE"))
       if (atoi(np) != 0) pl->spec_prune_q = pl->spec_prune_p = false;
     if ((rc = dalloc(&pl->d_twf, twf.size(), &ws)) || (rc = dalloc(&pl->d_twrf, twrf.size(), &ws))) {
       plan_free(pl.get());
@@ -2172,10 +2183,10 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     pl->fin_smem = sizeof(double2) * (size_t)FIN_WARPS * 4 * (size_t)q;
     if (p <= FINV_MAX_P) {
       pl->fin_kr = p <= 32 ? 1 : p <= 64 ? 2 : 4;
-      pl->use_tile = getenv("COVGPU_FIN_WALK") == nullptr || atoi(getenv("COVGPU_FIN_WALK")) == 0;
+      pl->use_tile = hook_env("COVGPU_FIN_WALK") == nullptr || atoi(hook_env("COVGPU_FIN_WALK")) == 0;
       pl->ft_nwarp = ft_nwarp(p);
       pl->ft_ck = ft_ckstep(p, q);
-      if (const char* ce = getenv("COVGPU_FT_CK")) {  // (test hook)
+      if (const char* ce = hook_env("COVGPU_FT_CK")) {  // (test hook)
         const int v = atoi(ce);
         if (v == 4 || v == 8 || v == 16) pl->ft_ck = v;
       }
@@ -2600,7 +2611,7 @@ static int execute_host_pipelined(covgpu_plan_t pl, const void* A_host, void* R_
   const size_t esz = pl->dtype == COVGPU_C128 ? 16 : 8;
   const long long B = pl->batch;
   long long nsub = 32;  // cfg4: 16 -> 3.38 ms, 32 -> 3.03 ms, 64 -> 3.72 ms (bidirectional PCIe floor 2.68 ms)
-  if (const char* e = getenv("COVGPU_PIPE_SUBBATCHES")) nsub = std::max(2, atoi(e));
+  if (const char* e = hook_env("COVGPU_PIPE_SUBBATCHES")) nsub = std::max(2, atoi(e));
   const long long nch = std::min<long long>(nsub, B);
   const long long sub = (B + nch - 1) / nch;
   const long long tail = B - (B - 1) / sub * sub;  // size of the last sub-batch
@@ -2712,7 +2723,7 @@ static PFN_cuStreamWriteValue32_v11070 stream_write_value() {
 // Sets up the copy stream, band flag and event on first use.
 static bool stream_a_in_bands(covgpu_plan* pl, size_t a_bytes) {
   if (!pl->use_mma || pl->batch != 1 || a_bytes < (8u << 20) || !stream_write_value()) return false;
-  if (const char* e = getenv("COVGPU_NO_BAND_H2D"))
+  if (const char* e = hook_env("COVGPU_NO_BAND_H2D"))
     if (atoi(e) != 0) return false;
   if (!pl->d_band_flag) {
     if (cudaMalloc(&pl->d_band_flag, sizeof(unsigned)) != cudaSuccess ||
@@ -2856,7 +2867,7 @@ static bool chunked_copy_out(covgpu_plan* pl, int layout) {
   // chunk launches cost more than the overlap gains, 0.353 -> 0.447 ms)
   const long long D = pl->pr.PQ;
   if (pl->pr.Q < 24 || D * (D + 1) / 2 * 16 < (32LL << 20)) return false;
-  if (const char* e = getenv("COVGPU_NO_CHUNKED_D2H"))
+  if (const char* e = hook_env("COVGPU_NO_CHUNKED_D2H"))
     if (atoi(e) != 0) return false;
   if (!pl->d_fin_state) {
     // events first: the state buffer marks a completed setup

@@ -52,8 +52,11 @@ class OpCounters:
     """Exact operation counts of one estimate (``engine.py:42-75``).
 
     multiplications = sum of mu over UC = UM (Eq. 4.6) — every product is
-    formed exactly once.  additions follows the GPU path: one accumulate per
-    product plus two per slot for the diagonal-segment walk.
+    formed exactly once (the paper's count; the default spectral engine gets
+    the same sums with far fewer hardware multiplies).  additions is a MODEL,
+    not a count of executed instructions: one accumulate per product plus two
+    per slot for the diagonal-segment walk — the direct CUDA-core kernels'
+    arithmetic (the reference's figure is backend-specific too).
     """
 
     multiplications: int

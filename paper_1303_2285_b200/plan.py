@@ -109,7 +109,7 @@ class Plan:
         _native.check(rc, "covgpu_plan_wait")
 
     # ---- which sum kernels run (include/covgpu.h: covgpu_plan_path) ----
-    PATH_SPECTRAL, PATH_TENSOR, PATH_ROWBAND = 1, 2, 4
+    PATH_SPECTRAL, PATH_TENSOR, PATH_ROWBAND, PATH_SNAPSHOT = 1, 2, 4, 8
 
     @property
     def path(self) -> int:

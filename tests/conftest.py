@@ -1,3 +1,4 @@
+import os
 import sys
 from pathlib import Path
 
@@ -7,6 +8,10 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(Path(__file__).resolve().parent))
+
+# the library's COVGPU_* switches (engine forcing for the parity tests) are
+# honoured only under this flag (csrc/covgpu.cu hook_env)
+os.environ.setdefault("COVGPU_TEST_HOOKS", "1")
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 

@@ -872,3 +872,56 @@ def test_row_bands_bitwise_across_gpu_counts(cuda, name):
         got = simulate_rowband(bufs, win)
         assert torch.equal(got, ref), world
     plan.close()
+
+
+@pytest.mark.parametrize("n,m,p,q,batch", [
+    (128, 128, 8, 16, 9),    # the cfg4 shape
+    (127, 125, 8, 16, 3),    # N, M ragged: last chunk partial, columns past M zero-padded
+    (14, 30, 8, 16, 2),      # N = 2P-2, M = 2Q-2: no core rows / core columns, edges only
+    (50, 128, 2, 2, 4),      # smallest window: one lag of each sign, one strip column
+    (33, 17, 3, 9, 5),       # short rows (M << FFT length), odd sizes
+    (128, 64, 7, 11, 2),
+    (9, 128, 5, 16, 3),      # fewer rows than a chunk and a half
+])
+def test_snapshot_kernel_vs_oracle(cuda, n, m, p, q, batch, monkeypatch):
+    """K2 (snap.cuh): the FP32 per-snapshot spectral sums against the C
+    oracle on cfg4's shape and on ragged / degenerate small shapes; exactly
+    Hermitian; a snapshot alone == the same snapshot in a batch, packed ==
+    dense upper triangle, and the CUDA-core engine (COVGPU_NO_SNAP=1) agrees
+    within the complex64 tolerance."""
+    from oracle import covoracle_c
+    from paper_1303_2285_b200.plan import Plan
+
+    rng = np.random.default_rng(n * 131 + m * 17 + p * 5 + q)
+    stack = (rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m))).astype(np.complex64)
+    ad = torch.as_tensor(stack, device=cuda)
+    win = WindowSpec(p, q)
+    plan = Plan(n, m, win, batch=batch, dtype=torch.complex64, device=cuda)
+    assert plan.path & Plan.PATH_SNAPSHOT and not plan.spectral
+    out = plan.alloc_output()
+    plan.execute(ad, out)
+    got = out.reshape(batch, p * q, p * q).cpu().numpy()
+    pk = plan.alloc_output("packed")
+    plan.execute(ad, pk, "packed")
+    pkn = pk.reshape(batch, -1).cpu().numpy()
+    plan.close()
+    single = Plan(n, m, win, batch=1, dtype=torch.complex64, device=cuda)
+    o1 = single.alloc_output()
+    single.execute(ad[batch - 1:].contiguous(), o1)
+    assert np.array_equal(o1.reshape(p * q, p * q).cpu().numpy(), got[batch - 1])
+    single.close()
+    monkeypatch.setenv("COVGPU_NO_SNAP", "1")
+    direct = Plan(n, m, win, batch=batch, dtype=torch.complex64, device=cuda)
+    assert not direct.path & Plan.PATH_SNAPSHOT
+    od = direct.alloc_output()
+    direct.execute(ad, od)
+    gd = od.reshape(batch, p * q, p * q).cpu().numpy()
+    direct.close()
+    k = (n - p + 1) * (m - q + 1)
+    for b in range(batch):
+        assert_hermitian(got[b])
+        assert np.array_equal(packed_of(got[b]), pkn[b])
+        ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), p, q) / k
+        err = co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref)
+        assert err <= TOL32, (b, err)
+        assert co.rel_frobenius(got[b].astype(np.complex128), gd[b].astype(np.complex128)) <= TOL32

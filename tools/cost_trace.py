@@ -4,6 +4,7 @@ reference's task_id,dr,dc,cost format, plus its rank correlation with the
 reference's cost model mu = pair_count (and mu (1 + eta), engine.py:86-92).
 Usage: python tools/cost_trace.py cfg3 profiles/r02_cost_trace_cfg3.csv"""
 import json
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 import sys
 from pathlib import Path
 

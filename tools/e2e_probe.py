@@ -1,5 +1,6 @@
 """Which earlier use of a plan changes the synchronous host-path time (dev aid)."""
 import sys, time
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch

@@ -1,6 +1,7 @@
 """Synchronous host-path time of a workload (dev aid): pinned buffers,
 covgpu_plan_execute_host, packed R, median of K calls."""
 import sys, time
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch

@@ -2,6 +2,7 @@
 report every shape whose result differs from the C oracle or between runs
 (dev aid for races / uninitialised reads)."""
 import os
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 import sys
 from pathlib import Path
 

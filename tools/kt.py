@@ -1,5 +1,6 @@
 """Per-kernel CUDA-event times of one config (development aid)."""
 import os, sys
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch

@@ -1,4 +1,5 @@
 import sys, time
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 sys.path.insert(0, '/root/repo')
 import torch
 from paper_1303_2285_b200 import WindowSpec

@@ -1,5 +1,6 @@
 """One warm plan execute of a workload (for ncu captures)."""
 import sys
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch

@@ -4,6 +4,7 @@
 finalize in all three layouts, a batched complex64 stack, the host-buffer
 paths (sync and async) and the row-band parts.  Prints one line per case."""
 import os
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 import sys
 from pathlib import Path
 

@@ -1,5 +1,6 @@
 """K2 (snap.cuh) against the C oracle and the CUDA-core path (dev aid)."""
 import os, sys
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np

@@ -1,6 +1,7 @@
 """Spectral core sums vs the tensor-core path (development aid): relF,
 per-class worst error, and CUDA-event step / per-kernel times."""
 import os, sys
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch

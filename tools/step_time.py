@@ -1,6 +1,7 @@
 """CUDA-event step time of a workload with the default plan (overlapped
 streams, no per-kernel timing), L2 flushed between steps (dev aid)."""
 import sys
+__import__("os").environ.setdefault("COVGPU_TEST_HOOKS", "1")  # COVGPU_* switches are test hooks
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
