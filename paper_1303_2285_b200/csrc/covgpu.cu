@@ -1410,8 +1410,9 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));
       static cudaError_t attr = cudaFuncSetAttribute(k_snap_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
       if (attr != cudaSuccess) return fail(COVGPU_ECUDA, "k_snap_spec shared-memory attribute");
-      k_snap_spec<<<(unsigned)B, K2_THREADS, k2_smem_bytes(pr.N, pr.Q), st>>>(
-          (const float2*)A, pr, B, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol);
+      k_snap_spec<<<(unsigned)B, K2_THREADS, k2_smem_bytes(pr.N, pr.P, pr.Q), st>>>(
+          (const float2*)A, pr, B, pl->nclasses, pl->d_cls_slot, pl->d_cls, pl->d_ccpart, pl->d_ccol, pl->tot_ccol,
+          pl->d_rc, pl->tot_rc);
       snap = true;
     }
   }
@@ -1430,7 +1431,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     ++launches;
     mark("edge_cols");
   }
-  if (pl->S > 0 && !pl->spec_edges) {
+  if (pl->S > 0 && !pl->spec_edges && !snap) {  // (the snapshot kernel also yields RC')
     switch (pl->D) {
       case 4: launch_edge<T, 4>(pl, A, es); break;
       case 8: launch_edge<T, 8>(pl, A, es); break;
@@ -1988,7 +1989,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   // (snap.cuh).  A function of the shape only (never of the batch), so a
   // snapshot alone and in a batch run the same arithmetic
   pl->use_snap = !pl->use_spec && dtype == COVGPU_C64 && pl->clean && class_ids == nullptr && m <= K2_L && p >= 2 &&
-                 p <= K2_E && q >= 2 && q <= K2_MAXQ && k2_smem_bytes((int)n, (int)q) <= 110 * 1024;
+                 p <= K2_E && q >= 2 && q <= K2_MAXQ && k2_smem_bytes((int)n, (int)p, (int)q) <= 110 * 1024;
   if (const char* ns = hook_env("COVGPU_NO_SNAP")) pl->use_snap = pl->use_snap && atoi(ns) == 0;  // (test hook)
   pl->S = p - 1;
   pl->ndg = (q + pl->D - 1) / pl->D;
@@ -2037,7 +2038,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       pl->nseg = (int)std::min(seg, 16LL);
     }
   }
-  if (pl->use_spec) pl->nseg = 1;  // RC' in one piece (k_spec_rc)
+  if (pl->use_spec || pl->use_snap) pl->nseg = 1;  // RC' in one piece (k_spec_rc / k_snap_spec)
   const int nuc = (int)covgpu_num_classes(p, q);
   std::vector<char> sel(nuc, class_ids ? 0 : 1);
   if (class_ids) {

@@ -43,8 +43,10 @@ constexpr int K2_W = 2 * K2_E - 1; // lag window of the edge-column pairs
 constexpr int K2_MAXQ = 16;
 constexpr int K2_THREADS = 256;
 
-__host__ __device__ inline size_t k2_smem_bytes(int N, int Q) {
-  return sizeof(float2) * ((size_t)(K2_XR + 2 * K2_CH) * K2_RS + (size_t)2 * N * (Q - 1) + 64 + 64);
+constexpr int K2_ERS = 129;        // strip-row stride (odd: the strip's rows fall in distinct banks)
+__host__ __device__ inline size_t k2_smem_bytes(int N, int P, int Q) {
+  return sizeof(float2) * ((size_t)(K2_XR + 2 * K2_CH) * K2_RS + (size_t)2 * N * (Q - 1) + 64 + 64 +
+                           (size_t)2 * (P - 1) * K2_ERS);
 }
 
 __device__ __forceinline__ int k2_pad(int i) { return i + (i >> 3); }
@@ -123,7 +125,7 @@ __device__ __forceinline__ void k2_fft128(float2* u, float2* row, int tl, const 
 __global__ void __launch_bounds__(K2_THREADS, 2)
     k_snap_spec(const float2* __restrict__ A, Problem pr, int B, int nclasses, const int* __restrict__ cls_slot,
                 const ClassDesc* __restrict__ cls, double2* __restrict__ ccpart, double2* __restrict__ ccol,
-                long long tot_ccol) {
+                long long tot_ccol, double2* __restrict__ rc, long long tot_rc) {
   extern __shared__ __align__(16) unsigned char k2raw[];
   const int N = pr.N, M = pr.M, P = pr.P, Q = pr.Q, S1 = Q - 1;
   float2* const xr = reinterpret_cast<float2*>(k2raw);           // X ring [K2_XR][K2_RS]
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
   float2* const sr = sl + (size_t)N * S1;                        // right strip [N][Q-1]
   float2* const tw64 = sr + (size_t)N * S1;                      // w_64^k
   float2* const tw128 = tw64 + 64;                               // w_128^k, k < 64
+  float2* const er = tw128 + 64;                                 // strip rows [2][P-1][K2_ERS] (edge-row sums)
+  const int S = P - 1;
   const int t = threadIdx.x, b = blockIdx.x;
   const float2* Ab = A + (long long)b * N * M;
 
@@ -147,6 +151,12 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
     const int r = i / S1, j = i - r * S1;
     sl[i] = Ab[(long long)r * M + j];
     sr[i] = Ab[(long long)r * M + (M - S1) + j];
+  }
+  // the top / bottom P-1 strip rows (edge-row sums), zero beyond column M
+  for (int i = t; i < 2 * S * K2_L; i += K2_THREADS) {
+    const int row = i / K2_L, c = i - row * K2_L;
+    const int ra = row < S ? row : N - S + (row - S);
+    er[row * K2_ERS + c] = c < M ? Ab[(long long)ra * M + c] : make_float2(0.f, 0.f);
   }
   __syncthreads();
 
@@ -322,6 +332,57 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
       const ClassDesc& cd = cls[slot];
       const int ac = cd.qu - 1;  // = Q - 1 - dc > j1
       ccol[(long long)b * tot_ccol + cd.ccol_off + (side ? ac : 0) + j1] = make_double2((double)cr[e], (double)ci[e]);
+    }
+  }
+  // ---- edge-row sums RC' (edge.cuh k_edge_rows): ordered row pairs (r1, r2)
+  // of one strip x column lags dc < Q, summed over the slot-0 box columns
+  // c in [0, M-Q]; thread = (strip, pair, group of K2_E column lags), the
+  // second-element columns in a rotating register window
+  const int ndg = (Q + K2_E - 1) / K2_E;
+  for (int item = t; item < 2 * S * S * ndg; item += K2_THREADS) {
+    const int g = item % ndg;
+    const int pq = item / ndg % (S * S), strip = item / (ndg * S * S);
+    const int i1 = pq % S, i2 = pq / S, dr = i2 - i1, dc0 = g * K2_E;
+    const float2* x = er + (strip * S + i1) * K2_ERS;
+    const float2* y = er + (strip * S + i2) * K2_ERS;
+    float cr[K2_E], ci[K2_E], vr[K2_E], vi[K2_E];
+#pragma unroll
+    for (int d = 0; d < K2_E; ++d) cr[d] = ci[d] = vr[d] = vi[d] = 0.f;
+#pragma unroll
+    for (int d = 0; d < K2_E - 1; ++d) {  // y columns dc0 .. dc0 + 6 (column c = 0's lags but the last)
+      const float2 v = y[min(dc0 + d, K2_L - 1)];
+      vr[d] = v.x;
+      vi[d] = v.y;
+    }
+    for (int c0 = 0; c0 <= M - Q; c0 += K2_E) {
+#pragma unroll
+      for (int cc = 0; cc < K2_E; ++cc) {
+        const int c = c0 + cc;
+        float2 xv = x[min(c, K2_L - 1)];
+        if (c > M - Q) xv = make_float2(0.f, 0.f);
+        const float2 yn = y[min(c + dc0 + K2_E - 1, K2_L - 1)];  // (columns past M are zero)
+        vr[(cc + K2_E - 1) % K2_E] = yn.x;
+        vi[(cc + K2_E - 1) % K2_E] = yn.y;
+#pragma unroll
+        for (int d = 0; d < K2_E; ++d) {
+          const int sl_ = (cc + d) % K2_E;  // column c + dc0 + d
+          cr[d] = fmaf(xv.x, vr[sl_], cr[d]);
+          ci[d] = fmaf(xv.y, vr[sl_], ci[d]);
+          cr[d] = fmaf(xv.y, vi[sl_], cr[d]);
+          ci[d] = fmaf(-xv.x, vi[sl_], ci[d]);
+        }
+      }
+    }
+    const int i = min(i1, i2);
+#pragma unroll
+    for (int d = 0; d < K2_E; ++d) {
+      const int dc = dc0 + d;
+      if (dc >= Q || !in_uc(dr, dc, P, Q)) continue;
+      const int slot = cls_slot[class_index(dr, dc, P, Q)];
+      if (slot < 0) continue;
+      const ClassDesc& cd = cls[slot];
+      const int k = strip ? (cd.pv - 1) + i : i;
+      rc[(long long)b * tot_rc + cd.rc_off + k] = make_double2((double)cr[d], (double)ci[d]);
     }
   }
 }
