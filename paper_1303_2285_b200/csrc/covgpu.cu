@@ -173,6 +173,10 @@ struct covgpu_plan {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_h2d = nullptr;
   cudaEvent_t ev_strips = nullptr;  // spectral host path: edge columns + strip rows copied
+  // spectral host path: one event per row band of A (recorded between the band
+  // copies — unlike a stream memory operation it leaves no gap between two
+  // DMA transfers: 16 bands x ~7 us at cfg5)
+  std::vector<cudaEvent_t> ev_band;
   bool use_erm = false;
   int erm_dct = 1;
   const void* erm_ptr = nullptr;
@@ -386,6 +390,9 @@ void plan_free(covgpu_plan* pl) {
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->ev_h2d) cudaEventDestroy(pl->ev_h2d);
   if (pl->ev_strips) cudaEventDestroy(pl->ev_strips);
+  for (cudaEvent_t e : pl->ev_band)
+    if (e) cudaEventDestroy(e);
+  pl->ev_band.clear();
   cudaFree(pl->d_ecm_tickets);
   if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
   if (pl->ev_done) cudaEventDestroy(pl->ev_done);
@@ -961,8 +968,11 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     auto fft_upto = [&](int m) {  // rows of bands [fft_done, m] outside the strips
       for (; fft_done <= m && fft_done < nb; ++fft_done) {
         const int k = fft_done, r0 = std::max(S, k * br), r1 = std::min(N - S, (k + 1) * br);
-        stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
-                            CU_STREAM_WAIT_VALUE_GEQ);
+        if (k < (int)pl->ev_band.size() && pl->ev_band[k])
+          cudaStreamWaitEvent(st, pl->ev_band[k], 0);
+        else
+          stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
+                              CU_STREAM_WAIT_VALUE_GEQ);
         if (r1 <= r0) continue;
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
                   pl->d_fx, pl->d_fy, r0, r1 - r0);
@@ -2829,8 +2839,14 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
         CUDA_TRY(cudaMemcpyAsync(dA + r0 * row_bytes, hA + r0 * row_bytes, (r1 - r0) * row_bytes,
                                  cudaMemcpyHostToDevice, pl->copy_stream));
       }
-      if (wv(pl->copy_stream, (CUdeviceptr)pl->d_band_flag, base + (unsigned)k + 1u, 0) != CUDA_SUCCESS)
+      if (strips_first) {
+        // the spectral path waits per band on the host side: an event per band
+        if ((int)pl->ev_band.size() < nb) pl->ev_band.resize(nb, nullptr);
+        if (!pl->ev_band[k]) CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_band[k], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(pl->ev_band[k], pl->copy_stream));
+      } else if (wv(pl->copy_stream, (CUdeviceptr)pl->d_band_flag, base + (unsigned)k + 1u, 0) != CUDA_SUCCESS) {
         return fail(COVGPU_ECUDA, "cuStreamWriteValue32");
+      }
     }
     CUDA_TRY(cudaEventRecord(pl->ev_h2d, pl->copy_stream));
     pl->band_wait = true;
@@ -2893,8 +2909,8 @@ static bool chunked_copy_out(covgpu_plan* pl, int layout) {
   // small first chunks: the copy-out starts early (the first rows are the longest)
   const int Q = pl->pr.Q;
   pl->fin_ubound[0] = 0;
-  pl->fin_ubound[1] = std::max(1, Q / 16);
-  pl->fin_ubound[2] = std::max(pl->fin_ubound[1] + 1, Q / 4);
+  pl->fin_ubound[1] = std::max(1, Q / 32);
+  pl->fin_ubound[2] = std::max(pl->fin_ubound[1] + 1, Q / 6);
   pl->fin_ubound[3] = Q;
   pl->fin_nchunks = 3;
   return true;
