@@ -1098,11 +1098,21 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     // blocked short-lag correlation (edgeblk.cuh) on the side stream: reads
     // only A's strips.  Timing names: spec_ccol = column strips, spec_rc = row strips
     mark("spec_dft");
-    launch_edges_blocked<T>(pl, A, es, true, part, nparts);
-    mark("spec_ccol");
-    launch_edges_blocked<T>(pl, A, es, false, part, nparts);
+    if (band_mode) {
+      // host path: the strip rows arrived first, the edge columns are complete
+      // only with the last band of A
+      launch_edges_blocked<T>(pl, A, es, false, part, nparts);
+      CUDA_TRY_V(cudaStreamWaitEvent(es, pl->ev_h2d, 0));
+      launch_edges_blocked<T>(pl, A, es, true, part, nparts);
+      mark("spec_ccol");
+    } else {
+      launch_edges_blocked<T>(pl, A, es, true, part, nparts);
+      mark("spec_ccol");
+      launch_edges_blocked<T>(pl, A, es, false, part, nparts);
+    }
   } else if (pl->spec_edges) {
     mark("spec_dft");
+    if (band_mode) CUDA_TRY_V(cudaStreamWaitEvent(es, pl->ev_h2d, 0));  // (edge columns of every row)
     {
       cudaStream_t st_main = st;
       st = es;  // SPEC_LOGL launches on `st`
@@ -2802,27 +2812,21 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
     auto wv = stream_write_value();
     const unsigned base = pl->band_base;
     const bool strips_first = pl->use_spec && pl->batch == 1;
-    const int S = pr.P - 1, Sc = pr.Q - 1;
+    const int S = pr.P - 1;
     char* dA = (char*)pl->hA;
     const char* hA = (const char*)A_host;
-    const size_t mid0 = (size_t)Sc * esz, midw = (size_t)(pr.M - 2 * Sc) * esz;
     if (strips_first) {
-      // spectral engine: the edge columns (all rows) and the top / bottom strip
-      // rows first — the edge sums need only these — then the other rows' middle
-      // columns in bands
+      // spectral engine: the top / bottom strip rows first (whole rows, two
+      // contiguous copies) — the edge-row sums, the strip-row spectra and the
+      // walk's corner blocks need only these — then the other rows in bands
+      // of whole rows (contiguous copies at the full link rate; the
+      // edge-column sums wait for the last band and run beside the last
+      // band's correlation)
       if (!pl->ev_strips) CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_strips, cudaEventDisableTiming));
-      if (Sc > 0) {
-        CUDA_TRY(cudaMemcpy2DAsync(dA, row_bytes, hA, row_bytes, (size_t)Sc * esz, pr.N, cudaMemcpyHostToDevice,
-                                   pl->copy_stream));
-        CUDA_TRY(cudaMemcpy2DAsync(dA + (size_t)(pr.M - Sc) * esz, row_bytes, hA + (size_t)(pr.M - Sc) * esz,
-                                   row_bytes, (size_t)Sc * esz, pr.N, cudaMemcpyHostToDevice, pl->copy_stream));
-      }
-      if (S > 0 && midw > 0) {
-        CUDA_TRY(cudaMemcpy2DAsync(dA + mid0, row_bytes, hA + mid0, row_bytes, midw, S, cudaMemcpyHostToDevice,
-                                   pl->copy_stream));
-        CUDA_TRY(cudaMemcpy2DAsync(dA + (size_t)(pr.N - S) * row_bytes + mid0, row_bytes,
-                                   hA + (size_t)(pr.N - S) * row_bytes + mid0, row_bytes, midw, S,
-                                   cudaMemcpyHostToDevice, pl->copy_stream));
+      if (S > 0) {
+        CUDA_TRY(cudaMemcpyAsync(dA, hA, (size_t)S * row_bytes, cudaMemcpyHostToDevice, pl->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(dA + (size_t)(pr.N - S) * row_bytes, hA + (size_t)(pr.N - S) * row_bytes,
+                                 (size_t)S * row_bytes, cudaMemcpyHostToDevice, pl->copy_stream));
       }
       CUDA_TRY(cudaEventRecord(pl->ev_strips, pl->copy_stream));
     }
@@ -2831,14 +2835,10 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
       if (strips_first) {
         r0 = std::max(r0, S);
         r1 = std::min(r1, pr.N - S);
-        if (r1 > r0 && midw > 0)
-          CUDA_TRY(cudaMemcpy2DAsync(dA + (size_t)r0 * row_bytes + mid0, row_bytes,
-                                     hA + (size_t)r0 * row_bytes + mid0, row_bytes, midw, r1 - r0,
-                                     cudaMemcpyHostToDevice, pl->copy_stream));
-      } else {
+      }
+      if (r1 > r0)
         CUDA_TRY(cudaMemcpyAsync(dA + r0 * row_bytes, hA + r0 * row_bytes, (r1 - r0) * row_bytes,
                                  cudaMemcpyHostToDevice, pl->copy_stream));
-      }
       if (strips_first) {
         // the spectral path waits per band on the host side: an event per band
         if ((int)pl->ev_band.size() < nb) pl->ev_band.resize(nb, nullptr);
