@@ -2782,7 +2782,13 @@ int covgpu_plan_execute_host(covgpu_plan_t pl, const void* A_host, void* R_host,
   const size_t r_bytes = (size_t)r_elems * esz;
   std::lock_guard<std::mutex> lk(pl->host_mu);
   if (pl->batch >= 8) return execute_host_pipelined(pl, A_host, R_host, layout, scale);
-  if (!pl->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->host_stream, cudaStreamNonBlocking));
+  if (!pl->host_stream) {
+    // greatest priority: in the tail after the last band of A the main chain
+    // (last correlation, output FFTs, walk) goes before the side stream's edge sums
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CUDA_TRY(cudaStreamCreateWithPriority(&pl->host_stream, cudaStreamNonBlocking, hi));
+  }
   if (pl->hA_bytes < a_bytes) {
     cudaFree(pl->hA);
     pl->hA = nullptr;
@@ -2956,7 +2962,13 @@ int covgpu_plan_execute_host_async(covgpu_plan_t pl, const void* A_host, void* R
     r_elems = pl->batch * pl->compact_elems;
   const size_t r_bytes = (size_t)r_elems * esz;
   std::lock_guard<std::mutex> lk(pl->host_mu);
-  if (!pl->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->host_stream, cudaStreamNonBlocking));
+  if (!pl->host_stream) {
+    // greatest priority: in the tail after the last band of A the main chain
+    // (last correlation, output FFTs, walk) goes before the side stream's edge sums
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CUDA_TRY(cudaStreamCreateWithPriority(&pl->host_stream, cudaStreamNonBlocking, hi));
+  }
   if (!pl->as_in) {
     CUDA_TRY(cudaStreamCreateWithFlags(&pl->as_in, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&pl->as_out, cudaStreamNonBlocking));
