@@ -92,6 +92,12 @@ int64_t covgpu_plan_workspace_bytes(covgpu_plan_t plan);
 int32_t covgpu_plan_num_groups(covgpu_plan_t plan);
 int32_t covgpu_plan_launches(covgpu_plan_t plan);
 
+/* Environment: the library reads no configuration from the environment.  The
+ * COVGPU_* switches in csrc/covgpu.cu (engine forcing and kernel variants for
+ * the parity tests and for the comparison runs of bench.py) are test hooks,
+ * honoured only when COVGPU_TEST_HOOKS=1 is set before the first plan is made;
+ * cached plans are keyed on them. */
+
 /* Which sum kernels the plan runs (bit flags): COVGPU_PATH_SPECTRAL — the
  * core / edge sums in the frequency domain (row and column FFTs, per-frequency
  * row-lag correlation); COVGPU_PATH_TENSOR — the core sums as Toeplitz GEMMs

@@ -17,6 +17,7 @@ cap() {  # name regex count cfg
 }
 cap r02_ncu_fin_cfg5_$V k_fin_tile 3 cfg5
 cap r02_ncu_corr_cfg5_$V k_spec_corr_smem 1 cfg5
-cap r02_ncu_bulk_cfg4_$V k_bulk_tma 1 cfg4
+cap r02_ncu_snap_cfg4_$V k_snap_spec 1 cfg4
 cap r02_ncu_eb_cfg5_$V k_eb_pairs 2 cfg5
+python tools/e2e_timeline.py cfg5 > gpurun_out/r02_e2e_timeline_cfg5_$V.txt 2>&1
 ls gpurun_out | grep $V
