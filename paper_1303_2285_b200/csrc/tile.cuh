@@ -82,9 +82,14 @@ inline int ft_ckstep(int P, int Q) {
 // Corner blocks per (snapshot, column j of the (Q-1)-column strips), widened
 // to double, in the layout one step's SMEM copy takes as is: first operands
 // TL, TR, BL, BR ([PP] each: rows [0, P-1) of A's top / bottom strip, zero
-// beyond), then second operands TL, TR, BL, BR ([2P] each: the P-1 strip rows
-// and a zero, twice — index (r1 + c) mod P then needs no wrap).
-__host__ __device__ inline int ft_colw(int P, int PP) { return 4 * PP + 8 * P; }
+// beyond), then second operands TL, TR, BL, BR ([2 PP] each: the P-1 strip
+// rows and a zero, twice — index (r1 + c) mod P then needs no wrap — zero
+// beyond 2P; the block strides depend on the instantiation only, so every
+// SMEM offset of the walk is a compile-time constant).
+__host__ __device__ inline int ft_colw(int P, int PP) {
+  (void)P;
+  return 12 * PP;
+}
 
 // SMEM per unit: strip vectors [2 bufs][subs][colw + 8] double2 (8 zeros of
 // slack: rows past P read in range), row-group totals [2 bufs][T1, B1, T2,
@@ -166,8 +171,9 @@ __global__ void k_corners_d(const typename CT<T>::c* __restrict__ A, Problem pr,
     blk = x / PP;
     i = x % PP;
   } else {
-    blk = (x - 4 * PP) / (2 * P);
-    i = (x - 4 * PP) % (2 * P) % P;
+    blk = (x - 4 * PP) / (2 * PP);
+    i = (x - 4 * PP) % (2 * PP);
+    i = i < 2 * P ? i % P : S;  // (beyond the doubled strip: zero)
   }
   double2 v = make_double2(0.0, 0.0);
   if (i < S) {
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
   const int e0 = max(u_lo, u_begin), e1 = min(u_hi, u_end);
   if (e0 >= e1) return;
   const bool resume = e0 > u_lo;
-  const int cw = ft_colw(P, PP), vstride = (int)ft_vec_elems(P, PP);
+  constexpr int cw = 12 * PP, vstride = cw + 8;  // ft_colw, ft_vec_elems
   unsigned char* sb = ft_smem + (size_t)us * ft_unit_smem(P, NWARP, SUBS, sizeof(C2));
   double2* const vec = (double2*)sb;
   double2* const tot0 = (double2*)(sb + ft_vec_bytes(P, NWARP, SUBS));
@@ -384,12 +390,13 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
   };
   int u = e0;
   prefetch(u, u & 1);
+  const double2* const vbase = vec + sub * vstride + r0;  // this thread's rows of buffer 0
 
   const long long D = pr.PQ;
   C2* const Rb = R + (long long)bs * r_bstride;
   const bool zero_im = dc == 0 && c == 0;  // class (0,0): R's real main diagonal (rows < bnd = P)
   const long long ostep = (long long)P * (D + 1);  // block (u, u+dc) -> (u+1, u+1+dc)
-  const int P2 = 2 * P;
+  constexpr int P2 = 2 * PP;  // stride of the second-operand blocks
   // rows k >= kb of this thread belong to segment 2 (the second class; the
   // block column wraps from P-1 to 0 there).  wstr: some lane of the warp
   // holds rows of both segments (a function of the geometry only)
@@ -537,8 +544,8 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
     mrowp += ostep;
     if (u < ac) {
       // every row (no guards): rows and entries outside the strip read zeros
-      const double2* va = vec + (buf * SUBS + sub) * vstride + r0;
-      const double2* vq = vec + (buf * SUBS + sub) * vstride + 4 * PP + r2_0;
+      const double2* va = vbase + buf * (SUBS * vstride);
+      const double2* vq = va + (4 * PP - r0) + r2_0;
 #pragma unroll
       for (int k = 0; k < FT_RPT; ++k) {
         ft_rank2(fT[k], va[PP + k], vq[P2 + k], va[k], vq[k]);
