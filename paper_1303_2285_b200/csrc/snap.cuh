@@ -11,19 +11,22 @@
 //     CC(dr, dc) = (1/L) FFT_128(G(dr, .))[dc]
 // for all 2P-1 <= 15 row lags at once (P <= 8, M <= 128, Q <= 16).
 //
-// CTA = one snapshot, 256 threads.  Rows go through in chunks of 8:
-//   transform phase: 16 groups of 16 threads, group g -> X (g < 8) or Y of row
-//     8 j + (g & 7): the row is read from global memory once per transform
-//     (coalesced), radix-8 x radix-8 x radix-2 Stockham passes in place in the
-//     destination row of the X ring (4 chunks) / Y ring (2 chunks);
+// CTA = one snapshot, 256 threads.  Rows go through in chunks of 16:
+//   transform phase: 16 groups of 16 threads, group g -> row 16 j + g, read
+//     from global memory once (coalesced; the next chunk's row is prefetched
+//     under the correlation) and transformed twice — X and Y, the two masked
+//     versions, pass by pass together: radix-8 x radix-8 x radix-2 Stockham
+//     passes in place in the destination rows of the X ring (3 chunks) / Y
+//     ring (2 chunks);
 //   correlation phase for the Y rows of chunk j-1 (their X rows r2 - dr lie in
 //     chunks j-2 .. j): thread = (frequency f, lag sign), 8 lags in registers.
 // After the last chunk the G rows are transformed in place (one group per
 // lag) and the first Q outputs go to the plan's CC array (one partial per
 // class); finally the edge-column sums CCol (core rows x the Q-1 edge columns
 // of each side: correlations of pairs of strip columns along the rows, one
-// pair per thread, the 15 lags in a rotating register window) come straight
-// from the strips staged in shared memory at the start.
+// pair per thread, the 15 lags in a rotating register window) and the
+// edge-row sums RC' (ordered strip-row pairs x column lags) come from the
+// strips, staged in the rings' shared memory once the core sums are done.
 // FP32 arithmetic throughout (complex64 bar: 1e-5 relative Frobenius; measured
 // ~1e-6); every sum has a fixed order, nothing depends on the batch size.
 #pragma once
@@ -36,17 +39,20 @@ namespace covgpu {
 
 constexpr int K2_L = 128;          // FFT length (M <= 128)
 constexpr int K2_RS = 144;         // SMEM row stride: 128 + one pad per 8
-constexpr int K2_CH = 8;           // rows per chunk
-constexpr int K2_XR = 4 * K2_CH;   // X ring rows
+constexpr int K2_CH = 16;          // rows per chunk (one row per 16-thread group: its X and its Y transform)
+constexpr int K2_XR = 3 * K2_CH;   // X ring rows (chunks j-2 .. j)
 constexpr int K2_E = 8;            // lags per correlation thread
 constexpr int K2_W = 2 * K2_E - 1; // lag window of the edge-column pairs
 constexpr int K2_MAXQ = 16;
 constexpr int K2_THREADS = 256;
 
 constexpr int K2_ERS = 129;        // strip-row stride (odd: the strip's rows fall in distinct banks)
+// twiddles + max(the rings of the core sums, the strips of the edge sums staged
+// in the same memory afterwards)
 __host__ __device__ inline size_t k2_smem_bytes(int N, int P, int Q) {
-  return sizeof(float2) * ((size_t)(K2_XR + 2 * K2_CH) * K2_RS + (size_t)2 * N * (Q - 1) + 64 + 64 +
-                           (size_t)2 * (P - 1) * K2_ERS);
+  const size_t rings = (size_t)(K2_XR + 2 * K2_CH) * K2_RS;
+  const size_t strips = (size_t)2 * N * (Q - 1) + (size_t)2 * (P - 1) * K2_ERS;
+  return sizeof(float2) * (128 + (rings > strips ? rings : strips));
 }
 
 __device__ __forceinline__ int k2_pad(int i) { return i + (i >> 3); }
@@ -122,19 +128,74 @@ __device__ __forceinline__ void k2_fft128(float2* u, float2* row, int tl, const 
   __syncwarp();
 }
 
+// Two transforms by the same 16 threads, pass by pass (twice the independent
+// work between the warp barriers)
+__device__ __forceinline__ void k2_fft128x2(float2* u, float2* v, float2* rowu, float2* rowv, int tl,
+                                            const float2* tw64, const float2* tw128) {
+  k2_dft8(u);
+  k2_dft8(v);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    rowu[k2_pad(8 * tl + r)] = u[r];
+    rowv[k2_pad(8 * tl + r)] = v[r];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    u[r] = rowu[k2_pad(tl + 16 * r)];
+    v[r] = rowv[k2_pad(tl + 16 * r)];
+  }
+  __syncwarp();
+  const int k = tl & 7;
+#pragma unroll
+  for (int r = 1; r < 8; ++r) {
+    const float2 w = tw64[r * k];
+    u[r] = k2_mul(u[r], w);
+    v[r] = k2_mul(v[r], w);
+  }
+  k2_dft8(u);
+  k2_dft8(v);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    rowu[k2_pad((tl - k) * 8 + k + 8 * r)] = u[r];
+    rowv[k2_pad((tl - k) * 8 + k + 8 * r)] = v[r];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int i = tl + 16 * it;
+    const float2 w = tw128[i];
+    u[2 * it] = rowu[k2_pad(i)];
+    u[2 * it + 1] = k2_mul(rowu[k2_pad(i + 64)], w);
+    v[2 * it] = rowv[k2_pad(i)];
+    v[2 * it + 1] = k2_mul(rowv[k2_pad(i + 64)], w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int i = tl + 16 * it;
+    rowu[k2_pad(i)] = k2_add(u[2 * it], u[2 * it + 1]);
+    rowu[k2_pad(i + 64)] = k2_sub(u[2 * it], u[2 * it + 1]);
+    rowv[k2_pad(i)] = k2_add(v[2 * it], v[2 * it + 1]);
+    rowv[k2_pad(i + 64)] = k2_sub(v[2 * it], v[2 * it + 1]);
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(K2_THREADS, 2)
     k_snap_spec(const float2* __restrict__ A, Problem pr, int B, int nclasses, const int* __restrict__ cls_slot,
                 const ClassDesc* __restrict__ cls, double2* __restrict__ ccpart, double2* __restrict__ ccol,
                 long long tot_ccol, double2* __restrict__ rc, long long tot_rc) {
   extern __shared__ __align__(16) unsigned char k2raw[];
   const int N = pr.N, M = pr.M, P = pr.P, Q = pr.Q, S1 = Q - 1;
-  float2* const xr = reinterpret_cast<float2*>(k2raw);           // X ring [K2_XR][K2_RS]
-  float2* const yr = xr + K2_XR * K2_RS;                         // Y ring [2][K2_CH][K2_RS]
-  float2* const sl = yr + 2 * K2_CH * K2_RS;                     // left strip [N][Q-1]
-  float2* const sr = sl + (size_t)N * S1;                        // right strip [N][Q-1]
-  float2* const tw64 = sr + (size_t)N * S1;                      // w_64^k
+  float2* const tw64 = reinterpret_cast<float2*>(k2raw);         // w_64^k
   float2* const tw128 = tw64 + 64;                               // w_128^k, k < 64
-  float2* const er = tw128 + 64;                                 // strip rows [2][P-1][K2_ERS] (edge-row sums)
+  float2* const xr = tw128 + 64;                                 // X ring [K2_XR][K2_RS]
+  float2* const yr = xr + K2_XR * K2_RS;                         // Y ring [2][K2_CH][K2_RS]
+  // (after the core sums, in the rings' memory:)
+  float2* const sl = xr;                                         // left strip [N][Q-1]
+  float2* const sr = sl + (size_t)N * S1;                        // right strip [N][Q-1]
+  float2* const er = sr + (size_t)N * S1;                        // strip rows [2][P-1][K2_ERS] (edge-row sums)
   const int S = P - 1;
   const int t = threadIdx.x, b = blockIdx.x;
   const float2* Ab = A + (long long)b * N * M;
@@ -145,18 +206,6 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
     tw64[t] = make_float2(c, s);
     sincospif(-(float)t / 64.f, &s, &c);
     tw128[t] = make_float2(c, s);
-  }
-  // the strips (edge-column sums): columns [0, Q-1) and [M-Q+1, M) of every row
-  for (int i = t; i < N * S1; i += K2_THREADS) {
-    const int r = i / S1, j = i - r * S1;
-    sl[i] = Ab[(long long)r * M + j];
-    sr[i] = Ab[(long long)r * M + (M - S1) + j];
-  }
-  // the top / bottom P-1 strip rows (edge-row sums), zero beyond column M
-  for (int i = t; i < 2 * S * K2_L; i += K2_THREADS) {
-    const int row = i / K2_L, c = i - row * K2_L;
-    const int ra = row < S ? row : N - S + (row - S);
-    er[row * K2_ERS + c] = c < M ? Ab[(long long)ra * M + c] : make_float2(0.f, 0.f);
   }
   __syncthreads();
 
@@ -177,27 +226,27 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
 #pragma unroll
   for (int e = 0; e < K2_E; ++e) wr[e] = wi[e] = 0.f;
   const float2* const xb = xr + k2_pad(f);
-  // this group's transform of chunk j: the row's 8 inputs per thread, masked
-  // (x: first-element columns c <= M-Q; y: second-element columns c >= Q-1)
-  const bool isy = grp >= 8;
+  // this group's row of chunk j: 8 inputs per thread (both transforms mask them)
   auto load_row = [&](int j, float2* u) {
-    const int row = j * K2_CH + (grp & 7);
+    const int row = j * K2_CH + grp;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int c = tl + 16 * r;
-      const bool on = j < nchunks && row < N && c < M && (isy ? c >= Q - 1 : c <= M - Q);
-      u[r] = on ? Ab[(long long)row * M + c] : make_float2(0.f, 0.f);
+      u[r] = (j < nchunks && row < N && c < M) ? Ab[(long long)row * M + c] : make_float2(0.f, 0.f);
     }
   };
   auto corr = [&](auto hs, int jc) {
     constexpr int H = decltype(hs)::value;
     const float2* yb = yr + (jc & 1) * K2_CH * K2_RS + k2_pad(f);
+    int rslot = (jc * K2_CH + (H ? 0 : K2_E)) % K2_XR;  // ring slot of the entering row
 #pragma unroll
-    for (int tt = 0; tt < K2_CH; ++tt) {
-      const int r2 = jc * K2_CH + tt;
+    for (int t2 = 0; t2 < K2_CH; ++t2) {
+      const int tt = t2 % K2_E;
+      const int r2 = jc * K2_CH + t2;
       const int rin = H ? r2 : r2 + K2_E;  // the row entering the window (slot tt either way)
-      float2 x = xb[(rin & (K2_XR - 1)) * K2_RS];
-      float2 y = yb[tt * K2_RS];
+      float2 x = xb[rslot * K2_RS];
+      rslot = rslot + 1 == K2_XR ? 0 : rslot + 1;
+      float2 y = yb[t2 * K2_RS];
       if (H ? rin > N - P : (rin < P - 1 || rin >= N)) x = make_float2(0.f, 0.f);
       if (H ? (r2 < P - 1 || r2 >= N) : r2 > N - P) y = make_float2(0.f, 0.f);
       wr[tt] = x.x;
@@ -217,9 +266,16 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
   load_row(0, u);
   for (int j = 0; j <= nchunks; ++j) {
     if (j < nchunks) {
-      const int row = j * K2_CH + (grp & 7);
-      float2* dst = isy ? yr + ((j & 1) * K2_CH + (grp & 7)) * K2_RS : xr + (row & (K2_XR - 1)) * K2_RS;
-      k2_fft128(u, dst, tl, tw64, tw128);
+      const int row = j * K2_CH + grp;
+      // x: first-element columns c <= M-Q; y: second-element columns c >= Q-1
+      float2 v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int c = tl + 16 * r;
+        v[r] = c >= Q - 1 ? u[r] : make_float2(0.f, 0.f);
+        if (c > M - Q) u[r] = make_float2(0.f, 0.f);
+      }
+      k2_fft128x2(u, v, xr + (row % K2_XR) * K2_RS, yr + ((j & 1) * K2_CH + grp) * K2_RS, tl, tw64, tw128);
     }
     load_row(j + 1, u);  // the next chunk's row: its latency hides under the correlation
     __syncthreads();
@@ -227,10 +283,10 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
       // half 0's window before r2 = 0: rows 1 .. 7 (row 8 enters at r2 = 0)
 #pragma unroll
       for (int x = 1; x < K2_E; ++x) {
-        float2 v = xb[x * K2_RS];
-        if (x < P - 1 || x >= N) v = make_float2(0.f, 0.f);
-        wr[x] = v.x;
-        wi[x] = v.y;
+        float2 w = xb[x * K2_RS];
+        if (x < P - 1 || x >= N) w = make_float2(0.f, 0.f);
+        wr[x] = w.x;
+        wi[x] = w.y;
       }
     }
     if (j >= 1) {
@@ -269,6 +325,21 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
     }
   }
 
+  // ---- the strips of the edge sums, staged in the rings' memory -------------
+  __syncthreads();  // (the G rows are read)
+  // columns [0, Q-1) and [M-Q+1, M) of every row: thread = (row mod 16, column)
+  if (tl < S1)
+    for (int r = grp; r < N; r += 16) {
+      sl[r * S1 + tl] = Ab[(long long)r * M + tl];
+      sr[r * S1 + tl] = Ab[(long long)r * M + (M - S1) + tl];
+    }
+  // the top / bottom P-1 strip rows, zero beyond column M
+  for (int row = t >> 7; row < 2 * S; row += 2) {
+    const int c = t & 127, ra = row < S ? row : N - S + (row - S);
+    er[row * K2_ERS + c] = c < M ? Ab[(long long)ra * M + c] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+
   // ---- edge-column sums: pairs (j1 <= j2) of one strip's columns ------------
   const int npairs = S1 * (S1 + 1) / 2;
   for (int item = t; item < 2 * npairs; item += K2_THREADS) {
@@ -296,21 +367,36 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
         wi[x] = v.y;
       }
     }
-    for (int r2base = 0; r2base < N; r2base += K2_W) {
+    // one block of K2_W rows; interior blocks (every row and every entering
+    // row valid for both lag signs, the window already holding actual values)
+    // run without masks and without the re-mask load
+    auto block = [&](auto masked, int r2base) {
+      constexpr bool MASK = decltype(masked)::value;
+      const float2* px = st + (r2base + K2_E - 1) * S1 + j1;
+      const float2* py = st + r2base * S1 + j2;
 #pragma unroll
       for (int tt = 0; tt < K2_W; ++tt) {
-        const int r2 = r2base + tt, rin = r2 + K2_E - 1;
-        float2 xin = make_float2(0.f, 0.f), xc = xin, y = xin;
-        if (rin < N && rin >= P - 1) xin = st[rin * S1 + j1];
-        if (r2 <= N - P) xc = st[r2 * S1 + j1];
-        if (r2 < N) y = st[r2 * S1 + j2];
-        wr[(tt + K2_E - 1) % K2_W] = xin.x;
-        wi[(tt + K2_E - 1) % K2_W] = xin.y;
-        wr[tt] = xc.x;
-        wi[tt] = xc.y;
-        // second-element row masks: lags >= 0 need r2 >= P-1, lags < 0 need r2 <= N-P
-        const float ypx = r2 >= P - 1 ? y.x : 0.f, ypy = r2 >= P - 1 ? y.y : 0.f;
-        const float ynx = r2 <= N - P ? y.x : 0.f, yny = r2 <= N - P ? y.y : 0.f;
+        float ypx, ypy, ynx, yny;
+        if constexpr (MASK) {
+          const int r2 = r2base + tt, rin = r2 + K2_E - 1;
+          float2 xin = make_float2(0.f, 0.f), xc = xin, y = xin;
+          if (rin < N && rin >= P - 1) xin = px[tt * S1];
+          if (r2 <= N - P) xc = st[r2 * S1 + j1];
+          if (r2 < N) y = py[tt * S1];
+          wr[(tt + K2_E - 1) % K2_W] = xin.x;
+          wi[(tt + K2_E - 1) % K2_W] = xin.y;
+          wr[tt] = xc.x;
+          wi[tt] = xc.y;
+          // second-element row masks: lags >= 0 need r2 >= P-1, lags < 0 need r2 <= N-P
+          ypx = r2 >= P - 1 ? y.x : 0.f, ypy = r2 >= P - 1 ? y.y : 0.f;
+          ynx = r2 <= N - P ? y.x : 0.f, yny = r2 <= N - P ? y.y : 0.f;
+        } else {
+          const float2 xin = px[tt * S1], y = py[tt * S1];
+          wr[(tt + K2_E - 1) % K2_W] = xin.x;
+          wi[(tt + K2_E - 1) % K2_W] = xin.y;
+          ypx = ynx = y.x;
+          ypy = yny = y.y;
+        }
 #pragma unroll
         for (int e = 0; e < K2_W; ++e) {
           const int dr = e - (K2_E - 1);
@@ -322,6 +408,14 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
           ci[e] = fmaf(-wr[s], yy, ci[e]);
         }
       }
+    };
+    for (int r2base = 0; r2base < N; r2base += K2_W) {
+      // interior: rows r2 in [P-1, N-P] and entering rows r2 + 7 < N throughout
+      // (entering rows >= P-1 follows; rows behind r2 were re-masked in range)
+      if (r2base >= P - 1 + K2_E - 1 && r2base + K2_W - 1 + K2_E - 1 <= N - P)
+        block(std::false_type{}, r2base);
+      else
+        block(std::true_type{}, r2base);
     }
 #pragma unroll
     for (int e = 0; e < K2_W; ++e) {
@@ -354,13 +448,20 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
       vr[d] = v.x;
       vi[d] = v.y;
     }
-    for (int c0 = 0; c0 <= M - Q; c0 += K2_E) {
+    auto cols = [&](auto masked, int c0) {
+      constexpr bool MASK = decltype(masked)::value;
 #pragma unroll
       for (int cc = 0; cc < K2_E; ++cc) {
         const int c = c0 + cc;
-        float2 xv = x[min(c, K2_L - 1)];
-        if (c > M - Q) xv = make_float2(0.f, 0.f);
-        const float2 yn = y[min(c + dc0 + K2_E - 1, K2_L - 1)];  // (columns past M are zero)
+        float2 xv, yn;
+        if constexpr (MASK) {
+          xv = x[min(c, K2_L - 1)];
+          if (c > M - Q) xv = make_float2(0.f, 0.f);
+          yn = y[min(c + dc0 + K2_E - 1, K2_L - 1)];  // (columns past M are zero)
+        } else {
+          xv = x[c];
+          yn = y[c + dc0 + K2_E - 1];
+        }
         vr[(cc + K2_E - 1) % K2_E] = yn.x;
         vi[(cc + K2_E - 1) % K2_E] = yn.y;
 #pragma unroll
@@ -372,6 +473,12 @@ __global__ void __launch_bounds__(K2_THREADS, 2)
           ci[d] = fmaf(-xv.x, vi[sl_], ci[d]);
         }
       }
+    };
+    for (int c0 = 0; c0 <= M - Q; c0 += K2_E) {
+      if (c0 + K2_E - 1 <= M - Q && c0 + dc0 + 2 * K2_E - 2 < K2_L)
+        cols(std::false_type{}, c0);
+      else
+        cols(std::true_type{}, c0);
     }
     const int i = min(i1, i2);
 #pragma unroll
