@@ -9,24 +9,29 @@ A step = one full estimate of R for the configured workload (default cfg5:
 GPU).  `value` is dense R entries per second with A resident in HBM; every
 step is bracketed by a barrier and device syncs, timed with CUDA events on the
 launch stream, and L2 is flushed (256 MiB write) between steps.  Under
-torchrun the sums are split into row bands (spectral / tensor-core plans:
-one all-reduce of the per-band sums, class-range finalize) or the offset
-classes are sharded (strong scaling: total work fixed), A is broadcast from
-rank 0 inside the timed region over NCCL, and the time is the max over ranks.
+torchrun the sums are split into a fixed number of row parts (spectral /
+tensor-core plans: every rank runs its parts on the rows it holds, one
+all-to-all hands each rank the slices its class range needs, the parts are
+added in part order, each rank finalizes its range — R bitwise the same at
+any GPU count) or the offset classes are sharded (strong scaling: total work
+fixed); the time is the max over ranks.
 
 Extra keys: `kernel_ms` / `kernel_roofline` (every kernel's CUDA-event time
-and its own roofline: FP64 kernels against the DFMA / DMMA loop probes
-measured on this GPU right before the run, memory-bound kernels against
+and its own roofline: FP64 / FP32 kernels against the DFMA / FFMA / DMMA loop
+probes measured on this GPU right before the run, memory-bound kernels against
 MEASURED_PEAKS.json's HBM figure, each with its algorithmic flops or bytes),
-`roofline` (the dominant kernel's entry), `tensor_core_path` /
-`cuda_core_path` (the same workload on the other two sum engines),
-`packed_output` (the same step writing the packed upper triangle, the
-reference's own output layout, instead of dense Hermitian R),
-`cpu_baseline` (the oracle's multithreaded
-C port of the reference's class kernel on this host's cores, bounded sample,
-extrapolated by product count), `e2e` (same metric through the C ABI with
-pinned HOST buffers: H2D of A + compute + D2H of the packed triangle, wall
-clock), `clocks` (nvidia-smi sampled during the timed region).
+`roofline` (the dominant kernel's entry; `traffic` = its DRAM bytes per launch
+from the committed ncu capture), `tensor_core_path` / `cuda_core_path` (the
+same workload on the other sum engines), `packed_output` (the same step
+writing the packed upper triangle, the reference's own output layout, instead
+of dense Hermitian R), `cpu_baseline` (the oracle's multithreaded C port of
+the reference's class kernel on this host's cores over the FULL workload — a
+batch: whole snapshots — no extrapolation), `cpu_baseline_stock` (the
+unmodified reference package from baseline/_ref on a bounded sample), `e2e`
+(same metric through the C ABI with pinned HOST buffers: H2D of A + compute +
+D2H of the packed triangle, wall clock, mean of the K calls), `e2e_pipelined`
+(the streaming form, two estimates in flight), `clocks` (nvidia-smi sampled
+during the timed region).
 """
 
 from __future__ import annotations
