@@ -247,7 +247,8 @@ struct covgpu_plan {
   int nev = 0;
   // side stream for the edge-row / corner kernels (overlap with the bulk)
   cudaStream_t side_stream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t delta_stream = nullptr;  // the walk's corner blocks / chunk updates (beside the edge sums)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_djoin = nullptr;
   cudaEvent_t ev_d0 = nullptr;  // spectral: dr = 0 sums (side stream) done
   // end-to-end host path: cached stream and device buffers
   cudaStream_t host_stream = nullptr;
@@ -364,6 +365,8 @@ void plan_free(covgpu_plan* pl) {
     if (e) cudaEventDestroy(e);
   if (pl->host_stream) cudaStreamDestroy(pl->host_stream);
   if (pl->side_stream) cudaStreamDestroy(pl->side_stream);
+  if (pl->delta_stream) cudaStreamDestroy(pl->delta_stream);
+  if (pl->ev_djoin) cudaEventDestroy(pl->ev_djoin);
   if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
   if (pl->ev_join) cudaEventDestroy(pl->ev_join);
   if (pl->ev_d0) cudaEventDestroy(pl->ev_d0);
@@ -1383,21 +1386,30 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   if (pl->band_wait)
     CUDA_TRY(cudaStreamWaitEvent(es, pl->use_spec && pl->batch == 1 ? pl->ev_strips : pl->ev_h2d, 0));
   mark("start");
+  bool dfork = false;
   if (pl->use_tile && !pl->ks_out) {
     // the tile walk's corner blocks and per-chunk state updates need only the
-    // corners of A: first on the side stream, under the sums
+    // corners of A: on a stream of their own, under the sums and beside the
+    // edge sums of the side stream
+    cudaStream_t ds = fork && pl->delta_stream ? pl->delta_stream : es;
+    if (ds != es) {
+      CUDA_TRY(cudaEventRecord(pl->ev_djoin, es));  // (es already follows the fork and the host-path copies)
+      CUDA_TRY(cudaStreamWaitEvent(ds, pl->ev_djoin, 0));
+      dfork = true;
+    }
     const int PP = 8 * pl->ft_nwarp;
     const long long nc = (long long)(pr.Q - 1) * ft_colw(pr.P, PP) * B;
     if (nc > 0) {
-      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, es>>>(A, pr, B, PP, (double2*)pl->d_corners);
+      k_corners_d<T><<<(unsigned)((nc + 255) / 256), 256, 0, ds>>>(A, pr, B, PP, (double2*)pl->d_corners);
       ++launches;
     }
     if (pl->n_dunits > 0) {
       launch_fin_tile<T>(pl, pl->d_dunits, pl->n_dunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0,
-                         COVGPU_DENSE, 0, 1 << 30, nullptr, 0, INT_MAX, es, true);
-      launch_ck_scan(pl, es);
+                         COVGPU_DENSE, 0, 1 << 30, nullptr, 0, INT_MAX, ds, true);
+      launch_ck_scan(pl, ds);
       launches += 2;
     }
+    if (dfork) CUDA_TRY(cudaEventRecord(pl->ev_djoin, ds));
     if (!fork) mark("fin_delta");
   }
   // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
@@ -1490,6 +1502,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     CUDA_TRY(cudaEventRecord(pl->ev_join, es));
     CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
   }
+  if (dfork) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_djoin, 0));
   if (pl->use_tile) {
     // tile finalize straight into the requested layout; u-chunks for the
     // host path (rows [P u0, P u1) of R are complete after a chunk, an event
@@ -2279,7 +2292,15 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
   if (pl->clean) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    // small estimates are launch- / latency-bound chains: the walk's chunk
+    // updates get a stream of their own beside the edge sums (cfg3 0.094 ->
+    // 0.087 ms, cfg2 0.092 -> 0.084); large ones are throughput-bound and lose
+    // ~1 % to the extra concurrency (cfg5 0.463 -> 0.469 ms), so they keep one
+    // side stream
+    const bool small = batch * n * m <= (1LL << 20);
     if (cudaStreamCreateWithPriority(&pl->side_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        (small && cudaStreamCreateWithPriority(&pl->delta_stream, cudaStreamNonBlocking, lo) != cudaSuccess) ||
+        cudaEventCreateWithFlags(&pl->ev_djoin, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&pl->ev_d0, cudaEventDisableTiming) != cudaSuccess) {
