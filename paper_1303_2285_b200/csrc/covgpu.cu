@@ -2043,7 +2043,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     const long long want = 148LL * 32 * 16 * 4;
     const long long len = std::max(1LL, m - 2LL * q + 2);
     long long seg = threads > 0 ? (want + threads - 1) / threads : 1;
-    seg = std::min(seg, std::max(1LL, len / 64));
+    seg = std::min(seg, std::max(1LL, len / 16));  // (short chains: the walk is latency-bound)
     pl->nseg = (int)std::max(1LL, std::min(seg, 16LL));
   }
 
