@@ -771,8 +771,11 @@ std::vector<double2> spec_twiddles(int logL) {
 
 // G partial slots reserved for the banded correlation of the host path
 constexpr int kMaxBandSlots = 32;
-// rows per H2D band of the single-snapshot host path: ~16 bands, >= 64 rows
-int host_band_rows(long long n) { return (int)std::max(64LL, (n + 15) / 16); }
+// rows per H2D band of the single-snapshot host path: ~9 bands, >= 64 rows (the band
+// count is also the correlation's row-segment count: 64 f-blocks x 9 = 576 CTAs
+// = 3.9 waves of 148, and fewer, longer segments than 16 — less per-CTA
+// prologue / epilogue and G partial traffic: cfg5 step 0.463 -> 0.452 ms)
+int host_band_rows(long long n) { return (int)std::max(64LL, (n + 8) / 9); }
 
 // Spectral kernels are instantiated for FFT lengths 2^6 .. 2^12; SPEC_LOGL
 // dispatches a launch on the runtime log2 length (SMEM attribute set once per
