@@ -253,8 +253,9 @@ def bench_config(w, layout: str, world: int = 1, rowband: bool = False, sums_mib
     """The `config` object both arms print (same keys, same values)."""
     return {"workload": w.name, "n": w.n, "m": w.m, "p": w.p, "q": w.q, "batch": w.batch,
             "input": w.dtype, "output": layout, "l2": "flushed between steps (256 MiB write)",
-            "parallelism": (f"row-band x{world}: per-band sums, one all-reduce of [CC|CCol|RC'] "
-                            f"({sums_mib:.1f} MiB), class-range finalize")
+            "parallelism": (f"row parts x{world}: 8 fixed row parts of the sums, one all-to-all of the slices of "
+                            f"[CC|CCol|RC'] each rank's class range reads ({sums_mib:.1f} MiB received per rank), "
+                            f"parts added in order, class-range finalize")
             if rowband else (f"class-shard x{world}" if world > 1 else "single GPU")}
 
 
@@ -338,7 +339,7 @@ def main() -> None:
     win = WindowSpec(w.p, w.q)
     tdt = torch.complex128 if w.dtype == "c128" else torch.complex64
     # N > 1: row bands (every rank on the spectral / tensor-core sums of its
-    # band, one all-reduce of the per-band sums) where the plan supports them,
+    # parts, one all-to-all of the per-part sums' slices) where the plan supports them,
     # else class shards
     plan = Plan(w.n, w.m, win, batch=w.batch, dtype=tdt, device=dev)
     rowband = (world > 1 or args.rowband) and plan.supports_rowband
