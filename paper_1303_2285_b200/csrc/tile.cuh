@@ -24,19 +24,22 @@
 // F_T / F_B of its 8 entries in registers.  Per step u: the row-group totals
 // of both segments meet in SMEM (one unit barrier per step) to give each
 // warp its carries; a warp's store of row r1 covers 32 consecutive columns
-// (mod P) of R's row P u + r1; dense R's mirrored block (u+dc, u) is written
-// one step later from a double-buffered SMEM stage, again as row segments;
-// the strip columns of the next step are prefetched with cp.async.
+// (mod P) of R's row P u + r1 (straight-line stores under a predicate);
+// dense R's mirrored block (u+dc, u) is written from an SMEM stage, again as
+// row segments (units of 2 - 4 warps: double-buffered, one step later; 8
+// warps: one buffer and a second barrier, so two units fit an SM); the strip
+// columns of the next step are prefetched with cp.async.
 //
-// Walks are cut at u = 16 j: the same kernel in DELTA mode adds up each
-// 16-step chunk's updates (from zero; it reads only the corner blocks of A,
-// so it runs first, off the critical path), and a unit starting at u_lo = 16 j
-// takes F(u_lo) = F(0) + delta_1 + ... + delta_j.  Every unit walks <= 16
-// steps and the launch fills the SMs.  The cut grid is a
-// fixed function of u, and every value depends only on its class's sums and
-// the fixed 8-row grouping: class subsets (shards), layouts, batches and
-// u-chunked launches give the same bits; packed R equals dense R's upper
-// triangle bitwise.
+// Walks are cut at u = ck j (ck = 4, 8 or 16 by window size, ft_ckstep): the
+// same kernel in DELTA mode adds up each ck-step chunk's updates (from zero;
+// it reads only the corner blocks of A, so it runs first, off the critical
+// path), k_ck_scan sums them in chunk order, and a unit starting at
+// u_lo = ck j takes F(u_lo) = F(0) + (delta_1 + ... + delta_j).  Every unit
+// walks <= ck steps and the launch fills the SMs.  The cut grid is a fixed
+// function of the window and of u, and every value depends only on its
+// class's sums and the fixed 8-row grouping: class subsets (shards), layouts,
+// batches and u-chunked launches give the same bits; packed R equals dense
+// R's upper triangle bitwise.
 #pragma once
 
 #include <type_traits>
