@@ -228,6 +228,11 @@ __device__ inline void ft_init_entry(int r1, int c, int P, const FtLane& L, cons
   const int v = seg1 ? r1 : r1 - bnd, ar = seg1 ? P - c - 1 : c - 1;
   if (r1 >= P || (seg1 ? L.slot1 : L.slot2) < 0 || v >= ar) return;
   const double2* rcp = rcb + (seg1 ? L.rc1 : L.rc2) * nseg;
+  if (nseg == 1) {  // one column segment: two plain loads (the 8 rows' loads of a thread go out together)
+    fT = rcp[v];
+    fB = rcp[ar + v];
+    return;
+  }
   for (int g = 0; g < nseg; ++g) {
     fT = cadd(fT, rcp[(long long)v * nseg + g]);
     fB = cadd(fB, rcp[(long long)(ar + v) * nseg + g]);
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
         if (L.slot2 >= 0) g2 = cadd(g2, ccpart[((long long)bs * nclasses + L.slot2) * npart + k]);
       }
     }
-#pragma unroll 4
+#pragma unroll 8
     for (int j = w; j < ac; j += NWARP) {
       const int o = j < u_lo ? ac + j : j;
       if (L.slot1 >= 0) g1 = cadd(g1, clb[L.cl1 + o]);
