@@ -123,3 +123,34 @@ def test_plan_cache_survives_eviction_under_threads(cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+def test_env_switches_are_ignored_without_the_test_hook_flag(cuda):
+    """The COVGPU_* switches are test hooks: a process without
+    COVGPU_TEST_HOOKS=1 takes the product path whatever they say."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import torch\n"
+        "from paper_1303_2285_b200 import WindowSpec\n"
+        "from paper_1303_2285_b200.plan import Plan\n"
+        "p = Plan(64, 64, WindowSpec(4, 8), batch=2, dtype=torch.complex64)\n"
+        "q = Plan(300, 300, WindowSpec(8, 8), dtype=torch.complex128)\n"
+        "print(p.path, q.path)\n" % str(root)
+    )
+    env = {k: v for k, v in os.environ.items() if not k.startswith("COVGPU_")}
+    env.update({"COVGPU_NO_SNAP": "1", "COVGPU_SPECTRAL": "1"})
+    plain = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert plain.returncode == 0, plain.stderr
+    hooked = subprocess.run([sys.executable, "-c", code], env={**env, "COVGPU_TEST_HOOKS": "1"},
+                            capture_output=True, text=True, timeout=300)
+    assert hooked.returncode == 0, hooked.stderr
+    snap, small = (int(x) for x in plain.stdout.split())
+    assert snap & 8 and not small & 1          # product path: snapshot kernel, direct kernels for the small shape
+    snap_h, small_h = (int(x) for x in hooked.stdout.split())
+    assert not snap_h & 8 and small_h & 1      # hooks honoured: CUDA-core engine, spectral engine forced
