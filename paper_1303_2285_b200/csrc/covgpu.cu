@@ -140,6 +140,14 @@ struct covgpu_plan {
   bool spec_smem = false;  // k_spec_corr_smem (P <= 64) instead of the L2-fed k_spec_corr
   int spec_e = 16;         // row lags per k_spec_corr_smem warp (16: up to 8 warps, 8: up to 16 warps)
   int spec_stages = 2;
+  // symmetric core sums (spectral.cuh k_spec_fft modes 2 / 3): one spectrum per
+  // row under one core-column mask, only the row lags dr >= 0 correlated; the
+  // difference to CC is a correlation of the two 2Q-2 column strips (second,
+  // small spectral problem: spec2_*), added as a second CC partial
+  bool spec_sym = false;
+  int spec2_logL = 0, spec2_nseg = 1;
+  SpecLayout spec2_lay{};
+  double2 *d_tw2 = nullptr, *d_twf2 = nullptr, *d_fx2 = nullptr, *d_fy2 = nullptr, *d_gp2 = nullptr;
   // spectral edge sums: column FFTs of length Lr = 2^spec_logLr (CCol), the
   // unmasked strip-row spectra (RC')
   bool spec_edges = false;
@@ -413,6 +421,11 @@ void plan_free(covgpu_plan* pl) {
   if (pl->out_stream) cudaStreamDestroy(pl->out_stream);
   for (auto& e : pl->ev_fin_chunk)
     if (e) cudaEventDestroy(e);
+  cudaFree(pl->d_tw2);
+  cudaFree(pl->d_twf2);
+  cudaFree(pl->d_fx2);
+  cudaFree(pl->d_fy2);
+  cudaFree(pl->d_gp2);
   cudaFree(pl->d_tw);
   cudaFree(pl->d_fx);
   cudaFree(pl->d_fy);
@@ -916,9 +929,14 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   // row spectra -> dr = 0 per-row transforms, correlation -> output FFT ->
   // edge rows
   // correlation launch for chunk range `part_` of `nparts_` into G slots [slot0, slot0 + nseg_)
-  auto corr_smem = [&](int nseg_, int part_, int nparts_, int slot0, int nslots) {
-    const size_t sm = pl->spec_stages * spec_corr_stage_bytes(pr.P) + 16 * pl->spec_stages;
-    const unsigned blocks = (unsigned)(B * pl->spec_lay.nfb * nseg_);
+  const bool sym = pl->spec_sym && nparts == 1;  // (row parts keep the two-mask sums)
+  auto corr_launch = [&](cudaStream_t cs, long long nb_, const double2* fx, const double2* fy, const SpecLayout& lay_,
+                         double2* gp, bool posonly, int nseg_, int part_, int nparts_, int slot0, int nslots) {
+    const int e = pl->spec_e;
+    const int ngrp = posonly ? (pr.P + e - 1) / e : pl->spec_ngrp;
+    const int stages = posonly ? 2 : pl->spec_stages;
+    const size_t sm = stages * spec_corr_stage_bytes(pr.P, posonly) + 16 * stages;
+    const unsigned blocks = (unsigned)(nb_ * lay_.nfb * nseg_);
     auto kern = pl->spec_e == 8 ? &k_spec_corr_smem<8, 16> : &k_spec_corr_smem<16, 8>;
     {
       static std::mutex mu;
@@ -929,9 +947,25 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
         done.push_back((const void*)kern);
       }
     }
-    kern<<<blocks, pl->spec_ngrp * 32, sm, st>>>(pl->d_fx, pl->d_fy, pr, pl->spec_lay, nseg_, part_, nparts_,
-                                                pl->spec_stages, pl->d_gp, slot0, nslots);
+    kern<<<blocks, ngrp * 32, sm, cs>>>(fx, fy, pr, lay_, nseg_, part_, nparts_, stages, gp, slot0, nslots,
+                                        posonly ? 1 : 0);
   };
+  auto corr_smem = [&](int nseg_, int part_, int nparts_, int slot0, int nslots) {
+    corr_launch(st, B, pl->d_fx, sym ? pl->d_fx : pl->d_fy, pl->spec_lay, pl->d_gp, sym, nseg_, part_, nparts_,
+                slot0, nslots);
+  };
+  // row spectra of rows [r0, r0 + nr): X and Y (two column masks), or the one
+  // symmetric spectrum
+  auto fft_rows = [&](int r0, int nr) {
+    if (nr <= 0) return;
+    if (sym)
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * nr, A, pr, 2, pl->spec_lay, pl->d_tw, pl->d_fx, pl->d_fy,
+                r0, nr);
+    else
+      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * nr * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
+                pl->d_fy, r0, nr);
+  };
+  const double2* const fy_rows = sym ? pl->d_fx : pl->d_fy;  // second-element spectrum of the dr = 0 rows
   if (nparts > 1) {
     // only this part's edge pairs are computed: the others' CCol / RC' stay zero
     if (pl->spec_edges) {
@@ -956,10 +990,8 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     // the rest of the H2D.
     const int N = pr.N;
     CUDA_TRY_V(cudaStreamWaitEvent(st, pl->ev_strips, 0));
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * S * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
-              pl->d_fy, 0, S);
-    SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * S * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
-              pl->d_fy, N - S, S);
+    fft_rows(0, S);
+    fft_rows(N - S, S);
     if (pl->spec_edges && !pl->spec_blk)
       SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
                 pl->d_fy0, 0, N);
@@ -980,14 +1012,13 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
           stream_wait_value()(st, (CUdeviceptr)pl->d_band_flag, pl->band_base + (unsigned)k + 1u,
                               CU_STREAM_WAIT_VALUE_GEQ);
         if (r1 <= r0) continue;
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
-                  pl->d_fx, pl->d_fy, r0, r1 - r0);
+        fft_rows(r0, r1 - r0);
         // dr = 0 rows: the core rows [P-1, N-P] = the non-strip rows
         if (pl->spec_prune_q)
-          SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (r1 - r0), pl->d_fx, pl->d_fy, pr,
+          SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (r1 - r0), pl->d_fx, fy_rows, pr,
                     pl->spec_lay, pl->d_tw, pl->d_twf, r0, r1 - r0, rz - ra + 1, r0 - ra, pl->d_d0p);
         else
-          SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (r1 - r0), pl->d_fx, pl->d_fy, pr,
+          SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (r1 - r0), pl->d_fx, fy_rows, pr,
                     pl->spec_lay, pl->d_tw, pl->d_twf, r0, r1 - r0, rz - ra + 1, r0 - ra, pl->d_d0p);
       }
     };
@@ -1009,7 +1040,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     }
     mark("spec_fft");
     k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
-                                                       pl->d_cls_slot, pl->d_ccpart);
+                                                       pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1);
     if (pl->spec_edges && !pl->spec_blk && es != st) {
       const cudaStream_t st_main = st;
       st = es;
@@ -1039,13 +1070,10 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
                           {pr.N - S, pr.N}};
       for (auto& rg : ranges) {
         const int r0 = std::max(0, rg[0]), r1 = std::min(pr.N, rg[1]);
-        if (r1 > r0)
-          SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * (r1 - r0) * 2, A, pr, 0, pl->spec_lay, pl->d_tw,
-                    pl->d_fx, pl->d_fy, r0, r1 - r0);
+        if (r1 > r0) fft_rows(r0, r1 - r0);
       }
     } else {
-      SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * pr.N * 2, A, pr, 0, pl->spec_lay, pl->d_tw, pl->d_fx,
-                pl->d_fy, 0, pr.N);
+      fft_rows(0, pr.N);
     }
     if (pl->spec_edges && !pl->spec_blk)
       SPEC_LOGL(pl->spec_logL, SpecK<T>::template fft, B * 2 * S, A, pr, 1, pl->spec_lay, pl->d_tw, pl->d_fx,
@@ -1062,13 +1090,13 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     }
     if (rz >= ra)
       if (pl->spec_prune_q)
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr,
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (rz - ra + 1), pl->d_fx, fy_rows, pr,
                   pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
       else
-        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, pl->d_fy, pr,
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, fy_rows, pr,
                   pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
     k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
-                                                       pl->d_cls_slot, pl->d_ccpart);
+                                                       pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1);
     if (pl->spec_edges && !pl->spec_blk && es != st_main)
       if (pl->spec_prune_q)
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
@@ -1096,10 +1124,10 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   }
   if (pl->spec_prune_q)
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template dftp, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
-              pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
+              pl->nclasses, pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1, 0, sym ? 1 : 0, 0, 0);
   else
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template dft, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
-              pl->nclasses, pl->d_cls_slot, pl->d_ccpart);
+              pl->nclasses, pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1, 0, sym ? 1 : 0, 0, 0);
   if (pl->spec_edges && pl->spec_blk) {
     // blocked short-lag correlation (edgeblk.cuh) on the side stream: reads
     // only A's strips.  Timing names: spec_ccol = column strips, spec_rc = row strips
@@ -1143,6 +1171,27 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template rc, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
                   pl->spec_lay, pl->d_tw, pl->d_twf, pl->d_cls_slot, pl->d_cls, pl->d_rc, pl->tot_rc, part, nparts,
                   B * 2 * (long long)S * S);
+  }
+  if (sym) {
+    mark("spec_rc");
+    // the strips' correction E(dr, dc) (all lags, dr = 0 included) as the second
+    // CC partial: a small spectral problem on the two 2Q-2 column strips, on the
+    // side stream (host path: the edge columns are complete with the last band)
+    const cudaStream_t st_main = st;
+    if (es != st) st = es;
+    if (band_mode) CUDA_TRY_V(cudaStreamWaitEvent(st, pl->ev_h2d, 0));
+    SPEC_LOGL(pl->spec2_logL, SpecK<T>::template fft, B * 2 * pr.N * 2, A, pr, 3, pl->spec2_lay, pl->d_tw2, pl->d_fx2,
+              pl->d_fy2, 0, pr.N);
+    const int ns2 = pl->spec2_nseg;
+    corr_launch(st, 2 * B, pl->d_fx2, pl->d_fy2, pl->spec2_lay, pl->d_gp2, false, ns2, 0, 1, 0, ns2);
+    const int L2 = 1 << pl->spec2_logL;
+    if (ns2 > 1) {
+      const long long per_seg = (long long)(2 * pr.P - 1) * L2, tot = 2 * B * per_seg;
+      k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp2, ns2, per_seg, tot);
+    }
+    SPEC_LOGL(pl->spec2_logL, SpecK<T>::template dft, 2 * B * (2 * pr.P - 1), pl->d_gp2, pl->d_tw2, pl->d_twf2, pr,
+              ns2, pl->nclasses, pl->d_cls_slot, pl->d_ccpart, 3, 1, 0, 1, 1);
+    st = st_main;
   }
 }
 
@@ -1455,9 +1504,10 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     if (pl->band_wait) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_h2d, 0));  // no per-band waits here
     launch_bulk_variant<T>(pl, A, st, pl->bulk_variant);
   }
-  const int npart = pl->use_spec || snap ? 1 : mma ? pl->mma_g : pl->ncb * pl->nrs;
+  const int npart = pl->use_spec ? (pl->spec_sym && pl->ks_nparts == 1 ? 3 : 1) : snap ? 1 : mma ? pl->mma_g : pl->ncb * pl->nrs;
   ++launches;
-  mark(pl->use_spec ? (pl->spec_edges ? "spec_rc" : "spec_dft") : mma ? "bulk_dmma" : snap ? "snap_spec" : "bulk");
+  mark(pl->use_spec ? (pl->spec_edges ? (npart == 3 ? "spec_strips" : "spec_rc") : "spec_dft")
+                    : mma ? "bulk_dmma" : snap ? "snap_spec" : "bulk");
   if (mma && !pl->spec_edges) {  // edge-column sums: tensor cores, else CUDA-core bulk on the edge column blocks
     if (!(pl->use_ecm && launch_edge_cols_dmma(pl, (const double2*)A, es))) {
       if (pl->ks_nparts > 1) return fail(COVGPU_ECUDA, "row-band sums: edge-column kernel unavailable");
@@ -1731,7 +1781,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_NO_SYM",
                         "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
@@ -2019,6 +2069,30 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       }
       const long long d0rows = n - 2LL * p + 2;
       pl->spec_nd0 = (int)std::max(1LL, d0rows);  // N = 2P-2: no core rows
+      // symmetric core sums: one mask [Q-1, M-Q] for both elements makes the
+      // row-lag correlation conjugate-symmetric in dr (half the lags, one
+      // spectrum per row); CC = that + the correlations inside the first and
+      // the last 2Q-2 columns (second problem: the two strips as a batch of
+      // two, FFT length >= 2Q-2), one extra CC partial per strip.  Needs the staged
+      // correlation kernel, the blocked edge sums (they read A, not the X
+      // spectra) and non-overlapping strips (M >= 3Q)
+      int lg2 = 6;
+      while ((1 << lg2) < 2 * q - 2) ++lg2;
+      // (large estimates only: small ones are launch-latency chains that the
+      // extra strip launches make longer — cfg3 0.087 -> 0.112 ms)
+      pl->spec_sym = pl->spec_smem && pl->spec_blk && m >= 3LL * q && q >= 2 && lg2 <= 12 && n * m >= (1LL << 21);
+      if (const char* nsy = hook_env("COVGPU_NO_SYM")) pl->spec_sym = pl->spec_sym && atoi(nsy) == 0;
+      if (pl->spec_sym) {
+        pl->spec2_logL = lg2;
+        pl->spec2_lay.nfb = (1 << lg2) / 32;
+        pl->spec2_lay.padr = pl->spec_lay.padr;
+        pl->spec2_lay.np = pl->spec_lay.np;
+        // row segments of the strips' correlation: one wave of 1-CTA/SM blocks,
+        // >= 2 chunks each (per-CTA pipeline fill and epilogue are as long as ~2 chunks)
+        const long long nch2 = (n + SC_RC - 1) / SC_RC;
+        const long long per2 = 2 * batch * pl->spec2_lay.nfb;
+        pl->spec2_nseg = (int)std::max(1LL, std::min({148 / std::max(1LL, per2), nch2 / 2, 32LL}));
+      }
     }
   }
   // small complex64 snapshots: the sums of a whole snapshot inside one CTA
@@ -2179,6 +2253,24 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         cudaMemcpy(pl->d_tw, tw.data(), sizeof(double2) * L, cudaMemcpyHostToDevice) != cudaSuccess) {
       plan_free(pl.get());
       return fail(COVGPU_ECUDA, "twiddle upload");
+    }
+    if (pl->spec_sym) {
+      const size_t L2 = (size_t)1 << pl->spec2_logL;
+      const std::vector<double2> tw2 = spec_twiddles(pl->spec2_logL), twf2 = full_table(pl->spec2_logL);
+      const size_t fxe2 = (size_t)2 * batch * pl->spec2_lay.nfb * pl->spec2_lay.np * 32;
+      if ((rc = dalloc(&pl->d_tw2, L2, &ws)) || (rc = dalloc(&pl->d_twf2, L2, &ws)) ||
+          (rc = dalloc(&pl->d_fx2, fxe2, &ws)) || (rc = dalloc(&pl->d_fy2, fxe2, &ws)) ||
+          (rc = dalloc(&pl->d_gp2, (size_t)2 * batch * std::max(pl->spec2_nseg, 1) * (2 * p - 1) * L2, &ws))) {
+        plan_free(pl.get());
+        return rc;
+      }
+      if (cudaMemset(pl->d_fx2, 0, sizeof(double2) * fxe2) != cudaSuccess ||
+          cudaMemset(pl->d_fy2, 0, sizeof(double2) * fxe2) != cudaSuccess ||
+          cudaMemcpy(pl->d_tw2, tw2.data(), sizeof(double2) * tw2.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(pl->d_twf2, twf2.data(), sizeof(double2) * L2, cudaMemcpyHostToDevice) != cudaSuccess) {
+        plan_free(pl.get());
+        return fail(COVGPU_ECUDA, "strip twiddle upload");
+      }
     }
     if (pl->spec_edges && pl->spec_blk) {
       const std::vector<double2> twc = spec_twiddles(pl->ebc.logLb), twr2 = spec_twiddles(pl->ebr.logLb);

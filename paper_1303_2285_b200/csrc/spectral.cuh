@@ -305,6 +305,12 @@ struct SpecLayout {
 // (columns c <= M-Q), 1 -> Y_r (columns c >= Q-1).  mode 1 (edge rows):
 // CTA = (b, strip row s of 2(P-1)) -> Y0_s, the unmasked row of the top
 // strip [0, P-1) / bottom strip [N-P+1, N).  Zero-padded to L = 2^LOGL.
+// mode 2 (symmetric core sums): CTA = (b, row r) -> X_r only, the row under
+// ONE mask for both elements, the core columns [Q-1, M-Q].  mode 3 (the
+// strips' correction of the symmetric sums): "snapshot" 2 b + s = strip s of
+// snapshot b, the first (s = 0) / last (s = 1) 2Q-2 columns of the row at
+// positions [0, 2Q-2); which 0 -> the strip's first-element columns
+// [0, Q-1), which 1 -> its second-element columns [Q-1, 2Q-2).
 template <typename T, int LOGL>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_fft(long long nitems, const typename CT<T>::c* __restrict__ A, Problem pr, int mode, SpecLayout lay,
@@ -319,15 +325,24 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   int r, clo, chi;
   long long orow;
   double2* out;
-  if (mode == 0) {  // rows [row0, row0 + nrows)
-    const int which = (int)(t & 1);
+  int which = 0, strip = 0;
+  if (mode == 0 || mode == 3) {  // rows [row0, row0 + nrows)
+    which = (int)(t & 1);
     t >>= 1;
     r = row0 + (int)(t % nrows);
-    const long long b = t / nrows;
+    const long long b = t / nrows;  // (mode 3: 2 snapshot + strip)
     clo = which ? Q - 1 : 0;
     chi = which ? M - 1 : M - Q;
-    orow = b * N + r;
+    strip = (int)(b & 1);
+    orow = (mode == 3 ? b >> 1 : b) * N + r;
     out = (which ? FY : FX) + lay.at(b, r, 0);
+  } else if (mode == 2) {
+    r = row0 + (int)(t % nrows);
+    const long long b = t / nrows;
+    clo = Q - 1;
+    chi = M - Q;
+    orow = b * N + r;
+    out = FX + lay.at(b, r, 0);
   } else {
     const int sr = (int)(t % (2 * S));
     const long long b = t / (2 * S);
@@ -338,11 +353,18 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     out = FY + (b * 2 * S + sr) * (long long)L;  // row-major (mode 1 stride: 32 per block)
   }
   const typename CT<T>::c* row = A + orow * (long long)M;
-  const long long fstride = mode == 0 ? (long long)lay.np * 32 : 32;  // next 32-frequency block
+  const long long fstride = mode != 1 ? (long long)lay.np * 32 : 32;  // next 32-frequency block
   const bool ok = si.valid;
+  const int W2 = 2 * Q - 2;
   spec_fft_block<LOGL>(
       sb, si.tl, tw,
-      [&](int idx) { return (ok && idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0); },
+      [&](int idx) {
+        if (mode == 3) {
+          const bool in = ok && idx < W2 && (which ? idx >= Q - 1 : idx < Q - 1);
+          return in ? widen2(row[strip ? M - W2 + idx : idx]) : make_double2(0.0, 0.0);
+        }
+        return (ok && idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0);
+      },
       [&](int idx, double2 v) {
         if (ok) out[(idx >> 5) * fstride + (idx & 31)] = v;
       });
@@ -658,8 +680,11 @@ __global__ void __launch_bounds__(SPEC_CW * 32, 2)
 constexpr int SC_RC = 32;
 constexpr size_t SC_SMEM_BUDGET = 220 * 1024;
 
-__host__ __device__ inline size_t spec_corr_stage_bytes(int P) {
-  return sizeof(double2) * 32 * (size_t)(2 * SC_RC + 2 * P - 2);
+// (posonly: the symmetric sums keep the lags dr >= 0 only — the second
+// element's rows [R, R+SC_RC) are the tail of the first element's rows
+// [R-(P-1), R+SC_RC) of the same spectrum: one copy)
+__host__ __device__ inline size_t spec_corr_stage_bytes(int P, bool posonly = false) {
+  return sizeof(double2) * 32 * (size_t)(posonly ? SC_RC + P - 1 : 2 * SC_RC + 2 * P - 2);
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -675,12 +700,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 template <int E, int MAXW>
 __global__ void __launch_bounds__(MAXW * 32, 1)
     k_spec_corr_smem(const double2* __restrict__ FX, const double2* __restrict__ FY, Problem pr, SpecLayout lay,
-                     int nseg, int part, int nparts, int stages, double2* __restrict__ Gp, int slot0, int nslots) {
+                     int nseg, int part, int nparts, int stages, double2* __restrict__ Gp, int slot0, int nslots,
+                     int posonly) {
   const int NG = blockDim.x >> 5;
   extern __shared__ __align__(128) unsigned char scraw[];
   const int P = pr.P, N = pr.N;
-  const int nlag = 2 * P - 1, XR = SC_RC + 2 * P - 2;
-  const size_t stage_bytes = spec_corr_stage_bytes(P);
+  const int nlag = 2 * P - 1, XR = posonly ? SC_RC + P - 1 : SC_RC + 2 * P - 2;
+  const size_t stage_bytes = spec_corr_stage_bytes(P, posonly != 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(scraw + stages * stage_bytes);
   uint64_t* empty = full + stages;
   long long t = blockIdx.x;
@@ -703,9 +729,13 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
     const int R = (ca + k) * SC_RC;
     unsigned char* st = scraw + s * stage_bytes;
     mbar_expect_tx(&full[s], (unsigned)stage_bytes);
-    bulk_g2s(st, fyb + (long long)R * 32, (unsigned)(sizeof(double2) * 32 * SC_RC), &full[s]);
-    bulk_g2s(st + sizeof(double2) * 32 * SC_RC, fxb + (long long)(R - (P - 1)) * 32,
-             (unsigned)(sizeof(double2) * 32 * XR), &full[s]);
+    if (posonly) {
+      bulk_g2s(st, fxb + (long long)(R - (P - 1)) * 32, (unsigned)(sizeof(double2) * 32 * XR), &full[s]);
+    } else {
+      bulk_g2s(st, fyb + (long long)R * 32, (unsigned)(sizeof(double2) * 32 * SC_RC), &full[s]);
+      bulk_g2s(st + sizeof(double2) * 32 * SC_RC, fxb + (long long)(R - (P - 1)) * 32,
+               (unsigned)(sizeof(double2) * 32 * XR), &full[s]);
+    }
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -721,7 +751,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
   // per-ROW masks — dr >= 0: y rows r2 >= P-1, x rows r1 <= N-P; dr < 0:
   // y rows r2 <= N-P, x rows r1 >= P-1 — applied once per row as it enters
   // the registers, with no per-lag predicates
-  const int ngn = (P - 1 + E - 1) / E;
+  const int ngn = posonly ? 0 : (P - 1 + E - 1) / E;
   const bool neg = w < ngn;
   const int dr0 = neg ? -(P - 1) + w * E : (w - ngn) * E;
   const int drmax = neg ? -1 : P - 1;
@@ -739,8 +769,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
     const int s = k % stages;
     mbar_wait(&full[s], (k / stages) & 1);
     const int R = (ca + k) * SC_RC;
-    const double2* Y = reinterpret_cast<const double2*>(scraw + s * stage_bytes) + lane;
-    const double2* X = Y + 32 * SC_RC;
+    const double2* const S0 = reinterpret_cast<const double2*>(scraw + s * stage_bytes) + lane;
+    const double2* X = posonly ? S0 : S0 + 32 * SC_RC;
+    const double2* Y = posonly ? S0 + 32 * (P - 1) : S0;
     // window: slot kk holds X row t = R - dr0 - (E-1) + kk (stage row xoff - (E-1) + kk; clamped
     // stage rows only feed lags past the warp's range).  Filled at the
     // segment's first chunk only: SC_RC is a multiple of E, so at a chunk
@@ -852,7 +883,7 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
 // order, then a fixed-shape tree over the threads — deterministic.
 __global__ void __launch_bounds__(256)
     k_spec_d0sum(const double2* __restrict__ D0p, int nd0, Problem pr, int nclasses,
-                 const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+                 const int* __restrict__ cls_slot, double2* __restrict__ ccpart, int cc_stride) {
   __shared__ double2 red[256];
   const int Q = pr.Q;
   const int dc = (int)(blockIdx.x % Q);
@@ -870,7 +901,7 @@ __global__ void __launch_bounds__(256)
   }
   if (t == 0) {
     const int cid = cls_slot[class_index(0, dc, pr.P, Q)];
-    if (cid >= 0) ccpart[b * nclasses + cid] = red[0];
+    if (cid >= 0) ccpart[(b * nclasses + cid) * cc_stride] = red[0];
   }
 }
 
@@ -904,7 +935,8 @@ template <int LOGL, bool PRUNE = false>
 __global__ void __launch_bounds__(spec_threads<LOGL>())
     k_spec_dft(long long nitems, const double2* __restrict__ Gp, const double2* __restrict__ tw,
                const double2* __restrict__ twf, Problem pr,
-               int nseg, int nclasses, const int* __restrict__ cls_slot, double2* __restrict__ ccpart) {
+               int nseg, int nclasses, const int* __restrict__ cls_slot, double2* __restrict__ ccpart, int cc_stride,
+               int cc_part, int sym, int with_d0, int strips) {
   extern __shared__ double2 sbuf[];
   constexpr int L = 1 << LOGL;
   const int P = pr.P, Q = pr.Q;
@@ -912,16 +944,25 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
   double2* sb;
   const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
   const int li = (int)(si.item % nlag);
-  const long long b = si.item / nlag;
+  const long long bg = si.item / nlag;  // G's snapshot index (strips: 2 snapshot + strip, one CC partial per strip)
+  const long long b = strips ? bg >> 1 : bg;
+  if (strips) cc_part += (int)(bg & 1);
   const int dr = li - (P - 1);
-  const bool ok = si.valid && dr != 0;  // dr = 0: k_spec_d0sum
-  const double2* g = Gp + (b * nseg * nlag + li) * (long long)L;
+  const bool ok = si.valid && (dr != 0 || with_d0);  // dr = 0: k_spec_d0sum (unless with_d0)
+  // sym: only G(dr >= 0, .) exists and G(-d, f) = conj(G(d, f)), so the lag
+  // -d transforms the conjugate of lag d's row
+  const bool cj = sym && dr < 0;
+  const double2* g = Gp + (bg * nseg * nlag + (cj ? (P - 1) - dr : li)) * (long long)L;
   const double inv = 1.0 / (double)L;
-  auto ld = [&](int idx) { return ok ? g[idx] : make_double2(0.0, 0.0); };  // segment 0: the ordered sum
+  auto ld = [&](int idx) {  // segment 0: the ordered sum
+    if (!ok) return make_double2(0.0, 0.0);
+    const double2 v = g[idx];
+    return cj ? make_double2(v.x, -v.y) : v;
+  };
   auto stf = [&](int idx, double2 v) {
-    if (ok && idx < Q && (dr > 0 || idx > 0)) {
+    if (ok && idx < Q && (dr >= 0 || idx > 0)) {
       const int cid = cls_slot[class_index(dr, idx, P, Q)];
-      if (cid >= 0) ccpart[b * nclasses + cid] = make_double2(v.x * inv, v.y * inv);
+      if (cid >= 0) ccpart[(b * nclasses + cid) * cc_stride + cc_part] = make_double2(v.x * inv, v.y * inv);
     }
   };
   if constexpr (PRUNE)
