@@ -505,15 +505,23 @@ def main() -> None:
         if kernel_ms[name] <= 0:
             continue
         if name == "spec_corr":
-            macs = sum((n - 2 * p + 2 + abs(dr)) for dr in range(-(p - 1), p) if dr != 0) * L * B * sf
+            # symmetric core sums (plans that also run the strips' correction):
+            # only the lags dr > 0 are correlated, the others are conjugates
+            symc = "spec_strips" in kernel_ms
+            macs = sum((n - 2 * p + 2 + abs(dr)) for dr in range(1 if symc else -(p - 1), p) if dr != 0) * L * B * sf
             per_kernel[name] = fp_roof(name, 6.0 * macs, "6 flops (Gauss form: 3 real FMAs) x sum over row "
-                                       "lags dr != 0 of |core rows(dr)| x L frequencies (one complex MAC "
-                                       "per row, frequency and lag)")
+                                       "lags " + ("dr > 0 (G(-dr) = conj G(dr))" if symc else "dr != 0") +
+                                       " of |core rows(dr)| x L frequencies (one complex MAC per row, "
+                                       "frequency and lag)")
             per_kernel[name]["complex_mac_equivalent_tflops"] = 8.0 * macs / (kernel_ms[name] * 1e-3) / 1e12
         elif name == "spec_fft":
-            nb = (2 * n * m * esz_in + 2 * n * L * 16 + 2 * (p - 1) * (m * esz_in + L * 16)) * B
-            per_kernel[name] = hbm_roof(name, nb, "A read twice + the X / Y row spectra written "
-                                        "(+ the unmasked edge-row spectra)")
+            if "spec_strips" in kernel_ms:
+                nb = (n * m * esz_in + n * L * 16) * B
+                per_kernel[name] = hbm_roof(name, nb, "A read once + the one row spectrum written")
+            else:
+                nb = (2 * n * m * esz_in + 2 * n * L * 16 + 2 * (p - 1) * (m * esz_in + L * 16)) * B
+                per_kernel[name] = hbm_roof(name, nb, "A read twice + the X / Y row spectra written "
+                                            "(+ the unmasked edge-row spectra)")
         elif name == "bulk_dmma":
             per_kernel[name] = fp_roof(name, 6.0 * core_p * B * sf,
                                        "6 flops (Gauss 3 real FMAs) x core products", pk=peak_dmma,

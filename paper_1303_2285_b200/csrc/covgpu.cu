@@ -256,6 +256,7 @@ struct covgpu_plan {
   // side stream for the edge-row / corner kernels (overlap with the bulk)
   cudaStream_t side_stream = nullptr;
   cudaStream_t delta_stream = nullptr;  // the walk's corner blocks / chunk updates (beside the edge sums)
+  cudaStream_t cur_ds = nullptr;        // this execute's third stream (nullptr: none)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_djoin = nullptr;
   cudaEvent_t ev_d0 = nullptr;  // spectral: dr = 0 sums (side stream) done
   // end-to-end host path: cached stream and device buffers
@@ -1119,8 +1120,9 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   }
   mark("spec_corr");
   if (gslots > 1) {  // row-segment partials -> slot 0, in order
-    const long long per_seg = (long long)(2 * pr.P - 1) * L, tot = B * per_seg;
-    k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, gslots, per_seg, tot);
+    const long long per_seg = (long long)(2 * pr.P - 1) * L;
+    const long long e_lo = sym ? (long long)(pr.P - 1) * L : 0, e_cnt = per_seg - e_lo, tot = B * e_cnt;
+    k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, gslots, per_seg, e_lo, e_cnt, tot);
   }
   if (pl->spec_prune_q)
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template dftp, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
@@ -1178,7 +1180,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     // CC partial: a small spectral problem on the two 2Q-2 column strips, on the
     // side stream (host path: the edge columns are complete with the last band)
     const cudaStream_t st_main = st;
-    if (es != st) st = es;
+    if (es != st) st = pl->cur_ds ? pl->cur_ds : es;  // (the third stream, after the walk's chunk updates)
     if (band_mode) CUDA_TRY_V(cudaStreamWaitEvent(st, pl->ev_h2d, 0));
     SPEC_LOGL(pl->spec2_logL, SpecK<T>::template fft, B * 2 * pr.N * 2, A, pr, 3, pl->spec2_lay, pl->d_tw2, pl->d_fx2,
               pl->d_fy2, 0, pr.N);
@@ -1187,7 +1189,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     const int L2 = 1 << pl->spec2_logL;
     if (ns2 > 1) {
       const long long per_seg = (long long)(2 * pr.P - 1) * L2, tot = 2 * B * per_seg;
-      k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp2, ns2, per_seg, tot);
+      k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp2, ns2, per_seg, 0, per_seg, tot);
     }
     SPEC_LOGL(pl->spec2_logL, SpecK<T>::template dft, 2 * B * (2 * pr.P - 1), pl->d_gp2, pl->d_tw2, pl->d_twf2, pr,
               ns2, pl->nclasses, pl->d_cls_slot, pl->d_ccpart, 3, 1, 0, 1, 1);
@@ -1461,7 +1463,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       launch_ck_scan(pl, ds);
       launches += 2;
     }
-    if (dfork) CUDA_TRY(cudaEventRecord(pl->ev_djoin, ds));
+    pl->cur_ds = dfork ? ds : nullptr;
     if (!fork) mark("fin_delta");
   }
   // core sums: FP64 tensor cores when the plan allows, else the CUDA-core
@@ -1555,7 +1557,11 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
     CUDA_TRY(cudaEventRecord(pl->ev_join, es));
     CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join, 0));
   }
-  if (dfork) CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_djoin, 0));
+  if (dfork) {
+    CUDA_TRY(cudaEventRecord(pl->ev_djoin, pl->cur_ds));
+    CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_djoin, 0));
+    pl->cur_ds = nullptr;
+  }
   if (pl->use_tile) {
     // tile finalize straight into the requested layout; u-chunks for the
     // host path (rows [P u0, P u1) of R are complete after a chunk, an event
@@ -2391,10 +2397,11 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     // updates get a stream of their own beside the edge sums (cfg3 0.094 ->
     // 0.087 ms, cfg2 0.092 -> 0.084); large ones are throughput-bound and lose
     // ~1 % to the extra concurrency (cfg5 0.463 -> 0.469 ms), so they keep one
-    // side stream
+    // side stream — unless they run the symmetric core sums, whose side work
+    // (edge sums + the strips' correction) is longer than the main chain
     const bool small = batch * n * m <= (1LL << 20);
     if (cudaStreamCreateWithPriority(&pl->side_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        (small && cudaStreamCreateWithPriority(&pl->delta_stream, cudaStreamNonBlocking, lo) != cudaSuccess) ||
+        ((small || pl->spec_sym) && cudaStreamCreateWithPriority(&pl->delta_stream, cudaStreamNonBlocking, lo) != cudaSuccess) ||
         cudaEventCreateWithFlags(&pl->ev_djoin, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming) != cudaSuccess ||

@@ -908,10 +908,13 @@ __global__ void __launch_bounds__(256)
 // G partials of the row segments summed in order into segment 0 (one thread
 // per (b, dr, f): the output FFT below then reads one value per frequency)
 __global__ void __launch_bounds__(256)
-    k_spec_gsum(double2* __restrict__ Gp, int nseg, long long per_seg, long long total) {
+    k_spec_gsum(double2* __restrict__ Gp, int nseg, long long per_seg, long long e_lo, long long e_cnt,
+                long long total) {
+  // elements [e_lo, e_lo + e_cnt) of every snapshot's [lag][f] block (the
+  // symmetric sums fill the lags dr >= 0 only)
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const long long b = t / per_seg, e = t % per_seg;
+  const long long b = t / e_cnt, e = e_lo + t % e_cnt;
   double2* g = Gp + b * nseg * per_seg + e;
   double2 v[8];
   double2 s = g[0];
