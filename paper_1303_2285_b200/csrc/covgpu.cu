@@ -1787,7 +1787,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_NO_SYM",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_NO_SYM", "COVGPU_SYM",
                         "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
@@ -2088,6 +2088,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       // extra strip launches make longer — cfg3 0.087 -> 0.112 ms)
       pl->spec_sym = pl->spec_smem && pl->spec_blk && m >= 3LL * q && q >= 2 && lg2 <= 12 && n * m >= (1LL << 21);
       if (const char* nsy = hook_env("COVGPU_NO_SYM")) pl->spec_sym = pl->spec_sym && atoi(nsy) == 0;
+      if (const char* fsy = hook_env("COVGPU_SYM"))  // (test hook: also below the size gate)
+        if (atoi(fsy) != 0) pl->spec_sym = pl->spec_smem && pl->spec_blk && m >= 3LL * q && q >= 2 && lg2 <= 12;
       if (pl->spec_sym) {
         pl->spec2_logL = lg2;
         pl->spec2_lay.nfb = (1 << lg2) / 32;
@@ -2307,7 +2309,8 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
     }
   }
   if (pl->clean) {
-    const size_t npart = (size_t)std::max(pl->ncb * pl->nrs, pl->use_mma ? pl->mma_g : 0);
+    // (symmetric spectral sums: three CC partials per class — core, left strip, right strip)
+    const size_t npart = (size_t)std::max({pl->ncb * pl->nrs, pl->use_mma ? pl->mma_g : 0, pl->spec_sym ? 3 : 1});
     if ((rc = dalloc(&pl->d_ccpart, (size_t)batch * nc * npart, &ws)) ||
         (rc = dalloc(&pl->d_ccol, (size_t)(batch * std::max(pl->tot_ccol, 1LL) * pl->nrs), &ws)) ||
         (rc = dalloc(&pl->d_rc, (size_t)(batch * std::max(pl->tot_rc, 1LL) * pl->nseg), &ws)) ||

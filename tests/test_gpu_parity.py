@@ -83,6 +83,7 @@ def test_c4_sweep(cuda, golden, spectral, monkeypatch):
     (COVGPU_SPECTRAL=1: P, Q >= 2, Q <= 64, clean shapes)."""
     if spectral:
         monkeypatch.setenv("COVGPU_SPECTRAL", "1")
+        monkeypatch.setenv("COVGPU_SYM", "1")  # (symmetric core sums where M >= 3Q)
     worst = 0.0
     for i, (n, m, p, q, seed) in enumerate(c4_instances()):
         a = ref_random(n, m, seed)
@@ -439,6 +440,7 @@ def test_random_shapes_fuzz(cuda, spectral, monkeypatch):
     rng = np.random.default_rng(20261020 + (7 if spectral else 0))
     if spectral:
         monkeypatch.setenv("COVGPU_SPECTRAL", "1")
+        monkeypatch.setenv("COVGPU_SYM", "1")  # the symmetric core sums wherever M >= 3Q allows them
     worst = {np.complex128: 0.0, np.complex64: 0.0}
     for it in range(60):
         n = int(rng.integers(1, 160))
@@ -925,3 +927,58 @@ def test_snapshot_kernel_vs_oracle(cuda, n, m, p, q, batch, monkeypatch):
         err = co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref)
         assert err <= TOL32, (b, err)
         assert co.rel_frobenius(got[b].astype(np.complex128), gd[b].astype(np.complex128)) <= TOL32
+
+
+@pytest.mark.parametrize("n,m,p,q,batch,dt", [
+    (96, 120, 12, 10, 1, np.complex128),
+    (100, 77, 12, 20, 3, np.complex64),     # M just above 3Q, complex64 inputs, batch
+    (70, 200, 9, 32, 2, np.complex128),     # wide strips (62 columns each side)
+    (64, 96, 2, 2, 1, np.complex128),       # smallest window: one lag >= 0, 2-column strips
+    (140, 200, 64, 64, 1, np.complex128),   # P = Q = 64 on few rows: M = 3Q + 8
+    (257, 300, 33, 17, 1, np.complex128),   # odd sizes, P > 32
+])
+def test_symmetric_core_sums_vs_oracle(cuda, n, m, p, q, batch, dt, monkeypatch):
+    """The symmetric core sums (one column mask, lags dr >= 0 only, the
+    strips' correction as extra CC partials) forced on small and ragged
+    shapes against the C oracle, and against the two-mask sums
+    (COVGPU_NO_SYM=1) — cfg5 runs them by default."""
+    from oracle import covoracle_c
+    from paper_1303_2285_b200.plan import Plan
+
+    monkeypatch.setenv("COVGPU_SPECTRAL", "1")
+    monkeypatch.setenv("COVGPU_SYM", "1")
+    rng = np.random.default_rng(n * 13 + m * 5 + p + q)
+    stack = (rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m))).astype(dt)
+    tdt = torch.complex128 if dt == np.complex128 else torch.complex64
+    ad = torch.as_tensor(stack, device=cuda)
+    plan = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=tdt, device=cuda)
+    assert plan.spectral
+    out = plan.alloc_output()
+    plan.execute(ad, out)
+    got = out.reshape(batch, p * q, p * q).cpu().numpy()
+    plan.set_timing(True)  # (the kernel names of a timed execute tell which sums ran)
+    plan.execute(ad, out)
+    assert "spec_strips" in plan.kernel_names()
+    assert np.array_equal(out.reshape(batch, p * q, p * q).cpu().numpy(), got)
+    plan.set_timing(False)
+    pk = plan.alloc_output("packed")
+    plan.execute(ad, pk, "packed")
+    pkn = pk.reshape(batch, -1).cpu().numpy()
+    plan.close()
+    monkeypatch.delenv("COVGPU_SYM")
+    monkeypatch.setenv("COVGPU_NO_SYM", "1")
+    two = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=tdt, device=cuda)
+    o2 = two.alloc_output()
+    two.set_timing(True)
+    two.execute(ad, o2)
+    assert "spec_strips" not in two.kernel_names() and "spec_corr" in two.kernel_names()
+    g2 = o2.reshape(batch, p * q, p * q).cpu().numpy()
+    two.close()
+    k = (n - p + 1) * (m - q + 1)
+    tol = TOL64 if dt == np.complex128 else TOL32
+    for b in range(batch):
+        assert_hermitian(got[b])
+        assert np.array_equal(packed_of(got[b]), pkn[b])
+        ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), p, q) / k
+        assert co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref) <= tol, b
+        assert co.rel_frobenius(got[b].astype(np.complex128), g2[b].astype(np.complex128)) <= tol
