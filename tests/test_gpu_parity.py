@@ -553,7 +553,9 @@ def test_tensor_core_path_vs_gram_and_cuda_cores(cuda, n, m, p, q, batch, spectr
 
 
 @pytest.mark.parametrize("n,m,p,q,spectral", [(1024, 1024, 64, 64, True), (1500, 900, 40, 50, True),
-                                              (1024, 1024, 64, 64, False)])
+                                              (1024, 1024, 64, 64, False),
+                                              (1536, 1536, 64, 64, True),   # above the gate of the symmetric core sums
+                                              (1024, 1100, 33, 50, "sym")])  # the same, forced on a smaller shape
 def test_host_path_streams_a_in_bands_bitwise(cuda, n, m, p, q, spectral, monkeypatch):
     """Single-snapshot host path: A is copied in row bands (spectral engine:
     edge columns and strip rows first) while the kernels run (band counter
@@ -564,11 +566,13 @@ def test_host_path_streams_a_in_bands_bitwise(cuda, n, m, p, q, spectral, monkey
 
     if not spectral:
         monkeypatch.setenv("COVGPU_NO_SPECTRAL", "1")
+    if spectral == "sym":
+        monkeypatch.setenv("COVGPU_SYM", "1")
     rng = np.random.default_rng(5)
     a = torch.from_numpy(rng.standard_normal((1, n, m)) + 1j * rng.standard_normal((1, n, m))).pin_memory()
     win = WindowSpec(p, q)
     plan = Plan(n, m, win, dtype=torch.complex128, device=cuda)
-    assert plan.spectral == spectral
+    assert plan.spectral == bool(spectral)
     dev = plan.alloc_output("packed")
     plan.execute(a.to(cuda), dev, "packed")
     out = torch.empty(plan.output_elems("packed"), dtype=torch.complex128).pin_memory()
