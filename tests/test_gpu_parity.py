@@ -741,7 +741,8 @@ def test_streaming_host_path_matches_sync(cuda):
         assert torch.equal(r, g)
 
 
-@pytest.mark.parametrize("n,m,p,q,force_spectral", [(32, 32, 4, 4, False), (120, 100, 12, 16, True)])
+@pytest.mark.parametrize("n,m,p,q,force_spectral", [(32, 32, 4, 4, False), (120, 100, 12, 16, True),
+                                                    (130, 140, 20, 24, "sym")])  # three streams in the graph
 def test_graph_replay_bitwise(cuda, n, m, p, q, force_spectral, monkeypatch):
     """Repeated executes on the same buffers are captured into a CUDA graph
     (from the second call) and replayed; every replay reads the buffer's
@@ -750,6 +751,8 @@ def test_graph_replay_bitwise(cuda, n, m, p, q, force_spectral, monkeypatch):
 
     if force_spectral:
         monkeypatch.setenv("COVGPU_SPECTRAL", "1")
+    if force_spectral == "sym":
+        monkeypatch.setenv("COVGPU_SYM", "1")  # symmetric core sums: the strips' chain on the third stream
     plan = Plan(n, m, WindowSpec(p, q), dtype=torch.complex128, device=cuda)
     monkeypatch.setenv("COVGPU_NO_GRAPH", "1")
     ref_plan = Plan(n, m, WindowSpec(p, q), dtype=torch.complex128, device=cuda)
