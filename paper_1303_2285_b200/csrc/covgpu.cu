@@ -2084,9 +2084,11 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
       // spectra) and non-overlapping strips (M >= 3Q)
       int lg2 = 6;
       while ((1 << lg2) < 2 * q - 2) ++lg2;
-      // (large estimates only: small ones are launch-latency chains that the
-      // extra strip launches make longer — cfg3 0.087 -> 0.112 ms)
-      pl->spec_sym = pl->spec_smem && pl->spec_blk && m >= 3LL * q && q >= 2 && lg2 <= 12 && n * m >= (1LL << 21);
+      // (not the smallest spectral plans: launch-latency chains where the extra
+      // strip launches cancel the gain — 512 x 512, P = Q = 32: 0.0880 vs
+      // 0.0883 ms; 1024 x 1024, P = Q = 32: 0.132 -> 0.110 ms; 2048 x 2048,
+      // P = Q = 16: 0.263 -> 0.183 ms)
+      pl->spec_sym = pl->spec_smem && pl->spec_blk && m >= 3LL * q && q >= 2 && lg2 <= 12 && n * m >= (1LL << 19);
       if (const char* nsy = hook_env("COVGPU_NO_SYM")) pl->spec_sym = pl->spec_sym && atoi(nsy) == 0;
       if (const char* fsy = hook_env("COVGPU_SYM"))  // (test hook: also below the size gate)
         if (atoi(fsy) != 0) pl->spec_sym = pl->spec_smem && pl->spec_blk && m >= 3LL * q && q >= 2 && lg2 <= 12;
