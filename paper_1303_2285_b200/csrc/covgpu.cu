@@ -233,6 +233,7 @@ struct covgpu_plan {
   int ft_ck = FT_CK;          // checkpoint spacing of the tile walk (ft_ckstep)
   int4* d_dunits = nullptr;   // DELTA-mode units (all classes) and for the class range
   long long n_dunits = 0;
+  bool ck_tiled = false;      // chunk updates by k_ck_delta (P >= 32); d_dunits then holds its units
   int4* d_rdunits = nullptr;
   long long n_rdunits = 0;
   // chunked walk for the synchronous host path (covgpu_plan_execute_host):
@@ -1314,6 +1315,22 @@ std::vector<int4> fin_tile_units(const covgpu_plan* pl, int lo, int hi, bool del
   };
   std::vector<Piece> pieces;
   const int lanes = ft_lanes(P), subs = 32 / lanes;  // snapshots per warp
+  if (delta && pl->ck_tiled) {
+    // k_ck_delta units: (snapshot, dc, top / bottom, chunk) of every column
+    // offset that holds a class of the range
+    std::vector<int4> units;
+    for (int dc = 0; dc < Q; ++dc) {
+      bool any = false;
+      for (int dr = 0; dr < 2 * P - 1 && !any; ++dr) any = has[(size_t)dr * Q + dc];
+      if (!any) continue;
+      const int qu = Q - dc;
+      for (int u0 = 0; u0 + pl->ft_ck < qu; u0 += pl->ft_ck)
+        for (long long b = 0; b < pl->batch; ++b)
+          for (int which = 0; which < 2; ++which)
+            units.push_back(make_int4((int)b, dc, which, u0 | ((u0 + pl->ft_ck) << 16)));
+    }
+    return units;
+  }
   for (int dc = 0; dc < Q; ++dc) {
     const int qu = Q - dc;
     for (int u0 = 0; u0 < qu; u0 += pl->ft_ck) {
@@ -1368,6 +1385,26 @@ void launch_fin_tile(covgpu_plan* pl, const int4* units, long long nunits, const
   }
 #undef FT_LAY
 #undef FT_LAUNCH
+}
+
+// the chunk updates delta_j of the units' (snapshot, dc, chunk)s: k_ck_delta
+// for P >= 32, else the tile kernel's DELTA mode (same values)
+template <typename T>
+void launch_ck_delta(covgpu_plan* pl, const int4* dunits, long long ndunits, cudaStream_t st) {
+  if (ndunits <= 0) return;
+  if (pl->ck_tiled) {
+    const int P = pl->pr.P, nsub = (P + CKD_SUB - 1) / CKD_SUB;
+    const int tw = (std::min(P, CKD_SUB) + CKD_T - 1) / CKD_T;
+    const int threads = (tw * tw + 31) / 32 * 32;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k_ck_delta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ckd_smem(FT_CK));
+    (void)attr;
+    k_ck_delta<<<(unsigned)(ndunits * nsub * nsub), threads, ckd_smem(pl->ft_ck), st>>>(
+        (const double2*)pl->d_corners, P, pl->pr.Q, 8 * pl->ft_nwarp, dunits, nsub, tw, pl->d_ck, pl->ft_ck);
+    return;
+  }
+  launch_fin_tile<T>(pl, dunits, ndunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0, COVGPU_DENSE, 0,
+                     1 << 30, nullptr, 0, INT_MAX, st, true);
 }
 
 // chunk updates -> running sums over the chunks (tile.cuh k_ck_scan)
@@ -1458,8 +1495,7 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
       ++launches;
     }
     if (pl->n_dunits > 0) {
-      launch_fin_tile<T>(pl, pl->d_dunits, pl->n_dunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0,
-                         COVGPU_DENSE, 0, 1 << 30, nullptr, 0, INT_MAX, ds, true);
+      launch_ck_delta<T>(pl, pl->d_dunits, pl->n_dunits, ds);
       launch_ck_scan(pl, ds);
       launches += 2;
     }
@@ -1725,8 +1761,7 @@ int finalize_from_sums(covgpu_plan* pl, const void* A_dev, const double2* sums, 
       ndunits = pl->n_rdunits;
     }
     if (ndunits > 0) {
-      launch_fin_tile<T>(pl, dunits, ndunits, nullptr, 1, nullptr, nullptr, 1, nullptr, 0, 1.0, COVGPU_DENSE, 0,
-                         1 << 30, nullptr, 0, INT_MAX, st, true);
+      launch_ck_delta<T>(pl, dunits, ndunits, st);
       launch_ck_scan(pl, st);
     }
     launch_fin_tile<T>(pl, units, nunits, cc, 1, cl, rc, 1, (C2*)R_dev, r_bstride, scale, layout, 0, 1 << 30,
@@ -1787,7 +1822,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_NO_SYM", "COVGPU_SYM",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_CK_WALK", "COVGPU_NO_SYM", "COVGPU_SYM",
                         "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
@@ -2330,6 +2365,7 @@ int covgpu_plan_create(covgpu_plan_t* out, int device, int64_t batch, int64_t n,
         const int v = atoi(ce);
         if (v == 4 || v == 8 || v == 16) pl->ft_ck = v;
       }
+      pl->ck_tiled = p >= 32 && hook_env("COVGPU_CK_WALK") == nullptr;  // (hook: chunk updates by the walk kernel)
       pl->h_units = fin_tile_units(pl.get(), 0, pl->nclasses);
       pl->n_units = (long long)pl->h_units.size();
       if (pl->use_tile && ft_nck(q, pl->ft_ck) > 0) {

@@ -598,6 +598,81 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
   }
 }
 
+// k_ck_delta: the chunk updates of windows with P >= 32 as a register-tiled
+// rank-2 update in R-block coordinates (the DELTA mode of k_fin_tile holds one
+// circular diagonal per lane and re-reads the second operand per row: LSU
+// bound).  Unit = (snapshot, dc, chunk, top / bottom strip); CTA = one 32 x 32
+// sub-block of the P x P state, thread = 4 x 4 entries (r1, r2): per step 8
+// first-operand and 8 second-operand loads feed 16 rank-2 updates.  Every
+// entry takes the same FMA sequence as the walk (ft_rank2, steps ascending
+// from zero): the values equal the DELTA mode's bitwise.  Output layout as
+// there: ck[b][dc][j][T, B][r1][c], c = (r2 - r1) mod P.
+constexpr int CKD_T = 4;     // tile side per thread
+constexpr int CKD_SUB = 32;  // sub-block side per CTA (cfg5: 768 CTAs of 64 threads)
+// SMEM: the chunk's strip columns [step][l1, h1, l2, h2][CKD_SUB] (l / h: left /
+// right strip column, 1 / 2: rows r1 of column u / rows r2 of column u + dc);
+// the second operands are stored tile-interleaved (entry e at (e % 4) (CKD_SUB / 4) +
+// e / 4), so the threads of a tile row read consecutive values
+__host__ __device__ inline size_t ckd_smem(int ckstep) { return (size_t)ckstep * 4 * CKD_SUB * sizeof(double2); }
+__global__ void __launch_bounds__(256, 2)
+    k_ck_delta(const double2* __restrict__ corners, int P, int Q, int PP, const int4* __restrict__ units, int nsub,
+               int tw, double2* __restrict__ ck, int ckstep) {
+  extern __shared__ __align__(16) unsigned char ckd_sm[];
+  double2* const sm = (double2*)ckd_sm;
+  const int ns2 = nsub * nsub;
+  const int4 un = units[blockIdx.x / ns2];
+  const int sb = blockIdx.x % ns2;
+  const int rb1 = CKD_SUB * (sb / nsub), rb2 = CKD_SUB * (sb % nsub);  // (rb + 31 < PP: PP is a multiple of 32 >= P)
+  const int b = un.x, dc = un.y, which = un.z, u0 = un.w & 0xffff, u1 = un.w >> 16;
+  const int cw = 12 * PP;
+  // first-operand blocks of the corner layout: [TL, TR, BL, BR][PP]; the
+  // second operands of column u + dc are that column's first-operand blocks
+  const double2* cb = corners + (long long)b * (Q - 1) * cw + (which ? 2 * PP : 0);
+  for (int x = threadIdx.x; x < (u1 - u0) * 4 * CKD_SUB; x += blockDim.x) {
+    const int e = x % CKD_SUB, blk = x / CKD_SUB % 4, st = x / (4 * CKD_SUB);
+    const double2 v = __ldg(cb + (long long)(u0 + st + (blk >= 2 ? dc : 0)) * cw + ((blk & 1) ? PP : 0) +
+                            (blk >= 2 ? rb2 : rb1) + e);
+    sm[(st * 4 + blk) * CKD_SUB + (blk >= 2 ? (e % CKD_T) * (CKD_SUB / CKD_T) + e / CKD_T : e)] = v;
+  }
+  __syncthreads();
+  const int ty = threadIdx.x / tw, tx = threadIdx.x % tw;
+  const int r1 = rb1 + CKD_T * ty, r2 = rb2 + CKD_T * tx;
+  if (ty >= tw || r1 >= P || r2 >= P) return;
+  double2 f[CKD_T][CKD_T];
+#pragma unroll
+  for (int i = 0; i < CKD_T; ++i)
+#pragma unroll
+    for (int j = 0; j < CKD_T; ++j) f[i][j] = make_double2(0.0, 0.0);
+  const double2* s1 = sm + CKD_T * ty;
+  const double2* s2 = sm + 2 * CKD_SUB + tx;
+#pragma unroll 2
+  for (int u = u0; u < u1; ++u) {
+    double2 l1[CKD_T], h1[CKD_T], l2[CKD_T], h2[CKD_T];
+#pragma unroll
+    for (int i = 0; i < CKD_T; ++i) {
+      l1[i] = s1[i];
+      h1[i] = s1[CKD_SUB + i];
+      l2[i] = s2[i * (CKD_SUB / CKD_T)];
+      h2[i] = s2[CKD_SUB + i * (CKD_SUB / CKD_T)];
+    }
+#pragma unroll
+    for (int i = 0; i < CKD_T; ++i)
+#pragma unroll
+      for (int j = 0; j < CKD_T; ++j) ft_rank2(f[i][j], h1[i], h2[j], l1[i], l2[j]);
+    s1 += 4 * CKD_SUB;
+    s2 += 4 * CKD_SUB;
+  }
+  const long long per = (long long)P * P;
+  double2* o = ck + ((((long long)b * Q + dc) * ft_nck(Q, ckstep) + u0 / ckstep) * 2 + which) * per;
+#pragma unroll
+  for (int i = 0; i < CKD_T; ++i)
+#pragma unroll
+    for (int j = 0; j < CKD_T; ++j) {
+      const int a = r1 + i, e = r2 + j;
+      if (a < P && e < P) o[(long long)a * P + (e >= a ? e - a : e - a + P)] = f[i][j];
+    }
+}
+
 // The per-chunk state updates of one (snapshot, dc) summed in chunk order,
 // in place: ck[j] <- delta_1 + ... + delta_{j+1}.  Thread per element of the
 // [T, B][row][c] block; chunk j of column offset dc exists while

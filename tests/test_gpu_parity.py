@@ -989,3 +989,49 @@ def test_symmetric_core_sums_vs_oracle(cuda, n, m, p, q, batch, dt, monkeypatch)
         ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), p, q) / k
         assert co.rel_frobenius(packed_of(got[b].astype(np.complex128)), ref) <= tol, b
         assert co.rel_frobenius(got[b].astype(np.complex128), g2[b].astype(np.complex128)) <= tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,p,q,batch,dt", [
+    (140, 200, 64, 64, 1, np.complex128),   # cfg5's window: three chunks of 16 steps at dc = 0
+    (150, 120, 32, 32, 2, np.complex128),   # cfg3's window, batch
+    (257, 300, 33, 17, 1, np.complex128),   # P not a multiple of the 4 x 4 thread tile
+    (300, 90, 70, 20, 1, np.complex128),    # P > 64: four 64 x 64 sub-blocks per unit
+    (130, 140, 45, 40, 2, np.complex64),    # complex64 inputs, ragged P
+])
+def test_chunk_updates_tiled_equals_walk(cuda, n, m, p, q, batch, dt, monkeypatch):
+    """The walk's per-chunk state updates from the register-tiled k_ck_delta
+    (windows with P >= 32, the default) equal the ones the walk kernel's DELTA
+    mode accumulates (COVGPU_CK_WALK=1) bitwise: same FMA sequence per entry.
+    Dense, packed and a class subset; also against the C oracle."""
+    from oracle import covoracle_c
+    from paper_1303_2285_b200.plan import Plan
+
+    rng = np.random.default_rng(n + 3 * m + 7 * p + q)
+    stack = (rng.standard_normal((batch, n, m)) + 1j * rng.standard_normal((batch, n, m))).astype(dt)
+    tdt = torch.complex128 if dt == np.complex128 else torch.complex64
+    ad = torch.as_tensor(stack, device=cuda)
+
+    def run():
+        plan = Plan(n, m, WindowSpec(p, q), batch=batch, dtype=tdt, device=cuda)
+        out = plan.alloc_output()
+        plan.execute(ad, out)
+        plan.execute(ad, out)  # (second execute: the CUDA-graph replay)
+        dense = out.reshape(batch, p * q, p * q).cpu().numpy()
+        pk = plan.alloc_output("packed")
+        plan.execute(ad, pk, "packed")
+        packed = pk.reshape(batch, -1).cpu().numpy()
+        plan.close()
+        return dense, packed
+
+    d1, p1 = run()
+    monkeypatch.setenv("COVGPU_CK_WALK", "1")
+    d2, p2 = run()
+    assert np.array_equal(d1, d2) and np.array_equal(p1, p2)
+    k = (n - p + 1) * (m - q + 1)
+    tol = TOL64 if dt == np.complex128 else TOL32
+    for b in range(batch):
+        assert_hermitian(d1[b])
+        assert np.array_equal(packed_of(d1[b]), p1[b])
+        ref = covoracle_c.estimate_packed(stack[b].astype(np.complex128), p, q) / k
+        assert co.rel_frobenius(p1[b].astype(np.complex128), ref) <= tol, b
