@@ -248,6 +248,7 @@ struct covgpu_plan {
   long long ws_bytes = 0;
   size_t fin_smem = 0;
   int launches = 0;
+  int spec_launches = 0;  // kernels launch_spectral enqueued (counted at the launch sites)
   // optional per-kernel timing of the last execute (events on its stream)
   bool timing = false;
   static constexpr int kMaxEv = 12;
@@ -842,6 +843,7 @@ void spec_attr(K* fn, int logL) {
     const long long items_ = (long long)(GRID);                                                 \
     fn_<<<(unsigned)((items_ + spec_g<LG>() - 1) / spec_g<LG>()), spec_threads<LG>(),           \
           sizeof(double2) * spec_g<LG>() * spec_sb_elems<LG>(), st>>>(items_, __VA_ARGS__);     \
+    ++pl->spec_launches;                                                                        \
   } while (0)
 
 template <typename T>
@@ -866,6 +868,12 @@ struct SpecK {
   template <int LG>
   static auto rowacp() {
     if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_rowac<LG, true>; else return &k_spec_rowac<LG, false>;
+  }
+  template <int LG>
+  static auto fftac() { return &k_spec_fft_ac<T, LG, false>; }
+  template <int LG>
+  static auto fftacp() {
+    if constexpr (LG >= SPEC_LOGOUT + 3) return &k_spec_fft_ac<T, LG, true>; else return &k_spec_fft_ac<T, LG, false>;
   }
   template <int LG>
   static auto dftp() {
@@ -904,6 +912,7 @@ void launch_edges_blocked(covgpu_plan* pl, const typename CT<T>::c* A, cudaStrea
                     ntj = (g.nlines + EbTile<LG>::TJ - 1) / EbTile<LG>::TJ, ntiles = B * 2 * nti * ntj;     \
     fp<<<(unsigned)((ntiles + nparts - 1) / nparts), 1 << LG, eb_pairs_smem<LG>(), st>>>(                   \
         SP, pr, g, cols ? 1 : 0, tw, pl->d_cls_slot, pl->d_cls, dst, tot, part, nparts, ntiles);            \
+    pl->spec_launches += 2;                                                                                 \
   } while (0)
   switch (g.logLb) {
     case 6: EB_LAUNCH(6); break;
@@ -951,6 +960,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     }
     kern<<<blocks, ngrp * 32, sm, cs>>>(fx, fy, pr, lay_, nseg_, part_, nparts_, stages, gp, slot0, nslots,
                                         posonly ? 1 : 0);
+    ++pl->spec_launches;
   };
   auto corr_smem = [&](int nseg_, int part_, int nparts_, int slot0, int nslots) {
     corr_launch(st, B, pl->d_fx, sym ? pl->d_fx : pl->d_fy, pl->spec_lay, pl->d_gp, sym, nseg_, part_, nparts_,
@@ -982,6 +992,18 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
   int gslots = pl->spec_nseg;  // G partial slots the output FFT sums
   bool corr_done = false;
   const bool band_mode = pl->band_wait && B == 1 && stream_wait_value();
+  // The blocked edge sums read only A: with a side stream they go first, under
+  // the row FFTs and the correlation (queued behind the dr = 0 row transforms
+  // they started after the correlation and ended ~50 us after the main chain
+  // at cfg5).  Timing mode keeps them after the output FFT (one stream).
+  const bool edges_first = pl->spec_edges && pl->spec_blk && !band_mode && es != st && !hook_env("COVGPU_EDGES_LAST");
+  // symmetric sums on the device path: the dr = 0 row transforms run inside
+  // the row-FFT kernel (k_spec_fft_ac)
+  const bool fuse_d0 = sym && !band_mode && rz >= ra && !hook_env("COVGPU_NO_FUSE_D0");
+  if (edges_first) {
+    launch_edges_blocked<T>(pl, A, es, true, part, nparts);
+    launch_edges_blocked<T>(pl, A, es, false, part, nparts);
+  }
   if (band_mode) {
     // host path streaming A: the copy stream sends the edge columns and the
     // top / bottom strip rows first (ev_strips), then the remaining rows in
@@ -1043,6 +1065,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     mark("spec_fft");
     k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
                                                        pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1);
+    ++pl->spec_launches;
     if (pl->spec_edges && !pl->spec_blk && es != st) {
       const cudaStream_t st_main = st;
       st = es;
@@ -1074,6 +1097,13 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
         const int r0 = std::max(0, rg[0]), r1 = std::min(pr.N, rg[1]);
         if (r1 > r0) fft_rows(r0, r1 - r0);
       }
+    } else if (fuse_d0) {
+      if (pl->spec_prune_q)
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template fftacp, B * pr.N, A, pr, pl->spec_lay, pl->d_tw, pl->d_twf,
+                  pl->d_fx, 0, pr.N, ra, rz - ra + 1, pl->d_d0p);
+      else
+        SPEC_LOGL(pl->spec_logL, SpecK<T>::template fftac, B * pr.N, A, pr, pl->spec_lay, pl->d_tw, pl->d_twf,
+                  pl->d_fx, 0, pr.N, ra, rz - ra + 1, pl->d_d0p);
     } else {
       fft_rows(0, pr.N);
     }
@@ -1090,15 +1120,18 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       cudaStreamWaitEvent(es, pl->ev_d0, 0);
       st = es;
     }
-    if (rz >= ra)
+    if (rz >= ra && !fuse_d0)
       if (pl->spec_prune_q)
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowacp, B * (rz - ra + 1), pl->d_fx, fy_rows, pr,
                   pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
       else
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template rowac, B * (rz - ra + 1), pl->d_fx, fy_rows, pr,
                   pl->spec_lay, pl->d_tw, pl->d_twf, ra, rz - ra + 1, rz - ra + 1, 0, pl->d_d0p);
-    k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, st>>>(pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses,
-                                                       pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1);
+    // (fused dr = 0 rows: only this small sum is left — on the main stream, the
+    // side stream is busy with the edge sums until the end)
+    k_spec_d0sum<<<(unsigned)(B * pr.Q), 256, 0, fuse_d0 && edges_first && !hook_env("COVGPU_D0_SIDE") ? st_main : st>>>(
+        pl->d_d0p, std::max(0, rz - ra + 1), pr, pl->nclasses, pl->d_cls_slot, pl->d_ccpart, sym ? 3 : 1);
+    ++pl->spec_launches;
     if (pl->spec_edges && !pl->spec_blk && es != st_main)
       if (pl->spec_prune_q)
         SPEC_LOGL(pl->spec_logL, SpecK<T>::template rcp, (B * 2 * (long long)S * S + nparts - 1) / nparts, pl->d_fx, pl->d_fy0, pr,
@@ -1118,12 +1151,14 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     k_spec_corr<SPEC_E><<<(unsigned)(B * pl->spec_nseg * pl->spec_nfb * pl->spec_ngrp), SPEC_CW * 32, 0, st>>>(
         pl->d_fx, pl->d_fy, pr, pl->spec_lay, L, pl->spec_nfb, pl->spec_ngrp, pl->spec_nseg, part, nparts,
         pl->d_gp);
+    ++pl->spec_launches;
   }
   mark("spec_corr");
   if (gslots > 1) {  // row-segment partials -> slot 0, in order
     const long long per_seg = (long long)(2 * pr.P - 1) * L;
     const long long e_lo = sym ? (long long)(pr.P - 1) * L : 0, e_cnt = per_seg - e_lo, tot = B * e_cnt;
     k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp, gslots, per_seg, e_lo, e_cnt, tot);
+    ++pl->spec_launches;
   }
   if (pl->spec_prune_q)
     SPEC_LOGL(pl->spec_logL, SpecK<T>::template dftp, B * (2 * pr.P - 1), pl->d_gp, pl->d_tw, pl->d_twf, pr, gslots,
@@ -1142,7 +1177,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
       CUDA_TRY_V(cudaStreamWaitEvent(es, pl->ev_h2d, 0));
       launch_edges_blocked<T>(pl, A, es, true, part, nparts);
       mark("spec_ccol");
-    } else {
+    } else if (!edges_first) {
       launch_edges_blocked<T>(pl, A, es, true, part, nparts);
       mark("spec_ccol");
       launch_edges_blocked<T>(pl, A, es, false, part, nparts);
@@ -1191,6 +1226,7 @@ void launch_spectral(covgpu_plan* pl, const typename CT<T>::c* A, cudaStream_t s
     if (ns2 > 1) {
       const long long per_seg = (long long)(2 * pr.P - 1) * L2, tot = 2 * B * per_seg;
       k_spec_gsum<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->d_gp2, ns2, per_seg, 0, per_seg, tot);
+      ++pl->spec_launches;
     }
     SPEC_LOGL(pl->spec2_logL, SpecK<T>::template dft, 2 * B * (2 * pr.P - 1), pl->d_gp2, pl->d_tw2, pl->d_twf2, pr,
               ns2, pl->nclasses, pl->d_cls_slot, pl->d_ccpart, 3, 1, 0, 1, 1);
@@ -1507,8 +1543,9 @@ int launch_all(covgpu_plan* pl, const void* A_dev, void* R_dev, int layout, doub
   bool mma = false;
   if (pl->use_spec) {
     // (band_wait: launch_spectral waits per band for the row FFTs, then for all of A)
+    pl->spec_launches = 0;
     launch_spectral<T>(pl, A, st, es, mark);
-    launches += 8;  // rowac, fft x2, corr, gsum, dft, colfft, ccol, rc
+    launches += pl->spec_launches;
     mma = true;
   }
   if constexpr (sizeof(T) == 8) {
@@ -1822,7 +1859,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_CK_WALK", "COVGPU_NO_SYM", "COVGPU_SYM",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_CK_WALK", "COVGPU_EDGES_LAST", "COVGPU_NO_FUSE_D0", "COVGPU_NO_SYM", "COVGPU_SYM",
                         "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";

@@ -878,6 +878,55 @@ __global__ void __launch_bounds__(spec_threads<LOGL>())
     spec_fft_block<LOGL>(sb, si.tl, tw, ld, stf);
 }
 
+// k_spec_fft mode 2 with the dr = 0 row transform of k_spec_rowac fused (the
+// symmetric core sums on the device path: one spectrum per row, X_r = Y_r):
+// the CTA writes its row's spectrum, then transforms X_r conj(X_r) read back
+// from the row it just wrote (L2 / L1, not HBM) — the same values in the
+// same order as k_spec_rowac on that spectrum, so D0p is bitwise the same;
+// the separate kernel's re-read of every spectrum and its launch are gone.
+// Rows outside the core rows [row_a, row_a + nd0) run the second transform
+// without storing (the FFT's barriers are CTA-wide).
+template <typename T, int LOGL, bool PRUNE = false>
+__global__ void __launch_bounds__(spec_threads<LOGL>())
+    k_spec_fft_ac(long long nitems, const typename CT<T>::c* __restrict__ A, Problem pr, SpecLayout lay,
+                  const double2* __restrict__ tw, const double2* __restrict__ twf, double2* FX, int row0, int nrows,
+                  int row_a, int nd0, double2* __restrict__ D0p) {
+  extern __shared__ double2 sbuf[];
+  constexpr int L = 1 << LOGL;
+  double2* sb;
+  const SpecItem si = spec_item<LOGL>(nitems, sb, sbuf);
+  const int M = pr.M, Q = pr.Q;
+  const int r = row0 + (int)(si.item % nrows);
+  const long long b = si.item / nrows;
+  const int clo = Q - 1, chi = M - Q;
+  double2* out = FX + lay.at(b, r, 0);
+  const typename CT<T>::c* row = A + (b * pr.N + r) * (long long)M;
+  const long long fs = (long long)lay.np * 32;  // next 32-frequency block
+  const bool ok = si.valid;
+  spec_fft_block<LOGL>(
+      sb, si.tl, tw,
+      [&](int idx) { return (ok && idx >= clo && idx <= chi) ? widen2(row[idx]) : make_double2(0.0, 0.0); },
+      [&](int idx, double2 v) {
+        if (ok) out[(idx >> 5) * fs + (idx & 31)] = v;
+      });
+  __syncthreads();  // the row's spectrum is visible to the CTA; sb is free
+  const bool core = ok && r >= row_a && r < row_a + nd0;
+  const double inv = 1.0 / (double)L;
+  double2* d0 = D0p + (b * nd0 + (r - row_a)) * (long long)Q;
+  auto ld = [&](int idx) {
+    if (!core) return make_double2(0.0, 0.0);
+    const double2 x = out[(idx >> 5) * fs + (idx & 31)];
+    return make_double2(fma(x.x, x.x, x.y * x.y), fma(x.y, x.x, -x.x * x.y));  // x conj(x), as k_spec_rowac forms it
+  };
+  auto stf = [&](int idx, double2 v) {
+    if (core && idx < Q) d0[idx] = make_double2(v.x * inv, v.y * inv);
+  };
+  if constexpr (PRUNE)
+    spec_fft_pruned<LOGL>(sb, si.tl, tw, twf, ld, stf);
+  else
+    spec_fft_block<LOGL>(sb, si.tl, tw, ld, stf);
+}
+
 // CC(0, dc) = sum over the band's core rows of the per-row transforms
 // (k_spec_rowac): CTA = (b, dc), thread = a contiguous run of rows summed in
 // order, then a fixed-shape tree over the threads — deterministic.
