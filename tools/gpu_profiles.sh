@@ -15,9 +15,12 @@ cap() {  # name regex count cfg
   ncu -i /tmp/$1.ncu-rep --page details --csv > gpurun_out/$1_details.csv 2>/dev/null
   rm -f /tmp/$1.ncu-rep
 }
-cap r02_ncu_fin_cfg5_$V k_fin_tile 3 cfg5
+cap r02_ncu_fin_cfg5_$V k_fin_tile 2 cfg5
 cap r02_ncu_corr_cfg5_$V k_spec_corr_smem 1 cfg5
 cap r02_ncu_snap_cfg4_$V k_snap_spec 1 cfg4
 cap r02_ncu_eb_cfg5_$V k_eb_pairs 2 cfg5
+cap r02_ncu_fftac_cfg5_$V k_spec_fft_ac 1 cfg5
+cap r02_ncu_ckdelta_cfg5_$V k_ck_delta 1 cfg5
+python tools/step_timeline.py cfg5 > gpurun_out/r02_step_timeline_cfg5_$V.txt 2>&1
 python tools/e2e_timeline.py cfg5 > gpurun_out/r02_e2e_timeline_cfg5_$V.txt 2>&1
 ls gpurun_out | grep $V
