@@ -1859,7 +1859,7 @@ struct PlanKey {
 std::string path_env() {
   std::string e;
   for (const char* k : {"COVGPU_SPECTRAL", "COVGPU_NO_SPECTRAL", "COVGPU_NO_MMA", "COVGPU_NO_MMA_EDGE",
-                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_CK_WALK", "COVGPU_EDGES_LAST", "COVGPU_NO_FUSE_D0", "COVGPU_NO_SYM", "COVGPU_SYM",
+                        "COVGPU_NO_TMA", "COVGPU_MMA_KIND", "COVGPU_SPEC_NO_SMEM", "COVGPU_NO_DIRECT", "COVGPU_SPEC_E", "COVGPU_NO_GRAPH", "COVGPU_NO_SNAP", "COVGPU_FT_CK", "COVGPU_CK_WALK", "COVGPU_EDGES_LAST", "COVGPU_NO_FUSE_D0", "COVGPU_D0_SIDE", "COVGPU_NO_SYM", "COVGPU_SYM",
                         "COVGPU_SPEC_NO_PRUNE", "COVGPU_EDGE_PAIRFFT"}) {
     const char* v = getenv(k);
     e += v ? v : "-";
