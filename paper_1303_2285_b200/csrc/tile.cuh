@@ -242,6 +242,9 @@ __device__ inline void ft_init_entry(int r1, int c, int P, const FtLane& L, cons
 #ifndef FT_MINB
 #define FT_MINB 2
 #endif
+#ifndef FT_DENSE_CS
+#define FT_DENSE_CS true  // dense R's stores evict-first as well
+#endif
 // DELTA: unit = (snapshots, dc, band, chunk [16 (j-1), 16 j)); the chunk's
 // state updates from zero go to ck[b][dc][j-1][T, B][row][c] (no output).
 // LANES < 32: a warp holds 32 / LANES snapshots (lane = (snapshot, c)).
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
       const int src = msrc0 + k - (k >= mwrap ? P : 0);
       C2 val = stg[src * 32];
       val.y = -val.y;
-      ft_store<false>(mrow + src, val, (mmask >> k) & 1u);
+      ft_store<FT_DENSE_CS>(mrow + src, val, (mmask >> k) & 1u);
       mrow += D;
     }
   };
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(FtCfg<NWARP>::THREADS, NWARP == 8 ? FT_MINB : 
       if constexpr (PACKED)
         ft_store<true>(rk + colk, val, on);
       else if constexpr (DENSE)
-        ft_store<false>(rk + colk, val, on);
+        ft_store<FT_DENSE_CS>(rk + colk, val, on);
       else
         ft_store<false>(rk, val, on);
       if constexpr (DENSE) stg[k * 32] = val;
